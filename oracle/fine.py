@@ -1,0 +1,160 @@
+"""Fine solvers F_n, F_n', F_n'^* and offsets b_n -- TEST INFRASTRUCTURE ONLY.
+
+Paper: the fine solver is backward Euler with equidistant steps;
+F_n is affine, F_n v = F_n' v + b_n with b_n := F_n 0 (eq.
+F_n_affine); the adjoint F_n'^* is defined by (F_n'^* w, v) = (w, F_n' v)
+(P:271-273), which for a product of m step solves is the product of the
+transposed solves in reverse order.
+
+One step of interval n (1-based), j = 1..m, global index g = (n-1)*m + j:
+        (I + dt A) u_j = u_{j-1} + dt f(t_g)            (reading Z3)
+
+1D: each step is one Thomas solve (oracle/csrc/oracle_thomas.c), pivots from
+    the exact row sums of I + dt A (reading R-ACC).
+2D: A = T(x)I + I(x)T (5-point, Dirichlet).  The step is solved exactly by
+    the classical fast-Poisson partial diagonalisation: transform the x index
+    with the orthogonal sine matrix S (T = S diag(lam) S), then for every
+    x-mode i solve the tridiagonal system ((1 + dt lam_i) I + dt T) in y with
+    Thomas.  The state stays x-transformed across the m steps of one call
+    (every step is still one exact linear solve); input and output are
+    physical-space vectors.  Pinned against a dense direct solve.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from ._clib import thomas_batch
+
+
+# --------------------------------------------------------------------- 1D
+class Op1D:
+    """A = tridiag(sub, diag, sup) on n interior points, time step dt, m steps.
+
+    rowsum/colsum: exact row/column sums of A (problem data); when given, the
+    Thomas pivots use the row-sum recurrence (oracle_thomas.c, reading R-ACC)."""
+
+    def __init__(self, sub, diag, sup, dt: float, m: int, rowsum=None, colsum=None):
+        self.n = len(diag)
+        self.A = (np.asarray(sub, float), np.asarray(diag, float), np.asarray(sup, float))
+        self.dt, self.m = float(dt), int(m)
+        a, d, c = self.A
+        # I + dt A, and its row sums 1 + dt * rowsum(A)
+        self.T = (dt * a, 1.0 + dt * d, dt * c)
+        self.T_rs = None if rowsum is None else 1.0 + dt * np.asarray(rowsum, float)
+        # (I + dt A)^T: T^T[i, i-1] = T[i-1, i]; its row sums are T's column sums
+        subT = np.zeros(self.n)
+        supT = np.zeros(self.n)
+        subT[1:] = self.T[2][:-1]
+        supT[:-1] = self.T[0][1:]
+        self.TT = (subT, self.T[1], supT)
+        self.TT_rs = None if colsum is None else 1.0 + dt * np.asarray(colsum, float)
+
+    def dense_A(self) -> np.ndarray:
+        a, d, c = self.A
+        return np.diag(d) + np.diag(a[1:], -1) + np.diag(c[:-1], 1)
+
+
+def fine_1d(op: Op1D, interval: int, X: np.ndarray, mode: str = "linear", src=None,
+            src_index=None) -> np.ndarray:
+    """Apply F_n (mode 'affine'), F_n' ('linear') or F_n'^* ('adjoint') to rows of X.
+
+    X: (nvec, n).  src = (space[R, n], time[R, N*m], amp[nsrc, R]); src_index[v]
+    selects the source of vector v (default 0).  Returns a new array.
+    """
+    X = np.array(X, dtype=np.float64, order="C", copy=True)
+    if X.ndim == 1:
+        return fine_1d(op, interval, X[None, :], mode, src, src_index)[0]
+    nvec = X.shape[0]
+    if mode == "adjoint":
+        # transposed solves in reverse step order (all steps share A here, so the
+        # reversal only matters formally; no source term in F'^*).
+        for _ in range(op.m):
+            thomas_batch(*op.TT, X, rowsum=op.TT_rs)
+        return X
+    for j in range(1, op.m + 1):
+        if mode == "affine" and src is not None:
+            space, time, amp = src
+            g = (interval - 1) * op.m + j
+            idx = np.zeros(nvec, dtype=int) if src_index is None else np.asarray(src_index)
+            coef = amp[idx] * time[:, g - 1][None, :]          # (nvec, R)
+            X += op.dt * (coef @ space)                          # f(x_i, t_g)
+        thomas_batch(*op.T, X, rowsum=op.T_rs)
+    return X
+
+
+# --------------------------------------------------------------------- 2D
+def sine_matrix(n: int) -> np.ndarray:
+    """Orthogonal symmetric S_ij = sqrt(2/(n+1)) sin((i+1)(j+1) pi/(n+1))."""
+    i = np.arange(1, n + 1, dtype=np.float64)
+    return np.sqrt(2.0 / (n + 1)) * np.sin(np.outer(i, i) * np.pi / (n + 1))
+
+
+class Op2D:
+    """A = T(x)I + I(x)T with T = tridiag(sub, diag, sup) (constant coefficients)."""
+
+    def __init__(self, sub, diag, sup, dt: float, m: int, rowsum=None):
+        self.n = len(diag)
+        n = self.n
+        self.A1 = (np.asarray(sub, float), np.asarray(diag, float), np.asarray(sup, float))
+        self.dt, self.m = float(dt), int(m)
+        a, d, c = self.A1
+        # eigenpairs of the constant-coefficient T: T = S diag(lam) S
+        assert np.allclose(a[1:], a[1]) and np.allclose(d, d[0]) and np.allclose(c[:-1], c[0])
+        self.S = sine_matrix(n)
+        i = np.arange(1, n + 1, dtype=np.float64)
+        # lam_i = d + 2c cos(i pi/(n+1)) = -4c sin^2(i pi / (2(n+1))) (d = -2c), no cancellation
+        assert np.allclose(d[0], -2.0 * c[0])
+        self.lam = -4.0 * c[0] * np.sin(i * np.pi / (2.0 * (n + 1))) ** 2
+        self.Ty = (dt * a, 1.0 + dt * d, dt * c)   # I + dt T  (the y-direction part)
+        # row sums of the line systems (1 + dt lam_i) I + dt T: 1 + dt rowsum(T), + shift
+        self.Ty_rs = None if rowsum is None else 1.0 + dt * np.asarray(rowsum, float)
+
+    def dense_A(self) -> np.ndarray:
+        a, d, c = self.A1
+        T = np.diag(d) + np.diag(a[1:], -1) + np.diag(c[:-1], 1)
+        I = np.eye(self.n)
+        return np.kron(T, I) + np.kron(I, T)
+
+
+def fine_2d(op: Op2D, interval: int, X: np.ndarray, mode: str = "linear", src=None) -> np.ndarray:
+    """X: (nvec, n, n) [vector, x-index, y-index].  A is symmetric and time
+    independent, so F'^* = F' (mode 'adjoint' == 'linear').  src = (gx, gy)."""
+    X = np.array(X, dtype=np.float64, copy=True)
+    if X.ndim == 2:
+        return fine_2d(op, interval, X[None], mode, src)[0]
+    nvec, n = X.shape[0], op.n
+    S = op.S
+    V = np.ascontiguousarray(np.einsum("ij,bjk->bik", S, X))      # x-transform
+    shift = np.tile(op.dt * op.lam, nvec)
+    for j in range(1, op.m + 1):
+        if mode == "affine" and src is not None:
+            gx, gy = src
+            g = (interval - 1) * op.m + j
+            Sg = S @ gx[:, g - 1, :].T                                 # (n, nb)
+            V += op.dt * (Sg @ gy[:, g - 1, :])[None]                  # S f_g
+        thomas_batch(*op.Ty, V.reshape(nvec * n, n), shift, rowsum=op.Ty_rs)
+    return np.einsum("ij,bjk->bik", S, V)
+
+
+# ---------------------------------------------------------------- dispatch
+def make_op(cfg):
+    from workloads import generators as G
+    if cfg.dim == 1:
+        rs, cs = G.operator_1d_sums(cfg)
+        return Op1D(*G.operator_1d(cfg), cfg.dt, cfg.m, rowsum=rs, colsum=cs)
+    return Op2D(*G.laplacian_1d_for_2d(cfg), cfg.dt, cfg.m,
+                rowsum=G.laplacian_1d_for_2d_sums(cfg))
+
+
+def fine(op, interval, X, mode="linear", src=None, src_index=None):
+    if isinstance(op, Op1D):
+        return fine_1d(op, interval, X, mode, src, src_index)
+    return fine_2d(op, interval, X, mode, src)
+
+
+def sequential_reference(op, u0, N: int, src=None, src_index=None):
+    """u_{n+1} = F_{n+1} u_n, 0 <= n < N.  u0: (nvec, ...) batch."""
+    out = [np.array(u0, dtype=np.float64)]
+    for n in range(1, N + 1):
+        out.append(fine(op, n, out[-1], "affine", src, src_index))
+    return np.stack(out)

@@ -1,0 +1,98 @@
+"""Randomized SVD of the transfer operator F_n' -- TEST INFRASTRUCTURE ONLY.
+
+Follows P:258-299 ("Computation of G_n", steps 1-6) in the paper's order:
+
+ 1. draw l = R_n + p random vectors omega_i (oracle/rng.py) and compute
+    F_n' omega_i;
+ 2. orthonormal basis w_1..w_l of W = span{F_n' omega_i};
+ 3. compute F_n'^* w_i;
+ 4. orthonormal basis v_1..v_l of span{F_n'^* w_i};
+ 5. M_ij := (F_n'^* w_i, v_j), its SVD M = Psi Sigma Phi^T, and
+    psi_r = sum_i Psi_{i,r} w_i,  phi_r = sum_i Phi_{i,r} v_i
+    -- the paper's P:293-294 prints w and v the other way round; the printed
+    assignment does not give the SVD of P_W F_n' (SURVEY finding 4, pinned
+    in tests by ||F' - G'|| = sigma_{k+1}); reading Z5;
+ 6. return the first R_n triples.
+
+Spectral coarse solver (eq. spectral_G):
+    G_n v = sum_{r <= R_n} psi_r sigma_r (phi_r, v) + b_n.
+Euclidean inner product throughout (V = R^m case; reading Z1).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .fine import Op1D, fine
+from .linalg import householder_qr, jacobi_svd
+from .rng import gaussian_sketch
+
+
+@dataclass
+class Truncated:
+    U: np.ndarray       # (n_dof, k)  left singular vectors psi_r
+    sigma: np.ndarray   # (l,)        all computed singular values of P_W F_n'
+    V: np.ndarray       # (n_dof, k)  right singular vectors phi_r
+    k: int
+
+    def apply_linear(self, X: np.ndarray) -> np.ndarray:
+        """G_n' x for rows x of X (n_vec, n_dof)."""
+        s = self.sigma[: self.k]
+        return ((X @ self.V) * s) @ self.U.T
+
+
+def _as_vectors(op, cols: np.ndarray) -> np.ndarray:
+    """(n_dof, l) column block -> fine-solver batch layout."""
+    if isinstance(op, Op1D):
+        return np.ascontiguousarray(cols.T)
+    n = op.n
+    return np.ascontiguousarray(cols.T.reshape(-1, n, n))
+
+
+def _as_columns(op, vecs: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(vecs.reshape(vecs.shape[0], -1).T)
+
+
+def rsvd_interval(op, interval: int, k: int, p: int, seed: int) -> Truncated:
+    """Steps 1-6 for the 1-based interval n = `interval`."""
+    l = k + p
+    n_dof = op.n if isinstance(op, Op1D) else op.n * op.n
+    # step 1
+    Omega = gaussian_sketch(seed, interval - 1, n_dof, l)
+    Y = _as_columns(op, fine(op, interval, _as_vectors(op, Omega), "linear"))
+    # step 2
+    W, _ = householder_qr(Y)
+    # step 3
+    Z = _as_columns(op, fine(op, interval, _as_vectors(op, W), "adjoint"))
+    # step 4
+    Vb, _ = householder_qr(Z)
+    # step 5: M_ij = (F'^* w_i, v_j)
+    M = Z.T @ Vb
+    Psi, sig, Phi = jacobi_svd(M)
+    U = W @ Psi[:, :k]
+    V = Vb @ Phi[:, :k]
+    # step 6
+    return Truncated(U=U, sigma=sig, V=V, k=k)
+
+
+def exact_truncated(Fdense: np.ndarray, k: int) -> Truncated:
+    """Truncated SVD of a dense F' (tiny grids only): eq. svd / spectral_G."""
+    from .linalg import jacobi_svd as _svd
+    Uf, s, Vf = _svd(Fdense)
+    return Truncated(U=Uf[:, :k], sigma=s, V=Vf[:, :k], k=k)
+
+
+def dense_transfer(op, interval: int = 1, mode: str = "linear") -> np.ndarray:
+    """Matrix of F_n' by applying it to every unit vector (tiny grids only)."""
+    n_dof = op.n if isinstance(op, Op1D) else op.n * op.n
+    E = np.eye(n_dof)
+    return _as_columns(op, fine(op, interval, _as_vectors(op, E), mode))
+
+
+def delta_eps(truncs) -> tuple:
+    """delta := max_n sigma_{n,1}, eps := max_n sigma_{n,R_n+1} (P:407-411,
+    with the computed sigma_{n,k+1} as the estimate; Z19)."""
+    delta = max(t.sigma[0] for t in truncs)
+    eps = max(t.sigma[t.k] if t.k < len(t.sigma) else 0.0 for t in truncs)
+    return delta, eps
