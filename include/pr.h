@@ -1,0 +1,228 @@
+/* pr.h -- C ABI of the B200-native spectral-coarse-solver Parareal hot path.
+ *
+ * Gander, Ohlberger, Rave, "A Parareal Algorithm with Spectral Coarse Solver"
+ * (arXiv 2508.08873).  Citations "P:n" are lines of the paper's LaTeX source
+ * (reference/PAPER.md); "§" are its sections.
+ *
+ * The library computes, on one GPU, for the time intervals it owns:
+ *   - the fine solver F_n (backward Euler), its linear part F_n',
+ *     the adjoint F_n'^* and offsets b_n = F_n 0 (eq. F_n_affine,
+ *     P:162-167)                                       -> pr_fine_propagate
+ *   - the randomized SVD of F_n' (§2.1 steps 1-6) giving the
+ *     spectral coarse solvers G_n' = U_n Sigma_n V_n^T (eq. spectral_G,
+ *     P:186-195)                                       -> pr_build_coarse
+ *   - the Parareal iteration (eq. def_Parareal) with the update
+ *     norms of the a posteriori bound      -> pr_parareal
+ *   - the a priori / a posteriori bounds -> pr_bounds
+ *
+ * Conventions (all functions):
+ *   - Every call returns pr_status; PR_OK = 0.  No call aborts the process.
+ *     pr_last_error() returns a thread-local message for the last failure.
+ *   - Arguments are validated before any launch: a PR_EINVAL / PR_EDIM call
+ *     writes nothing.  After PR_ENOCONV / PR_ECUDA outputs are undefined.
+ *   - `double*` buffers are owned by the caller.  Unless stated "host", they
+ *     are device pointers (e.g. torch CUDA tensors).  Handles (pr_op,
+ *     pr_coarse) are owned by the library and freed only by *_destroy.
+ *   - Work is enqueued asynchronously on the caller's `stream` (a
+ *     cudaStream_t passed as void*; NULL = legacy default stream), except
+ *     functions documented as synchronizing.
+ *   - Interval indices are 0-based: q = n - 1 for the paper's interval n,
+ *     covering (t_q, t_{q+1}] = (q*m*dt, (q+1)*m*dt].
+ *   - Floating point is fp64 throughout.
+ *
+ * Vector storage ("op layout"), chosen by the operator:
+ *   1D (pr_op_create_tridiag): `rows` = n.  A batch of B vectors is a
+ *     row-major (n x ld) array with the vector index fastest: element (i, c)
+ *     at U[i*ld + c], ld >= B.  (Coalesced across vectors for the stepper.)
+ *   2D (pr_op_create_sep2d, n x n interior grid): `rows` = (n+1)^2.  Vector c
+ *     is contiguous at U[c*ld + ix*(n+1) + iy], ld >= (n+1)^2, where ix, iy in
+ *     0..n and index 0 is the (zero) Dirichlet ghost row/column; interior
+ *     point (ix, iy) >= 1 sits at x = ix*h, y = iy*h, h = 1/(n+1).  Ghost
+ *     entries of inputs must be 0; outputs keep them 0.
+ */
+#ifndef PR_H
+#define PR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PR_OK = 0,
+    PR_EINVAL = 1,     /* bad argument (null pointer, negative size, bad mode)   */
+    PR_EDIM = 2,       /* dimension mismatch between arguments and handles        */
+    PR_ESINGULAR = 3,  /* zero/negative pivot in an operator factorization        */
+    PR_ENOCONV = 4,    /* CholeskyQR or Jacobi SVD did not converge               */
+    PR_EUNAVAIL = 5,   /* quantity not available (e.g. eps needs p >= 1)          */
+    PR_EOOM = 6,       /* device allocation failed                                */
+    PR_ECUDA = 7       /* CUDA runtime error (message in pr_last_error)           */
+} pr_status;
+
+const char *pr_last_error(void);
+int pr_version(void);
+
+typedef struct pr_op_s *pr_op;
+typedef struct pr_coarse_s *pr_coarse;
+
+/* ------------------------------------------------------------------ operator */
+
+/* 1D operator: A = tridiag(sub, diag, sup) (host arrays of length n; sub[0]
+ * and sup[n-1] ignored), semi-discretisation u_t = -A u + f.  The fine step is
+ * (I + dt A) u_{j+1} = u_j + dt f(t_{j+1}).  rowsum / colsum
+ * (host, length n, may be NULL) are the exact row / column sums of A: when
+ * given, the LU and UL pivots of I + dt A are computed from them (DESIGN.md
+ * reading R-ACC: relative accuracy independent of dt/h^2 for diagonally
+ * dominant M-matrices); when NULL they are formed as sub+diag+sup.  The
+ * factorization runs once, in a device kernel.  Synchronizing.
+ * Errors: EINVAL (n < 2, dt <= 0, null arrays), ESINGULAR (pivot <= 0 or
+ * non-finite), EOOM, ECUDA. */
+pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, const double *sup,
+                               const double *rowsum, const double *colsum, double dt,
+                               pr_op *out);
+
+/* 2D operator: 5-point Laplacian on the unit square with homogeneous
+ * Dirichlet conditions, n x n interior points, A = T (x) I + I (x) T,
+ * T = tridiag(-1, 2, -1)/h^2.  Solved in the sine eigenbasis of T (DESIGN.md
+ * "K2").  Synchronizing.  Errors: EINVAL (n < 2, (n+1) % 16 != 0, dt <= 0). */
+pr_status pr_op_create_sep2d(int n, double dt, pr_op *out);
+
+pr_status pr_op_destroy(pr_op op);
+
+/* Storage rows of one vector (n in 1D, (n+1)^2 in 2D), spatial dimension, n. */
+pr_status pr_op_info(pr_op op, long *rows, int *dim, int *n);
+
+/* -------------------------------------------------------------------- source */
+enum { PR_SRC_NONE = 0, PR_SRC_SEP1D = 1, PR_SRC_BUMP2D = 2 };
+
+/* Host-sampled separable source term (device pointers):
+ *   PR_SRC_SEP1D:  f_s(x_i, t_g) = sum_r amp[s*nterms + r] * space[r*n + i] * time[r*nsteps + g-1]
+ *   PR_SRC_BUMP2D: f(x_ix, y_iy, t_g) = sum_b gx[(b*nsteps + g-1)*(n+1) + ix] * gy[(b*nsteps + g-1)*(n+1) + iy]
+ *                  (index 0 of gx/gy is the ghost and must be 0)
+ * g = q*m + j is the global step (1-based) of step j of interval q; the
+ * source of step g is evaluated at t_g = g*dt (reading Z3). */
+typedef struct {
+    int kind;
+    int nterms;          /* R (1D terms) or number of bumps (2D), 1..8            */
+    int nsrc;            /* number of independent sources S (1D); 1 for 2D        */
+    int nsteps;          /* length of the time axis (>= (last interval+1)*m)      */
+    const double *space; /* 1D */
+    const double *time;  /* 1D */
+    const double *amp;   /* 1D */
+    const double *gx;    /* 2D */
+    const double *gy;    /* 2D */
+} pr_source;
+
+/* ---------------------------------------------------------- fine propagation */
+enum { PR_LINEAR = 0, PR_ADJOINT = 1, PR_AFFINE = 2 };
+
+/* m backward-Euler steps of interval q = first_interval + c / vecs_per_interval
+ * applied to each of the B vectors c of U_in (op layout, stride ld_in):
+ *   PR_LINEAR:  U_out = F_q' U_in                 (no source)
+ *   PR_ADJOINT: U_out = F_q'^* U_in               (transposed steps, reverse order)
+ *   PR_AFFINE:  U_out = F_q U_in = F_q' U_in + b_q (source f; vector c uses
+ *               source c % f->nsrc; eq. F_n_affine)
+ * U_in == NULL means a zero input (so PR_AFFINE gives b_q).  offset (nullable,
+ * op layout, stride ld_off) is added to the result: F' u + b_q from a stored
+ * b_q.  U_in may equal U_out (in place) when ld_in == ld_out.
+ * Errors: EINVAL (mode, m < 0, B < 0, vecs_per_interval < 1, missing source
+ * for PR_AFFINE with f->kind mismatched to the op), EDIM (ld too small). */
+pr_status pr_fine_propagate(pr_op op, int mode, int first_interval, int m, int B,
+                            int vecs_per_interval, const pr_source *f,
+                            const double *U_in, long ld_in, double *U_out, long ld_out,
+                            const double *offset, long ld_off, void *stream);
+
+/* The Gaussian test vectors of rSVD step 1: Omega_q (rows x l)
+ * for intervals q = first_interval .. first_interval + n_intervals - 1 into
+ * out (op layout, vector (q - first_interval)*l + c, stride ld).  Philox4x64-10,
+ * key (seed, 0), counter (i/4, c, q, 0), Box-Muller (reading R-RNG);
+ * 2D numbers interior DOFs i = (ix-1)*n + (iy-1).  pr_build_coarse generates
+ * the same values fused into its first stepper pass; this entry exists so the
+ * generator can be checked on its own. */
+pr_status pr_gaussian_sketch(pr_op op, int first_interval, int n_intervals, int l, uint64_t seed,
+                             double *out, long ld, void *stream);
+
+/* ------------------------------------------------------------ coarse solvers */
+
+/* Randomized SVD of F_q' for q = first_interval .. first_interval
+ * + n_local - 1 of N_total intervals, rank k, oversampling p (l = k + p <= 128,
+ * l <= rows):
+ *   1. Y = F_q' Omega_q, Omega generated in the stepper (pr_gaussian_sketch)
+ *   2. W = orth(Y)      iterated shifted CholeskyQR (reading Z7)
+ *   3. Z = F_q'^* W
+ *   4. V R_Z = Z        (same orthonormalisation, R_Z accumulated)
+ *   5. M = R_Z^T (= (F'^* w_i, v_j)), M = Psi Sigma Phi^T by one-sided Jacobi;
+ *      psi_r = W Psi_r, phi_r = V Phi_r (swapped reading of P:293-294, Z5)
+ *   6. keep r <= k.
+ * Seeds depend only on (seed, q, column), so results do not depend on how the
+ * intervals are sharded.  The handle also precomputes the reduced sweep
+ * matrices C_q = Sigma_q V_q^T U_{q-1}.
+ * Asynchronous; errors detected on the device (no convergence) are reported by
+ * pr_coarse_info.  Errors: EINVAL, EDIM (l > 128 or l > rows), EOOM. */
+pr_status pr_build_coarse(pr_op op, int N_total, int first_interval, int n_local, int m,
+                          int k, int p, uint64_t seed, void *stream, pr_coarse *out);
+
+/* Synchronizing.  k, l, n_local, first_interval, m; delta = max_q sigma_{q,1}
+ * and eps = max_q sigma_{q,k+1} over the local intervals (eq.
+ * bounds_delta_eps; eps uses the computed sigma_{k+1});
+ * sigma_host (nullable, host, n_local*l) all computed singular values;
+ * qr_passes (nullable, host, 2) the CholeskyQR pass counts of steps 2 and 4.
+ * Returns PR_ENOCONV if a QR or SVD failed to converge on the device, and
+ * PR_EUNAVAIL for eps when p == 0 (eps set to NaN). */
+pr_status pr_coarse_info(pr_coarse G, int *k, int *l, int *n_local, int *first_interval, int *m,
+                         double *delta, double *eps, double *sigma_host, int *qr_passes);
+
+/* Device views of the factors: U and V are (n_local, rows, k) row-major
+ * (U[(q*rows + i)*k + r]), sigma is (n_local, l).  Owned by the handle. */
+pr_status pr_coarse_factors(pr_coarse G, const double **U, const double **V, const double **sigma);
+
+/* Y = G_q' X = U_q Sigma_q V_q^T X for nvec probe vectors (op layout). */
+pr_status pr_coarse_apply(pr_coarse G, int q_local, int nvec, const double *X, long ldx,
+                          double *Y, long ldy, void *stream);
+
+pr_status pr_coarse_destroy(pr_coarse G);
+
+/* ----------------------------------------------------------------- Parareal */
+
+/* Parareal (eq. def_Parareal) over all N intervals of G (which must
+ * hold every interval, first_interval = 0), nsrc independent sources sharing
+ * G' (Remark affine_g_n), with G_n = G_n' + b_n:
+ *   b_q = F_q 0                                    (PR_AFFINE from zero)
+ *   u^0_0 = u0, u^0_{q+1} = G_{q+1} u^0_q           (initialisation)
+ *   u^{k+1}_{q+1} = F_{q+1} u^k_q + G'_{q+1} u^{k+1}_q - G'_{q+1} u^k_q
+ * for K_iter iterations.  The fine solves of an iteration run as one batched
+ * stepper launch (F' u + b_q); the sequential part runs in the reduced
+ * coordinates e_q = C_q e_{q-1} + (q_q - p_q) of dimension k (DESIGN.md
+ * "reduced sweep"; exact algebra, no approximation).
+ *   u0       device, nsrc vectors (op layout, stride ld_u0)
+ *   U_out    device, (N+1)*nsrc vectors, vector j*nsrc + s = u^K_j of source s
+ *            (op layout, stride ld_out); also used as the iteration state.
+ *   upd_host host, nullable, K_iter x (N+1) x nsrc: ||u^k_j - u^{k-1}_j||, k = 1..K
+ *   bnorm_host host, nullable, (N+1) x nsrc: ||b_j|| with b_0 := u0
+ *   hist     device, nullable: if given, u^k (all (N+1)*nsrc vectors, same
+ *            layout as U_out) is stored at hist + k*hist_stride, k = 0..K.
+ * Synchronizing (at the end, to fill the host arrays).
+ * Errors: EINVAL, EDIM (G not covering all intervals, source/op mismatch). */
+pr_status pr_parareal(pr_coarse G, pr_op op, int nsrc, const double *u0, long ld_u0,
+                      const pr_source *f, int K_iter, double *U_out, long ld_out,
+                      double *upd_host, double *bnorm_host, double *hist, long hist_stride,
+                      void *stream);
+
+/* --------------------------------------------------------------------- bounds */
+
+/* Host only.  delta, eps (eq. bounds_delta_eps), bnorm[m] = ||b_m|| (b_0 =
+ * u0), m = 0..N; upd[(k-1)*(N+1) + n] = ||u^k_n - u^{k-1}_n||, k = 1..K.
+ * Outputs (host, nullable):
+ *   apriori[k*(N+1) + n], k = 0..K: eq. error_bound_initial (k = 0) and
+ *                                   eq. error_bound_eps_delta2 (k >= 1)
+ *   apost[(k-1)*(N+1) + n], k = 1..K: eq. apost_bound
+ *   apost_sup[k-1]: eq. apost_bound_sup (NaN if delta >= 1)
+ * Binomials are evaluated in log space.  Errors: EINVAL. */
+pr_status pr_bounds(double delta, double eps, int N, int K, const double *bnorm,
+                    const double *upd, double *apriori, double *apost, double *apost_sup);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PR_H */

@@ -1,0 +1,215 @@
+"""Python API over the C ABI (include/pr.h): handles + torch-tensor marshalling.
+
+Tensors are CUDA fp64 tensors in the operator's layout:
+  1D: a batch of B vectors is a (n, ld) row-major tensor, vector c = column c;
+  2D: a batch of B vectors is a (B, ld) tensor (ld >= (n+1)^2), vector c =
+      row c, each a padded (n+1) x (n+1) grid with a zero ghost row/col 0.
+No arithmetic of the method runs here; see include/pr.h for the semantics.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from ._lib import PR_ADJOINT, PR_AFFINE, PR_LINEAR, check  # noqa: F401
+
+
+def _stream(stream=None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    assert t.is_cuda and t.dtype == torch.float64, "expected a CUDA float64 tensor"
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _hptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def _ld(t, dim: int) -> int:
+    """Leading dimension of a 1D (n, ld) or 2D (B, ld) batch tensor."""
+    assert t.dim() == 2 and t.stride(1) == 1, "batch tensors must be 2D with unit inner stride"
+    return int(t.stride(0))
+
+
+class Operator:
+    def __init__(self, handle: ctypes.c_void_p):
+        self._h = handle
+        rows = ctypes.c_long()
+        dim = ctypes.c_int()
+        n = ctypes.c_int()
+        check(L.lib().pr_op_info(self._h, ctypes.byref(rows), ctypes.byref(dim), ctypes.byref(n)),
+              "pr_op_info")
+        self.rows, self.dim, self.n = rows.value, dim.value, n.value
+
+    @classmethod
+    def tridiag(cls, sub, diag, sup, dt: float, rowsum=None, colsum=None) -> "Operator":
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (sub, diag, sup)]
+        rs = None if rowsum is None else np.ascontiguousarray(rowsum, dtype=np.float64)
+        cs = None if colsum is None else np.ascontiguousarray(colsum, dtype=np.float64)
+        h = ctypes.c_void_p()
+        check(L.lib().pr_op_create_tridiag(len(arrs[1]), *[_hptr(a) for a in arrs],
+                                           _hptr(rs) if rs is not None else None,
+                                           _hptr(cs) if cs is not None else None,
+                                           float(dt), ctypes.byref(h)), "pr_op_create_tridiag")
+        return cls(h)
+
+    @classmethod
+    def sep2d(cls, n: int, dt: float) -> "Operator":
+        h = ctypes.c_void_p()
+        check(L.lib().pr_op_create_sep2d(int(n), float(dt), ctypes.byref(h)), "pr_op_create_sep2d")
+        return cls(h)
+
+    def close(self):
+        if self._h:
+            L.lib().pr_op_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def fine_propagate(self, mode: int, first_interval: int, m: int, U_in, U_out,
+                       vecs_per_interval: int = 1, source: "SourceTerm" = None, offset=None,
+                       B: int = None, stream=None):
+        if B is None:
+            B = U_out.shape[1] if self.dim == 1 else U_out.shape[0]
+        src = ctypes.byref(source.struct) if source is not None else None
+        check(L.lib().pr_fine_propagate(
+            self._h, int(mode), int(first_interval), int(m), int(B), int(vecs_per_interval), src,
+            _ptr(U_in), _ld(U_in, self.dim) if U_in is not None else 0,
+            _ptr(U_out), _ld(U_out, self.dim),
+            _ptr(offset), _ld(offset, self.dim) if offset is not None else 0,
+            _stream(stream)), "pr_fine_propagate")
+        return U_out
+
+    def gaussian_sketch(self, first_interval: int, n_intervals: int, l: int, seed: int, out,
+                        stream=None):
+        check(L.lib().pr_gaussian_sketch(self._h, int(first_interval), int(n_intervals), int(l),
+                                         ctypes.c_uint64(int(seed)), _ptr(out), _ld(out, self.dim),
+                                         _stream(stream)), "pr_gaussian_sketch")
+        return out
+
+
+class SourceTerm:
+    """Keeps the device tensors alive alongside the pr_source struct."""
+
+    def __init__(self, kind, nterms, nsrc, nsteps, tensors: dict):
+        self.tensors = tensors
+        st = L.Source()
+        st.kind, st.nterms, st.nsrc, st.nsteps = kind, nterms, nsrc, nsteps
+        for key in ("space", "time", "amp", "gx", "gy"):
+            t = tensors.get(key)
+            setattr(st, key, t.data_ptr() if t is not None else None)
+        self.struct = st
+
+    @classmethod
+    def sep1d(cls, space, time, amp, device="cuda") -> "SourceTerm":
+        t = {k: torch.as_tensor(np.ascontiguousarray(v), dtype=torch.float64, device=device)
+             for k, v in (("space", space), ("time", time), ("amp", amp))}
+        R, nsteps = t["time"].shape
+        return cls(L.PR_SRC_SEP1D, R, t["amp"].shape[0], nsteps, t)
+
+    @classmethod
+    def bump2d(cls, gx_padded, gy_padded, device="cuda") -> "SourceTerm":
+        t = {k: torch.as_tensor(np.ascontiguousarray(v), dtype=torch.float64, device=device)
+             for k, v in (("gx", gx_padded), ("gy", gy_padded))}
+        nb, nsteps, _ = t["gx"].shape
+        return cls(L.PR_SRC_BUMP2D, nb, 1, nsteps, t)
+
+    @classmethod
+    def none(cls) -> "SourceTerm":
+        return cls(L.PR_SRC_NONE, 0, 1, 0, {})
+
+
+class Coarse:
+    """Spectral coarse solvers G_q' = U_q Sigma_q V_q^T of the owned intervals."""
+
+    def __init__(self, handle):
+        self._h = handle
+
+    @classmethod
+    def build(cls, op: Operator, N_total: int, m: int, k: int, p: int, seed: int,
+              first_interval: int = 0, n_local: int = None, stream=None) -> "Coarse":
+        if n_local is None:
+            n_local = N_total - first_interval
+        h = ctypes.c_void_p()
+        check(L.lib().pr_build_coarse(op._h, int(N_total), int(first_interval), int(n_local),
+                                      int(m), int(k), int(p), ctypes.c_uint64(int(seed)),
+                                      _stream(stream), ctypes.byref(h)), "pr_build_coarse")
+        return cls(h)
+
+    def info(self, raise_on_error: bool = True) -> dict:
+        k, l, nl, first, m = (ctypes.c_int() for _ in range(5))
+        delta, eps = ctypes.c_double(), ctypes.c_double()
+        st0 = L.lib().pr_coarse_info(self._h, ctypes.byref(k), ctypes.byref(l), ctypes.byref(nl),
+                                     ctypes.byref(first), ctypes.byref(m), None, None, None, None)
+        if st0 in (L.PR_EINVAL, L.PR_ECUDA):
+            check(st0, "pr_coarse_info")
+        sig = np.zeros(nl.value * l.value)
+        passes = (ctypes.c_int * 2)()
+        st = L.lib().pr_coarse_info(self._h, None, None, None, None, None, ctypes.byref(delta),
+                                    ctypes.byref(eps), _hptr(sig), passes)
+        if raise_on_error and st not in (L.PR_OK, L.PR_EUNAVAIL):
+            check(st, "pr_coarse_info")
+        return dict(k=k.value, l=l.value, n_local=nl.value, first_interval=first.value, m=m.value,
+                    delta=delta.value, eps=eps.value, sigma=sig.reshape(nl.value, l.value),
+                    qr_passes=(passes[0], passes[1]), status=st)
+
+    def apply(self, q_local: int, X, Y, dim: int, stream=None):
+        nvec = X.shape[1] if dim == 1 else X.shape[0]
+        check(L.lib().pr_coarse_apply(self._h, int(q_local), int(nvec), _ptr(X), _ld(X, dim),
+                                      _ptr(Y), _ld(Y, dim), _stream(stream)), "pr_coarse_apply")
+        return Y
+
+    def close(self):
+        if self._h:
+            L.lib().pr_coarse_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def parareal(G: Coarse, op: Operator, u0, source: SourceTerm, K: int, U_out, nsrc: int = 1,
+             hist=None, stream=None):
+    """Returns (upd[K, N+1, nsrc], bnorm[N+1, nsrc]) host arrays; U_out holds u^K."""
+    nvec = (U_out.shape[1] if op.dim == 1 else U_out.shape[0])
+    Np1 = nvec // nsrc
+    upd = np.zeros((max(K, 0), Np1, nsrc))
+    bn = np.zeros((Np1, nsrc))
+    hs = int(hist.stride(0)) if hist is not None else 0
+    check(L.lib().pr_parareal(G._h, op._h, int(nsrc), _ptr(u0), _ld(u0, op.dim),
+                              ctypes.byref(source.struct), int(K), _ptr(U_out), _ld(U_out, op.dim),
+                              _hptr(upd) if K > 0 else None, _hptr(bn),
+                              _ptr(hist) if hist is not None else None, hs, _stream(stream)),
+          "pr_parareal")
+    return upd, bn
+
+
+def bounds(delta: float, eps: float, bnorm: np.ndarray, upd: np.ndarray):
+    """bnorm: (N+1,), upd: (K, N+1) -> dict of a priori / a posteriori bounds."""
+    bnorm = np.ascontiguousarray(bnorm, dtype=np.float64)
+    upd = np.ascontiguousarray(upd, dtype=np.float64)
+    N = bnorm.shape[0] - 1
+    K = upd.shape[0]
+    apri = np.zeros((K + 1, N + 1))
+    apost = np.zeros((max(K, 1), N + 1))
+    sup = np.zeros(max(K, 1))
+    check(L.lib().pr_bounds(float(delta), float(eps), N, K, _hptr(bnorm),
+                            _hptr(upd) if K > 0 else None, _hptr(apri),
+                            _hptr(apost) if K > 0 else None, _hptr(sup) if K > 0 else None),
+          "pr_bounds")
+    return dict(apriori=apri, apost=apost[:K], apost_sup=sup[:K])

@@ -1,0 +1,697 @@
+// k_linalg.cu -- dense kernels of the randomized SVD and of the Parareal
+// correction (CUDA path; no oracle code).
+//
+//   K4 xty / reduce_parts : tall-skinny X^T Y per interval, split over row
+//                           chunks, fixed-order reduction (deterministic)
+//   K5 chol / trsm        : iterated shifted CholeskyQR (rSVD steps 2 and 4,
+//                           P:269-275; reading Z7)
+//   K6 jacobi             : one-sided Jacobi SVD of M = R_Z^T, one CTA per
+//                           interval (step 5)
+//   K7 lift               : U = W Psi_k, V = V Phi_k (steps 5-6)
+//   K8/K9 sweep, expand   : reduced Parareal correction (eq. def_Parareal,
+//                           P:144-151) and update norms
+#include <float.h>
+
+#include "pr_internal.cuh"
+
+namespace pr {
+
+// ------------------------------------------------------------------ X^T Y
+constexpr int XT_THREADS = 256;
+constexpr int XT_TR = 32;       // rows per smem tile
+
+int xty_chunks(long rows, int nbatch)
+{
+    // enough CTAs to fill the machine twice, at least 64 rows per chunk
+    long want = (2L * num_sms() + nbatch - 1) / nbatch;
+    long maxc = (rows + 63) / 64;
+    long c = want < maxc ? want : maxc;
+    if (c < 1) c = 1;
+    if (c > 256) c = 256;
+    return (int)c;
+}
+
+template <int BPT>
+__global__ void __launch_bounds__(XT_THREADS) k_xty(XtY p)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int b = blockIdx.y, t = blockIdx.x;
+    if (p.skip && p.skip[b] == 2) return;
+    const int A4 = (p.a + 3) & ~3, C4 = (p.c + 3) & ~3;
+    double *Xs = sm;                     // [XT_TR][A4]
+    double *Ys = sm + XT_TR * A4;        // [XT_TR][C4]
+    const bool same = (p.X == p.Y) && (p.xbs == p.ybs) && (p.xrs == p.yrs) && (p.xcs == p.ycs) &&
+                      (p.a == p.c);
+    if (same) Ys = Xs;
+    const int nbi = A4 / 4, nbj = C4 / 4;
+    const int nblk = nbi * nbj;
+    double acc[BPT][16];
+#pragma unroll
+    for (int q = 0; q < BPT; ++q)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) acc[q][e] = 0.0;
+
+    const long r0 = (long)t * p.chunk_rows;
+    long r1 = r0 + p.chunk_rows;
+    if (r1 > p.rows) r1 = p.rows;
+    const double *Xb = p.X + (long)b * p.xbs;
+    const double *Yb = p.Y + (long)b * p.ybs;
+
+    for (long rt = r0; rt < r1; rt += XT_TR) {
+        __syncthreads();
+        // cooperative coalesced tile loads (zero-filled beyond rows / columns)
+        auto load = [&](const double *Bp, long rs, long cs, int ncol, int C, double *dst) {
+            const int tot = XT_TR * C;
+            for (int idx = threadIdx.x; idx < tot; idx += XT_THREADS) {
+                int r, j;
+                if (cs == 1) { r = idx / C; j = idx % C; }
+                else { j = idx / XT_TR; r = idx % XT_TR; }
+                long row = rt + r;
+                double v = 0.0;
+                if (row < r1 && j < ncol) v = Bp[row * rs + (long)j * cs];
+                dst[r * C + j] = v;
+            }
+        };
+        load(Xb, p.xrs, p.xcs, p.a, A4, Xs);
+        if (!same) load(Yb, p.yrs, p.ycs, p.c, C4, Ys);
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < BPT; ++q) {
+            int blk = threadIdx.x + q * XT_THREADS;
+            if (blk < nblk) {
+                int bi = blk / nbj, bj = blk % nbj;
+#pragma unroll 4
+                for (int r = 0; r < XT_TR; ++r) {
+                    const double2 *xp = reinterpret_cast<const double2 *>(Xs + r * A4 + 4 * bi);
+                    const double2 *yp = reinterpret_cast<const double2 *>(Ys + r * C4 + 4 * bj);
+                    double2 x01 = xp[0], x23 = xp[1], y01 = yp[0], y23 = yp[1];
+                    double x[4] = {x01.x, x01.y, x23.x, x23.y};
+                    double y[4] = {y01.x, y01.y, y23.x, y23.y};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int v = 0; v < 4; ++v) acc[q][u * 4 + v] = fma(x[u], y[v], acc[q][u * 4 + v]);
+                }
+            }
+        }
+    }
+    double *out = p.part + ((long)b * p.nchunk + t) * p.a * p.c;
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        int blk = threadIdx.x + q * XT_THREADS;
+        if (blk < nblk) {
+            int bi = blk / nbj, bj = blk % nbj;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    int i = 4 * bi + u, j = 4 * bj + v;
+                    if (i < p.a && j < p.c) out[(long)i * p.c + j] = acc[q][u * 4 + v];
+                }
+        }
+    }
+}
+
+cudaError_t launch_xty(const XtY &p, cudaStream_t s)
+{
+    const int A4 = (p.a + 3) & ~3, C4 = (p.c + 3) & ~3;
+    const int nblk = (A4 / 4) * (C4 / 4);
+    const int bpt = (nblk + XT_THREADS - 1) / XT_THREADS;
+    size_t smem = (size_t)XT_TR * (A4 + C4) * sizeof(double);
+    dim3 grid(p.nchunk, p.nbatch);
+    cudaError_t e;
+#define XT_LAUNCH(K)                                                                        \
+    e = cudaFuncSetAttribute(k_xty<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                         \
+    k_xty<K><<<grid, XT_THREADS, smem, s>>>(p);
+    if (bpt <= 1) { XT_LAUNCH(1) }
+    else if (bpt <= 2) { XT_LAUNCH(2) }
+    else if (bpt <= 4) { XT_LAUNCH(4) }
+    else return cudaErrorInvalidValue;
+#undef XT_LAUNCH
+    return cudaGetLastError();
+}
+
+__global__ void k_reduce_parts(const double *part, int nbatch, int nchunk, int a, int c,
+                               const double *rowscale, long rsbs, double *out)
+{
+    long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    long per = (long)a * c;
+    if (idx >= per * nbatch) return;
+    int b = (int)(idx / per);
+    long e = idx % per;
+    int i = (int)(e / c);
+    const double *pp = part + (long)b * nchunk * per + e;
+    double sum = 0.0;
+    for (int t = 0; t < nchunk; ++t) sum += pp[(long)t * per];
+    if (rowscale) sum *= rowscale[(long)b * rsbs + i];
+    out[idx] = sum;
+}
+
+cudaError_t launch_reduce_parts(const double *part, int nbatch, int nchunk, int a, int c,
+                                const double *rowscale, long rowscale_bs, double *out,
+                                cudaStream_t s)
+{
+    long tot = (long)a * c * nbatch;
+    if (tot == 0) return cudaSuccess;
+    k_reduce_parts<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(part, nbatch, nchunk, a, c,
+                                                                 rowscale, rowscale_bs, out);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- CholeskyQR control
+// One CTA per interval.  Shifted CholeskyQR (Fukaya et al. 2020):
+//   G = Q^T Q, s = 11 (rows*l + l(l+1)) u ||G||_F, R^T R = G + s I, Q <- Q R^{-1};
+// repeated while ||G - I||_F >= 1/2, then two unshifted passes (CholeskyQR2).
+constexpr int CH_THREADS = 256;
+
+__global__ void __launch_bounds__(CH_THREADS) k_chol(CholArgs a)
+{
+    extern __shared__ __align__(16) double G[];   // l x l
+    __shared__ double red[CH_THREADS];
+    __shared__ int sflag;
+    const int b = blockIdx.x;
+    const int l = a.l;
+    const int st = a.state[b];
+    if (st == 2) {
+        if (threadIdx.x == 0) a.act[b] = 0;
+        return;
+    }
+    const long per = (long)l * l;
+    auto load_G = [&]() {
+        for (int e = threadIdx.x; e < l * l; e += CH_THREADS) {
+            const double *pp = a.part + (long)b * a.nchunk * per + e;
+            double s = 0.0;
+            for (int t = 0; t < a.nchunk; ++t) s += pp[(long)t * per];
+            G[e] = s;
+        }
+        __syncthreads();
+    };
+    load_G();
+    // ||G||_F and ||G - I||_F (fixed-order tree reduction)
+    double f1 = 0.0, f2 = 0.0;
+    for (int e = threadIdx.x; e < l * l; e += CH_THREADS) {
+        double g = G[e];
+        f1 += g * g;
+        double d = g - ((e / l == e % l) ? 1.0 : 0.0);
+        f2 += d * d;
+    }
+    red[threadIdx.x] = f1;
+    __syncthreads();
+    for (int w = CH_THREADS / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    const double normG = sqrt(red[0]);
+    __syncthreads();
+    red[threadIdx.x] = f2;
+    __syncthreads();
+    for (int w = CH_THREADS / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    const double offI = sqrt(red[0]);
+    __syncthreads();
+
+    const bool plain = (st == 1) || (offI < 0.5);
+    double shift = plain ? 0.0
+                         : 11.0 * ((double)a.nrows * l + (double)l * (l + 1)) * DBL_EPSILON * 0.5 *
+                               normG;
+    if (!(normG > 0.0)) shift = 1.0;   // zero block: any SPD shift; Q stays zero
+    int attempt = 0;
+    for (;;) {
+        if (shift > 0.0) {
+            for (int i = threadIdx.x; i < l; i += CH_THREADS) G[i * l + i] += shift;
+        }
+        if (threadIdx.x == 0) sflag = 0;
+        __syncthreads();
+        // right-looking Cholesky on the upper triangle: G = R^T R
+        for (int j = 0; j < l; ++j) {
+            if (threadIdx.x == 0) {
+                double d = G[j * l + j];
+                if (!(d > 0.0) || !isfinite(d)) { sflag = 1; d = 1.0; }
+                G[j * l + j] = sqrt(d);
+            }
+            __syncthreads();
+            const double piv = G[j * l + j];
+            for (int k = j + 1 + threadIdx.x; k < l; k += CH_THREADS) G[j * l + k] /= piv;
+            __syncthreads();
+            const int rem = l - j - 1;
+            for (int e = threadIdx.x; e < rem * rem; e += CH_THREADS) {
+                int i = j + 1 + e / rem, k = j + 1 + e % rem;
+                if (k >= i) G[i * l + k] -= G[j * l + i] * G[j * l + k];
+            }
+            __syncthreads();
+        }
+        if (!sflag) break;
+        // breakdown: reload and retry with a larger shift
+        __syncthreads();
+        if (++attempt > 30) {
+            if (threadIdx.x == 0) atomicExch(a.fail, 1);
+            break;
+        }
+        load_G();
+        shift = (shift > 0.0 ? shift * 100.0 : DBL_EPSILON * (normG > 0 ? normG : 1.0));
+    }
+    // write R (upper, zero below)
+    double *Rb = a.R + (long)b * per;
+    for (int e = threadIdx.x; e < l * l; e += CH_THREADS) {
+        int i = e / l, k = e % l;
+        Rb[e] = (k >= i) ? G[e] : 0.0;
+    }
+    // Rtot <- R * Rtot  (row i of the product needs rows >= i of the old Rtot)
+    if (a.Rtot) {
+        double *Tb = a.Rtot + (long)b * per;
+        __syncthreads();
+        for (int i = 0; i < l; ++i) {
+            double v[1];
+            for (int k = threadIdx.x; k < l; k += CH_THREADS) {
+                double s = 0.0;
+                for (int j = i; j < l; ++j) s += G[i * l + j] * Tb[(long)j * l + k];
+                v[0] = s;
+                // all reads of row i of Tb for this column happen above before the write
+                __syncwarp();
+                Tb[(long)i * l + k] = v[0];
+            }
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) {
+        int ns = plain ? (st == 1 ? 2 : 1) : 0;
+        a.state[b] = ns;
+        a.act[b] = 1;
+        if (ns != 2) atomicAdd(a.active, 1);
+    }
+}
+
+cudaError_t launch_chol(const CholArgs &a, cudaStream_t s)
+{
+    size_t smem = (size_t)a.l * a.l * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_chol<<<a.nbatch, CH_THREADS, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+// Q <- Q R^{-1} row by row (forward substitution q R = y), one thread per row.
+constexpr int TS_ROWS = 64;
+
+__global__ void __launch_bounds__(TS_ROWS) k_trsm(double *Q, long bs, long rs, long cs, long rows,
+                                                  int l, const double *R, const int *act)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int b = blockIdx.y;
+    if (!act[b]) return;
+    double *Rs = sm;                    // l x l
+    double *Ys = sm + l * l;            // TS_ROWS x (l+1)
+    const int ld = l + 1;
+    const double *Rb = R + (long)b * l * l;
+    for (int e = threadIdx.x; e < l * l; e += TS_ROWS) Rs[e] = Rb[e];
+    const long r0 = (long)blockIdx.x * TS_ROWS;
+    double *Qb = Q + (long)b * bs;
+    for (int e = threadIdx.x; e < TS_ROWS * l; e += TS_ROWS) {
+        int r, j;
+        if (cs == 1) { r = e / l; j = e % l; } else { j = e / TS_ROWS; r = e % TS_ROWS; }
+        long row = r0 + r;
+        Ys[r * ld + j] = (row < rows) ? Qb[row * rs + (long)j * cs] : 0.0;
+    }
+    __syncthreads();
+    double *y = Ys + threadIdx.x * ld;
+    for (int j = 0; j < l; ++j) {
+        double t = y[j];
+        for (int i = 0; i < j; ++i) t = fma(-y[i], Rs[i * l + j], t);
+        y[j] = t / Rs[j * l + j];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < TS_ROWS * l; e += TS_ROWS) {
+        int r, j;
+        if (cs == 1) { r = e / l; j = e % l; } else { j = e / TS_ROWS; r = e % TS_ROWS; }
+        long row = r0 + r;
+        if (row < rows) Qb[row * rs + (long)j * cs] = Ys[r * ld + j];
+    }
+}
+
+cudaError_t launch_trsm(double *Q, long bs, long rs, long cs, long rows, int l, int nbatch,
+                        const double *R, const int *act, cudaStream_t s)
+{
+    size_t smem = ((size_t)l * l + (size_t)TS_ROWS * (l + 1)) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)((rows + TS_ROWS - 1) / TS_ROWS), nbatch);
+    k_trsm<<<grid, TS_ROWS, smem, s>>>(Q, bs, rs, cs, rows, l, R, act);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ Jacobi SVD
+// One-sided (Hestenes) Jacobi on the columns of A = M = R_Z^T, parallel
+// round-robin ordering (circle method), one warp per column pair.
+constexpr int JW = 8;   // warps per CTA
+
+__global__ void __launch_bounds__(32 * JW) k_jacobi(const double *Rtot, int l, double *Psi,
+                                                     double *sigma, double *Phi, int *fail)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int b = blockIdx.x;
+    const int L = (l + 1) & ~1;             // even number of columns (zero pad)
+    double *A = sm;                          // column-major: A[col*l + row]
+    double *V = sm + (size_t)L * l;          // column-major: V[col*L + row]
+    double *sig = V + (size_t)L * L;         // L
+    __shared__ int rotated;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double *Tb = Rtot + (long)b * l * l;
+    // A[:, j] = M[:, j] = R_Z[j, :]^T
+    for (int e = threadIdx.x; e < L * l; e += 32 * JW) {
+        int j = e / l, i = e % l;
+        A[e] = (j < l) ? Tb[(long)j * l + i] : 0.0;
+    }
+    for (int e = threadIdx.x; e < L * L; e += 32 * JW) V[e] = ((e / L) == (e % L)) ? 1.0 : 0.0;
+    __syncthreads();
+    const double tol = (double)l * DBL_EPSILON;
+    int sweep = 0;
+    for (; sweep < 60; ++sweep) {
+        if (threadIdx.x == 0) rotated = 0;
+        __syncthreads();
+        for (int rnd = 0; rnd < L - 1; ++rnd) {
+            for (int k = warp; k < L / 2; k += JW) {
+                int p, q;
+                if (k == 0) { p = rnd; q = L - 1; }
+                else { p = (rnd + k) % (L - 1); q = (rnd - k + (L - 1)) % (L - 1); }
+                if (p > q) { int t = p; p = q; q = t; }
+                double *ap = A + (size_t)p * l, *aq = A + (size_t)q * l;
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int i = lane; i < l; i += 32) {
+                    double x = ap[i], y = aq[i];
+                    al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    al += __shfl_xor_sync(0xffffffffu, al, o);
+                    be += __shfl_xor_sync(0xffffffffu, be, o);
+                    ga += __shfl_xor_sync(0xffffffffu, ga, o);
+                }
+                if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+                    double zeta = (be - al) / (2.0 * ga);
+                    double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                    double c = 1.0 / sqrt(1.0 + t * t);
+                    double s = c * t;
+                    for (int i = lane; i < l; i += 32) {
+                        double x = ap[i], y = aq[i];
+                        ap[i] = c * x - s * y;
+                        aq[i] = s * x + c * y;
+                    }
+                    double *vp = V + (size_t)p * L, *vq = V + (size_t)q * L;
+                    for (int i = lane; i < L; i += 32) {
+                        double x = vp[i], y = vq[i];
+                        vp[i] = c * x - s * y;
+                        vq[i] = s * x + c * y;
+                    }
+                    if (lane == 0) rotated = 1;
+                }
+            }
+            __syncthreads();
+        }
+        if (!rotated) break;
+        __syncthreads();
+    }
+    if (sweep >= 60 && threadIdx.x == 0) atomicExch(fail, 1);
+    // singular values = column norms
+    for (int j = warp; j < L; j += JW) {
+        double s = 0.0;
+        for (int i = lane; i < l; i += 32) s = fma(A[(size_t)j * l + i], A[(size_t)j * l + i], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) sig[j] = sqrt(s);
+    }
+    __syncthreads();
+    // sort descending (rank by counting; ties by index), sign convention, write
+    for (int j = warp; j < l; j += JW) {
+        double sj = sig[j];
+        int rank = 0;
+        for (int t = 0; t < L; ++t) {
+            double st = sig[t];
+            if (st > sj || (st == sj && t < j)) ++rank;
+        }
+        // largest-|.| entry of the right vector positive (reading Z10)
+        const double *vj = V + (size_t)j * L;
+        double best = -1.0, sgnv = 1.0;
+        int bi = 0;
+        for (int i = 0; i < l; ++i) {
+            double av = fabs(vj[i]);
+            if (av > best) { best = av; bi = i; }
+        }
+        sgnv = (vj[bi] < 0.0) ? -1.0 : 1.0;
+        (void)bi;
+        double inv = (sj > 0.0) ? 1.0 / sj : 0.0;
+        for (int i = lane; i < l; i += 32) {
+            Psi[((long)b * l + i) * l + rank] = sgnv * A[(size_t)j * l + i] * inv;
+            Phi[((long)b * l + i) * l + rank] = sgnv * vj[i];
+        }
+        if (lane == 0) sigma[(long)b * l + rank] = sj;
+    }
+}
+
+cudaError_t launch_jacobi(const double *Rtot, int nbatch, int l, double *Psi, double *sigma,
+                          double *Phi, int *fail, cudaStream_t s)
+{
+    int L = (l + 1) & ~1;
+    size_t smem = ((size_t)L * l + (size_t)L * L + L) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_jacobi<<<nbatch, 32 * JW, smem, s>>>(Rtot, l, Psi, sigma, Phi, fail);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ lift
+constexpr int LF_ROWS = 32;
+constexpr int LF_THREADS = 256;
+
+__global__ void __launch_bounds__(LF_THREADS) k_lift(const double *X, long xbs, long xrs, long xcs,
+                                                     long rows, int l, const double *Cm, int ldc,
+                                                     int k, double *out)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int b = blockIdx.y;
+    double *Cs = sm;                 // l x k
+    double *Xs = sm + l * k;         // LF_ROWS x (l+1)
+    const int ld = l + 1;
+    const double *Cb = Cm + (long)b * l * ldc;
+    for (int e = threadIdx.x; e < l * k; e += LF_THREADS) Cs[e] = Cb[(long)(e / k) * ldc + e % k];
+    const long r0 = (long)blockIdx.x * LF_ROWS;
+    const double *Xb = X + (long)b * xbs;
+    for (int e = threadIdx.x; e < LF_ROWS * l; e += LF_THREADS) {
+        int r, j;
+        if (xcs == 1) { r = e / l; j = e % l; } else { j = e / LF_ROWS; r = e % LF_ROWS; }
+        long row = r0 + r;
+        Xs[r * ld + j] = (row < rows) ? Xb[row * xrs + (long)j * xcs] : 0.0;
+    }
+    __syncthreads();
+    double *ob = out + (long)b * rows * k;
+    for (int e = threadIdx.x; e < LF_ROWS * k; e += LF_THREADS) {
+        int r = e / k, c = e % k;
+        long row = r0 + r;
+        if (row >= rows) continue;
+        double s = 0.0;
+        for (int j = 0; j < l; ++j) s = fma(Xs[r * ld + j], Cs[j * k + c], s);
+        ob[row * k + c] = s;
+    }
+}
+
+cudaError_t launch_lift(const double *X, long xbs, long xrs, long xcs, long rows, int l,
+                        const double *Cm, int ldc, int k, int nbatch, double *out, cudaStream_t s)
+{
+    size_t smem = ((size_t)l * k + (size_t)LF_ROWS * (l + 1)) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(k_lift, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)((rows + LF_ROWS - 1) / LF_ROWS), nbatch);
+    k_lift<<<grid, LF_THREADS, smem, s>>>(X, xbs, xrs, xcs, rows, l, Cm, ldc, k, out);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------- sweep
+// e_j = C_j e_{j-1} + (q_j - p_j), e_{-1} = 0: the only sequential part of a
+// Parareal iteration, in k-dimensional reduced coordinates.
+constexpr int SW_THREADS = 1024;
+
+__global__ void __launch_bounds__(SW_THREADS) k_sweep(const double *C, const double *q,
+                                                      const double *p, int N, int k, int S,
+                                                      double *e)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int kS = k * S;
+    double *eo = sm;             // previous e (k x S)
+    double *en = sm + kS;        // new e
+    double *Cs = sm + 2 * kS;    // k x k
+    for (int i = threadIdx.x; i < kS; i += SW_THREADS) eo[i] = 0.0;
+    __syncthreads();
+    for (int j = 0; j < N; ++j) {
+        const double *Cj = C + (long)j * k * k;
+        for (int i = threadIdx.x; i < k * k; i += SW_THREADS) Cs[i] = (j > 0) ? Cj[i] : 0.0;
+        __syncthreads();
+        const double *qj = q + (long)j * kS;
+        const double *pj = p ? p + (long)j * kS : nullptr;
+        for (int o = threadIdx.x; o < kS; o += SW_THREADS) {
+            int r = o / S, s = o % S;
+            double acc = qj[o] - (pj ? pj[o] : 0.0);
+            for (int t = 0; t < k; ++t) acc = fma(Cs[r * k + t], eo[t * S + s], acc);
+            en[o] = acc;
+            e[(long)j * kS + o] = acc;
+        }
+        __syncthreads();
+        double *tmp = eo; eo = en; en = tmp;
+    }
+}
+
+cudaError_t launch_sweep(const double *C, const double *q, const double *p, int N, int k, int S,
+                         double *e, cudaStream_t s)
+{
+    size_t smem = ((size_t)2 * k * S + (size_t)k * k) * sizeof(double);
+    cudaError_t er = cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (er != cudaSuccess) return er;
+    k_sweep<<<1, SW_THREADS, smem, s>>>(C, q, p, N, k, S, e);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------- expand
+constexpr int EX_THREADS = 256;
+
+__global__ void __launch_bounds__(EX_THREADS) k_expand(Expand a)
+{
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double red[EX_THREADS];
+    const int b = blockIdx.y, t = blockIdx.x;
+    const int k = a.k, S = a.S;
+    double *es = sm;   // k x S
+    const double *eb = a.e + (long)b * k * S;
+    for (int i = threadIdx.x; i < k * S; i += EX_THREADS) es[i] = eb[i];
+    __syncthreads();
+    const int per = EX_THREADS / S;          // threads per source (S <= 256)
+    const int s = threadIdx.x % S;
+    const int ty = threadIdx.x / S;
+    const bool act = ty < per;
+    const long r0 = (long)t * a.chunk_rows;
+    long r1 = r0 + a.chunk_rows;
+    if (r1 > a.rows) r1 = a.rows;
+    const double *Ub = a.U + (long)b * a.Ubs;
+    const long v = (long)b * S + s;
+    double nrm = 0.0;
+    if (act) {
+        for (long row = r0 + ty; row < r1; row += per) {
+            const double *ur = Ub + row * k;
+            double acc = a.base ? a.base[row * a.brs + v * a.bvs] : 0.0;
+            for (int r = 0; r < k; ++r) acc = fma(ur[r], es[r * S + s], acc);
+            double *o = a.out + row * a.ors + v * a.ovs;
+            if (a.normpart) {
+                double d = acc - *o;
+                nrm = fma(d, d, nrm);
+            }
+            *o = acc;
+        }
+    }
+    if (a.normpart) {
+        red[threadIdx.x] = act ? nrm : 0.0;
+        __syncthreads();
+        if (threadIdx.x < S) {
+            double sum = 0.0;
+            for (int y = 0; y < per; ++y) sum += red[y * S + threadIdx.x];
+            a.normpart[((long)b * S + threadIdx.x) * a.nchunk + t] = sum;
+        }
+    }
+}
+
+cudaError_t launch_expand(const Expand &a, cudaStream_t s)
+{
+    if (a.S > EX_THREADS) return cudaErrorInvalidValue;
+    size_t smem = (size_t)a.k * a.S * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid(a.nchunk, a.nbatch);
+    k_expand<<<grid, EX_THREADS, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+__global__ void k_norm_finish(const double *part, int nvec, int nchunk, double *out)
+{
+    int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= nvec) return;
+    double s = 0.0;
+    for (int t = 0; t < nchunk; ++t) s += part[(long)v * nchunk + t];
+    out[v] = sqrt(s);
+}
+
+cudaError_t launch_norm_finish(const double *part, int nvec, int nchunk, double *out, cudaStream_t s)
+{
+    if (nvec == 0) return cudaSuccess;
+    k_norm_finish<<<(nvec + 127) / 128, 128, 0, s>>>(part, nvec, nchunk, out);
+    return cudaGetLastError();
+}
+
+__global__ void k_vecnorm_parts(const double *X, long rs, long vs, long rows, int nvec, int nchunk,
+                                long chunk_rows, double *part)
+{
+    __shared__ double red[256];
+    const int v = blockIdx.y, t = blockIdx.x;
+    const long r0 = (long)t * chunk_rows;
+    long r1 = r0 + chunk_rows;
+    if (r1 > rows) r1 = rows;
+    double s = 0.0;
+    for (long r = r0 + threadIdx.x; r < r1; r += 256) {
+        double x = X[r * rs + (long)v * vs];
+        s = fma(x, x, s);
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[(long)v * nchunk + t] = red[0];
+}
+
+cudaError_t launch_vecnorm_parts(const double *X, long rs, long vs, long rows, int nvec, int nchunk,
+                                 long chunk_rows, double *part, cudaStream_t s)
+{
+    if (nvec == 0) return cudaSuccess;
+    dim3 grid(nchunk, nvec);
+    k_vecnorm_parts<<<grid, 256, 0, s>>>(X, rs, vs, rows, nvec, nchunk, chunk_rows, part);
+    return cudaGetLastError();
+}
+
+__global__ void k_copy_vectors(const double *in, long irs, long ivs, double *out, long ors, long ovs,
+                               long rows, int nvec)
+{
+    long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    long tot = rows * nvec;
+    if (idx >= tot) return;
+    long r, v;
+    if (ivs == 1 || ovs == 1) { r = idx / nvec; v = idx % nvec; }   // vector index fastest
+    else { v = idx / rows; r = idx % rows; }
+    out[r * ors + v * ovs] = in[r * irs + v * ivs];
+}
+
+cudaError_t launch_copy_vectors(const double *in, long irs, long ivs, double *out, long ors, long ovs,
+                                long rows, int nvec, cudaStream_t s)
+{
+    long tot = rows * nvec;
+    if (tot == 0) return cudaSuccess;
+    k_copy_vectors<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(in, irs, ivs, out, ors, ovs, rows, nvec);
+    return cudaGetLastError();
+}
+
+__global__ void k_eye(double *R, int nbatch, int l)
+{
+    long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    long per = (long)l * l;
+    if (idx >= per * nbatch) return;
+    long e = idx % per;
+    R[idx] = (e / l == e % l) ? 1.0 : 0.0;
+}
+
+cudaError_t launch_eye(double *R, int nbatch, int l, cudaStream_t s)
+{
+    long tot = (long)l * l * nbatch;
+    if (tot == 0) return cudaSuccess;
+    k_eye<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(R, nbatch, l);
+    return cudaGetLastError();
+}
+
+}  // namespace pr

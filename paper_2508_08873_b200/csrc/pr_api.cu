@@ -1,0 +1,673 @@
+// pr_api.cu -- the C ABI of include/pr.h: validation, handles, workspace and
+// the host-side orchestration of the kernels (no numerical work on the host
+// except the O(N^2) scalar bound formulas of pr_bounds).
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <unordered_map>
+
+#include "pr_internal.cuh"
+
+namespace pr {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+pr_status cuda_fail(cudaError_t e, const char *where)
+{
+    char buf[512];
+    snprintf(buf, sizeof buf, "CUDA error %d (%s) at %s", (int)e, cudaGetErrorString(e), where);
+    g_err = buf;
+    if (e == cudaErrorMemoryAllocation) return PR_EOOM;
+    return PR_ECUDA;
+}
+
+// --------------------------------------------------------------- workspace
+static std::mutex g_ws_mu;
+static std::multimap<size_t, void *> g_ws_free;
+static std::unordered_map<void *, size_t> g_ws_size;
+
+void *ws_alloc(size_t bytes)
+{
+    if (bytes == 0) bytes = 256;
+    bytes = (bytes + 255) & ~(size_t)255;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto it = g_ws_free.lower_bound(bytes);
+    if (it != g_ws_free.end() && it->first <= 2 * bytes + (64 << 20)) {
+        void *p = it->second;
+        g_ws_free.erase(it);
+        return p;
+    }
+    void *p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        // release cached blocks and retry once
+        for (auto &kv : g_ws_free) {
+            cudaFree(kv.second);
+            g_ws_size.erase(kv.second);
+        }
+        g_ws_free.clear();
+        if (cudaMalloc(&p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+    }
+    g_ws_size[p] = bytes;
+    return p;
+}
+
+void ws_free(void *p)
+{
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto it = g_ws_size.find(p);
+    if (it == g_ws_size.end()) return;
+    g_ws_free.emplace(it->second, p);
+}
+
+int num_sms()
+{
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
+            sms = 148;
+    }
+    return sms;
+}
+
+// RAII set of workspace buffers, released in stream order at scope exit.
+struct Scratch {
+    std::vector<void *> bufs;
+    ~Scratch() { for (void *p : bufs) ws_free(p); }
+    template <class T>
+    T *get(size_t count)
+    {
+        void *p = ws_alloc(count * sizeof(T));
+        if (p) bufs.push_back(p);
+        return (T *)p;
+    }
+};
+
+#define PR_ALLOC(ptr, T, count, S)                                   \
+    do {                                                             \
+        ptr = (S).get<T>(count);                                     \
+        if (!ptr) { ::pr::set_error("out of device memory"); return PR_EOOM; } \
+    } while (0)
+
+// Strides of vector v / row i in the op layout with leading dimension ld.
+struct Lay {
+    long rs, vs;
+};
+static inline Lay lay(const Op &op, long ld) { return op.dim == 1 ? Lay{ld, 1} : Lay{1, ld}; }
+
+// -------------------------------------------------------------- QR driver
+// Iterated shifted CholeskyQR of nb blocks Q_b (rows x l), in place.
+static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double *Rtot, int *fail,
+                        int *passes_out, cudaStream_t s)
+{
+    Scratch S;
+    Lay L = lay(op, ld);
+    const long rows = op.rows;
+    const long xbs = (op.dim == 1) ? (long)l : (long)l * ld;
+    int nchunk = xty_chunks(rows, nb);
+    long chunk_rows = (rows + nchunk - 1) / nchunk;
+    double *part, *R;
+    int *state, *act, *active;
+    PR_ALLOC(part, double, (size_t)nb * nchunk * l * l, S);
+    PR_ALLOC(R, double, (size_t)nb * l * l, S);
+    PR_ALLOC(state, int, nb, S);
+    PR_ALLOC(act, int, nb, S);
+    PR_ALLOC(active, int, 1, S);
+    int *h_active = nullptr;
+    PR_CUDA(cudaMallocHost(&h_active, sizeof(int)));
+    struct HostFree { int *p; ~HostFree() { cudaFreeHost(p); } } hf{h_active};
+    PR_CUDA(cudaMemsetAsync(state, 0, nb * sizeof(int), s));
+    if (Rtot) PR_CUDA(launch_eye(Rtot, nb, l, s));
+    int pass = 0;
+    for (;;) {
+        ++pass;
+        XtY x{state, Q, xbs, L.rs, L.vs, l, Q, xbs, L.rs, L.vs, l, rows, nb, nchunk, chunk_rows, part};
+        PR_CUDA(launch_xty(x, s));
+        PR_CUDA(cudaMemsetAsync(active, 0, sizeof(int), s));
+        CholArgs c{part, nchunk, nb, l, rows, state, act, R, Rtot, active, fail};
+        PR_CUDA(launch_chol(c, s));
+        PR_CUDA(launch_trsm(Q, xbs, L.rs, L.vs, rows, l, nb, R, act, s));
+        PR_CUDA(cudaMemcpyAsync(h_active, active, sizeof(int), cudaMemcpyDeviceToHost, s));
+        PR_CUDA(cudaStreamSynchronize(s));
+        if (*h_active == 0) break;
+        if (pass >= 24) {
+            set_error("CholeskyQR did not converge in 24 passes");
+            if (passes_out) *passes_out = pass;
+            return PR_ENOCONV;
+        }
+    }
+    if (passes_out) *passes_out = pass;
+    return PR_OK;
+}
+
+// One fine-propagation launch (1D or 2D), shared by the ABI and the drivers.
+static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi,
+                           const pr_source *f, const double *in, long ld_in, double *out,
+                           long ld_out, const double *off, long ld_off, int sketch,
+                           unsigned long long seed, cudaStream_t s)
+{
+    if (B == 0) return PR_OK;
+    if (op.dim == 2) {
+        Sep2dArgs a{&op, mode, q0, m, B, vpi, f, in, ld_in, out, ld_out, off, ld_off};
+        if (sketch) {
+            PR_CUDA(cudaMemset2DAsync(out, ld_out * sizeof(double), 0, op.rows * sizeof(double), B, s));
+            PR_CUDA(launch_sketch(2, op.n, op.rows, q0, B / vpi, vpi, seed, out, 1, ld_out, s));
+            a.in = out;
+            a.ld_in = ld_out;
+        }
+        return run_sep2d(a, s);
+    }
+    Scratch S;
+    StepArgs a{};
+    a.n = op.n;
+    a.B = B;
+    a.m = m;
+    a.DN = (mode == PR_ADJOINT) ? op.dn_tr : op.dn_fw;
+    a.UP = (mode == PR_ADJOINT) ? op.up_tr : op.up_fw;
+    a.in = in; a.ld_in = ld_in;
+    a.out = out; a.ld_out = ld_out;
+    a.off = off; a.ld_off = ld_off;
+    a.sketch = sketch;
+    a.seed = seed;
+    a.q0 = q0;
+    a.vpi = vpi;
+    a.R = 0;
+    a.dt = op.dt;
+    if (mode == PR_AFFINE && f && f->kind == PR_SRC_SEP1D && f->nterms > 0) {
+        double *spT;
+        PR_ALLOC(spT, double, (size_t)op.n * f->nterms, S);
+        PR_CUDA(launch_transpose(f->space, f->nterms, op.n, spT, s));
+        a.R = f->nterms;
+        a.spaceT = spT;
+        a.time = f->time;
+        a.amp = f->amp;
+        a.nsteps = f->nsteps;
+        a.nsrc = f->nsrc;
+    }
+    PR_CUDA(launch_stepper_1d(a, s));
+    return PR_OK;
+}
+
+}  // namespace pr
+
+using namespace pr;
+
+// =================================================================== ABI
+extern "C" {
+
+const char *pr_last_error(void) { return g_err.c_str(); }
+int pr_version(void) { return 1; }
+
+pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, const double *sup,
+                               const double *rowsum, const double *colsum, double dt, pr_op *out)
+{
+    PR_REQUIRE(out, PR_EINVAL, "out is NULL");
+    PR_REQUIRE(n >= 2 && sub && diag && sup, PR_EINVAL, "n < 2 or NULL operator arrays");
+    PR_REQUIRE(dt > 0.0 && isfinite(dt), PR_EINVAL, "dt must be positive");
+    PR_REQUIRE((rowsum == nullptr) == (colsum == nullptr), PR_EINVAL,
+               "give both rowsum and colsum or neither");
+    *out = nullptr;
+    pr_op h = new pr_op_s();
+    Op &op = h->op;
+    op.dim = 1;
+    op.n = n;
+    op.rows = n;
+    op.dt = dt;
+    double *d_in = nullptr;
+    int *d_bad = nullptr;
+    const size_t nb = (size_t)n * sizeof(double);
+    auto fail = [&](pr_status st) {
+        cudaFree(d_in);
+        cudaFree(d_bad);
+        cudaFree(op.dn_fw); cudaFree(op.up_fw); cudaFree(op.dn_tr); cudaFree(op.up_tr);
+        delete h;
+        return st;
+    };
+    cudaError_t e = cudaMalloc(&d_in, 5 * nb);
+    if (e == cudaSuccess) e = cudaMalloc(&d_bad, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&op.dn_fw, n * sizeof(Coef));
+    if (e == cudaSuccess) e = cudaMalloc(&op.up_fw, n * sizeof(Coef));
+    if (e == cudaSuccess) e = cudaMalloc(&op.dn_tr, n * sizeof(Coef));
+    if (e == cudaSuccess) e = cudaMalloc(&op.up_tr, n * sizeof(Coef));
+    if (e != cudaSuccess) return fail(cuda_fail(e, "pr_op_create_tridiag alloc"));
+    double *dsub = d_in, *ddiag = d_in + n, *dsup = d_in + 2 * n, *drs = d_in + 3 * n, *dcs = d_in + 4 * n;
+    e = cudaMemcpy(dsub, sub, nb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(ddiag, diag, nb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dsup, sup, nb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && rowsum) e = cudaMemcpy(drs, rowsum, nb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && colsum) e = cudaMemcpy(dcs, colsum, nb, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(d_bad, 0, sizeof(int));
+    if (e == cudaSuccess)
+        e = launch_factor_1d(n, dsub, dsup, rowsum ? drs : nullptr, ddiag, dt, 0, op.dn_fw, op.up_fw, d_bad, 0);
+    if (e == cudaSuccess)
+        e = launch_factor_1d(n, dsub, dsup, colsum ? dcs : nullptr, ddiag, dt, 1, op.dn_tr, op.up_tr, d_bad, 0);
+    int bad = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "pr_op_create_tridiag factor"));
+    if (bad) {
+        set_error("non-positive or non-finite pivot in the factorisation of I + dt A");
+        return fail(PR_ESINGULAR);
+    }
+    cudaFree(d_in);
+    cudaFree(d_bad);
+    *out = h;
+    return PR_OK;
+}
+
+pr_status pr_op_destroy(pr_op h)
+{
+    if (!h) return PR_OK;
+    Op &op = h->op;
+    cudaFree(op.dn_fw); cudaFree(op.up_fw); cudaFree(op.dn_tr); cudaFree(op.up_tr);
+    cudaFree(op.S); cudaFree(op.lam);
+    delete h;
+    return PR_OK;
+}
+
+pr_status pr_op_info(pr_op h, long *rows, int *dim, int *n)
+{
+    PR_REQUIRE(h, PR_EINVAL, "op is NULL");
+    if (rows) *rows = h->op.rows;
+    if (dim) *dim = h->op.dim;
+    if (n) *n = h->op.n;
+    return PR_OK;
+}
+
+static pr_status check_source(const Op &op, const pr_source *f, int q0, int m, int nint)
+{
+    PR_REQUIRE(f, PR_EINVAL, "PR_AFFINE needs a source (kind PR_SRC_NONE for none)");
+    if (f->kind == PR_SRC_NONE) return PR_OK;
+    PR_REQUIRE(f->nterms >= 1 && f->nterms <= 8, PR_EINVAL, "source nterms must be 1..8");
+    PR_REQUIRE((long)f->nsteps >= (long)(q0 + nint) * m, PR_EDIM, "source time axis too short");
+    if (op.dim == 1) {
+        PR_REQUIRE(f->kind == PR_SRC_SEP1D, PR_EDIM, "1D operator needs a PR_SRC_SEP1D source");
+        PR_REQUIRE(f->nsrc >= 1 && f->space && f->time && f->amp, PR_EINVAL, "incomplete 1D source");
+    } else {
+        PR_REQUIRE(f->kind == PR_SRC_BUMP2D, PR_EDIM, "2D operator needs a PR_SRC_BUMP2D source");
+        PR_REQUIRE(f->gx && f->gy, PR_EINVAL, "incomplete 2D source");
+    }
+    return PR_OK;
+}
+
+pr_status pr_fine_propagate(pr_op h, int mode, int first_interval, int m, int B,
+                            int vecs_per_interval, const pr_source *f, const double *U_in,
+                            long ld_in, double *U_out, long ld_out, const double *offset,
+                            long ld_off, void *stream)
+{
+    PR_REQUIRE(h && U_out, PR_EINVAL, "NULL op or output");
+    const Op &op = h->op;
+    PR_REQUIRE(mode == PR_LINEAR || mode == PR_ADJOINT || mode == PR_AFFINE, PR_EINVAL, "bad mode");
+    PR_REQUIRE(m >= 0 && B >= 0 && vecs_per_interval >= 1 && first_interval >= 0, PR_EINVAL,
+               "negative size or vecs_per_interval < 1");
+    long minld = (op.dim == 1) ? B : op.rows;
+    PR_REQUIRE(ld_out >= minld && (!U_in || ld_in >= minld) && (!offset || ld_off >= minld), PR_EDIM,
+               "leading dimension too small");
+    if (mode == PR_AFFINE) {
+        int nint = (B + vecs_per_interval - 1) / vecs_per_interval;
+        pr_status st = check_source(op, f, first_interval, m, nint);
+        if (st != PR_OK) return st;
+        if (op.dim == 1 && f->kind == PR_SRC_SEP1D)
+            PR_REQUIRE(vecs_per_interval % f->nsrc == 0, PR_EDIM,
+                       "vecs_per_interval must be a multiple of nsrc");
+    }
+    return propagate(op, mode, first_interval, m, B, vecs_per_interval,
+                     mode == PR_AFFINE ? f : nullptr, U_in, ld_in, U_out, ld_out, offset, ld_off,
+                     0, 0, (cudaStream_t)stream);
+}
+
+pr_status pr_gaussian_sketch(pr_op h, int first_interval, int n_intervals, int l, uint64_t seed,
+                             double *out, long ld, void *stream)
+{
+    PR_REQUIRE(h && out, PR_EINVAL, "NULL op or output");
+    const Op &op = h->op;
+    PR_REQUIRE(first_interval >= 0 && n_intervals >= 0 && l >= 1, PR_EINVAL, "bad sizes");
+    long nvec = (long)n_intervals * l;
+    PR_REQUIRE(ld >= (op.dim == 1 ? nvec : op.rows), PR_EDIM, "leading dimension too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    Lay L = lay(op, ld);
+    if (op.dim == 2 && nvec > 0)
+        PR_CUDA(cudaMemset2DAsync(out, ld * sizeof(double), 0, op.rows * sizeof(double), nvec, s));
+    PR_CUDA(launch_sketch(op.dim, op.n, op.rows, first_interval, n_intervals, l, seed, out, L.rs,
+                          L.vs, s));
+    return PR_OK;
+}
+
+// ------------------------------------------------------------ build
+pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local, int m, int k,
+                          int p, uint64_t seed, void *stream, pr_coarse *out)
+{
+    PR_REQUIRE(h && out, PR_EINVAL, "NULL op or out");
+    const Op &op = h->op;
+    PR_REQUIRE(N_total >= 1 && n_local >= 1 && first_interval >= 0 &&
+                   first_interval + n_local <= N_total && m >= 1 && k >= 1 && p >= 0,
+               PR_EINVAL, "bad interval range or rank");
+    const int l = k + p;
+    PR_REQUIRE(l <= 112 && l <= op.rows, PR_EDIM, "l = k + p must be <= 112 and <= rows");
+    cudaStream_t s = (cudaStream_t)stream;
+    *out = nullptr;
+    pr_coarse G = new pr_coarse_s();
+    G->N_total = N_total; G->first = first_interval; G->nloc = n_local; G->m = m;
+    G->k = k; G->p = p; G->l = l; G->rows = op.rows; G->dim = op.dim;
+    const long rows = op.rows;
+    const int nl = n_local;
+    G->U = (double *)ws_alloc((size_t)nl * rows * k * sizeof(double));
+    G->V = (double *)ws_alloc((size_t)nl * rows * k * sizeof(double));
+    G->sigma = (double *)ws_alloc((size_t)nl * l * sizeof(double));
+    G->C = (double *)ws_alloc((size_t)nl * k * k * sizeof(double));
+    G->fail = (int *)ws_alloc(2 * sizeof(int));
+    if (!G->U || !G->V || !G->sigma || !G->C || !G->fail) {
+        pr_coarse_destroy(G);
+        set_error("out of device memory");
+        return PR_EOOM;
+    }
+    auto bail = [&](pr_status st) { pr_coarse_destroy(G); return st; };
+    cudaError_t e = cudaMemsetAsync(G->fail, 0, 2 * sizeof(int), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(G->C, 0, (size_t)nl * k * k * sizeof(double), s);
+    if (e != cudaSuccess) return bail(cuda_fail(e, "build init"));
+    {
+        Scratch S;
+        const long B = (long)nl * l;
+        const long ld = (op.dim == 1) ? ((B + 1) & ~1L) : rows;   // even ld: 16-B rows
+        double *Y = S.get<double>((size_t)rows * (op.dim == 1 ? ld : B));
+        double *Z = S.get<double>((size_t)rows * (op.dim == 1 ? ld : B));
+        double *Rtot = S.get<double>((size_t)nl * l * l);
+        double *Psi = S.get<double>((size_t)nl * l * l);
+        double *Phi = S.get<double>((size_t)nl * l * l);
+        if (!Y || !Z || !Rtot || !Psi || !Phi) { set_error("out of device memory"); return bail(PR_EOOM); }
+        pr_status st;
+        // step 1: Y = F' Omega (Omega generated inside the stepper)
+        st = propagate(op, PR_LINEAR, first_interval, m, (int)B, l, nullptr, nullptr, ld, Y, ld,
+                       nullptr, 0, 1, seed, s);
+        if (st != PR_OK) return bail(st);
+        // step 2: W = orth(Y)
+        st = cholqr(op, Y, ld, nl, l, nullptr, G->fail, &G->qr_passes[0], s);
+        if (st != PR_OK) return bail(st);
+        // step 3: Z = F'^* W
+        st = propagate(op, PR_ADJOINT, first_interval, m, (int)B, l, nullptr, Y, ld, Z, ld,
+                       nullptr, 0, 0, 0, s);
+        if (st != PR_OK) return bail(st);
+        // step 4: V R_Z = Z
+        st = cholqr(op, Z, ld, nl, l, Rtot, G->fail, &G->qr_passes[1], s);
+        if (st != PR_OK) return bail(st);
+        // step 5: M = R_Z^T = Psi Sigma Phi^T
+        e = launch_jacobi(Rtot, nl, l, Psi, G->sigma, Phi, G->fail + 1, s);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "jacobi"));
+        // steps 5-6: psi = W Psi_k, phi = V Phi_k
+        Lay L = lay(op, ld);
+        const long xbs = (op.dim == 1) ? (long)l : (long)l * ld;
+        e = launch_lift(Y, xbs, L.rs, L.vs, rows, l, Psi, l, k, nl, G->U, s);
+        if (e == cudaSuccess) e = launch_lift(Z, xbs, L.rs, L.vs, rows, l, Phi, l, k, nl, G->V, s);
+        if (e != cudaSuccess) return bail(cuda_fail(e, "lift"));
+        // reduced sweep matrices C_q = Sigma_q V_q^T U_{q-1}, local q >= 1
+        if (nl >= 2) {
+            int nb = nl - 1;
+            int nchunk = xty_chunks(rows, nb);
+            long cr = (rows + nchunk - 1) / nchunk;
+            double *part = S.get<double>((size_t)nb * nchunk * k * k);
+            if (!part) { set_error("out of device memory"); return bail(PR_EOOM); }
+            XtY x{nullptr, G->V + rows * k, rows * k, k, 1, k, G->U, rows * k, k, 1, k, rows, nb,
+                  nchunk, cr, part};
+            e = launch_xty(x, s);
+            if (e == cudaSuccess)
+                e = launch_reduce_parts(part, nb, nchunk, k, k, G->sigma + l, l, G->C + (long)k * k, s);
+            if (e != cudaSuccess) return bail(cuda_fail(e, "sweep matrices"));
+        }
+    }
+    *out = G;
+    return PR_OK;
+}
+
+pr_status pr_coarse_info(pr_coarse G, int *k, int *l, int *n_local, int *first_interval, int *m,
+                         double *delta, double *eps, double *sigma_host, int *qr_passes)
+{
+    PR_REQUIRE(G, PR_EINVAL, "NULL handle");
+    PR_CUDA(cudaDeviceSynchronize());
+    if (k) *k = G->k;
+    if (l) *l = G->l;
+    if (n_local) *n_local = G->nloc;
+    if (first_interval) *first_interval = G->first;
+    if (m) *m = G->m;
+    if (qr_passes) { qr_passes[0] = G->qr_passes[0]; qr_passes[1] = G->qr_passes[1]; }
+    std::vector<double> sig((size_t)G->nloc * G->l);
+    PR_CUDA(cudaMemcpy(sig.data(), G->sigma, sig.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    int fl[2] = {0, 0};
+    PR_CUDA(cudaMemcpy(fl, G->fail, sizeof fl, cudaMemcpyDeviceToHost));
+    if (sigma_host) memcpy(sigma_host, sig.data(), sig.size() * sizeof(double));
+    double dl = 0.0, ep = 0.0;
+    for (int q = 0; q < G->nloc; ++q) {
+        dl = std::max(dl, sig[(size_t)q * G->l]);
+        if (G->p > 0) ep = std::max(ep, sig[(size_t)q * G->l + G->k]);
+    }
+    if (delta) *delta = dl;
+    if (eps) *eps = (G->p > 0) ? ep : NAN;
+    if (fl[0]) { set_error("CholeskyQR broke down on the device"); return PR_ENOCONV; }
+    if (fl[1]) { set_error("Jacobi SVD did not converge in 60 sweeps"); return PR_ENOCONV; }
+    if (G->p == 0 && eps) { set_error("eps needs p >= 1"); return PR_EUNAVAIL; }
+    return PR_OK;
+}
+
+pr_status pr_coarse_factors(pr_coarse G, const double **U, const double **V, const double **sigma)
+{
+    PR_REQUIRE(G, PR_EINVAL, "NULL handle");
+    if (U) *U = G->U;
+    if (V) *V = G->V;
+    if (sigma) *sigma = G->sigma;
+    return PR_OK;
+}
+
+pr_status pr_coarse_apply(pr_coarse G, int q_local, int nvec, const double *X, long ldx, double *Y,
+                          long ldy, void *stream)
+{
+    PR_REQUIRE(G && X && Y, PR_EINVAL, "NULL argument");
+    PR_REQUIRE(q_local >= 0 && q_local < G->nloc && nvec >= 1 && nvec <= 128, PR_EINVAL,
+               "bad interval or nvec (1..128)");
+    const long rows = G->rows;
+    const int k = G->k;
+    long minld = (G->dim == 1) ? nvec : rows;
+    PR_REQUIRE(ldx >= minld && ldy >= minld, PR_EDIM, "leading dimension too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    Scratch S;
+    Lay Lx = (G->dim == 1) ? Lay{ldx, 1} : Lay{1, ldx};
+    Lay Ly = (G->dim == 1) ? Lay{ldy, 1} : Lay{1, ldy};
+    int nchunk = xty_chunks(rows, 1);
+    long cr = (rows + nchunk - 1) / nchunk;
+    double *part, *ev;
+    PR_ALLOC(part, double, (size_t)nchunk * k * nvec, S);
+    PR_ALLOC(ev, double, (size_t)k * nvec, S);
+    const double *Vq = G->V + (long)q_local * rows * k;
+    const double *Uq = G->U + (long)q_local * rows * k;
+    XtY x{nullptr, Vq, 0, k, 1, k, X, 0, Lx.rs, Lx.vs, nvec, rows, 1, nchunk, cr, part};
+    PR_CUDA(launch_xty(x, s));
+    PR_CUDA(launch_reduce_parts(part, 1, nchunk, k, nvec, G->sigma + (long)q_local * G->l, 0, ev, s));
+    Expand ex{Y, Ly.rs, Ly.vs, nullptr, 0, 0, Uq, 0, ev, k, nvec, 1, rows, nchunk, cr, nullptr};
+    PR_CUDA(launch_expand(ex, s));
+    return PR_OK;
+}
+
+pr_status pr_coarse_destroy(pr_coarse G)
+{
+    if (!G) return PR_OK;
+    ws_free(G->U); ws_free(G->V); ws_free(G->sigma); ws_free(G->C); ws_free(G->fail);
+    delete G;
+    return PR_OK;
+}
+
+// ---------------------------------------------------------------- Parareal
+pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_u0,
+                      const pr_source *f, int K_iter, double *U_out, long ld_out, double *upd_host,
+                      double *bnorm_host, double *hist, long hist_stride, void *stream)
+{
+    PR_REQUIRE(G && h && u0 && U_out, PR_EINVAL, "NULL argument");
+    const Op &op = h->op;
+    PR_REQUIRE(G->first == 0 && G->nloc == G->N_total, PR_EDIM,
+               "pr_parareal needs a coarse handle covering all intervals");
+    PR_REQUIRE(G->rows == op.rows && G->dim == op.dim, PR_EDIM, "coarse handle / operator mismatch");
+    PR_REQUIRE(nsrc >= 1 && nsrc <= 128 && K_iter >= 0, PR_EINVAL, "nsrc must be 1..128, K_iter >= 0");
+    const int N = G->N_total, k = G->k, m = G->m, S = nsrc;
+    const long rows = op.rows;
+    const long nvec = (long)(N + 1) * S;
+    long minld = (op.dim == 1) ? nvec : rows;
+    PR_REQUIRE(ld_out >= minld, PR_EDIM, "ld_out too small");
+    PR_REQUIRE(ld_u0 >= (op.dim == 1 ? S : rows), PR_EDIM, "ld_u0 too small");
+    {
+        pr_status st = check_source(op, f, 0, m, N);
+        if (st != PR_OK) return st;
+        if (op.dim == 1 && f->kind == PR_SRC_SEP1D)
+            PR_REQUIRE(f->nsrc == S, PR_EDIM, "source nsrc must equal nsrc");
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    Scratch Sc;
+    const long ld = ld_out;          // Fu and b share U_out's layout
+    Lay L = lay(op, ld);
+    Lay L0 = lay(op, ld_u0);
+    const size_t arr = (op.dim == 1) ? (size_t)rows * ld : (size_t)nvec * ld;
+    double *Fu, *bb, *qv, *pv, *ev, *part, *npart, *upd, *bn;
+    PR_ALLOC(Fu, double, arr, Sc);
+    PR_ALLOC(bb, double, arr, Sc);
+    const size_t red = (size_t)N * k * S;
+    PR_ALLOC(qv, double, red, Sc);
+    PR_ALLOC(pv, double, red, Sc);
+    PR_ALLOC(ev, double, red, Sc);
+    const int nchunk = xty_chunks(rows, N);
+    const long cr = (rows + nchunk - 1) / nchunk;
+    PR_ALLOC(part, double, (size_t)N * nchunk * k * S, Sc);
+    PR_ALLOC(npart, double, (size_t)nvec * nchunk, Sc);
+    PR_ALLOC(upd, double, (size_t)(K_iter > 0 ? K_iter : 1) * nvec, Sc);
+    PR_ALLOC(bn, double, (size_t)nvec, Sc);
+    const long blk = (op.dim == 1) ? (long)S : (long)S * ld;   // element offset of one block
+
+    // u^k_0 = u0 in the state and in block 0 of Fu (Fu_0 := u0)
+    PR_CUDA(launch_copy_vectors(u0, L0.rs, L0.vs, U_out, L.rs, L.vs, rows, S, s));
+    PR_CUDA(launch_copy_vectors(u0, L0.rs, L0.vs, Fu, L.rs, L.vs, rows, S, s));
+    if (op.dim == 2) {
+        // ghost entries of every block must be zero (the 2D stepper keeps them zero)
+        PR_CUDA(cudaMemsetAsync(bb, 0, (size_t)S * ld * sizeof(double), s));
+    }
+    // offsets b_q = F_q 0 into blocks 1..N of bb
+    {
+        pr_status st = propagate(op, PR_AFFINE, 0, m, N * S, S, f, nullptr, ld, bb + blk, ld,
+                                 nullptr, 0, 0, 0, s);
+        if (st != PR_OK) return st;
+    }
+    // ||b_j|| (b_0 := u0)
+    PR_CUDA(launch_copy_vectors(u0, L0.rs, L0.vs, bb, L.rs, L.vs, rows, S, s));
+    PR_CUDA(launch_vecnorm_parts(bb, L.rs, L.vs, rows, (int)nvec, nchunk, cr, npart, s));
+    PR_CUDA(launch_norm_finish(npart, (int)nvec, nchunk, bn, s));
+    // Fu blocks 1..N := b (initialisation uses G_q u = G'_q u + b_q)
+    PR_CUDA(launch_copy_vectors(bb + blk, L.rs, L.vs, Fu + blk, L.rs, L.vs, rows, N * S, s));
+
+    const double *sig = G->sigma;
+    auto project = [&](const double *Yarr, double *outv) -> pr_status {
+        // outv_q = Sigma_q V_q^T Y[block q], q = 0..N-1
+        XtY x{nullptr, G->V, rows * k, k, 1, k, Yarr, blk, L.rs, L.vs, S, rows, N, nchunk, cr, part};
+        PR_CUDA(launch_xty(x, s));
+        PR_CUDA(launch_reduce_parts(part, N, nchunk, k, S, sig, G->l, outv, s));
+        return PR_OK;
+    };
+    auto expand = [&](bool norms) -> pr_status {
+        Expand ex{U_out + blk, L.rs, L.vs, Fu + blk, L.rs, L.vs, G->U, rows * k, ev, k, S, N, rows,
+                  nchunk, cr, norms ? npart + (size_t)S * nchunk : nullptr};
+        PR_CUDA(launch_expand(ex, s));
+        return PR_OK;
+    };
+    pr_status st;
+    // ---- initialisation: u^0_{q+1} = G_q u^0_q (p = 0)
+    if ((st = project(Fu, qv)) != PR_OK) return st;
+    PR_CUDA(launch_sweep(G->C, qv, nullptr, N, k, S, ev, s));
+    if ((st = expand(false)) != PR_OK) return st;
+    if (hist) {
+        PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, hist, L.rs, L.vs, rows, (int)nvec, s));
+    }
+    // ---- iterations
+    for (int it = 1; it <= K_iter; ++it) {
+        // fine solves of all intervals in one launch: Fu_{q+1} = F_q' u_q + b_q
+        st = propagate(op, PR_LINEAR, 0, m, N * S, S, nullptr, U_out, ld, Fu + blk, ld, bb + blk,
+                       ld, 0, 0, s);
+        if (st != PR_OK) return st;
+        if ((st = project(U_out, pv)) != PR_OK) return st;
+        if ((st = project(Fu, qv)) != PR_OK) return st;
+        PR_CUDA(launch_sweep(G->C, qv, pv, N, k, S, ev, s));
+        PR_CUDA(cudaMemsetAsync(npart, 0, (size_t)S * nchunk * sizeof(double), s));   // block 0
+        if ((st = expand(true)) != PR_OK) return st;
+        PR_CUDA(launch_norm_finish(npart, (int)nvec, nchunk, upd + (size_t)(it - 1) * nvec, s));
+        if (hist) {
+            PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, hist + (size_t)it * hist_stride, L.rs,
+                                        L.vs, rows, (int)nvec, s));
+        }
+    }
+    if (upd_host && K_iter > 0)
+        PR_CUDA(cudaMemcpyAsync(upd_host, upd, (size_t)K_iter * nvec * sizeof(double),
+                                cudaMemcpyDeviceToHost, s));
+    if (bnorm_host)
+        PR_CUDA(cudaMemcpyAsync(bnorm_host, bn, (size_t)nvec * sizeof(double), cudaMemcpyDeviceToHost, s));
+    PR_CUDA(cudaStreamSynchronize(s));
+    return PR_OK;
+}
+
+// ------------------------------------------------------------------ bounds
+static double log_binom(int n, int k)
+{
+    return lgamma((double)n + 1.0) - lgamma((double)k + 1.0) - lgamma((double)(n - k) + 1.0);
+}
+
+pr_status pr_bounds(double delta, double eps, int N, int K, const double *bnorm, const double *upd,
+                    double *apriori, double *apost, double *apost_sup)
+{
+    PR_REQUIRE(N >= 1 && K >= 0 && delta >= 0 && eps >= 0, PR_EINVAL, "bad bound arguments");
+    PR_REQUIRE(!apriori || bnorm, PR_EINVAL, "apriori needs bnorm");
+    PR_REQUIRE((!apost && !apost_sup) || upd, PR_EINVAL, "a posteriori bounds need upd");
+    const int W = N + 1;
+    if (apriori) {
+        for (int n = 0; n <= N; ++n) {
+            // eq. error_bound_initial
+            double s = 0.0;
+            for (int mm = 0; mm < n; ++mm)
+                s += std::min(2.0 * delta, (n - mm) * eps) * pow(delta, n - mm - 1) * bnorm[mm];
+            apriori[n] = s;
+        }
+        for (int k = 1; k <= K; ++k)
+            for (int n = 0; n <= N; ++n) {
+                // eq. error_bound_eps_delta2, log space
+                double s = 0.0;
+                if (eps > 0.0)
+                    for (int mm = 0; mm <= n - k - 1; ++mm) {
+                        if (!(bnorm[mm] > 0.0)) continue;
+                        double lg = log(2.0) + k * log(eps) + log_binom(n - mm, k) +
+                                    (n - mm - k) * (delta > 0 ? log(delta) : -INFINITY) + log(bnorm[mm]);
+                        if (n - mm - k == 0) lg = log(2.0) + k * log(eps) + log_binom(n - mm, k) + log(bnorm[mm]);
+                        s += exp(lg);
+                    }
+                apriori[(size_t)k * W + n] = s;
+            }
+    }
+    for (int k = 1; k <= K; ++k) {
+        const double *u = upd + (size_t)(k - 1) * W;
+        if (apost)
+            for (int n = 0; n <= N; ++n) {
+                double s = 0.0;   // eq. apost_bound
+                for (int mm = 1; mm <= n - 1; ++mm) s += pow(delta, n - mm - 1) * u[mm];
+                apost[(size_t)(k - 1) * W + n] = eps * s;
+            }
+        if (apost_sup) {
+            double mx = 0.0;
+            for (int n = 1; n <= N; ++n) mx = std::max(mx, u[n]);
+            apost_sup[k - 1] = (delta < 1.0) ? eps / (1.0 - delta) * mx : NAN;   // eq. apost_bound_sup
+        }
+    }
+    return PR_OK;
+}
+
+}  // extern "C"

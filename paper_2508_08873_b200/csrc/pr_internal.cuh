@@ -1,0 +1,199 @@
+// pr_internal.cuh -- shared internals of libpr (the CUDA path; no oracle code).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/pr.h"
+
+namespace pr {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string &msg);
+pr_status cuda_fail(cudaError_t e, const char *where);
+
+#define PR_CUDA(call)                                         \
+    do {                                                      \
+        cudaError_t _e = (call);                              \
+        if (_e != cudaSuccess) return ::pr::cuda_fail(_e, #call); \
+    } while (0)
+
+#define PR_CHECK_LAUNCH(where)                                \
+    do {                                                      \
+        cudaError_t _e = cudaGetLastError();                  \
+        if (_e != cudaSuccess) return ::pr::cuda_fail(_e, where); \
+    } while (0)
+
+#define PR_REQUIRE(cond, code, msg)                           \
+    do {                                                      \
+        if (!(cond)) { ::pr::set_error(msg); return code; }   \
+    } while (0)
+
+// -------------------------------------------------------- device workspace
+// Grow-only caching allocator: buffers returned by ws_free go back to a
+// size-keyed free list and are reused (no cudaFree/cudaMalloc, hence no
+// implicit device synchronisation, in repeated builds / Parareal runs).
+void *ws_alloc(size_t bytes);
+void ws_free(void *p);
+
+// Number of SMs of the current device (cached).
+int num_sms();
+
+// ---------------------------------------------------------------- operator
+struct Coef {             // one row of a fused stepper pass (32 B, aligned)
+    double a, b, c, d;
+};
+
+struct Op {
+    int dim = 1;
+    int n = 0;            // interior points per side
+    long rows = 0;        // storage rows of one vector
+    double dt = 0.0;
+    // 1D: pass coefficients for I + dt A (fw) and (I + dt A)^T (tr).
+    //   DN[i] = {ap_i, w_i, ga_i, 0}: down pass = UL back-substitution then LU forward
+    //   UP[i] = {cp_i, wt_i, gc_i, 0}: up pass   = LU back-substitution then UL forward
+    Coef *dn_fw = nullptr, *up_fw = nullptr, *dn_tr = nullptr, *up_tr = nullptr;
+    // 2D: P = n+1; S (P x P) sine matrix with zero row/col 0; lam[P] eigenvalues of T.
+    int P = 0;
+    double *S = nullptr;
+    double *lam = nullptr;
+};
+
+// --------------------------------------------------------------- kernels
+struct StepArgs {
+    int n;
+    long B;
+    int m;
+    const Coef *DN;
+    const Coef *UP;
+    const double *in;  long ld_in;     // null -> zero input
+    double *out;       long ld_out;
+    const double *off; long ld_off;    // null -> no offset
+    int sketch;                        // 1 -> input is Omega (Philox)
+    unsigned long long seed;
+    int q0;                            // first interval
+    int vpi;                           // vectors per interval
+    // source (PR_SRC_SEP1D) -- R == 0: none
+    int R;
+    const double *spaceT;              // (n x R) row-major (transposed copy)
+    const double *time;                // (R x nsteps)
+    const double *amp;                 // (S x R)
+    int nsteps;
+    int nsrc;
+    double dt;
+};
+
+cudaError_t launch_factor_1d(int n, const double *subA, const double *supA, const double *rsA,
+                             const double *diagA, double dt, int transpose, Coef *DN, Coef *UP,
+                             int *bad, cudaStream_t s);
+cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s);
+cudaError_t launch_sketch(int dim, int n, long rows, int q0, int nint, int l,
+                          unsigned long long seed, double *out, long rs, long vs, cudaStream_t s);
+cudaError_t launch_transpose(const double *in, int R, int n, double *out, cudaStream_t s);
+
+// Tall-skinny cross products: for batch b, chunk t of rows,
+//   part[((b*nchunk + t)*a + i)*c + j] = sum_{rows in chunk} X_b[row, i] * Y_b[row, j]
+// with X_b[row, i] = X[b*xbs + row*xrs + i*xcs] (likewise Y).
+struct XtY {
+    const int *skip;                  // nullable: batch b skipped when skip[b] == 2 (QR done)
+    const double *X; long xbs, xrs, xcs; int a;
+    const double *Y; long ybs, yrs, ycs; int c;
+    long rows;
+    int nbatch;
+    int nchunk;
+    long chunk_rows;
+    double *part;
+};
+cudaError_t launch_xty(const XtY &p, cudaStream_t s);
+int xty_chunks(long rows, int nbatch);
+
+// out[(b*a + i)*c + j] = scale_i(b) * sum_t part[...]  (fixed order over t)
+cudaError_t launch_reduce_parts(const double *part, int nbatch, int nchunk, int a, int c,
+                                const double *rowscale, long rowscale_bs, double *out,
+                                cudaStream_t s);
+
+// CholeskyQR control: per interval state machine + shifted Cholesky.
+struct CholArgs {
+    const double *part; int nchunk;   // Gram partials
+    int nbatch; int l; long nrows;    // nrows: rows of the block (shift formula)
+    int *state;                       // per batch: 0 shift phase, 1 one plain pass done, 2 done
+    int *act;                         // per batch: 1 if this pass applies R (written)
+    double *R;                        // per batch l x l (upper) for this pass
+    double *Rtot;                     // per batch l x l accumulated product (nullable)
+    int *active;                      // device counter of batches still active
+    int *fail;                        // device flag: Cholesky broke down
+};
+cudaError_t launch_chol(const CholArgs &a, cudaStream_t s);
+cudaError_t launch_trsm(double *Q, long bs, long rs, long cs, long rows, int l, int nbatch,
+                        const double *R, const int *act, cudaStream_t s);
+
+cudaError_t launch_jacobi(const double *Rtot, int nbatch, int l, double *Psi, double *sigma,
+                          double *Phi, int *fail, cudaStream_t s);
+
+// out_b[row, r] = sum_j X_b[row, j] * C_b[j, r]  (j < l, r < k); out is (nbatch, rows, k)
+cudaError_t launch_lift(const double *X, long xbs, long xrs, long xcs, long rows, int l,
+                        const double *Cm, int ldc, int k, int nbatch, double *out,
+                        cudaStream_t s);
+
+// sequential reduced sweep: e_j = C_j e_{j-1} + (q_j - p_j), j = 0..N-1
+// (C_0 unused: e_{-1} = 0).  All (k x S) row-major per interval.
+cudaError_t launch_sweep(const double *C, const double *q, const double *p, int N, int k, int S,
+                         double *e, cudaStream_t s);
+
+// expand: out[row, v] = base[row, v] + sum_r U_b[row, r] e_b[r, s]  for interval b,
+// source s, vector v = b*S + s (vector offsets in the out/base arrays given by
+// vbs), with optional partial squared norms of (new - old).
+struct Expand {
+    double *out; long ors, ovs;       // element (row, vec) at out[row*ors + vec*ovs]
+    const double *base; long brs, bvs;  // nullable
+    const double *U; long Ubs;        // U_b[row, r] at U[b*Ubs + row*k + r]
+    const double *e;                  // (nbatch, k, S)
+    int k, S, nbatch;
+    long rows;
+    int nchunk; long chunk_rows;
+    double *normpart;                 // nullable: (nbatch*S, nchunk)
+};
+cudaError_t launch_expand(const Expand &a, cudaStream_t s);
+// out[v] = sqrt(sum_t part[v*nchunk + t])
+cudaError_t launch_norm_finish(const double *part, int nvec, int nchunk, double *out,
+                               cudaStream_t s);
+// plain squared-norm partials of vectors (op layout)
+cudaError_t launch_vecnorm_parts(const double *X, long rs, long vs, long rows, int nvec,
+                                 int nchunk, long chunk_rows, double *part, cudaStream_t s);
+cudaError_t launch_eye(double *R, int nbatch, int l, cudaStream_t s);
+cudaError_t launch_copy_vectors(const double *in, long irs, long ivs, double *out, long ors,
+                                long ovs, long rows, int nvec, cudaStream_t s);
+
+// 2D separable stepper (k_sep2d.cu)
+struct Sep2dArgs {
+    const Op *op;
+    int mode;            // PR_LINEAR / PR_ADJOINT / PR_AFFINE
+    int q0, m, B, vpi;
+    const pr_source *f;
+    const double *in; long ld_in;
+    double *out; long ld_out;
+    const double *off; long ld_off;
+};
+pr_status run_sep2d(const Sep2dArgs &a, cudaStream_t s);
+
+}  // namespace pr
+
+// ------------------------------------------------------------- handles
+struct pr_op_s {
+    pr::Op op;
+};
+
+struct pr_coarse_s {
+    int N_total = 0, first = 0, nloc = 0, m = 0, k = 0, p = 0, l = 0;
+    long rows = 0;
+    int dim = 1;
+    double *U = nullptr;       // (nloc, rows, k)
+    double *V = nullptr;       // (nloc, rows, k)
+    double *sigma = nullptr;   // (nloc, l)
+    double *C = nullptr;       // (nloc, k, k): C_q = Sigma_q V_q^T U_{q-1} (q >= first+1)
+    int *fail = nullptr;       // device flags [0]: qr, [1]: svd
+    int qr_passes[2] = {0, 0};
+};

@@ -1,0 +1,213 @@
+"""GPU parity of the 1D CUDA path against the oracle (same seeded inputs),
+through the C ABI.  Tolerances: BASELINE.json north_star, 1e-10 normwise for
+fp64 states and singular values (reading Z11)."""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+
+from gpu_util import TAU_1D, empty_batch, from_gpu, gpu_op, gpu_source, relnorm, to_gpu
+from oracle.fine import fine, make_op, sequential_reference
+from oracle.parareal import parareal as oracle_parareal
+from oracle.rng import gaussian_sketch
+from oracle.rsvd import rsvd_interval
+from workloads import generators as G
+from workloads.configs import C1, C2, C4, get
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import torch
+    from paper_2508_08873_b200 import build as B
+    B.build()
+    assert torch.cuda.is_available()
+
+
+# ------------------------------------------------------------------ sketch
+@pytest.mark.parametrize("n,nint,l,q0", [(127, 3, 12, 0), (301, 2, 7, 5), (1001, 1, 40, 63)])
+def test_gaussian_sketch_matches_oracle(n, nint, l, q0):
+    cfg = replace(C1, n=n)
+    op = gpu_op(cfg)
+    out = empty_batch(cfg, nint * l)
+    op.gaussian_sketch(q0, nint, l, 2508088730, out)
+    got = out.cpu().numpy()
+    for j in range(nint):
+        ref = gaussian_sketch(2508088730, q0 + j, n, l)
+        # counter-based: identical integers, Box-Muller to a few ulps
+        np.testing.assert_allclose(got[:, j * l:(j + 1) * l], ref, rtol=0, atol=1e-14)
+
+
+# -------------------------------------------------------------- fine solver
+@pytest.mark.parametrize("name,n,m,B", [("C1", 127, 64, 12), ("C1", 127, 1, 6), ("C1", 127, 2, 5),
+                                        ("T4", 301, 16, 33), ("T4", 37, 7, 64), ("C2", 4095, 256, 10),
+                                        ("C4", 16383, 128, 6)])
+@pytest.mark.parametrize("mode", ["linear", "adjoint"])
+def test_fine_linear_adjoint(name, n, m, B, mode):
+    from paper_2508_08873_b200 import PR_ADJOINT, PR_LINEAR
+    cfg = replace(get(name), n=n, m=m)
+    op_o = make_op(cfg)
+    op_g = gpu_op(cfg)
+    rng = np.random.default_rng(n + m + B)
+    X = rng.standard_normal((B, n))
+    Ug = to_gpu(cfg, X)
+    out = empty_batch(cfg, B)
+    op_g.fine_propagate(PR_LINEAR if mode == "linear" else PR_ADJOINT, 2, m, Ug, out)
+    ref = fine(op_o, 3, X, mode)
+    got = from_gpu(cfg, out)
+    for v in range(B):
+        assert relnorm(got[v], ref[v]) <= TAU_1D, v
+
+
+@pytest.mark.parametrize("name,B,ld", [("T4", 5 * 4, 20), ("T4", 5 * 3, 17), ("C1", 8, 8)])
+def test_fine_affine_offset_and_inplace(name, B, ld):
+    from paper_2508_08873_b200 import PR_AFFINE, PR_LINEAR
+    cfg = get(name)
+    op_o, op_g = make_op(cfg), gpu_op(cfg)
+    src_g = gpu_source(cfg)
+    src_o = G.source_1d(cfg)
+    S = cfg.nsrc
+    nint = B // S
+    rng = np.random.default_rng(B)
+    X = rng.standard_normal((B, cfg.n))
+    Ug = to_gpu(cfg, X, ld)
+    out = empty_batch(cfg, B, ld)
+    q0 = 1
+    op_g.fine_propagate(PR_AFFINE, q0, cfg.m, Ug, out, vecs_per_interval=S, source=src_g)
+    got = from_gpu(cfg, out, B)
+    ref = np.zeros_like(X)
+    for j in range(nint):
+        sl = slice(j * S, (j + 1) * S)
+        ref[sl] = fine(op_o, q0 + j + 1, X[sl], "affine", src_o, np.arange(S))
+    for v in range(B):
+        assert relnorm(got[v], ref[v]) <= TAU_1D
+    # zero input == offsets b_q; then F'u + b via the offset path, in place
+    b = empty_batch(cfg, B, ld)
+    op_g.fine_propagate(PR_AFFINE, q0, cfg.m, None, b, vecs_per_interval=S, source=src_g)
+    op_g.fine_propagate(PR_LINEAR, q0, cfg.m, Ug, Ug, offset=b)
+    got2 = from_gpu(cfg, Ug, B)
+    for v in range(B):
+        assert relnorm(got2[v], ref[v]) <= TAU_1D
+
+
+def test_fine_m0_is_copy():
+    from paper_2508_08873_b200 import PR_LINEAR
+    cfg = C1
+    op_g = gpu_op(cfg)
+    X = np.random.default_rng(0).standard_normal((9, cfg.n))
+    out = empty_batch(cfg, 9)
+    op_g.fine_propagate(PR_LINEAR, 0, 0, to_gpu(cfg, X), out)
+    np.testing.assert_array_equal(from_gpu(cfg, out), X)
+
+
+# ------------------------------------------------------------------- build
+def _check_interval(cfg, Gg, q, info, probes=6):
+    """G_q' of the GPU vs the oracle's rSVD of the same interval (operator
+    norm on Gaussian probes, and sigma normwise)."""
+    import torch
+    op_o = make_op(cfg)
+    tr = rsvd_interval(op_o, q + 1, cfg.k, cfg.p, cfg.seed_omega)
+    s1 = tr.sigma[0]
+    assert np.max(np.abs(info["sigma"][q] - tr.sigma)) <= TAU_1D * s1
+    X = np.random.default_rng(q).standard_normal((probes, cfg.n))
+    Y = empty_batch(cfg, probes)
+    Gg.apply(q, to_gpu(cfg, X), Y, 1)
+    got = from_gpu(cfg, Y)
+    ref = tr.apply_linear(X)
+    for v in range(probes):
+        assert np.linalg.norm(got[v] - ref[v]) <= TAU_1D * s1 * np.linalg.norm(X[v])
+
+
+@pytest.mark.parametrize("name", ["C1", "T1", "T1k1", "T4"])
+def test_build_all_intervals(name):
+    from paper_2508_08873_b200 import Coarse
+    cfg = get(name)
+    Gg = Coarse.build(gpu_op(cfg), cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega)
+    info = Gg.info()
+    for q in range(cfg.N):
+        _check_interval(cfg, Gg, q, info)
+    sig = info["sigma"]
+    assert info["delta"] == np.max(sig[:, 0])
+    assert info["eps"] == np.max(sig[:, cfg.k])
+
+
+@pytest.mark.parametrize("name,qs", [("C2", (0, 31, 63)), ("C4", (0, 255))])
+def test_build_full_size_sampled_intervals(name, qs):
+    from paper_2508_08873_b200 import Coarse
+    cfg = get(name)
+    Gg = Coarse.build(gpu_op(cfg), cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega)
+    info = Gg.info()
+    for q in qs:
+        _check_interval(cfg, Gg, q, info)
+
+
+def test_build_sharded_equals_full():
+    """Seeds depend on (seed, q, column) only: building intervals [3, 7) alone
+    gives the same coarse operators as building all of them (S:495 analog)."""
+    from paper_2508_08873_b200 import Coarse
+    cfg = get("T1")
+    opg = gpu_op(cfg)
+    full = Coarse.build(opg, cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega).info()
+    part = Coarse.build(opg, cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega, first_interval=3,
+                        n_local=4).info()
+    np.testing.assert_array_equal(part["sigma"], full["sigma"][3:7])
+
+
+# ---------------------------------------------------------------- Parareal
+def _run_parareal(cfg, K=None, keep_hist=True):
+    import torch
+    from paper_2508_08873_b200 import Coarse, parareal
+    K = cfg.K if K is None else K
+    opg = gpu_op(cfg)
+    Gg = Coarse.build(opg, cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega)
+    info = Gg.info()
+    S = cfg.nsrc
+    u0 = np.stack([G.initial_value(cfg)] * S)
+    u0g = to_gpu(cfg, u0)
+    nvec = (cfg.N + 1) * S
+    Uo = empty_batch(cfg, nvec)
+    hist = None
+    if keep_hist:
+        hist = torch.zeros((K + 1,) + tuple(Uo.shape), dtype=torch.float64, device="cuda")
+    upd, bn = parareal(Gg, opg, u0g, gpu_source(cfg), K, Uo, nsrc=S, hist=hist)
+    return Gg, info, Uo, hist, upd, bn, u0
+
+
+@pytest.mark.parametrize("name", ["T1", "T4", "T1k1", "C1"])
+def test_parareal_all_iterates_match_oracle(name):
+    cfg = get(name)
+    Gg, info, Uo, hist, upd, bn, u0 = _run_parareal(cfg)
+    op_o = make_op(cfg)
+    truncs = [rsvd_interval(op_o, n, cfg.k, cfg.p, cfg.seed_omega) for n in range(1, cfg.N + 1)]
+    S = cfg.nsrc
+    res = oracle_parareal(op_o, truncs, u0, cfg.N, cfg.K, G.source_1d(cfg), np.arange(S))
+    scale = np.max(np.linalg.norm(res.U, axis=-1))
+    for k in range(cfg.K + 1):
+        got = from_gpu(cfg, hist[k]).reshape(cfg.N + 1, S, cfg.n)
+        err = np.max(np.linalg.norm(got - res.U[k], axis=-1))
+        assert err <= TAU_1D * scale, (k, err / scale)
+    # update norms ||u^k_n - u^{k-1}_n|| and offsets ||b_n|| (b_0 = u0)
+    assert np.max(np.abs(upd - res.upd[1:])) <= TAU_1D * scale
+    bref = np.linalg.norm(res.b, axis=-1)
+    bref[0] = np.linalg.norm(u0, axis=-1)
+    assert np.max(np.abs(bn - bref)) <= TAU_1D * np.max(bref)
+    np.testing.assert_array_equal(upd[:, 0], 0.0)
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_parareal_full_size_against_fine_solution(name):
+    """At full size the Parareal fixed point is the sequential fine solution
+    (P:136-139): compare sampled sources with the oracle's
+    sequential propagation, and finite termination u^k_n = u_n for n <= k."""
+    cfg = get(name)
+    Gg, info, Uo, hist, upd, bn, u0 = _run_parareal(cfg, keep_hist=False)
+    S = cfg.nsrc
+    sample = [0, S - 1] if S > 1 else [0]
+    op_o = make_op(cfg)
+    src = G.source_1d(cfg)
+    ref = sequential_reference(op_o, u0[sample], cfg.N, src, np.array(sample))
+    got = from_gpu(cfg, Uo).reshape(cfg.N + 1, S, cfg.n)[:, sample]
+    scale = np.max(np.linalg.norm(ref, axis=-1))
+    err = np.max(np.linalg.norm(got - ref, axis=-1))
+    assert err <= TAU_1D * scale, err / scale
