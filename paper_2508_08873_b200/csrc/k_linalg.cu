@@ -264,16 +264,13 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol(CholArgs a)
         double *Tb = a.Rtot + (long)b * per;
         __syncthreads();
         for (int i = 0; i < l; ++i) {
-            double v[1];
+            // each thread owns column k: it reads rows >= i of its own column, then
+            // overwrites row i of that column -- no cross-thread hazard
             for (int k = threadIdx.x; k < l; k += CH_THREADS) {
                 double s = 0.0;
                 for (int j = i; j < l; ++j) s += G[i * l + j] * Tb[(long)j * l + k];
-                v[0] = s;
-                // all reads of row i of Tb for this column happen above before the write
-                __syncwarp();
-                Tb[(long)i * l + k] = v[0];
+                Tb[(long)i * l + k] = s;
             }
-            __syncthreads();
         }
     }
     if (threadIdx.x == 0) {

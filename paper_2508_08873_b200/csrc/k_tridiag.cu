@@ -177,9 +177,9 @@ cudaError_t launch_transpose(const double *in, int R, int n, double *out, cudaSt
 
 // ----------------------------------------------------------------- stepper
 constexpr int GR = 32;   // rows per group (one coefficient row per lane)
-constexpr int PD = 3;    // groups in flight ahead of the one being computed
+constexpr int PD = 2;    // groups in flight ahead of the one being computed
 constexpr int RING = PD + 1;
-constexpr int SWARPS = 2;  // warps per CTA
+constexpr int SWARPS = 1;  // warps per CTA (small CTAs: every warp resident, fine balance)
 
 template <int VPT>
 struct VecT;

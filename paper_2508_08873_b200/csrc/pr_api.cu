@@ -3,6 +3,7 @@
 // except the O(N^2) scalar bound formulas of pr_bounds).
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -108,6 +109,25 @@ struct Lay {
 };
 static inline Lay lay(const Op &op, long ld) { return op.dim == 1 ? Lay{ld, 1} : Lay{1, ld}; }
 
+// PR_DEBUG_SYNC=1: synchronise and log after every orchestration stage.
+static bool debug_sync()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("PR_DEBUG_SYNC");
+        v = (e && *e && *e != '0') ? 1 : 0;
+    }
+    return v == 1;
+}
+
+static void stage(const char *what, cudaStream_t s)
+{
+    if (!debug_sync()) return;
+    cudaError_t e = cudaStreamSynchronize(s);
+    fprintf(stderr, "[pr] %s: %s\n", what, cudaGetErrorString(e));
+    fflush(stderr);
+}
+
 // -------------------------------------------------------------- QR driver
 // Iterated shifted CholeskyQR of nb blocks Q_b (rows x l), in place.
 static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double *Rtot, int *fail,
@@ -136,10 +156,13 @@ static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double 
         ++pass;
         XtY x{state, Q, xbs, L.rs, L.vs, l, Q, xbs, L.rs, L.vs, l, rows, nb, nchunk, chunk_rows, part};
         PR_CUDA(launch_xty(x, s));
+        stage("qr gram", s);
         PR_CUDA(cudaMemsetAsync(active, 0, sizeof(int), s));
         CholArgs c{part, nchunk, nb, l, rows, state, act, R, Rtot, active, fail};
         PR_CUDA(launch_chol(c, s));
+        stage("qr chol", s);
         PR_CUDA(launch_trsm(Q, xbs, L.rs, L.vs, rows, l, nb, R, act, s));
+        stage("qr trsm", s);
         PR_CUDA(cudaMemcpyAsync(h_active, active, sizeof(int), cudaMemcpyDeviceToHost, s));
         PR_CUDA(cudaStreamSynchronize(s));
         if (*h_active == 0) break;
@@ -392,25 +415,31 @@ pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local,
         st = propagate(op, PR_LINEAR, first_interval, m, (int)B, l, nullptr, nullptr, ld, Y, ld,
                        nullptr, 0, 1, seed, s);
         if (st != PR_OK) return bail(st);
+        stage("build step 1", s);
         // step 2: W = orth(Y)
         st = cholqr(op, Y, ld, nl, l, nullptr, G->fail, &G->qr_passes[0], s);
         if (st != PR_OK) return bail(st);
+        stage("build step 2", s);
         // step 3: Z = F'^* W
         st = propagate(op, PR_ADJOINT, first_interval, m, (int)B, l, nullptr, Y, ld, Z, ld,
                        nullptr, 0, 0, 0, s);
         if (st != PR_OK) return bail(st);
+        stage("build step 3", s);
         // step 4: V R_Z = Z
         st = cholqr(op, Z, ld, nl, l, Rtot, G->fail, &G->qr_passes[1], s);
         if (st != PR_OK) return bail(st);
+        stage("build step 4", s);
         // step 5: M = R_Z^T = Psi Sigma Phi^T
         e = launch_jacobi(Rtot, nl, l, Psi, G->sigma, Phi, G->fail + 1, s);
         if (e != cudaSuccess) return bail(cuda_fail(e, "jacobi"));
+        stage("build step 5 (jacobi)", s);
         // steps 5-6: psi = W Psi_k, phi = V Phi_k
         Lay L = lay(op, ld);
         const long xbs = (op.dim == 1) ? (long)l : (long)l * ld;
         e = launch_lift(Y, xbs, L.rs, L.vs, rows, l, Psi, l, k, nl, G->U, s);
         if (e == cudaSuccess) e = launch_lift(Z, xbs, L.rs, L.vs, rows, l, Phi, l, k, nl, G->V, s);
         if (e != cudaSuccess) return bail(cuda_fail(e, "lift"));
+        stage("build lift", s);
         // reduced sweep matrices C_q = Sigma_q V_q^T U_{q-1}, local q >= 1
         if (nl >= 2) {
             int nb = nl - 1;
