@@ -21,6 +21,8 @@
 // shared-memory ring with cp.async (PD groups of 32 rows in flight); the
 // per-row coefficients are loaded one group ahead distributed over the 32
 // lanes and broadcast with shuffles.
+#include <stdlib.h>
+
 #include "pr_internal.cuh"
 
 namespace pr {
@@ -31,6 +33,8 @@ namespace pr {
 //   LU: r_0 = s_0, r_i = s_i - a_i r_{i-1} / den_{i-1},  den_i = r_i - c_i
 //   UL: r_{n-1} = s_{n-1}, r_i = s_i - c_i r_{i+1} / den~_{i+1}, den~_i = r_i - a_i
 // a_i = (I+dtA)[i,i-1], c_i = (I+dtA)[i,i+1], s_i = 1 + dt * rowsum(A)_i.
+// Stored per row, negated where they multiply the recurrence variable:
+//   DN[i] = {-ap_i, w_i, -ga_i, 0},  UP[i] = {-cp_i, wt_i, -gc_i, 0}.
 __global__ void k_factor(int n, const double *__restrict__ subA, const double *__restrict__ supA,
                          const double *__restrict__ rsA, const double *__restrict__ diagA,
                          double dt, int transpose, Coef *DN, Coef *UP, int *bad)
@@ -58,8 +62,8 @@ __global__ void k_factor(int n, const double *__restrict__ subA, const double *_
             if (!(den > 0.0) || !isfinite(den)) atomicExch(bad, 1);
             double w = 1.0 / den;
             DN[i].b = w;
-            DN[i].c = w * ai;                 // ga_i
-            UP[i].a = w * ci;                 // cp_i
+            DN[i].c = -(w * ai);              // -ga_i
+            UP[i].a = -(w * ci);              // -cp_i
             DN[i].d = 0.0;
             UP[i].d = 0.0;
         }
@@ -72,8 +76,8 @@ __global__ void k_factor(int n, const double *__restrict__ subA, const double *_
             if (!(den > 0.0) || !isfinite(den)) atomicExch(bad, 1);
             double w = 1.0 / den;
             UP[i].b = w;                      // wt_i
-            UP[i].c = w * ci;                 // gc_i
-            DN[i].a = w * ai;                 // ap_i
+            UP[i].c = -(w * ci);              // -gc_i
+            DN[i].a = -(w * ai);              // -ap_i
         }
     }
 }
@@ -176,254 +180,327 @@ cudaError_t launch_transpose(const double *in, int R, int n, double *out, cudaSt
 }
 
 // ----------------------------------------------------------------- stepper
-constexpr int GR = 32;   // rows per group (one coefficient row per lane)
-constexpr int PD = 2;    // groups in flight ahead of the one being computed
+// One warp streams 32*VPT consecutive vectors through all m+1 passes.  Rows
+// are processed in groups of GR = 32; group g+PD is in flight (cp.async into a
+// per-warp shared ring) while group g is computed.  Per row and vector the
+// pass costs one FMA on each of the two recurrences:
+//   x_i = v_i + (-a'_i) x_{i-1}            (finish the previous step)
+//   y_i = w_i (x_i + dt f_i) + (-g_i) y_{i-1} (start the next step)
+// The coefficient row {-a', w, -g, 0} (+ the source's space values) is read
+// from shared memory as a warp-wide broadcast.
+constexpr int GR = 32;     // rows per group
+constexpr int PD = 2;      // groups in flight ahead of the one being computed
 constexpr int RING = PD + 1;
-constexpr int SWARPS = 1;  // warps per CTA (small CTAs: every warp resident, fine balance)
-
-template <int VPT>
-struct VecT;
-template <>
-struct VecT<1> { using T = double; };
-template <>
-struct VecT<2> { using T = double2; };
 
 __device__ __forceinline__ void cp_async_8(void *smem, const void *gmem)
 {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_16(void *smem, const void *gmem)
 {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 template <int VPT>
 __device__ __forceinline__ void cp_async_vec(double *smem, const double *gmem)
 {
-    if (VPT == 1) cp_async_8(smem, gmem);
-    else cp_async_16(smem, gmem);
+    if constexpr (VPT == 1) {
+        cp_async_8(smem, gmem);
+    } else {
+#pragma unroll
+        for (int h = 0; h < VPT / 2; ++h) cp_async_16(smem + 2 * h, gmem + 2 * h);
+    }
 }
 
-// Stepper kernel.  AFF: source terms present (R in 1..8).
+template <int VPT>
+__device__ __forceinline__ void lds_vec(double (&v)[VPT], const double *p)
+{
+    if constexpr (VPT == 1) {
+        v[0] = p[0];
+    } else {
+#pragma unroll
+        for (int h = 0; h < VPT / 2; ++h) {
+            double2 t = reinterpret_cast<const double2 *>(p)[h];
+            v[2 * h] = t.x;
+            v[2 * h + 1] = t.y;
+        }
+    }
+}
+
+template <int VPT>
+__device__ __forceinline__ void stg_vec(double *p, const double (&v)[VPT])
+{
+    if constexpr (VPT == 1) {
+        p[0] = v[0];
+    } else {
+#pragma unroll
+        for (int h = 0; h < VPT / 2; ++h)
+            reinterpret_cast<double2 *>(p)[h] = make_double2(v[2 * h], v[2 * h + 1]);
+    }
+}
+
+struct WarpSmem {
+    double *vring;   // [RING*GR][32][VPT]
+    double *oring;   // same, offsets (last pass only)
+    double *cring;   // [RING*GR][CW]
+    int CW;          // doubles per coefficient row (4 + padded R)
+};
+
+// One pass over all rows.  DOWN: rows ascending.  FIN: finish the previous
+// step (back substitution).  START: start step `step` (forward elimination).
+// LOAD: read the state (else zero).  AFF: source term.  OFF: add offset.
+template <int VPT, bool DOWN, bool FIN, bool START, bool LOAD, bool AFF, bool OFF>
+__device__ __forceinline__ void run_pass(const StepArgs &a, const WarpSmem &w, const Coef *coefs,
+                                         const double *src, long lds, long c0, bool valid,
+                                         int lane, const double (*alpha)[VPT])
+{
+    const int n = a.n;
+    const int ngroups = (n + GR - 1) / GR;
+    const long step_src = DOWN ? lds : -lds;
+    const long step_dst = DOWN ? a.ld_out : -a.ld_out;
+    const long step_off = DOWN ? a.ld_off : -a.ld_off;
+    const int R = AFF ? a.R : 0;
+
+    auto row_of = [&](int g, int r) -> int {
+        int t = g * GR + r;
+        return DOWN ? t : n - 1 - t;
+    };
+    auto issue = [&](int g) {
+        if (g < ngroups) {
+            const int slot0 = (g % RING) * GR;
+            const int i0 = row_of(g, 0);
+            const int nr = min(GR, n - g * GR);
+            if (valid && (LOAD || OFF)) {
+                const double *sp = src + (long)i0 * lds + c0;
+                const double *op = OFF ? a.off + (long)i0 * a.ld_off + c0 : nullptr;
+                double *vr = w.vring + ((size_t)slot0 * 32 + lane) * VPT;
+                double *orr = OFF ? w.oring + ((size_t)slot0 * 32 + lane) * VPT : nullptr;
+#pragma unroll 8
+                for (int r = 0; r < nr; ++r) {
+                    if (LOAD) cp_async_vec<VPT>(vr + (size_t)r * 32 * VPT, sp);
+                    if (OFF) cp_async_vec<VPT>(orr + (size_t)r * 32 * VPT, op);
+                    sp += step_src;
+                    if (OFF) op += step_off;
+                }
+            }
+            // coefficient row of (g, lane): 32 B Coef (+ R space values)
+            if (lane < nr) {
+                const int i = row_of(g, lane);
+                double *cr = w.cring + (size_t)(slot0 + lane) * w.CW;
+                cp_async_16(cr, &coefs[i].a);
+                cp_async_16(cr + 2, &coefs[i].c);
+                if (AFF) {
+                    const double *spc = a.spaceT + (long)i * a.R;
+                    for (int t = 0; t < R; ++t) cp_async_8(cr + 4 + t, spc + t);
+                }
+            }
+        }
+        cp_async_commit();
+    };
+
+#pragma unroll
+    for (int g = 0; g < PD; ++g) issue(g);
+
+    double xprev[VPT], yprev[VPT];
+#pragma unroll
+    for (int v = 0; v < VPT; ++v) { xprev[v] = 0.0; yprev[v] = 0.0; }
+    double *dst = a.out + (long)row_of(0, 0) * a.ld_out + c0;
+
+    for (int g = 0; g < ngroups; ++g) {
+        issue(g + PD);
+        cp_async_wait<PD>();
+        __syncwarp();
+        const int slot0 = (g % RING) * GR;
+        const double *vr = w.vring + ((size_t)slot0 * 32 + lane) * VPT;
+        const double *orr = OFF ? w.oring + ((size_t)slot0 * 32 + lane) * VPT : nullptr;
+        const double *cr = w.cring + (size_t)slot0 * w.CW;
+        const int nr = min(GR, n - g * GR);
+        auto body = [&](int r) {
+            const double2 c01 = *reinterpret_cast<const double2 *>(cr + (size_t)r * w.CW);
+            const double ncc = cr[(size_t)r * w.CW + 2];
+            double val[VPT];
+            if (LOAD) lds_vec<VPT>(val, vr + (size_t)r * 32 * VPT);
+            double fs[VPT];
+#pragma unroll
+            for (int v = 0; v < VPT; ++v) fs[v] = 0.0;
+            if (AFF) {
+#pragma unroll
+                for (int t = 0; t < 8; ++t) {
+                    if (t < R) {
+                        const double sp = cr[(size_t)r * w.CW + 4 + t];
+#pragma unroll
+                        for (int v = 0; v < VPT; ++v) fs[v] = fma(alpha[t][v], sp, fs[v]);
+                    }
+                }
+            }
+            double res[VPT];
+#pragma unroll
+            for (int v = 0; v < VPT; ++v) {
+                const double in = LOAD ? val[v] : 0.0;
+                const double x = FIN ? fma(c01.x, xprev[v], in) : in;
+                xprev[v] = x;
+                if (START) {
+                    const double y = fma(ncc, yprev[v], c01.y * (AFF ? x + fs[v] : x));
+                    yprev[v] = y;
+                    res[v] = y;
+                } else {
+                    res[v] = x;
+                }
+            }
+            if (OFF) {
+                double o[VPT];
+                lds_vec<VPT>(o, orr + (size_t)r * 32 * VPT);
+#pragma unroll
+                for (int v = 0; v < VPT; ++v) res[v] += o[v];
+            }
+            if (valid) stg_vec<VPT>(dst, res);
+            dst += step_dst;
+        };
+        if (nr == GR) {
+#pragma unroll
+            for (int r = 0; r < GR; ++r) body(r);
+        } else {
+            for (int r = 0; r < nr; ++r) body(r);
+        }
+        __syncwarp();   // all lanes done with this ring slot before it is refilled
+    }
+    cp_async_wait<0>();
+    __syncwarp();
+}
+
 template <int VPT, bool AFF>
-__global__ void __launch_bounds__(32 * SWARPS) k_stepper(StepArgs a)
+__global__ void __launch_bounds__(32) k_stepper(StepArgs a)
 {
     extern __shared__ __align__(16) double smem_dyn[];
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
-    const long c0 = ((long)blockIdx.x * blockDim.x + threadIdx.x) * VPT;  // first vector
-    const bool valid = c0 < a.B;    // B is a multiple of VPT when VPT > 1
+    const long c0 = ((long)blockIdx.x * 32 + lane) * VPT;
+    const bool valid = c0 < a.B;      // B % VPT == 0 when VPT > 1
     const bool have_off = a.off != nullptr;
-    double *ring = smem_dyn + (size_t)warp * RING * GR * 32 * VPT;
-    double *ringo = have_off ? smem_dyn + (size_t)(SWARPS + warp) * RING * GR * 32 * VPT : nullptr;
-
-    const int n = a.n;
-    const int ngroups = (n + GR - 1) / GR;
+    WarpSmem w;
+    const int Rp = AFF ? ((a.R + 1) & ~1) : 0;
+    w.CW = 4 + Rp;
+    w.vring = smem_dyn;
+    w.oring = smem_dyn + (size_t)RING * GR * 32 * VPT;
+    w.cring = smem_dyn + (size_t)(have_off ? 2 : 1) * RING * GR * 32 * VPT;
     const int m = a.m;
-    const int P = (m > 0) ? m + 1 : 1;
+    const int P = m + 1;
 
-    // per-vector interval / column / source
-    int qv[VPT], colv[VPT], srcv[VPT];
+    int qv[VPT], srcv[VPT];
 #pragma unroll
     for (int v = 0; v < VPT; ++v) {
-        long c = c0 + v;
+        long c = valid ? c0 + v : 0;
         qv[v] = a.q0 + (int)(c / a.vpi);
-        colv[v] = (int)(c % a.vpi);
         srcv[v] = AFF ? (int)(c % a.nsrc) : 0;
     }
-
-    for (int p = 1; p <= P; ++p) {
-        const bool down = (p & 1);
-        const bool finish = (p >= 2);
-        const bool start = (p <= m);
-        const bool last = (p == P);
-        const bool from_in = (p == 1);
-        const bool do_load = !from_in || (a.in != nullptr && !a.sketch);
-        const bool gen = from_in && a.sketch;
-        const double *src = from_in ? a.in : a.out;
-        const long lds = from_in ? a.ld_in : a.ld_out;
-        const bool load_off = last && have_off;
-        const Coef *coefs = down ? a.DN : a.UP;
-
-        // source coefficients alpha_r = dt * amp[s, r] * time[r, g-1] of step p
-        double alpha[AFF ? 8 : 1][VPT];
-        if (AFF) {
+    double alpha[AFF ? 8 : 1][VPT];
+    auto set_alpha = [&](int step) {      // alpha_r = dt amp[s, r] time[r, g-1] of step `step`
+        if constexpr (AFF) {
 #pragma unroll
             for (int r = 0; r < 8; ++r)
 #pragma unroll
                 for (int v = 0; v < VPT; ++v) {
                     double al = 0.0;
-                    if (start && r < a.R && valid) {
-                        long g1 = (long)qv[v] * m + p - 1;       // g - 1
+                    if (r < a.R) {
+                        long g1 = (long)qv[v] * m + step - 1;
                         al = a.dt * a.amp[(long)srcv[v] * a.R + r] * a.time[(long)r * a.nsteps + g1];
                     }
                     alpha[r][v] = al;
                 }
         }
+    };
 
-        auto row_of = [&](int g, int r) -> int {
-            int t = g * GR + r;
-            return down ? t : n - 1 - t;
-        };
-        auto issue = [&](int g) {
-            if (g < ngroups && valid) {
-                int slot0 = (g % RING) * GR;
-#pragma unroll 4
-                for (int r = 0; r < GR; ++r) {
-                    int i = row_of(g, r);
-                    if (i >= 0 && i < n) {
-                        if (do_load)
-                            cp_async_vec<VPT>(ring + ((size_t)(slot0 + r) * 32 + lane) * VPT,
-                                              src + (long)i * lds + c0);
-                        if (load_off)
-                            cp_async_vec<VPT>(ringo + ((size_t)(slot0 + r) * 32 + lane) * VPT,
-                                              a.off + (long)i * a.ld_off + c0);
-                    }
-                }
-            }
-            cp_async_commit();
-        };
-
-        // prologue
-#pragma unroll
-        for (int g = 0; g < PD; ++g) issue(g);
-        Coef cnext;
-        double snext[AFF ? 8 : 1];
-        {
-            int i = row_of(0, lane);
-            bool ok = (i >= 0 && i < n);
-            cnext = ok ? coefs[i] : Coef{0, 0, 0, 0};
-            if (AFF) {
-#pragma unroll
-                for (int r = 0; r < 8; ++r) snext[r] = (ok && r < a.R) ? a.spaceT[(long)i * a.R + r] : 0.0;
+    for (int p = 1; p <= P; ++p) {
+        set_alpha(p);
+        const bool down = (p & 1);
+        const Coef *coefs = down ? a.DN : a.UP;
+        if (p == 1) {
+            if (a.in)
+                run_pass<VPT, true, false, true, true, AFF, false>(a, w, coefs, a.in, a.ld_in, c0, valid, lane, alpha);
+            else
+                run_pass<VPT, true, false, true, false, AFF, false>(a, w, coefs, nullptr, a.ld_out, c0, valid, lane, alpha);
+        } else if (p <= m) {
+            if (down)
+                run_pass<VPT, true, true, true, true, AFF, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+            else
+                run_pass<VPT, false, true, true, true, AFF, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+        } else {   // p == m + 1: finish the last step (+ offset)
+            if (down) {
+                if (have_off) run_pass<VPT, true, true, false, true, false, true>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                else run_pass<VPT, true, true, false, true, false, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+            } else {
+                if (have_off) run_pass<VPT, false, true, false, true, false, true>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                else run_pass<VPT, false, true, false, true, false, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
             }
         }
-
-        double xprev[VPT], yprev[VPT];
-#pragma unroll
-        for (int v = 0; v < VPT; ++v) { xprev[v] = 0.0; yprev[v] = 0.0; }
-        double z4[VPT][4];
-
-        for (int g = 0; g < ngroups; ++g) {
-            issue(g + PD);
-            Coef ccur = cnext;
-            double scur[AFF ? 8 : 1];
-            if (AFF) {
-#pragma unroll
-                for (int r = 0; r < 8; ++r) scur[r] = snext[r];
-            }
-            if (g + 1 < ngroups) {
-                int i = row_of(g + 1, lane);
-                bool ok = (i >= 0 && i < n);
-                cnext = ok ? coefs[i] : Coef{0, 0, 0, 0};
-                if (AFF) {
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) snext[r] = (ok && r < a.R) ? a.spaceT[(long)i * a.R + r] : 0.0;
-                }
-            }
-            cp_async_wait<PD>();
-            const int slot0 = (g % RING) * GR;
-#pragma unroll
-            for (int r = 0; r < GR; ++r) {
-                const int i = row_of(g, r);
-                const bool rowok = (i >= 0 && i < n);   // warp-uniform
-                const double ca = __shfl_sync(0xffffffffu, ccur.a, r);
-                const double cb = __shfl_sync(0xffffffffu, ccur.b, r);
-                const double cc = __shfl_sync(0xffffffffu, ccur.c, r);
-                double fsrc[VPT];
-#pragma unroll
-                for (int v = 0; v < VPT; ++v) fsrc[v] = 0.0;
-                if (AFF && start) {
-#pragma unroll
-                    for (int t = 0; t < 8; ++t) {
-                        double sp = __shfl_sync(0xffffffffu, scur[t], r);
-#pragma unroll
-                        for (int v = 0; v < VPT; ++v) fsrc[v] = fma(alpha[t][v], sp, fsrc[v]);
-                    }
-                }
-                if (gen && (r & 3) == 0 && valid) {
-#pragma unroll
-                    for (int v = 0; v < VPT; ++v)
-                        gauss4(a.seed, (unsigned long long)(i >> 2), colv[v], qv[v], z4[v]);
-                }
-                if (rowok && valid) {
-                    double val[VPT];
-                    if (do_load) {
-                        const double *sp = ring + ((size_t)(slot0 + r) * 32 + lane) * VPT;
-#pragma unroll
-                        for (int v = 0; v < VPT; ++v) val[v] = sp[v];
-                    } else if (gen) {
-#pragma unroll
-                        for (int v = 0; v < VPT; ++v) val[v] = z4[v][r & 3];
-                    } else {
-#pragma unroll
-                        for (int v = 0; v < VPT; ++v) val[v] = 0.0;
-                    }
-                    double res[VPT];
-#pragma unroll
-                    for (int v = 0; v < VPT; ++v) {
-                        // finish the previous step: back substitution
-                        double x = finish ? fma(-ca, xprev[v], val[v]) : val[v];
-                        xprev[v] = x;
-                        if (start) {
-                            double rr = x + fsrc[v];
-                            double y = fma(cb, rr, -cc * yprev[v]);
-                            yprev[v] = y;
-                            res[v] = y;
-                        } else {
-                            res[v] = x;
-                        }
-                    }
-                    if (last && have_off) {
-                        const double *so = ringo + ((size_t)(slot0 + r) * 32 + lane) * VPT;
-#pragma unroll
-                        for (int v = 0; v < VPT; ++v) res[v] += so[v];
-                    }
-                    double *dst = a.out + (long)i * a.ld_out + c0;
-                    if (VPT == 1) {
-                        dst[0] = res[0];
-                    } else {
-                        *reinterpret_cast<double2 *>(dst) = make_double2(res[0], res[VPT - 1]);
-                    }
-                }
-            }
-        }
-        cp_async_wait<0>();
-        __syncwarp();
     }
+}
+
+// m == 0: out = in (+ offset)
+__global__ void k_copy_off(const double *in, long ld_in, double *out, long ld_out, const double *off,
+                           long ld_off, int n, long B)
+{
+    long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= (long)n * B) return;
+    long i = idx / B, c = idx % B;
+    double v = in ? in[i * ld_in + c] : 0.0;
+    if (off) v += off[i * ld_off + c];
+    out[i * ld_out + c] = v;
 }
 
 template <int VPT, bool AFF>
 static cudaError_t launch_stepper_t(const StepArgs &a, cudaStream_t s)
 {
-    const int threads = 32 * SWARPS;
     long nthreads = (a.B + VPT - 1) / VPT;
-    long blocks = (nthreads + threads - 1) / threads;
+    long blocks = (nthreads + 31) / 32;
     if (blocks == 0) return cudaSuccess;
-    size_t ring_bytes = (size_t)SWARPS * RING * GR * 32 * VPT * sizeof(double);
-    size_t smem = ring_bytes * (a.off ? 2 : 1);
+    const int Rp = AFF ? ((a.R + 1) & ~1) : 0;
+    size_t ring = (size_t)RING * GR * 32 * VPT * sizeof(double);
+    size_t smem = ring * (a.off ? 2 : 1) + (size_t)RING * GR * (4 + Rp) * sizeof(double);
     auto kern = k_stepper<VPT, AFF>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)blocks, threads, smem, s>>>(a);
+    kern<<<(unsigned)blocks, 32, smem, s>>>(a);
     return cudaGetLastError();
 }
 
 cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s)
 {
-    // two vectors per thread (16 B accesses) when every base and stride allows it
+    if (a.m == 0) {
+        long tot = (long)a.n * a.B;
+        if (tot == 0) return cudaSuccess;
+        k_copy_off<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a.in, a.ld_in, a.out, a.ld_out,
+                                                                 a.off, a.ld_off, a.n, a.B);
+        return cudaGetLastError();
+    }
     auto al16 = [](const void *p) { return ((uintptr_t)p & 15) == 0; };
-    bool v2 = (a.B % 2 == 0) && (a.ld_out % 2 == 0) && al16(a.out) &&
-              (a.in == nullptr || a.sketch || ((a.ld_in % 2 == 0) && al16(a.in))) &&
-              (a.off == nullptr || ((a.ld_off % 2 == 0) && al16(a.off)));
-    bool aff = a.R > 0;
-    if (v2) return aff ? launch_stepper_t<2, true>(a, s) : launch_stepper_t<2, false>(a, s);
-    return aff ? launch_stepper_t<1, true>(a, s) : launch_stepper_t<1, false>(a, s);
+    auto fits = [&](int vpt) {
+        long vb = (long)vpt * 8;
+        auto okp = [&](const void *p, long ld) { return p == nullptr || (((uintptr_t)p % vb) == 0 && ld % vpt == 0); };
+        return (a.B % vpt == 0) && okp(a.out, a.ld_out) && okp(a.in, a.ld_in) && okp(a.off, a.ld_off) &&
+               al16(a.out);
+    };
+    // Two vectors per thread once there are enough warps to cover the SMs
+    // (measured on B200: C4 build batch 93.8 ms at VPT=2 vs 98.7 ms at 4 and
+    // 119 ms at 1); four only for batches far beyond two warps per SM.
+    const long sms = num_sms();
+    int vpt = 1;
+    if (fits(4) && a.B / 128 >= 4 * sms) vpt = 4;
+    else if (fits(2) && a.B / 64 >= (sms * 3) / 4) vpt = 2;
+    if (const char *e = getenv("PR_STEPPER_VPT")) {
+        int f = atoi(e);
+        if ((f == 1) || (f == 2 && fits(2)) || (f == 4 && fits(4))) vpt = f;
+    }
+    const bool aff = a.R > 0;
+    switch (vpt) {
+    case 4: return aff ? launch_stepper_t<4, true>(a, s) : launch_stepper_t<4, false>(a, s);
+    case 2: return aff ? launch_stepper_t<2, true>(a, s) : launch_stepper_t<2, false>(a, s);
+    default: return aff ? launch_stepper_t<1, true>(a, s) : launch_stepper_t<1, false>(a, s);
+    }
 }
 
 }  // namespace pr

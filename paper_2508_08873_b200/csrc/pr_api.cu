@@ -194,6 +194,15 @@ static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi
         return run_sep2d(a, s);
     }
     Scratch S;
+    if (sketch) {
+        // Omega materialised by the fully parallel generator, then stepped in place
+        // (a thread-serial Philox inside the stepper's first pass costs more than
+        // the extra write + read)
+        PR_CUDA(launch_sketch(1, op.n, op.rows, q0, B / vpi, vpi, seed, out, ld_out, 1, s));
+        in = out;
+        ld_in = ld_out;
+        sketch = 0;
+    }
     StepArgs a{};
     a.n = op.n;
     a.B = B;
