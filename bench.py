@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark of the spectral-coarse-solver Parareal hot path (arXiv 2508.08873).
+
+One step = the whole hot path on one batch of synthetic input:
+    pr_build_coarse  (rSVD of F_n' on every interval: 2*l batched fine solves
+                      per interval + CholeskyQR + Jacobi SVD + lift)
+  + pr_parareal      (offsets b_n, initialisation, K iterations of batched fine
+                      solves + reduced coarse sweep + update norms)
+Metric (BASELINE.json): fine-solve DOF-steps/s of the step, plus the rSVD build
+and Parareal wall times.  Default workload: C4 (BASELINE.json configs[3], the
+largest 1D configuration; DESIGN.md "Benchmark workload" says why).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+Multi-GPU (torchrun, one rank per GPU): the build is sharded by intervals
+(no communication), the factors are all-gathered once, and Parareal is
+sharded by source terms (C4's 64 sources share G').
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "fine-solve DOF-steps/s (batched implicit Euler) + rSVD build & Parareal wall time"
+L2_BYTES = 126 * 2 ** 20
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _ncu_traffic(cfg_name):
+    """dram bytes per stepper launch from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "stepper_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(cfg_name)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------- workload
+class Workload:
+    """Device-resident inputs of one rank and the step function."""
+
+    def __init__(self, cfg, rank: int, world: int, dev):
+        import torch
+        from paper_2508_08873_b200 import Operator, SourceTerm
+        from workloads import generators as G
+        self.cfg, self.rank, self.world, self.dev = cfg, rank, world, dev
+        # interval shard (build) and source shard (Parareal)
+        self.q0, self.nq = _shard(cfg.N, rank, world)
+        self.s0, self.ns = _shard(cfg.nsrc, rank, world)
+        assert cfg.dim == 1, "bench.py drives the 1D configs (C1, C2, C4)"
+        self.host = dict(op=G.operator_1d(cfg), sums=G.operator_1d_sums(cfg))
+        space, time_, amp = G.source_1d(cfg)
+        self.host.update(space=space, time=time_, amp=amp[self.s0:self.s0 + self.ns])
+        u0 = G.initial_value(cfg)
+        self.host["u0"] = np.ascontiguousarray(np.stack([u0] * self.ns).T)     # (n, ns)
+        rs, cs = self.host["sums"]
+        self.op = Operator.tridiag(*self.host["op"], cfg.dt, rowsum=rs, colsum=cs)
+        self.src = SourceTerm.sep1d(space, time_, self.host["amp"])
+        self.u0 = torch.tensor(self.host["u0"], dtype=torch.float64, device=dev)
+        self.U = torch.empty((cfg.n, (cfg.N + 1) * self.ns), dtype=torch.float64, device=dev)
+
+    def dof_steps(self) -> float:
+        c = self.cfg
+        build = self.nq * 2 * c.l * c.n * c.m
+        par = (c.K + 1) * c.N * self.ns * c.n * c.m
+        return float(build + par)
+
+    def step(self, events=None):
+        """rSVD build (own intervals) [+ all-gather] + Parareal (own sources)."""
+        from paper_2508_08873_b200 import Coarse, parareal
+        c = self.cfg
+        G = Coarse.build(self.op, c.N, c.m, c.k, c.p, c.seed_omega, first_interval=self.q0,
+                         n_local=self.nq)
+        if self.world > 1:
+            G = _allgather_coarse(G, self)
+        if events is not None:
+            events.append(_event())
+        upd, bn = parareal(G, self.op, self.u0, self.src, c.K, self.U, nsrc=self.ns)
+        G.close()
+        return upd, bn
+
+
+def _shard(total: int, rank: int, world: int):
+    base, rem = divmod(total, world)
+    start = rank * base + min(rank, rem)
+    return start, base + (1 if rank < rem else 0)
+
+
+def _event():
+    import torch
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+def _allgather_coarse(G, wl):
+    raise NotImplementedError("multi-GPU factor all-gather is not built yet")
+
+
+# ----------------------------------------------------------- CPU oracle leg
+def oracle_sample(cfg):
+    """A bounded sample of the same workload on the host cores, through the
+    oracle as it stands: the rSVD of one interval (steps 1-6) and (K+1) fine
+    solves of that interval for every source (the offset b plus the K
+    Parareal fine solves).  Returns (dof_steps, seconds)."""
+    from oracle.fine import fine, make_op
+    from oracle.rsvd import rsvd_interval
+    from workloads import generators as G
+    op = make_op(cfg)
+    src = G.source_1d(cfg)
+    u0 = np.stack([G.initial_value(cfg)] * cfg.nsrc)
+    t0 = time.perf_counter()
+    rsvd_interval(op, 1, cfg.k, cfg.p, cfg.seed_omega)
+    x = np.zeros_like(u0)
+    for _ in range(cfg.K + 1):
+        x = fine(op, 1, u0, "affine", src, np.arange(cfg.nsrc))
+    dt = time.perf_counter() - t0
+    dof = 2 * cfg.l * cfg.n * cfg.m + (cfg.K + 1) * cfg.nsrc * cfg.n * cfg.m
+    return float(dof), dt
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    from workloads.configs import get
+    cfg = get(args.config)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": cfg.name, "dim": cfg.dim, "n": cfg.n, "N": cfg.N, "m": cfg.m, "k": cfg.k,
+              "p": cfg.p, "K": cfg.K, "nsrc": cfg.nsrc, "T": cfg.T,
+              "l2": "inputs larger than L2: %.2f GB state per stepper phase vs 126 MB L2"
+                    % (cfg.n * cfg.N * max(cfg.l, cfg.nsrc) * 8 / 1e9),
+              "parallelism": f"intervals+sources sharded over {args.gpus} GPU(s)"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from oracle import _clib
+        _clib.build()
+        for _ in range(args.warmup):
+            oracle_sample(cfg)
+        vals = []
+        for _ in range(args.steps):
+            dof, sec = oracle_sample(cfg)
+            vals.append((dof, sec))
+        dof = sum(v[0] for v in vals)
+        sec = sum(v[1] for v in vals)
+        value = dof / sec
+        sample = (f"rSVD of interval 1 + {cfg.K + 1} fine solves of interval 1 x {cfg.nsrc} sources "
+                  f"({vals[0][0]:.3g} DOF-steps per step)")
+        line = {"metric": METRIC, "value": value, "unit": "DOF-steps/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded generators, workloads/)", "config": config,
+                "impl": "reference",
+                "cpu_baseline": {"value": value, "unit": "DOF-steps/s", "cores": _cores(),
+                                 "kind": "oracle", "sample": sample},
+                "e2e": {"value": value, "unit": "DOF-steps/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2508_08873_b200 import counters, profile
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    wl = Workload(cfg, rank, world, dev)
+    for _ in range(args.warmup):
+        wl.step()
+    barrier()
+
+    # ---------------------------------------------------- timed device run
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    counters(reset=True)
+    profile(True)
+    barrier()
+    ev = [_event()]
+    mid = []
+    for _ in range(args.steps):
+        wl.step(events=mid)
+        ev.append(_event())
+    barrier()
+    profile(False)
+    clocks = sampler.stop()
+    total_ms = ev[0].elapsed_time(ev[-1])
+    build_ms = [ev[i].elapsed_time(mid[i]) for i in range(args.steps)]
+    par_ms = [mid[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    ctr = counters(reset=True)
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    dof_total = wl.dof_steps() * world if world == 1 else _sum_dof(wl, world)
+    value = dof_total / (ms_per_step / 1e3)
+
+    # ------------------------------------------------ roofline of K1 stepper
+    peak, peak_kind = _peaks()
+    st_ms = ctr["stepper_ms"] / max(ctr["stepper_launches"], 1)
+    st_dof = ctr["stepper_dof_steps"] / max(ctr["stepper_launches"], 1)
+    achieved = 16.0 * st_dof / (st_ms / 1e3) / 1e9 if st_ms > 0 else None
+    traffic = _ncu_traffic(cfg.name)
+    roofline = {"kernel": "k_stepper (K1, batched tridiagonal implicit Euler)", "bound": "hbm",
+                "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "algorithmic_bytes_per_launch": 16.0 * st_dof,
+                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+                "launches_timed": ctr["stepper_launches"],
+                "share_of_step": ctr["stepper_ms"] / total_ms if total_ms > 0 else None}
+
+    # ------------------------------------------------------------- e2e run
+    e2e = None
+    if not args.no_e2e:
+        e2e = _e2e(wl, args.steps, barrier, world)
+
+    # --------------------------------------------------------- CPU baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import _clib
+        _clib.build()
+        dof, sec = oracle_sample(cfg)
+        cpu = {"value": dof / sec, "unit": "DOF-steps/s", "cores": _cores(), "kind": "oracle",
+               "sample": f"rSVD of interval 1 + {cfg.K + 1} fine solves of interval 1 x "
+                         f"{cfg.nsrc} sources ({dof:.3g} DOF-steps, {sec:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "DOF-steps/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (seeded generators, workloads/)",
+                "config": config,
+                "build_ms": statistics.median(build_ms), "parareal_ms": statistics.median(par_ms),
+                "dof_steps_per_step": dof_total,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": ctr["kernel_launches"], "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def _sum_dof(wl, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([wl.dof_steps()], dtype=torch.float64, device=wl.dev)
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def _e2e(wl, steps, barrier, world):
+    """Same metric through the public API from HOST buffers: per step the
+    operator arrays, u0 and the source factors go host->device from pinned
+    memory, and the Parareal solution u^K (all interval boundaries) and the
+    update norms come back device->host."""
+    import torch
+    from paper_2508_08873_b200 import Coarse, Operator, SourceTerm, parareal
+    c = wl.cfg
+    pin = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
+           for k, v in (("space", wl.host["space"]), ("time", wl.host["time"]),
+                        ("amp", wl.host["amp"]), ("u0", wl.host["u0"]))}
+    out_host = torch.empty(tuple(wl.U.shape), dtype=torch.float64).pin_memory()
+    h2d = sum(t.numel() * 8 for t in pin.values()) + 5 * c.n * 8
+    d2h = out_host.numel() * 8
+    barrier()
+    e0 = _event()
+    for _ in range(steps):
+        rs, cs = wl.host["sums"]
+        op = Operator.tridiag(*wl.host["op"], c.dt, rowsum=rs, colsum=cs)      # host arrays
+        dv = {k: v.to(wl.dev, non_blocking=True) for k, v in pin.items()}
+        src = SourceTerm(1, dv["time"].shape[0], dv["amp"].shape[0], dv["time"].shape[1],
+                         {"space": dv["space"], "time": dv["time"], "amp": dv["amp"]})
+        G = Coarse.build(op, c.N, c.m, c.k, c.p, c.seed_omega, first_interval=wl.q0,
+                         n_local=wl.nq)
+        if world > 1:
+            G = _allgather_coarse(G, wl)
+        upd, bn = parareal(G, op, dv["u0"], src, c.K, wl.U, nsrc=wl.ns)
+        out_host.copy_(wl.U, non_blocking=True)
+        G.close()
+        op.close()
+    e1 = _event()
+    barrier()
+    ms = e0.elapsed_time(e1) / steps
+    t = torch.tensor([ms], dtype=torch.float64, device=wl.dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    dof = wl.dof_steps() if world == 1 else _sum_dof(wl, world)
+    return {"value": dof / (ms / 1e3), "unit": "DOF-steps/s", "ms_per_step": ms,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+
+if __name__ == "__main__":
+    main()

@@ -63,6 +63,16 @@ typedef enum {
 const char *pr_last_error(void);
 int pr_version(void);
 
+/* Instrumentation.  pr_profile(1) brackets every stepper launch (K1) with CUDA
+ * events on its stream.  pr_counters (host; synchronises on the recorded
+ * events) returns the number of kernels the library has launched, and the
+ * number, summed device time (ms) and DOF-steps (n * B * m) of the timed
+ * stepper launches since the last reset; reset != 0 clears them afterwards.
+ * All output pointers may be NULL. */
+pr_status pr_profile(int enable);
+pr_status pr_counters(int reset, long *kernel_launches, long *stepper_launches, double *stepper_ms,
+                      double *stepper_dof_steps);
+
 typedef struct pr_op_s *pr_op;
 typedef struct pr_coarse_s *pr_coarse;
 

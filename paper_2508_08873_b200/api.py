@@ -213,3 +213,18 @@ def bounds(delta: float, eps: float, bnorm: np.ndarray, upd: np.ndarray):
                             _hptr(apost) if K > 0 else None, _hptr(sup) if K > 0 else None),
           "pr_bounds")
     return dict(apriori=apri, apost=apost[:K], apost_sup=sup[:K])
+
+
+def profile(enable: bool = True):
+    check(L.lib().pr_profile(1 if enable else 0), "pr_profile")
+
+
+def counters(reset: bool = False) -> dict:
+    """Kernel launches of the library, and stepper launches / device ms /
+    DOF-steps timed with CUDA events while profiling was enabled."""
+    kl, sl = ctypes.c_long(), ctypes.c_long()
+    ms, dof = ctypes.c_double(), ctypes.c_double()
+    check(L.lib().pr_counters(1 if reset else 0, ctypes.byref(kl), ctypes.byref(sl),
+                              ctypes.byref(ms), ctypes.byref(dof)), "pr_counters")
+    return dict(kernel_launches=kl.value, stepper_launches=sl.value, stepper_ms=ms.value,
+                stepper_dof_steps=dof.value)

@@ -37,11 +37,12 @@ __global__ void __launch_bounds__(XT_THREADS) k_xty(XtY p)
     extern __shared__ __align__(16) double sm[];
     const int b = blockIdx.y, t = blockIdx.x;
     if (p.skip && p.skip[b] == 2) return;
-    const int A4 = (p.a + 3) & ~3, C4 = (p.c + 3) & ~3;
+    const int A4 = (p.a + 3) & ~3, C4 = (p.c + p.c2 + 3) & ~3;
     double *Xs = sm;                     // [XT_TR][A4]
     double *Ys = sm + XT_TR * A4;        // [XT_TR][C4]
+    const int ctot = p.c + p.c2;
     const bool same = (p.X == p.Y) && (p.xbs == p.ybs) && (p.xrs == p.yrs) && (p.xcs == p.ycs) &&
-                      (p.a == p.c);
+                      (p.a == p.c) && p.c2 == 0;
     if (same) Ys = Xs;
     const int nbi = A4 / 4, nbj = C4 / 4;
     const int nblk = nbi * nbj;
@@ -56,6 +57,7 @@ __global__ void __launch_bounds__(XT_THREADS) k_xty(XtY p)
     if (r1 > p.rows) r1 = p.rows;
     const double *Xb = p.X + (long)b * p.xbs;
     const double *Yb = p.Y + (long)b * p.ybs;
+    const double *Y2b = p.Y2 ? p.Y2 + (long)b * p.ybs : nullptr;
 
     for (long rt = r0; rt < r1; rt += XT_TR) {
         __syncthreads();
@@ -73,7 +75,27 @@ __global__ void __launch_bounds__(XT_THREADS) k_xty(XtY p)
             }
         };
         load(Xb, p.xrs, p.xcs, p.a, A4, Xs);
-        if (!same) load(Yb, p.yrs, p.ycs, p.c, C4, Ys);
+        if (!same) {
+            if (!Y2b) {
+                load(Yb, p.yrs, p.ycs, p.c, C4, Ys);
+            } else {
+                // columns [0, c) from Y, [c, c + c2) from Y2 (same strides)
+                const int tot = XT_TR * C4;
+                for (int idx = threadIdx.x; idx < tot; idx += XT_THREADS) {
+                    int r, j;
+                    if (p.ycs == 1) { r = idx / C4; j = idx % C4; }
+                    else { j = idx / XT_TR; r = idx % XT_TR; }
+                    long row = rt + r;
+                    double v = 0.0;
+                    if (row < r1 && j < ctot) {
+                        const double *src = (j < p.c) ? Yb : Y2b;
+                        int jj = (j < p.c) ? j : j - p.c;
+                        v = src[row * p.yrs + (long)jj * p.ycs];
+                    }
+                    Ys[r * C4 + j] = v;
+                }
+            }
+        }
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < BPT; ++q) {
@@ -95,7 +117,7 @@ __global__ void __launch_bounds__(XT_THREADS) k_xty(XtY p)
             }
         }
     }
-    double *out = p.part + ((long)b * p.nchunk + t) * p.a * p.c;
+    double *out = p.part + ((long)b * p.nchunk + t) * p.a * ctot;
 #pragma unroll
     for (int q = 0; q < BPT; ++q) {
         int blk = threadIdx.x + q * XT_THREADS;
@@ -106,7 +128,7 @@ __global__ void __launch_bounds__(XT_THREADS) k_xty(XtY p)
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
                     int i = 4 * bi + u, j = 4 * bj + v;
-                    if (i < p.a && j < p.c) out[(long)i * p.c + j] = acc[q][u * 4 + v];
+                    if (i < p.a && j < ctot) out[(long)i * ctot + j] = acc[q][u * 4 + v];
                 }
         }
     }
@@ -114,7 +136,7 @@ __global__ void __launch_bounds__(XT_THREADS) k_xty(XtY p)
 
 cudaError_t launch_xty(const XtY &p, cudaStream_t s)
 {
-    const int A4 = (p.a + 3) & ~3, C4 = (p.c + 3) & ~3;
+    const int A4 = (p.a + 3) & ~3, C4 = (p.c + p.c2 + 3) & ~3;
     const int nblk = (A4 / 4) * (C4 / 4);
     const int bpt = (nblk + XT_THREADS - 1) / XT_THREADS;
     size_t smem = (size_t)XT_TR * (A4 + C4) * sizeof(double);
@@ -123,6 +145,7 @@ cudaError_t launch_xty(const XtY &p, cudaStream_t s)
 #define XT_LAUNCH(K)                                                                        \
     e = cudaFuncSetAttribute(k_xty<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     if (e != cudaSuccess) return e;                                                         \
+    note_launch();                                                                          \
     k_xty<K><<<grid, XT_THREADS, smem, s>>>(p);
     if (bpt <= 1) { XT_LAUNCH(1) }
     else if (bpt <= 2) { XT_LAUNCH(2) }
@@ -154,6 +177,7 @@ cudaError_t launch_reduce_parts(const double *part, int nbatch, int nchunk, int 
 {
     long tot = (long)a * c * nbatch;
     if (tot == 0) return cudaSuccess;
+    note_launch();
     k_reduce_parts<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(part, nbatch, nchunk, a, c,
                                                                  rowscale, rowscale_bs, out);
     return cudaGetLastError();
@@ -214,9 +238,13 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol(CholArgs a)
     __syncthreads();
 
     const bool plain = (st == 1) || (offI < 0.5);
-    double shift = plain ? 0.0
-                         : 11.0 * ((double)a.nrows * l + (double)l * (l + 1)) * DBL_EPSILON * 0.5 *
-                               normG;
+    // Shift: 64 l u ||G||_F.  Much smaller than the worst-case bound of Fukaya
+    // et al. (11 (rows l + l(l+1)) u ||G||_2), so the small singular values grow
+    // by ~1/sqrt(64 l u) per pass instead of ~1/sqrt(11 rows l u) (fewer
+    // passes); a breakdown is caught below and retried with a 100x larger
+    // shift, and Q = Y R^{-1} by substitution keeps Y = Q R backward stable for
+    // any successful R.
+    double shift = plain ? 0.0 : 64.0 * l * (DBL_EPSILON * 0.5) * normG;
     if (!(normG > 0.0)) shift = 1.0;   // zero block: any SPD shift; Q stays zero
     int attempt = 0;
     for (;;) {
@@ -286,6 +314,7 @@ cudaError_t launch_chol(const CholArgs &a, cudaStream_t s)
     size_t smem = (size_t)a.l * a.l * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(k_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    note_launch();
     k_chol<<<a.nbatch, CH_THREADS, smem, s>>>(a);
     return cudaGetLastError();
 }
@@ -335,6 +364,7 @@ cudaError_t launch_trsm(double *Q, long bs, long rs, long cs, long rows, int l, 
     cudaError_t e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((rows + TS_ROWS - 1) / TS_ROWS), nbatch);
+    note_launch();
     k_trsm<<<grid, TS_ROWS, smem, s>>>(Q, bs, rs, cs, rows, l, R, act);
     return cudaGetLastError();
 }
@@ -454,6 +484,7 @@ cudaError_t launch_jacobi(const double *Rtot, int nbatch, int l, double *Psi, do
     size_t smem = ((size_t)L * l + (size_t)L * L + L) * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(k_jacobi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    note_launch();
     k_jacobi<<<nbatch, 32 * JW, smem, s>>>(Rtot, l, Psi, sigma, Phi, fail);
     return cudaGetLastError();
 }
@@ -500,108 +531,228 @@ cudaError_t launch_lift(const double *X, long xbs, long xrs, long xcs, long rows
     cudaError_t e = cudaFuncSetAttribute(k_lift, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((rows + LF_ROWS - 1) / LF_ROWS), nbatch);
+    note_launch();
     k_lift<<<grid, LF_THREADS, smem, s>>>(X, xbs, xrs, xcs, rows, l, Cm, ldc, k, out);
     return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------- sweep
-// e_j = C_j e_{j-1} + (q_j - p_j), e_{-1} = 0: the only sequential part of a
-// Parareal iteration, in k-dimensional reduced coordinates.
+// e_j = C_j e_{j-1} + d_j, e_{-1} = 0: the only sequential part of a Parareal
+// iteration, in k-dimensional reduced coordinates.  C_{j+1} and d_{j+1} are
+// prefetched with cp.async while step j is computed.
 constexpr int SW_THREADS = 1024;
 
-__global__ void __launch_bounds__(SW_THREADS) k_sweep(const double *C, const double *q,
-                                                      const double *p, int N, int k, int S,
-                                                      double *e)
+__device__ __forceinline__ void sw_cp8(double *dst, const double *src)
+{
+    unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src) : "memory");
+}
+
+__global__ void __launch_bounds__(SW_THREADS) k_sweep(const double *C, const double *d, int N, int k,
+                                                      int S, double *e)
 {
     extern __shared__ __align__(16) double sm[];
-    const int kS = k * S;
-    double *eo = sm;             // previous e (k x S)
-    double *en = sm + kS;        // new e
-    double *Cs = sm + 2 * kS;    // k x k
-    for (int i = threadIdx.x; i < kS; i += SW_THREADS) eo[i] = 0.0;
-    __syncthreads();
+    const int kS = k * S, kk = k * k;
+    double *eb[2] = {sm, sm + kS};
+    double *Cb[2] = {sm + 2 * kS, sm + 2 * kS + kk};
+    double *db[2] = {sm + 2 * kS + 2 * kk, sm + 3 * kS + 2 * kk};
+    for (int i = threadIdx.x; i < kS; i += SW_THREADS) eb[0][i] = 0.0;
+    auto fetch = [&](int j, int buf) {
+        if (j < N) {
+            const double *Cj = C + (long)j * kk;
+            const double *dj = d + (long)j * kS;
+            for (int i = threadIdx.x; i < kk; i += SW_THREADS) sw_cp8(Cb[buf] + i, Cj + i);
+            for (int i = threadIdx.x; i < kS; i += SW_THREADS) sw_cp8(db[buf] + i, dj + i);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    fetch(0, 0);
+    int cur = 0;
     for (int j = 0; j < N; ++j) {
-        const double *Cj = C + (long)j * k * k;
-        for (int i = threadIdx.x; i < k * k; i += SW_THREADS) Cs[i] = (j > 0) ? Cj[i] : 0.0;
+        fetch(j + 1, (j + 1) & 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         __syncthreads();
-        const double *qj = q + (long)j * kS;
-        const double *pj = p ? p + (long)j * kS : nullptr;
+        const double *Cs = Cb[j & 1];
+        const double *ds = db[j & 1];
+        const double *eo = eb[cur];
+        double *en = eb[cur ^ 1];
         for (int o = threadIdx.x; o < kS; o += SW_THREADS) {
-            int r = o / S, s = o % S;
-            double acc = qj[o] - (pj ? pj[o] : 0.0);
-            for (int t = 0; t < k; ++t) acc = fma(Cs[r * k + t], eo[t * S + s], acc);
+            const int r = o / S, s = o % S;
+            double acc = ds[o];
+            if (j > 0)
+                for (int t = 0; t < k; ++t) acc = fma(Cs[r * k + t], eo[t * S + s], acc);
             en[o] = acc;
             e[(long)j * kS + o] = acc;
         }
+        cur ^= 1;
         __syncthreads();
-        double *tmp = eo; eo = en; en = tmp;
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
-cudaError_t launch_sweep(const double *C, const double *q, const double *p, int N, int k, int S,
-                         double *e, cudaStream_t s)
+cudaError_t launch_sweep(const double *C, const double *d, int N, int k, int S, double *e,
+                         cudaStream_t s)
 {
-    size_t smem = ((size_t)2 * k * S + (size_t)k * k) * sizeof(double);
+    size_t smem = ((size_t)4 * k * S + (size_t)2 * k * k) * sizeof(double);
     cudaError_t er = cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (er != cudaSuccess) return er;
-    k_sweep<<<1, SW_THREADS, smem, s>>>(C, q, p, N, k, S, e);
+    note_launch();
+    k_sweep<<<1, SW_THREADS, smem, s>>>(C, d, N, k, S, e);
+    return cudaGetLastError();
+}
+
+// d[b][i][s] = sigma_b[i] * (sum_t part[b][t][i][S + s] - sum_t part[b][t][i][s])
+// from the partials of [p | q] = V_b^T [Y1_b | Y2_b]  (Y1 absent: pcols = 0).
+__global__ void k_reduce_pq(const double *part, int nbatch, int nchunk, int k, int S, int pcols,
+                            const double *sigma, long sbs, double *d)
+{
+    long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long per = (long)k * S;
+    if (idx >= per * nbatch) return;
+    const int b = (int)(idx / per);
+    const long e = idx % per;
+    const int i = (int)(e / S), s = (int)(e % S);
+    const int c = pcols + S;
+    const double *pp = part + (long)b * nchunk * k * c + (long)i * c;
+    double q = 0.0, p = 0.0;
+    for (int t = 0; t < nchunk; ++t) {
+        const double *row = pp + (long)t * k * c;
+        q += row[pcols + s];
+        if (pcols) p += row[s];
+    }
+    d[idx] = sigma[(long)b * sbs + i] * (q - p);
+}
+
+cudaError_t launch_reduce_pq(const double *part, int nbatch, int nchunk, int k, int S, int pcols,
+                             const double *sigma, long sbs, double *d, cudaStream_t s)
+{
+    long tot = (long)k * S * nbatch;
+    if (tot == 0) return cudaSuccess;
+    note_launch();
+    k_reduce_pq<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(part, nbatch, nchunk, k, S, pcols,
+                                                              sigma, sbs, d);
     return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------- expand
+// out[row, v] = base[row, v] + sum_r U_b[row, r] e_b[r, s], v = b*S + s.
+// U tile (EX_TR rows) staged in smem; each thread owns 4 sources of one row
+// per step; optional per-(b, s) partial ||new - old||^2 in fixed order.
 constexpr int EX_THREADS = 256;
+constexpr int EX_TR = 64;
 
 __global__ void __launch_bounds__(EX_THREADS) k_expand(Expand a)
 {
     extern __shared__ __align__(16) double sm[];
-    __shared__ double red[EX_THREADS];
     const int b = blockIdx.y, t = blockIdx.x;
     const int k = a.k, S = a.S;
-    double *es = sm;   // k x S
+    const int S4 = (S + 3) & ~3;
+    const int NS4 = S4 / 4;
+    const int RPP = EX_THREADS / NS4;
+    const int kp = k + 1;
+    double *es = sm;                         // k x S4
+    double *Us = sm + (size_t)k * S4;        // EX_TR x (k+1)
+    double *red = Us + (size_t)EX_TR * kp;   // RPP x NS4 x 4
     const double *eb = a.e + (long)b * k * S;
-    for (int i = threadIdx.x; i < k * S; i += EX_THREADS) es[i] = eb[i];
-    __syncthreads();
-    const int per = EX_THREADS / S;          // threads per source (S <= 256)
-    const int s = threadIdx.x % S;
-    const int ty = threadIdx.x / S;
-    const bool act = ty < per;
+    for (int i = threadIdx.x; i < k * S4; i += EX_THREADS) {
+        int r = i / S4, s = i % S4;
+        es[i] = (s < S) ? eb[(long)r * S + s] : 0.0;
+    }
+    const int ts = threadIdx.x % NS4, tr = threadIdx.x / NS4;
+    const bool act = tr < RPP;
     const long r0 = (long)t * a.chunk_rows;
     long r1 = r0 + a.chunk_rows;
     if (r1 > a.rows) r1 = a.rows;
-    const double *Ub = a.U + (long)b * a.Ubs;
-    const long v = (long)b * S + s;
-    double nrm = 0.0;
-    if (act) {
-        for (long row = r0 + ty; row < r1; row += per) {
-            const double *ur = Ub + row * k;
-            double acc = a.base ? a.base[row * a.brs + v * a.bvs] : 0.0;
-            for (int r = 0; r < k; ++r) acc = fma(ur[r], es[r * S + s], acc);
-            double *o = a.out + row * a.ors + v * a.ovs;
-            if (a.normpart) {
-                double d = acc - *o;
-                nrm = fma(d, d, nrm);
+    const double *__restrict__ Ub = a.U + (long)b * a.Ubs;
+    const double *__restrict__ base = a.base;
+    double *__restrict__ out = a.out;
+    const bool norms = a.normpart != nullptr;
+    // vectors handled by this thread: v = b*S + 4 ts + j, j < nj
+    const int nj = max(0, min(4, S - 4 * ts));
+    const long v0 = (long)b * S + 4 * ts;
+    double nrm[4] = {0.0, 0.0, 0.0, 0.0};
+    constexpr int RU = 4;                    // rows per thread in flight
+    for (long rt = r0; rt < r1; rt += EX_TR) {
+        const int nr = (int)min((long)EX_TR, r1 - rt);
+        __syncthreads();
+        const double *ut = Ub + rt * k;
+        for (int i = threadIdx.x; i < nr * k; i += EX_THREADS) Us[(i / k) * kp + i % k] = ut[i];
+        __syncthreads();
+        if (!act) continue;
+        for (int rl0 = tr; rl0 < nr; rl0 += RPP * RU) {
+            // issue every global load of RU rows first (memory-level parallelism)
+            double bv[RU][4], ov[RU][4];
+#pragma unroll
+            for (int q = 0; q < RU; ++q) {
+                const int rl = rl0 + q * RPP;
+                const long row = rt + rl;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const bool ok = (rl < nr) && (j < nj);
+                    bv[q][j] = (ok && base) ? base[row * a.brs + (v0 + j) * a.bvs] : 0.0;
+                    ov[q][j] = (ok && norms) ? out[row * a.ors + (v0 + j) * a.ovs] : 0.0;
+                }
             }
-            *o = acc;
+#pragma unroll
+            for (int q = 0; q < RU; ++q) {
+                const int rl = rl0 + q * RPP;
+                if (rl >= nr) break;
+                const long row = rt + rl;
+                double acc[4] = {bv[q][0], bv[q][1], bv[q][2], bv[q][3]};
+                const double *ur = Us + rl * kp;
+#pragma unroll 4
+                for (int r = 0; r < k; ++r) {
+                    const double u = ur[r];
+                    const double2 e01 = *reinterpret_cast<const double2 *>(es + r * S4 + 4 * ts);
+                    const double2 e23 = *reinterpret_cast<const double2 *>(es + r * S4 + 4 * ts + 2);
+                    acc[0] = fma(u, e01.x, acc[0]);
+                    acc[1] = fma(u, e01.y, acc[1]);
+                    acc[2] = fma(u, e23.x, acc[2]);
+                    acc[3] = fma(u, e23.y, acc[3]);
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (j < nj) {
+                        if (norms) {
+                            const double dlt = acc[j] - ov[q][j];
+                            nrm[j] = fma(dlt, dlt, nrm[j]);
+                        }
+                        out[row * a.ors + (v0 + j) * a.ovs] = acc[j];
+                    }
+                }
+            }
         }
     }
-    if (a.normpart) {
-        red[threadIdx.x] = act ? nrm : 0.0;
+    if (norms) {
         __syncthreads();
-        if (threadIdx.x < S) {
-            double sum = 0.0;
-            for (int y = 0; y < per; ++y) sum += red[y * S + threadIdx.x];
-            a.normpart[((long)b * S + threadIdx.x) * a.nchunk + t] = sum;
+        if (act)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) red[(tr * NS4 + ts) * 4 + j] = nrm[j];
+        __syncthreads();
+        if (tr == 0) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int s = 4 * ts + j;
+                if (s >= S) break;
+                double sum = 0.0;
+                for (int y = 0; y < RPP; ++y) sum += red[(y * NS4 + ts) * 4 + j];
+                a.normpart[((long)b * S + s) * a.nchunk + t] = sum;
+            }
         }
     }
 }
 
 cudaError_t launch_expand(const Expand &a, cudaStream_t s)
 {
-    if (a.S > EX_THREADS) return cudaErrorInvalidValue;
-    size_t smem = (size_t)a.k * a.S * sizeof(double);
+    if (a.S > 128 || a.k > 128) return cudaErrorInvalidValue;
+    const int S4 = (a.S + 3) & ~3;
+    const int NS4 = S4 / 4;
+    const int RPP = EX_THREADS / NS4;
+    size_t smem = ((size_t)a.k * S4 + (size_t)EX_TR * (a.k + 1) + (size_t)RPP * NS4 * 4) * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(k_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid(a.nchunk, a.nbatch);
+    note_launch();
     k_expand<<<grid, EX_THREADS, smem, s>>>(a);
     return cudaGetLastError();
 }
@@ -618,6 +769,7 @@ __global__ void k_norm_finish(const double *part, int nvec, int nchunk, double *
 cudaError_t launch_norm_finish(const double *part, int nvec, int nchunk, double *out, cudaStream_t s)
 {
     if (nvec == 0) return cudaSuccess;
+    note_launch();
     k_norm_finish<<<(nvec + 127) / 128, 128, 0, s>>>(part, nvec, nchunk, out);
     return cudaGetLastError();
 }
@@ -649,6 +801,7 @@ cudaError_t launch_vecnorm_parts(const double *X, long rs, long vs, long rows, i
 {
     if (nvec == 0) return cudaSuccess;
     dim3 grid(nchunk, nvec);
+    note_launch();
     k_vecnorm_parts<<<grid, 256, 0, s>>>(X, rs, vs, rows, nvec, nchunk, chunk_rows, part);
     return cudaGetLastError();
 }
@@ -670,6 +823,7 @@ cudaError_t launch_copy_vectors(const double *in, long irs, long ivs, double *ou
 {
     long tot = rows * nvec;
     if (tot == 0) return cudaSuccess;
+    note_launch();
     k_copy_vectors<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(in, irs, ivs, out, ors, ovs, rows, nvec);
     return cudaGetLastError();
 }
@@ -687,6 +841,7 @@ cudaError_t launch_eye(double *R, int nbatch, int l, cudaStream_t s)
 {
     long tot = (long)l * l * nbatch;
     if (tot == 0) return cudaSuccess;
+    note_launch();
     k_eye<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(R, nbatch, l);
     return cudaGetLastError();
 }

@@ -39,6 +39,12 @@ __global__ void k_factor(int n, const double *__restrict__ subA, const double *_
                          const double *__restrict__ rsA, const double *__restrict__ diagA,
                          double dt, int transpose, Coef *DN, Coef *UP, int *bad)
 {
+    // The recurrences are sequential: warp 0 walks top-down (LU), warp 1
+    // bottom-up (UL).  Each warp stages a chunk of (a_i, c_i, s_i) in shared
+    // memory with all its lanes, then lane 0 runs the recurrence on it.
+    constexpr int CH = 1024;
+    __shared__ double sa[2][CH], sc[2][CH], ss[2][CH];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto a_of = [&](int i) -> double {
         if (i <= 0) return 0.0;
         return dt * (transpose ? supA[i - 1] : subA[i]);
@@ -53,32 +59,43 @@ __global__ void k_factor(int n, const double *__restrict__ subA, const double *_
         double d = 1.0 + dt * diagA[i];
         return a_of(i) + d + c_of(i);
     };
-    if (threadIdx.x == 0) {                   // LU, top-down
-        double r = 0.0, den = 1.0;
-        for (int i = 0; i < n; ++i) {
-            double ai = a_of(i), ci = c_of(i);
-            r = (i == 0) ? s_of(0) : s_of(i) - ai * (r / den);
-            den = r - ci;
-            if (!(den > 0.0) || !isfinite(den)) atomicExch(bad, 1);
-            double w = 1.0 / den;
-            DN[i].b = w;
-            DN[i].c = -(w * ai);              // -ga_i
-            UP[i].a = -(w * ci);              // -cp_i
-            DN[i].d = 0.0;
-            UP[i].d = 0.0;
+    double r = 0.0, den = 1.0;
+    for (int base = 0; base < n; base += CH) {
+        const int cnt = min(CH, n - base);
+        for (int t = lane; t < cnt; t += 32) {
+            const int i = (w == 0) ? base + t : n - 1 - (base + t);
+            sa[w][t] = a_of(i);
+            sc[w][t] = c_of(i);
+            ss[w][t] = s_of(i);
         }
-    } else if (threadIdx.x == 1) {            // UL, bottom-up
-        double r = 0.0, den = 1.0;
-        for (int i = n - 1; i >= 0; --i) {
-            double ai = a_of(i), ci = c_of(i);
-            r = (i == n - 1) ? s_of(n - 1) : s_of(i) - ci * (r / den);
-            den = r - ai;
-            if (!(den > 0.0) || !isfinite(den)) atomicExch(bad, 1);
-            double w = 1.0 / den;
-            UP[i].b = w;                      // wt_i
-            UP[i].c = -(w * ci);              // -gc_i
-            DN[i].a = -(w * ai);              // -ap_i
+        __syncwarp();
+        if (lane == 0) {
+            for (int t = 0; t < cnt; ++t) {
+                const double ai = sa[w][t], ci = sc[w][t], si = ss[w][t];
+                if (w == 0) {                     // LU, top-down
+                    const int i = base + t;
+                    r = (i == 0) ? si : si - ai * (r / den);
+                    den = r - ci;
+                    if (!(den > 0.0) || !isfinite(den)) atomicExch(bad, 1);
+                    const double wv = 1.0 / den;
+                    DN[i].b = wv;
+                    DN[i].c = -(wv * ai);         // -ga_i
+                    UP[i].a = -(wv * ci);         // -cp_i
+                    DN[i].d = 0.0;
+                    UP[i].d = 0.0;
+                } else {                          // UL, bottom-up
+                    const int i = n - 1 - (base + t);
+                    r = (i == n - 1) ? si : si - ci * (r / den);
+                    den = r - ai;
+                    if (!(den > 0.0) || !isfinite(den)) atomicExch(bad, 1);
+                    const double wv = 1.0 / den;
+                    UP[i].b = wv;                 // wt_i
+                    UP[i].c = -(wv * ci);         // -gc_i
+                    DN[i].a = -(wv * ai);         // -ap_i
+                }
+            }
         }
+        __syncwarp();
     }
 }
 
@@ -86,7 +103,8 @@ cudaError_t launch_factor_1d(int n, const double *subA, const double *supA, cons
                                   const double *diagA, double dt, int transpose, Coef *DN,
                                   Coef *UP, int *bad, cudaStream_t s)
 {
-    k_factor<<<1, 32, 0, s>>>(n, subA, supA, rsA, diagA, dt, transpose, DN, UP, bad);
+    note_launch();
+    k_factor<<<1, 64, 0, s>>>(n, subA, supA, rsA, diagA, dt, transpose, DN, UP, bad);
     return cudaGetLastError();
 }
 
@@ -160,6 +178,7 @@ cudaError_t launch_sketch(int dim, int n, long rows, int q0, int nint, int l,
     if (total == 0) return cudaSuccess;
     int th = 256;
     long bl = (total + th - 1) / th;
+    note_launch();
     k_sketch<<<(unsigned)bl, th, 0, s>>>(dim, n, rows, q0, nint, l, seed, out, rs, vs);
     return cudaGetLastError();
 }
@@ -175,6 +194,7 @@ __global__ void k_transpose(const double *in, int R, int n, double *out)
 cudaError_t launch_transpose(const double *in, int R, int n, double *out, cudaStream_t s)
 {
     long total = (long)R * n;
+    note_launch();
     k_transpose<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(in, R, n, out);
     return cudaGetLastError();
 }
@@ -464,8 +484,13 @@ static cudaError_t launch_stepper_t(const StepArgs &a, cudaStream_t s)
     auto kern = k_stepper<VPT, AFF>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    const bool prof = profiling();
+    if (prof) stepper_timed_begin(s);
+    note_launch();
     kern<<<(unsigned)blocks, 32, smem, s>>>(a);
-    return cudaGetLastError();
+    e = cudaGetLastError();
+    if (prof) stepper_timed_end(s, (double)a.n * (double)a.B * (double)a.m);
+    return e;
 }
 
 cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s)
@@ -473,6 +498,7 @@ cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s)
     if (a.m == 0) {
         long tot = (long)a.n * a.B;
         if (tot == 0) return cudaSuccess;
+        note_launch();
         k_copy_off<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a.in, a.ld_in, a.out, a.ld_out,
                                                                  a.off, a.ld_off, a.n, a.B);
         return cudaGetLastError();

@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <unordered_map>
@@ -70,6 +71,39 @@ void ws_free(void *p)
     auto it = g_ws_size.find(p);
     if (it == g_ws_size.end()) return;
     g_ws_free.emplace(it->second, p);
+}
+
+// ---------------------------------------------------------------- counters
+static std::atomic<long> g_launches{0};
+static std::atomic<int> g_prof{0};
+struct TimedLaunch {
+    cudaEvent_t a, b;
+    double dof_steps;
+};
+static std::mutex g_prof_mu;
+static std::vector<TimedLaunch> g_timed;
+static thread_local cudaEvent_t g_pending_begin = nullptr;
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+bool profiling() { return g_prof.load(std::memory_order_relaxed) != 0; }
+
+void stepper_timed_begin(cudaStream_t s)
+{
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) { g_pending_begin = nullptr; return; }
+    cudaEventRecord(e, s);
+    g_pending_begin = e;
+}
+
+void stepper_timed_end(cudaStream_t s, double dof_steps)
+{
+    if (!g_pending_begin) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_timed.push_back({g_pending_begin, e, dof_steps});
+    g_pending_begin = nullptr;
 }
 
 int num_sms()
@@ -242,6 +276,35 @@ extern "C" {
 
 const char *pr_last_error(void) { return g_err.c_str(); }
 int pr_version(void) { return 1; }
+
+pr_status pr_profile(int enable)
+{
+    g_prof.store(enable ? 1 : 0);
+    return PR_OK;
+}
+
+pr_status pr_counters(int reset, long *kernel_launches, long *stepper_launches, double *stepper_ms,
+                      double *stepper_dof_steps)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    double ms = 0.0, dof = 0.0;
+    long n = 0;
+    for (auto &t : g_timed) {
+        float f = 0.f;
+        cudaEventSynchronize(t.b);
+        if (cudaEventElapsedTime(&f, t.a, t.b) == cudaSuccess) { ms += f; dof += t.dof_steps; ++n; }
+    }
+    if (kernel_launches) *kernel_launches = g_launches.load();
+    if (stepper_launches) *stepper_launches = n;
+    if (stepper_ms) *stepper_ms = ms;
+    if (stepper_dof_steps) *stepper_dof_steps = dof;
+    if (reset) {
+        for (auto &t : g_timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+        g_timed.clear();
+        g_launches.store(0);
+    }
+    return PR_OK;
+}
 
 pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, const double *sup,
                                const double *rowsum, const double *colsum, double dt, pr_op *out)
@@ -572,16 +635,15 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
     Lay L = lay(op, ld);
     Lay L0 = lay(op, ld_u0);
     const size_t arr = (op.dim == 1) ? (size_t)rows * ld : (size_t)nvec * ld;
-    double *Fu, *bb, *qv, *pv, *ev, *part, *npart, *upd, *bn;
+    double *Fu, *bb, *qv, *ev, *part, *npart, *upd, *bn;
     PR_ALLOC(Fu, double, arr, Sc);
     PR_ALLOC(bb, double, arr, Sc);
     const size_t red = (size_t)N * k * S;
     PR_ALLOC(qv, double, red, Sc);
-    PR_ALLOC(pv, double, red, Sc);
     PR_ALLOC(ev, double, red, Sc);
     const int nchunk = xty_chunks(rows, N);
     const long cr = (rows + nchunk - 1) / nchunk;
-    PR_ALLOC(part, double, (size_t)N * nchunk * k * S, Sc);
+    PR_ALLOC(part, double, (size_t)N * nchunk * k * 2 * S, Sc);
     PR_ALLOC(npart, double, (size_t)nvec * nchunk, Sc);
     PR_ALLOC(upd, double, (size_t)(K_iter > 0 ? K_iter : 1) * nvec, Sc);
     PR_ALLOC(bn, double, (size_t)nvec, Sc);
@@ -608,11 +670,13 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
     PR_CUDA(launch_copy_vectors(bb + blk, L.rs, L.vs, Fu + blk, L.rs, L.vs, rows, N * S, s));
 
     const double *sig = G->sigma;
-    auto project = [&](const double *Yarr, double *outv) -> pr_status {
-        // outv_q = Sigma_q V_q^T Y[block q], q = 0..N-1
-        XtY x{nullptr, G->V, rows * k, k, 1, k, Yarr, blk, L.rs, L.vs, S, rows, N, nchunk, cr, part};
+    // d_q = Sigma_q V_q^T (Fu[block q] - u[block q])   (one pass over V_q)
+    auto project = [&](bool with_p) -> pr_status {
+        XtY x{nullptr, G->V, rows * k, k, 1, k, with_p ? U_out : Fu, blk, L.rs, L.vs, S, rows, N,
+              nchunk, cr, part};
+        if (with_p) { x.Y2 = Fu; x.c2 = S; }
         PR_CUDA(launch_xty(x, s));
-        PR_CUDA(launch_reduce_parts(part, N, nchunk, k, S, sig, G->l, outv, s));
+        PR_CUDA(launch_reduce_pq(part, N, nchunk, k, S, with_p ? S : 0, sig, G->l, qv, s));
         return PR_OK;
     };
     auto expand = [&](bool norms) -> pr_status {
@@ -623,9 +687,10 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
     };
     pr_status st;
     // ---- initialisation: u^0_{q+1} = G_q u^0_q (p = 0)
-    if ((st = project(Fu, qv)) != PR_OK) return st;
-    PR_CUDA(launch_sweep(G->C, qv, nullptr, N, k, S, ev, s));
+    if ((st = project(false)) != PR_OK) return st;
+    PR_CUDA(launch_sweep(G->C, qv, N, k, S, ev, s));
     if ((st = expand(false)) != PR_OK) return st;
+    stage("parareal init", s);
     if (hist) {
         PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, hist, L.rs, L.vs, rows, (int)nvec, s));
     }
@@ -635,11 +700,14 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
         st = propagate(op, PR_LINEAR, 0, m, N * S, S, nullptr, U_out, ld, Fu + blk, ld, bb + blk,
                        ld, 0, 0, s);
         if (st != PR_OK) return st;
-        if ((st = project(U_out, pv)) != PR_OK) return st;
-        if ((st = project(Fu, qv)) != PR_OK) return st;
-        PR_CUDA(launch_sweep(G->C, qv, pv, N, k, S, ev, s));
+        stage("parareal fine", s);
+        if ((st = project(true)) != PR_OK) return st;
+        stage("parareal project", s);
+        PR_CUDA(launch_sweep(G->C, qv, N, k, S, ev, s));
+        stage("parareal sweep", s);
         PR_CUDA(cudaMemsetAsync(npart, 0, (size_t)S * nchunk * sizeof(double), s));   // block 0
         if ((st = expand(true)) != PR_OK) return st;
+        stage("parareal expand", s);
         PR_CUDA(launch_norm_finish(npart, (int)nvec, nchunk, upd + (size_t)(it - 1) * nvec, s));
         if (hist) {
             PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, hist + (size_t)it * hist_stride, L.rs,

@@ -42,6 +42,13 @@ void ws_free(void *p);
 // Number of SMs of the current device (cached).
 int num_sms();
 
+// Counters (pr_counters): every kernel launch of the library, and CUDA-event
+// timing of the stepper launches when profiling is enabled.
+void note_launch();
+bool profiling();
+void stepper_timed_begin(cudaStream_t s);
+void stepper_timed_end(cudaStream_t s, double dof_steps);
+
 // ---------------------------------------------------------------- operator
 struct Coef {             // one row of a fused stepper pass (32 B, aligned)
     double a, b, c, d;
@@ -105,7 +112,9 @@ struct XtY {
     int nbatch;
     int nchunk;
     long chunk_rows;
-    double *part;
+    double *part;                     // (nbatch, nchunk, a, c + c2)
+    const double *Y2 = nullptr;       // optional: columns [c, c + c2) from Y2 (Y's strides)
+    int c2 = 0;
 };
 cudaError_t launch_xty(const XtY &p, cudaStream_t s);
 int xty_chunks(long rows, int nbatch);
@@ -138,10 +147,13 @@ cudaError_t launch_lift(const double *X, long xbs, long xrs, long xcs, long rows
                         const double *Cm, int ldc, int k, int nbatch, double *out,
                         cudaStream_t s);
 
-// sequential reduced sweep: e_j = C_j e_{j-1} + (q_j - p_j), j = 0..N-1
-// (C_0 unused: e_{-1} = 0).  All (k x S) row-major per interval.
-cudaError_t launch_sweep(const double *C, const double *q, const double *p, int N, int k, int S,
-                         double *e, cudaStream_t s);
+// sequential reduced sweep: e_j = C_j e_{j-1} + d_j, j = 0..N-1 (C_0 unused:
+// e_{-1} = 0).  All (k x S) row-major per interval.
+cudaError_t launch_sweep(const double *C, const double *d, int N, int k, int S, double *e,
+                         cudaStream_t s);
+// d_b = Sigma_b (q_b - p_b) from X^T Y partials with columns [p (pcols = S or 0) | q (S)]
+cudaError_t launch_reduce_pq(const double *part, int nbatch, int nchunk, int k, int S, int pcols,
+                             const double *sigma, long sbs, double *d, cudaStream_t s);
 
 // expand: out[row, v] = base[row, v] + sum_r U_b[row, r] e_b[r, s]  for interval b,
 // source s, vector v = b*S + s (vector offsets in the out/base arrays given by
