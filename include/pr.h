@@ -95,7 +95,7 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
 /* 2D operator: 5-point Laplacian on the unit square with homogeneous
  * Dirichlet conditions, n x n interior points, A = T (x) I + I (x) T,
  * T = tridiag(-1, 2, -1)/h^2.  Solved in the sine eigenbasis of T (DESIGN.md
- * "K2").  Synchronizing.  Errors: EINVAL (n < 2, (n+1) % 16 != 0, dt <= 0). */
+ * "K2").  Synchronizing.  Errors: EINVAL (n < 2, (n+1) % 64 != 0, dt <= 0). */
 pr_status pr_op_create_sep2d(int n, double dt, pr_op *out);
 
 pr_status pr_op_destroy(pr_op op);
