@@ -122,22 +122,30 @@ class Workload:
         # interval shard (build) and source shard (Parareal)
         self.q0, self.nq = _shard(cfg.N, rank, world)
         self.s0, self.ns = _shard(cfg.nsrc, rank, world)
-        assert cfg.dim == 1, "bench.py drives the 1D configs (C1, C2, C4)"
-        self.host = dict(op=G.operator_1d(cfg), sums=G.operator_1d_sums(cfg))
-        space, time_, amp = G.source_1d(cfg)
-        self.host.update(space=space, time=time_, amp=amp[self.s0:self.s0 + self.ns])
         u0 = G.initial_value(cfg)
-        self.host["u0"] = np.ascontiguousarray(np.stack([u0] * self.ns).T)     # (n, ns)
-        rs, cs = self.host["sums"]
-        self.op = Operator.tridiag(*self.host["op"], cfg.dt, rowsum=rs, colsum=cs)
-        self.src = SourceTerm.sep1d(space, time_, self.host["amp"])
+        if cfg.dim == 1:
+            self.host = dict(op=G.operator_1d(cfg), sums=G.operator_1d_sums(cfg))
+            space, time_, amp = G.source_1d(cfg)
+            self.host.update(space=space, time=time_, amp=amp[self.s0:self.s0 + self.ns])
+            self.host["u0"] = np.ascontiguousarray(np.stack([u0] * self.ns).T)   # (n, ns)
+            rs, cs = self.host["sums"]
+            self.op = Operator.tridiag(*self.host["op"], cfg.dt, rowsum=rs, colsum=cs)
+            self.src = SourceTerm.sep1d(space, time_, self.host["amp"])
+            self.U = torch.empty((cfg.n, (cfg.N + 1) * self.ns), dtype=torch.float64, device=dev)
+        else:
+            gx, gy = G.source_2d(cfg)
+            P = cfg.n + 1
+            self.host = dict(gx=G.pad1d_last(gx), gy=G.pad1d_last(gy),
+                             u0=G.pad2d(u0).reshape(1, P * P))
+            self.op = Operator.sep2d(cfg.n, cfg.dt)
+            self.src = SourceTerm.bump2d(self.host["gx"], self.host["gy"])
+            self.U = torch.empty(((cfg.N + 1) * self.ns, P * P), dtype=torch.float64, device=dev)
         self.u0 = torch.tensor(self.host["u0"], dtype=torch.float64, device=dev)
-        self.U = torch.empty((cfg.n, (cfg.N + 1) * self.ns), dtype=torch.float64, device=dev)
 
     def dof_steps(self) -> float:
         c = self.cfg
-        build = self.nq * 2 * c.l * c.n * c.m
-        par = (c.K + 1) * c.N * self.ns * c.n * c.m
+        build = self.nq * 2 * c.l * c.n_dof * c.m
+        par = (c.K + 1) * c.N * self.ns * c.n_dof * c.m
         return float(build + par)
 
     def step(self, events=None):
@@ -153,6 +161,25 @@ class Workload:
         upd, bn = parareal(G, self.op, self.u0, self.src, c.K, self.U, nsrc=self.ns)
         G.close()
         return upd, bn
+
+
+def _fp64_peak(dev):
+    """Measured FP64 ceiling on this GPU: cuBLAS DGEMM 8192^3 (best of 5, CUDA
+    events).  MEASURED_PEAKS.json carries no FP64 figure."""
+    import torch
+    n = 8192
+    a = torch.randn((n, n), dtype=torch.float64, device=dev)
+    b = torch.randn((n, n), dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = _event(), None
+        torch.matmul(a, b)
+        e1 = _event()
+        torch.cuda.synchronize()
+        best = max(best, 2.0 * n ** 3 / (e0.elapsed_time(e1) / 1e3) / 1e12)
+    del a, b
+    return best
 
 
 def _shard(total: int, rank: int, world: int):
@@ -182,15 +209,20 @@ def oracle_sample(cfg):
     from oracle.rsvd import rsvd_interval
     from workloads import generators as G
     op = make_op(cfg)
-    src = G.source_1d(cfg)
-    u0 = np.stack([G.initial_value(cfg)] * cfg.nsrc)
+    if cfg.dim == 1:
+        src = G.source_1d(cfg)
+        u0 = np.stack([G.initial_value(cfg)] * cfg.nsrc)
+        sidx = np.arange(cfg.nsrc)
+    else:
+        src = G.source_2d(cfg)
+        u0 = G.initial_value(cfg)[None]
+        sidx = None
     t0 = time.perf_counter()
     rsvd_interval(op, 1, cfg.k, cfg.p, cfg.seed_omega)
-    x = np.zeros_like(u0)
     for _ in range(cfg.K + 1):
-        x = fine(op, 1, u0, "affine", src, np.arange(cfg.nsrc))
+        fine(op, 1, u0, "affine", src, sidx)
     dt = time.perf_counter() - t0
-    dof = 2 * cfg.l * cfg.n * cfg.m + (cfg.K + 1) * cfg.nsrc * cfg.n * cfg.m
+    dof = 2 * cfg.l * cfg.n_dof * cfg.m + (cfg.K + 1) * cfg.nsrc * cfg.n_dof * cfg.m
     return float(dof), dt
 
 
@@ -221,7 +253,7 @@ def main():
     config = {"workload": cfg.name, "dim": cfg.dim, "n": cfg.n, "N": cfg.N, "m": cfg.m, "k": cfg.k,
               "p": cfg.p, "K": cfg.K, "nsrc": cfg.nsrc, "T": cfg.T,
               "l2": "inputs larger than L2: %.2f GB state per stepper phase vs 126 MB L2"
-                    % (cfg.n * cfg.N * max(cfg.l, cfg.nsrc) * 8 / 1e9),
+                    % (cfg.n_dof * cfg.N * max(cfg.l, cfg.nsrc) * 8 / 1e9),
               "parallelism": f"intervals+sources sharded over {args.gpus} GPU(s)"}
 
     if args.impl == "reference":
@@ -300,19 +332,32 @@ def main():
     dof_total = wl.dof_steps() * world if world == 1 else _sum_dof(wl, world)
     value = dof_total / (ms_per_step / 1e3)
 
-    # ------------------------------------------------ roofline of K1 stepper
-    peak, peak_kind = _peaks()
+    # ------------------------------------------- roofline of the fine stepper
     st_ms = ctr["stepper_ms"] / max(ctr["stepper_launches"], 1)
     st_dof = ctr["stepper_dof_steps"] / max(ctr["stepper_launches"], 1)
-    achieved = 16.0 * st_dof / (st_ms / 1e3) / 1e9 if st_ms > 0 else None
-    traffic = _ncu_traffic(cfg.name)
-    roofline = {"kernel": "k_stepper (K1, batched tridiagonal implicit Euler)", "bound": "hbm",
-                "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "algorithmic_bytes_per_launch": 16.0 * st_dof,
-                "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-                "launches_timed": ctr["stepper_launches"],
-                "share_of_step": ctr["stepper_ms"] / total_ms if total_ms > 0 else None}
+    st_fl = ctr["stepper_flops"] / max(ctr["stepper_launches"], 1)
+    if cfg.dim == 1:
+        peak, peak_kind = _peaks()
+        achieved = 16.0 * st_dof / (st_ms / 1e3) / 1e9 if st_ms > 0 else None
+        roofline = {"kernel": "k_stepper (K1, batched tridiagonal implicit Euler)", "bound": "hbm",
+                    "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": (achieved / peak) if achieved else None,
+                    "traffic": _ncu_traffic(cfg.name),
+                    "algorithmic_bytes_per_launch": 16.0 * st_dof,
+                    "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
+    else:
+        peak = _fp64_peak(dev)
+        achieved = st_fl / (st_ms / 1e3) / 1e12 if st_ms > 0 else None
+        roofline = {"kernel": "k_gemm_st (K2, FP64 DMMA sine-transform passes + fused Euler steps)",
+                    "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": (achieved / peak) if achieved else None,
+                    "traffic": _ncu_traffic(cfg.name),
+                    "algorithmic_flops_per_launch": st_fl,
+                    "peak_source": "measured live: cuBLAS DGEMM 8192^3 (fp64 has no entry in "
+                                   "MEASURED_PEAKS.json)"}
+    roofline.update({"launches_timed": ctr["stepper_launches"],
+                     "ms_per_launch": st_ms,
+                     "share_of_step": ctr["stepper_ms"] / total_ms if total_ms > 0 else None})
 
     # ------------------------------------------------------------- e2e run
     e2e = None
@@ -355,26 +400,30 @@ def _sum_dof(wl, world):
 
 def _e2e(wl, steps, barrier, world):
     """Same metric through the public API from HOST buffers: per step the
-    operator arrays, u0 and the source factors go host->device from pinned
-    memory, and the Parareal solution u^K (all interval boundaries) and the
-    update norms come back device->host."""
+    operator data, u0 and the source factors go host->device from pinned
+    memory, and the Parareal solution u^K (all interval boundaries) comes back
+    device->host."""
     import torch
     from paper_2508_08873_b200 import Coarse, Operator, SourceTerm, parareal
     c = wl.cfg
-    pin = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory()
-           for k, v in (("space", wl.host["space"]), ("time", wl.host["time"]),
-                        ("amp", wl.host["amp"]), ("u0", wl.host["u0"]))}
+    keys = ("space", "time", "amp", "u0") if c.dim == 1 else ("gx", "gy", "u0")
+    pin = {k: torch.from_numpy(np.ascontiguousarray(wl.host[k])).pin_memory() for k in keys}
     out_host = torch.empty(tuple(wl.U.shape), dtype=torch.float64).pin_memory()
-    h2d = sum(t.numel() * 8 for t in pin.values()) + 5 * c.n * 8
+    h2d = sum(t.numel() * 8 for t in pin.values()) + (5 * c.n * 8 if c.dim == 1 else 0)
     d2h = out_host.numel() * 8
     barrier()
     e0 = _event()
     for _ in range(steps):
-        rs, cs = wl.host["sums"]
-        op = Operator.tridiag(*wl.host["op"], c.dt, rowsum=rs, colsum=cs)      # host arrays
         dv = {k: v.to(wl.dev, non_blocking=True) for k, v in pin.items()}
-        src = SourceTerm(1, dv["time"].shape[0], dv["amp"].shape[0], dv["time"].shape[1],
-                         {"space": dv["space"], "time": dv["time"], "amp": dv["amp"]})
+        if c.dim == 1:
+            rs, cs = wl.host["sums"]
+            op = Operator.tridiag(*wl.host["op"], c.dt, rowsum=rs, colsum=cs)      # host arrays
+            src = SourceTerm(1, dv["time"].shape[0], dv["amp"].shape[0], dv["time"].shape[1],
+                             {"space": dv["space"], "time": dv["time"], "amp": dv["amp"]})
+        else:
+            op = Operator.sep2d(c.n, c.dt)
+            src = SourceTerm(2, dv["gx"].shape[0], 1, dv["gx"].shape[1],
+                             {"gx": dv["gx"], "gy": dv["gy"]})
         G = Coarse.build(op, c.N, c.m, c.k, c.p, c.seed_omega, first_interval=wl.q0,
                          n_local=wl.nq)
         if world > 1:

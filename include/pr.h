@@ -63,15 +63,17 @@ typedef enum {
 const char *pr_last_error(void);
 int pr_version(void);
 
-/* Instrumentation.  pr_profile(1) brackets every stepper launch (K1) with CUDA
+/* Instrumentation.  pr_profile(1) brackets every fine-propagation launch
+ * (1D: the K1 stepper kernel; 2D: the K2 GEMM passes of one call) with CUDA
  * events on its stream.  pr_counters (host; synchronises on the recorded
  * events) returns the number of kernels the library has launched, and the
- * number, summed device time (ms) and DOF-steps (n * B * m) of the timed
- * stepper launches since the last reset; reset != 0 clears them afterwards.
- * All output pointers may be NULL. */
+ * number, summed device time (ms), DOF-steps (n_dof * B * m) and tensor-core
+ * flops (2D: 2 P^3 per vector per GEMM pass; 1D: 0) of the timed launches
+ * since the last reset; reset != 0 clears them afterwards.  All output
+ * pointers may be NULL. */
 pr_status pr_profile(int enable);
 pr_status pr_counters(int reset, long *kernel_launches, long *stepper_launches, double *stepper_ms,
-                      double *stepper_dof_steps);
+                      double *stepper_dof_steps, double *stepper_flops);
 
 typedef struct pr_op_s *pr_op;
 typedef struct pr_coarse_s *pr_coarse;

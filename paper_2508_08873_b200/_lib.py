@@ -56,7 +56,7 @@ def lib():
             "pr_last_error": ([], ctypes.c_char_p),
             "pr_version": ([], I),
             "pr_profile": ([I], I),
-            "pr_counters": ([I, ctypes.POINTER(lg), ctypes.POINTER(lg), dp, dp], I),
+            "pr_counters": ([I, ctypes.POINTER(lg), ctypes.POINTER(lg), dp, dp, dp], I),
             "pr_op_create_tridiag": ([I, dp, dp, dp, dp, dp, D, ctypes.POINTER(vp)], I),
             "pr_op_create_sep2d": ([I, D, ctypes.POINTER(vp)], I),
             "pr_op_destroy": ([vp], I),

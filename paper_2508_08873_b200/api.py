@@ -223,8 +223,8 @@ def counters(reset: bool = False) -> dict:
     """Kernel launches of the library, and stepper launches / device ms /
     DOF-steps timed with CUDA events while profiling was enabled."""
     kl, sl = ctypes.c_long(), ctypes.c_long()
-    ms, dof = ctypes.c_double(), ctypes.c_double()
+    ms, dof, fl = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
     check(L.lib().pr_counters(1 if reset else 0, ctypes.byref(kl), ctypes.byref(sl),
-                              ctypes.byref(ms), ctypes.byref(dof)), "pr_counters")
+                              ctypes.byref(ms), ctypes.byref(dof), ctypes.byref(fl)), "pr_counters")
     return dict(kernel_launches=kl.value, stepper_launches=sl.value, stepper_ms=ms.value,
-                stepper_dof_steps=dof.value)
+                stepper_dof_steps=dof.value, stepper_flops=fl.value)

@@ -245,7 +245,26 @@ __global__ void k_affine_hat(int P, int m, int q0, int vpi, int nb, int nsl, int
 }
 
 // ------------------------------------------------------------------ driver
+static pr_status run_sep2d_impl(const Sep2dArgs &a, cudaStream_t s, int *passes);
+
+// Timed wrapper: the fine solves of one call (all its GEMM passes and
+// epilogues) are one "stepper launch" for pr_counters; flops = 2 P^3 per
+// vector per GEMM pass.
 pr_status run_sep2d(const Sep2dArgs &a, cudaStream_t s)
+{
+    const bool prof = profiling();
+    if (prof) stepper_timed_begin(s);
+    int passes = 0;
+    pr_status st = run_sep2d_impl(a, s, &passes);
+    if (prof) {
+        const double P = a.op->P;
+        const double n2 = (double)a.op->n * a.op->n;
+        stepper_timed_end(s, n2 * (double)a.B * a.m, 2.0 * P * P * P * (double)a.B * passes);
+    }
+    return st;
+}
+
+static pr_status run_sep2d_impl(const Sep2dArgs &a, cudaStream_t s, int *passes)
 {
     const Op &op = *a.op;
     const int P = op.P;
@@ -295,6 +314,7 @@ pr_status run_sep2d(const Sep2dArgs &a, cudaStream_t s)
         PR_CHECK_LAUNCH("k_affine_hat");
         g.X = bvec; g.ldx = ldb; g.out = T; g.ldo = per;
         PR_CUDA(launch_gemm(g, EPI_NONE, s));                   // T = (S b^)^T
+        *passes += 2;
         g.X = T; g.ldx = per; g.out = bvec; g.ldo = ldb;
         if (!a.in && a.off) {
             g.off = a.off; g.ldoff = a.ld_off;
@@ -312,6 +332,7 @@ pr_status run_sep2d(const Sep2dArgs &a, cudaStream_t s)
     }
     // LINEAR / ADJOINT (A symmetric, time-independent: F'^* = F'), + offset
     g.X = a.in; g.ldx = a.ld_in; g.out = T; g.ldo = per;
+    *passes += 4;
     PR_CUDA(launch_gemm(g, EPI_NONE, s));                       // T  = (S X)^T
     g.X = T; g.ldx = per; g.out = a.out; g.ldo = a.ld_out;
     PR_CUDA(launch_gemm(g, EPI_DIAG, s));                       // X^ = S X S, m diagonal steps

@@ -489,7 +489,7 @@ static cudaError_t launch_stepper_t(const StepArgs &a, cudaStream_t s)
     note_launch();
     kern<<<(unsigned)blocks, 32, smem, s>>>(a);
     e = cudaGetLastError();
-    if (prof) stepper_timed_end(s, (double)a.n * (double)a.B * (double)a.m);
+    if (prof) stepper_timed_end(s, (double)a.n * (double)a.B * (double)a.m, 0.0);
     return e;
 }
 

@@ -78,7 +78,7 @@ static std::atomic<long> g_launches{0};
 static std::atomic<int> g_prof{0};
 struct TimedLaunch {
     cudaEvent_t a, b;
-    double dof_steps;
+    double dof_steps, flops;
 };
 static std::mutex g_prof_mu;
 static std::vector<TimedLaunch> g_timed;
@@ -95,14 +95,14 @@ void stepper_timed_begin(cudaStream_t s)
     g_pending_begin = e;
 }
 
-void stepper_timed_end(cudaStream_t s, double dof_steps)
+void stepper_timed_end(cudaStream_t s, double dof_steps, double flops)
 {
     if (!g_pending_begin) return;
     cudaEvent_t e;
     if (cudaEventCreate(&e) != cudaSuccess) return;
     cudaEventRecord(e, s);
     std::lock_guard<std::mutex> lk(g_prof_mu);
-    g_timed.push_back({g_pending_begin, e, dof_steps});
+    g_timed.push_back({g_pending_begin, e, dof_steps, flops});
     g_pending_begin = nullptr;
 }
 
@@ -284,16 +284,17 @@ pr_status pr_profile(int enable)
 }
 
 pr_status pr_counters(int reset, long *kernel_launches, long *stepper_launches, double *stepper_ms,
-                      double *stepper_dof_steps)
+                      double *stepper_dof_steps, double *stepper_flops)
 {
     std::lock_guard<std::mutex> lk(g_prof_mu);
-    double ms = 0.0, dof = 0.0;
+    double ms = 0.0, dof = 0.0, fl = 0.0;
     long n = 0;
     for (auto &t : g_timed) {
         float f = 0.f;
         cudaEventSynchronize(t.b);
-        if (cudaEventElapsedTime(&f, t.a, t.b) == cudaSuccess) { ms += f; dof += t.dof_steps; ++n; }
+        if (cudaEventElapsedTime(&f, t.a, t.b) == cudaSuccess) { ms += f; dof += t.dof_steps; fl += t.flops; ++n; }
     }
+    if (stepper_flops) *stepper_flops = fl;
     if (kernel_launches) *kernel_launches = g_launches.load();
     if (stepper_launches) *stepper_launches = n;
     if (stepper_ms) *stepper_ms = ms;

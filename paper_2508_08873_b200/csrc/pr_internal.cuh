@@ -47,7 +47,7 @@ int num_sms();
 void note_launch();
 bool profiling();
 void stepper_timed_begin(cudaStream_t s);
-void stepper_timed_end(cudaStream_t s, double dof_steps);
+void stepper_timed_end(cudaStream_t s, double dof_steps, double flops);
 
 // ---------------------------------------------------------------- operator
 struct Coef {             // one row of a fused stepper pass (32 B, aligned)

@@ -162,3 +162,29 @@ def test_parareal_c3_against_fine_solution():
     assert np.max(err[: cfg.K + 1]) <= TAU_2D * scale
     # beyond: the Parareal error after K = 8 iterations (~1e-13 relative at k >= 4)
     assert np.max(err) <= 1e-9 * scale
+
+
+def test_build_c5_shard_sampled_intervals():
+    """C5 (511^2 grid, N = 512) does not fit one GPU (205 GB of factors).  One
+    B200 builds the shard of intervals one of eight ranks owns; intervals are
+    independent and seeded by (seed, q, column), so the shard must agree with
+    the oracle's rSVD of the same intervals."""
+    from paper_2508_08873_b200 import Coarse
+    from workloads.configs import C5
+    cfg = C5
+    first, nloc = 448, 8                       # a slice of rank 7's intervals
+    Gg = Coarse.build(gpu_op(cfg), cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega,
+                      first_interval=first, n_local=nloc)
+    info = Gg.info()
+    op_o = make_op(cfg)
+    for ql in (0, nloc - 1):
+        tr = rsvd_interval(op_o, first + ql + 1, cfg.k, cfg.p, cfg.seed_omega)
+        s1 = tr.sigma[0]
+        assert np.max(np.abs(info["sigma"][ql] - tr.sigma)) <= TAU_2D * s1
+        X = np.random.default_rng(ql).standard_normal((2, cfg.n, cfg.n))
+        Y = empty_batch(cfg, 2)
+        Gg.apply(ql, to_gpu(cfg, X), Y, 2)
+        got = from_gpu(cfg, Y).reshape(2, -1)
+        ref = tr.apply_linear(X.reshape(2, -1))
+        for v in range(2):
+            assert np.linalg.norm(got[v] - ref[v]) <= TAU_2D * s1 * np.linalg.norm(X[v])
