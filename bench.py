@@ -12,9 +12,10 @@ largest 1D configuration; DESIGN.md "Benchmark workload" says why).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
 
-Multi-GPU (torchrun, one rank per GPU): the build is sharded by intervals
-(no communication), the factors are all-gathered once, and Parareal is
-sharded by source terms (C4's 64 sources share G').
+Multi-GPU (torchrun, one rank per GPU): intervals are sharded over the ranks.
+The build needs no communication; Parareal exchanges only the interval-
+boundary blocks (P2P) and the k-dimensional sweep data (all-gather) --
+paper_2508_08873_b200/parallel.py.  Strong scaling: the config is fixed.
 """
 from __future__ import annotations
 
@@ -119,9 +120,9 @@ class Workload:
         from paper_2508_08873_b200 import Operator, SourceTerm
         from workloads import generators as G
         self.cfg, self.rank, self.world, self.dev = cfg, rank, world, dev
-        # interval shard (build) and source shard (Parareal)
+        # interval shard: the build and the Parareal fine solves of intervals q0..q0+nq-1
         self.q0, self.nq = _shard(cfg.N, rank, world)
-        self.s0, self.ns = _shard(cfg.nsrc, rank, world)
+        self.s0, self.ns = 0, cfg.nsrc
         u0 = G.initial_value(cfg)
         if cfg.dim == 1:
             self.host = dict(op=G.operator_1d(cfg), sums=G.operator_1d_sums(cfg))
@@ -143,24 +144,34 @@ class Workload:
         self.u0 = torch.tensor(self.host["u0"], dtype=torch.float64, device=dev)
 
     def dof_steps(self) -> float:
+        """Fine-solve DOF-steps this rank performs per step."""
         c = self.cfg
         build = self.nq * 2 * c.l * c.n_dof * c.m
-        par = (c.K + 1) * c.N * self.ns * c.n_dof * c.m
+        par = (c.K + 1) * self.nq * self.ns * c.n_dof * c.m
         return float(build + par)
 
-    def step(self, events=None):
-        """rSVD build (own intervals) [+ all-gather] + Parareal (own sources)."""
+    def step(self, events=None, op=None, src=None, u0=None):
+        """rSVD build of the own intervals + Parareal (1 GPU: pr_parareal; N GPUs:
+        the interval-sharded orchestration of paper_2508_08873_b200.parallel)."""
         from paper_2508_08873_b200 import Coarse, parareal
         c = self.cfg
-        G = Coarse.build(self.op, c.N, c.m, c.k, c.p, c.seed_omega, first_interval=self.q0,
+        op = op or self.op
+        src = src or self.src
+        u0 = self.u0 if u0 is None else u0
+        G = Coarse.build(op, c.N, c.m, c.k, c.p, c.seed_omega, first_interval=self.q0,
                          n_local=self.nq)
-        if self.world > 1:
-            G = _allgather_coarse(G, self)
         if events is not None:
             events.append(_event())
-        upd, bn = parareal(G, self.op, self.u0, self.src, c.K, self.U, nsrc=self.ns)
+        if self.world == 1:
+            upd, bn = parareal(G, op, u0, src, c.K, self.U, nsrc=self.ns)
+        else:
+            from paper_2508_08873_b200.parallel import Blocks, Comm, LibprBackend, parareal_sharded
+            be = LibprBackend(op, G, c.N, self.q0, self.nq, c.m, c.k, self.ns, src)
+            rows = op.rows
+            blocks = Blocks(c.dim, rows, self.ns, self.dev)
+            self.U, upd = parareal_sharded(be, blocks, u0, c.K, Comm())
         G.close()
-        return upd, bn
+        return self.U
 
 
 def _fp64_peak(dev):
@@ -193,10 +204,6 @@ def _event():
     e = torch.cuda.Event(enable_timing=True)
     e.record()
     return e
-
-
-def _allgather_coarse(G, wl):
-    raise NotImplementedError("multi-GPU factor all-gather is not built yet")
 
 
 # ----------------------------------------------------------- CPU oracle leg
@@ -254,7 +261,7 @@ def main():
               "p": cfg.p, "K": cfg.K, "nsrc": cfg.nsrc, "T": cfg.T,
               "l2": "inputs larger than L2: %.2f GB state per stepper phase vs 126 MB L2"
                     % (cfg.n_dof * cfg.N * max(cfg.l, cfg.nsrc) * 8 / 1e9),
-              "parallelism": f"intervals+sources sharded over {args.gpus} GPU(s)"}
+              "parallelism": f"intervals sharded over {args.gpus} GPU(s) (P2P halos + all-gather of sweep data)"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -424,13 +431,8 @@ def _e2e(wl, steps, barrier, world):
             op = Operator.sep2d(c.n, c.dt)
             src = SourceTerm(2, dv["gx"].shape[0], 1, dv["gx"].shape[1],
                              {"gx": dv["gx"], "gy": dv["gy"]})
-        G = Coarse.build(op, c.N, c.m, c.k, c.p, c.seed_omega, first_interval=wl.q0,
-                         n_local=wl.nq)
-        if world > 1:
-            G = _allgather_coarse(G, wl)
-        upd, bn = parareal(G, op, dv["u0"], src, c.K, wl.U, nsrc=wl.ns)
-        out_host.copy_(wl.U, non_blocking=True)
-        G.close()
+        U = wl.step(op=op, src=src, u0=dv["u0"])
+        out_host.copy_(U, non_blocking=True)
         op.close()
     e1 = _event()
     barrier()

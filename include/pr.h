@@ -221,6 +221,41 @@ pr_status pr_parareal(pr_coarse G, pr_op op, int nsrc, const double *u0, long ld
                       double *upd_host, double *bnorm_host, double *hist, long hist_stride,
                       void *stream);
 
+/* ------------------------------------------------- distributed building blocks
+ * Stages of pr_parareal on the intervals a handle owns (first .. first+n_local-1),
+ * for an interval-sharded Parareal over several GPUs.  Arrays
+ * hold "blocks" of nsrc vectors (op layout, stride ld): block i of an
+ * input-side array belongs to boundary first+i (u_q, Fu_q), block i of an
+ * output-side array to boundary first+i+1.  All device pointers, asynchronous. */
+
+/* C_q = Sigma_q V_q^T U_{q-1} for the local q; for q = first, U_{first-1} is
+ * U_prev (rows x k row-major, e.g. the left neighbour's last U block; NULL ->
+ * C_first = 0, correct for first == 0).  pr_build_coarse already computes the
+ * C_q that need no neighbour. */
+pr_status pr_coarse_sweep_matrices(pr_coarse G, const double *U_prev, void *stream);
+
+/* Device copies of the handle's data (each pointer nullable): U, V as
+ * (n_local, rows, k), sigma (n_local, l), C (n_local, k, k). */
+pr_status pr_coarse_export(pr_coarse G, double *U, double *V, double *sigma, double *C, void *stream);
+
+/* Device copies of U_q and V_q (rows x k each, nullable) of local interval q_local. */
+pr_status pr_coarse_export_interval(pr_coarse G, int q_local, double *U_q, double *V_q, void *stream);
+
+/* d_i = Sigma_q V_q^T (Y2_i - Y1_i), q = first + i, i < n_local: d is
+ * (n_local, k, nsrc).  Y1 == NULL means zero (initialisation). */
+pr_status pr_coarse_project(pr_coarse G, int nsrc, const double *Y1, const double *Y2, long ld,
+                            double *d, void *stream);
+
+/* e_j = C_j e_{j-1} + d_j, j = 0..N-1, e_{-1} = 0 (C_0 ignored): the sequential
+ * coarse sweep in reduced coordinates; C (N, k, k), d and e (N, k, nsrc). */
+pr_status pr_reduced_sweep(const double *C, const double *d, int N, int k, int nsrc, double *e,
+                           void *stream);
+
+/* out_i = Fu_i + U_q e_i (q = first + i; Fu, out output-side blocks), and, if
+ * upd != NULL, upd[i*nsrc + s] = ||out_i,s(new) - out_i,s(old)||. */
+pr_status pr_coarse_expand(pr_coarse G, int nsrc, const double *Fu, const double *e, double *out,
+                           long ld, double *upd, void *stream);
+
 /* --------------------------------------------------------------------- bounds */
 
 /* Host only.  delta, eps (eq. bounds_delta_eps), bnorm[m] = ||b_m|| (b_0 =

@@ -22,7 +22,8 @@ PR_SRC_NONE, PR_SRC_SEP1D, PR_SRC_BUMP2D = 0, 1, 2
 EXPORTS = ["pr_last_error", "pr_version", "pr_profile", "pr_counters", "pr_op_create_tridiag", "pr_op_create_sep2d",
            "pr_op_destroy", "pr_op_info", "pr_fine_propagate", "pr_gaussian_sketch",
            "pr_build_coarse", "pr_coarse_info", "pr_coarse_factors", "pr_coarse_apply",
-           "pr_coarse_destroy", "pr_parareal", "pr_bounds"]
+           "pr_coarse_destroy", "pr_parareal", "pr_bounds", "pr_coarse_sweep_matrices",
+           "pr_coarse_export", "pr_coarse_export_interval", "pr_coarse_project", "pr_reduced_sweep", "pr_coarse_expand"]
 
 
 class PrError(RuntimeError):
@@ -70,6 +71,12 @@ def lib():
             "pr_coarse_destroy": ([vp], I),
             "pr_parareal": ([vp, vp, I, vp, lg, ctypes.POINTER(Source), I, vp, lg, dp, dp, vp, lg, vp], I),
             "pr_bounds": ([D, D, I, I, dp, dp, dp, dp, dp], I),
+            "pr_coarse_sweep_matrices": ([vp, vp, vp], I),
+            "pr_coarse_export": ([vp, vp, vp, vp, vp, vp], I),
+            "pr_coarse_export_interval": ([vp, I, vp, vp, vp], I),
+            "pr_coarse_project": ([vp, I, vp, vp, lg, vp, vp], I),
+            "pr_reduced_sweep": ([vp, vp, I, I, I, vp, vp], I),
+            "pr_coarse_expand": ([vp, I, vp, vp, vp, lg, vp, vp], I),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

@@ -171,6 +171,27 @@ class Coarse:
                                       _ptr(Y), _ld(Y, dim), _stream(stream)), "pr_coarse_apply")
         return Y
 
+    # ---- distributed building blocks (include/pr.h) ----
+    def sweep_matrices(self, U_prev=None, stream=None):
+        check(L.lib().pr_coarse_sweep_matrices(self._h, _ptr(U_prev), _stream(stream)),
+              "pr_coarse_sweep_matrices")
+
+    def export(self, U=None, V=None, sigma=None, C=None, stream=None):
+        check(L.lib().pr_coarse_export(self._h, _ptr(U), _ptr(V), _ptr(sigma), _ptr(C),
+                                       _stream(stream)), "pr_coarse_export")
+
+    def export_interval(self, q_local: int, U_q=None, V_q=None, stream=None):
+        check(L.lib().pr_coarse_export_interval(self._h, int(q_local), _ptr(U_q), _ptr(V_q),
+                                                _stream(stream)), "pr_coarse_export_interval")
+
+    def project(self, nsrc: int, Y1, Y2, ld: int, d, stream=None):
+        check(L.lib().pr_coarse_project(self._h, int(nsrc), _ptr(Y1), _ptr(Y2), int(ld), _ptr(d),
+                                        _stream(stream)), "pr_coarse_project")
+
+    def expand(self, nsrc: int, Fu, e, out, ld: int, upd=None, stream=None):
+        check(L.lib().pr_coarse_expand(self._h, int(nsrc), _ptr(Fu), _ptr(e), _ptr(out), int(ld),
+                                       _ptr(upd), _stream(stream)), "pr_coarse_expand")
+
     def close(self):
         if self._h:
             L.lib().pr_coarse_destroy(self._h)
@@ -228,3 +249,8 @@ def counters(reset: bool = False) -> dict:
                               ctypes.byref(ms), ctypes.byref(dof), ctypes.byref(fl)), "pr_counters")
     return dict(kernel_launches=kl.value, stepper_launches=sl.value, stepper_ms=ms.value,
                 stepper_dof_steps=dof.value, stepper_flops=fl.value)
+
+
+def reduced_sweep(C, d, N: int, k: int, nsrc: int, e, stream=None):
+    check(L.lib().pr_reduced_sweep(_ptr(C), _ptr(d), int(N), int(k), int(nsrc), _ptr(e),
+                                   _stream(stream)), "pr_reduced_sweep")

@@ -724,6 +724,102 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
     return PR_OK;
 }
 
+// ------------------------------------------------------ distributed stages
+pr_status pr_coarse_sweep_matrices(pr_coarse G, const double *U_prev, void *stream)
+{
+    PR_REQUIRE(G, PR_EINVAL, "NULL handle");
+    cudaStream_t s = (cudaStream_t)stream;
+    const long rows = G->rows;
+    const int k = G->k;
+    Scratch S;
+    if (!U_prev) {
+        PR_CUDA(cudaMemsetAsync(G->C, 0, (size_t)k * k * sizeof(double), s));
+        return PR_OK;
+    }
+    int nchunk = xty_chunks(rows, 1);
+    long cr = (rows + nchunk - 1) / nchunk;
+    double *part;
+    PR_ALLOC(part, double, (size_t)nchunk * k * k, S);
+    XtY x{nullptr, G->V, 0, k, 1, k, U_prev, 0, k, 1, k, rows, 1, nchunk, cr, part};
+    PR_CUDA(launch_xty(x, s));
+    PR_CUDA(launch_reduce_parts(part, 1, nchunk, k, k, G->sigma, 0, G->C, s));
+    return PR_OK;
+}
+
+pr_status pr_coarse_export(pr_coarse G, double *U, double *V, double *sigma, double *C, void *stream)
+{
+    PR_REQUIRE(G, PR_EINVAL, "NULL handle");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t f = (size_t)G->nloc * G->rows * G->k * sizeof(double);
+    if (U) PR_CUDA(cudaMemcpyAsync(U, G->U, f, cudaMemcpyDeviceToDevice, s));
+    if (V) PR_CUDA(cudaMemcpyAsync(V, G->V, f, cudaMemcpyDeviceToDevice, s));
+    if (sigma) PR_CUDA(cudaMemcpyAsync(sigma, G->sigma, (size_t)G->nloc * G->l * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (C) PR_CUDA(cudaMemcpyAsync(C, G->C, (size_t)G->nloc * G->k * G->k * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return PR_OK;
+}
+
+pr_status pr_coarse_export_interval(pr_coarse G, int q_local, double *U_q, double *V_q, void *stream)
+{
+    PR_REQUIRE(G && q_local >= 0 && q_local < G->nloc, PR_EINVAL, "bad handle or interval");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t f = (size_t)G->rows * G->k;
+    if (U_q) PR_CUDA(cudaMemcpyAsync(U_q, G->U + q_local * f, f * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (V_q) PR_CUDA(cudaMemcpyAsync(V_q, G->V + q_local * f, f * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    return PR_OK;
+}
+
+pr_status pr_coarse_project(pr_coarse G, int nsrc, const double *Y1, const double *Y2, long ld,
+                            double *d, void *stream)
+{
+    PR_REQUIRE(G && Y2 && d, PR_EINVAL, "NULL argument");
+    PR_REQUIRE(nsrc >= 1 && nsrc <= 128, PR_EINVAL, "nsrc must be 1..128");
+    const long rows = G->rows;
+    const int k = G->k, N = G->nloc, S = nsrc;
+    PR_REQUIRE(ld >= (G->dim == 1 ? (long)N * S : rows), PR_EDIM, "ld too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    Scratch Sc;
+    const Lay L = (G->dim == 1) ? Lay{ld, 1} : Lay{1, ld};
+    const long blk = (G->dim == 1) ? (long)S : (long)S * ld;
+    const int nchunk = xty_chunks(rows, N);
+    const long cr = (rows + nchunk - 1) / nchunk;
+    double *part;
+    PR_ALLOC(part, double, (size_t)N * nchunk * k * 2 * S, Sc);
+    XtY x{nullptr, G->V, rows * k, k, 1, k, Y1 ? Y1 : Y2, blk, L.rs, L.vs, S, rows, N, nchunk, cr, part};
+    if (Y1) { x.Y2 = Y2; x.c2 = S; }
+    PR_CUDA(launch_xty(x, s));
+    PR_CUDA(launch_reduce_pq(part, N, nchunk, k, S, Y1 ? S : 0, G->sigma, G->l, d, s));
+    return PR_OK;
+}
+
+pr_status pr_reduced_sweep(const double *C, const double *d, int N, int k, int nsrc, double *e,
+                           void *stream)
+{
+    PR_REQUIRE(C && d && e && N >= 1 && k >= 1 && nsrc >= 1, PR_EINVAL, "bad sweep arguments");
+    PR_CUDA(launch_sweep(C, d, N, k, nsrc, e, (cudaStream_t)stream));
+    return PR_OK;
+}
+
+pr_status pr_coarse_expand(pr_coarse G, int nsrc, const double *Fu, const double *e, double *out,
+                           long ld, double *upd, void *stream)
+{
+    PR_REQUIRE(G && Fu && e && out, PR_EINVAL, "NULL argument");
+    PR_REQUIRE(nsrc >= 1 && nsrc <= 128, PR_EINVAL, "nsrc must be 1..128");
+    const long rows = G->rows;
+    const int k = G->k, N = G->nloc, S = nsrc;
+    PR_REQUIRE(ld >= (G->dim == 1 ? (long)N * S : rows), PR_EDIM, "ld too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    Scratch Sc;
+    const Lay L = (G->dim == 1) ? Lay{ld, 1} : Lay{1, ld};
+    const int nchunk = xty_chunks(rows, N);
+    const long cr = (rows + nchunk - 1) / nchunk;
+    double *npart = nullptr;
+    if (upd) PR_ALLOC(npart, double, (size_t)N * S * nchunk, Sc);
+    Expand ex{out, L.rs, L.vs, Fu, L.rs, L.vs, G->U, rows * k, e, k, S, N, rows, nchunk, cr, npart};
+    PR_CUDA(launch_expand(ex, s));
+    if (upd) PR_CUDA(launch_norm_finish(npart, N * S, nchunk, upd, s));
+    return PR_OK;
+}
+
 // ------------------------------------------------------------------ bounds
 static double log_binom(int n, int k)
 {
