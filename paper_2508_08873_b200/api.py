@@ -35,7 +35,10 @@ def _hptr(a: np.ndarray):
 
 def _ld(t, dim: int) -> int:
     """Leading dimension of a 1D (n, ld) or 2D (B, ld) batch tensor."""
-    assert t.dim() == 2 and t.stride(1) == 1, "batch tensors must be 2D with unit inner stride"
+    assert t.dim() == 2 and (t.stride(1) == 1 or t.shape[1] == 1), \
+        "batch tensors must be 2D with unit inner stride"
+    if t.shape[0] == 1:             # a single row: any leading stride >= its length works
+        return max(int(t.stride(0)), int(t.shape[1]))
     return int(t.stride(0))
 
 
