@@ -319,53 +319,91 @@ cudaError_t launch_chol(const CholArgs &a, cudaStream_t s)
     return cudaGetLastError();
 }
 
-// Q <- Q R^{-1} row by row (forward substitution q R = y), one thread per row.
-constexpr int TS_ROWS = 64;
+// Q <- Q R^{-1} row by row: q R = y by right-looking substitution in column
+// blocks of TB = 32.  For block B the 32 unknowns live in registers: first the
+// contributions of all earlier blocks, y_j2 -= q_j R_j,j2 (q_j read back from
+// the row's shared-memory copy), then the in-block solve
+//   q_j = y_j / R_jj,  y_j2 -= q_j R_j,j2  (j2 > j, fully unrolled).
+// All updates of a column are independent FMAs; R rows are warp broadcasts.
+// A CTA loads R once and sweeps a chunk of TS_CHUNK rows in tiles of one row
+// per thread (R is l^2 doubles: reloading it per small tile dominated).
+constexpr int TB = 32;
+constexpr long TS_CHUNK = 2048;
 
-__global__ void __launch_bounds__(TS_ROWS) k_trsm(double *Q, long bs, long rs, long cs, long rows,
-                                                  int l, const double *R, const int *act)
+__global__ void __launch_bounds__(128) k_trsm(double *Q, long bs, long rs, long cs, long rows, int l,
+                                              const double *R, const int *act)
 {
     extern __shared__ __align__(16) double sm[];
     const int b = blockIdx.y;
     if (!act[b]) return;
-    double *Rs = sm;                    // l x l
-    double *Ys = sm + l * l;            // TS_ROWS x (l+1)
-    const int ld = l + 1;
+    const int nt = blockDim.x;
+    const int LP = (l + TB - 1) / TB * TB;   // padded width
+    double *Rs = sm;                          // LP x LP, diag = 1/R_jj, zero padded
+    double *Ys = sm + (size_t)LP * LP;        // nt x (LP + 1)
+    const int ld = LP + 1;
     const double *Rb = R + (long)b * l * l;
-    for (int e = threadIdx.x; e < l * l; e += TS_ROWS) Rs[e] = Rb[e];
-    const long r0 = (long)blockIdx.x * TS_ROWS;
+    for (int e = threadIdx.x; e < LP * LP; e += nt) {
+        const int i = e / LP, j = e % LP;
+        double v = 0.0;
+        if (i < l && j < l) v = (i == j) ? 1.0 / Rb[(long)i * l + j] : Rb[(long)i * l + j];
+        else if (i == j) v = 1.0;
+        Rs[e] = v;
+    }
     double *Qb = Q + (long)b * bs;
-    for (int e = threadIdx.x; e < TS_ROWS * l; e += TS_ROWS) {
-        int r, j;
-        if (cs == 1) { r = e / l; j = e % l; } else { j = e / TS_ROWS; r = e % TS_ROWS; }
-        long row = r0 + r;
-        Ys[r * ld + j] = (row < rows) ? Qb[row * rs + (long)j * cs] : 0.0;
-    }
-    __syncthreads();
-    double *y = Ys + threadIdx.x * ld;
-    for (int j = 0; j < l; ++j) {
-        double t = y[j];
-        for (int i = 0; i < j; ++i) t = fma(-y[i], Rs[i * l + j], t);
-        y[j] = t / Rs[j * l + j];
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < TS_ROWS * l; e += TS_ROWS) {
-        int r, j;
-        if (cs == 1) { r = e / l; j = e % l; } else { j = e / TS_ROWS; r = e % TS_ROWS; }
-        long row = r0 + r;
-        if (row < rows) Qb[row * rs + (long)j * cs] = Ys[r * ld + j];
+    const long c0 = (long)blockIdx.x * TS_CHUNK;
+    const long c1 = min(rows, c0 + TS_CHUNK);
+    double *yr = Ys + threadIdx.x * ld;
+    for (long r0 = c0; r0 < c1; r0 += nt) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < nt * LP; e += nt) {
+            int r, j;
+            if (cs == 1) { r = e / LP; j = e % LP; } else { j = e / nt; r = e % nt; }
+            const long row = r0 + r;
+            Ys[r * ld + j] = (row < c1 && j < l) ? Qb[row * rs + (long)j * cs] : 0.0;
+        }
+        __syncthreads();
+        for (int B = 0; B < LP; B += TB) {
+            double y[TB];
+#pragma unroll
+            for (int t = 0; t < TB; ++t) y[t] = yr[B + t];
+            for (int j = 0; j < B; ++j) {                 // earlier blocks
+                const double qj = -yr[j];
+                const double *Rj = Rs + (size_t)j * LP + B;
+#pragma unroll
+                for (int t = 0; t < TB; ++t) y[t] = fma(qj, Rj[t], y[t]);
+            }
+#pragma unroll
+            for (int t = 0; t < TB; ++t) {                // in-block solve
+                const double *Rj = Rs + (size_t)(B + t) * LP + B;
+                y[t] *= Rj[t];
+                const double qj = -y[t];
+#pragma unroll
+                for (int t2 = t + 1; t2 < TB; ++t2) y[t2] = fma(qj, Rj[t2], y[t2]);
+            }
+#pragma unroll
+            for (int t = 0; t < TB; ++t) yr[B + t] = y[t];
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < nt * LP; e += nt) {
+            int r, j;
+            if (cs == 1) { r = e / LP; j = e % LP; } else { j = e / nt; r = e % nt; }
+            const long row = r0 + r;
+            if (row < c1 && j < l) Qb[row * rs + (long)j * cs] = Ys[r * ld + j];
+        }
     }
 }
 
 cudaError_t launch_trsm(double *Q, long bs, long rs, long cs, long rows, int l, int nbatch,
                         const double *R, const int *act, cudaStream_t s)
 {
-    size_t smem = ((size_t)l * l + (size_t)TS_ROWS * (l + 1)) * sizeof(double);
+    const int LP = (l + TB - 1) / TB * TB;
+    const int nt = (LP <= 96) ? 128 : 64;
+    size_t smem = ((size_t)LP * LP + (size_t)nt * (LP + 1)) * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)((rows + TS_ROWS - 1) / TS_ROWS), nbatch);
+    dim3 grid((unsigned)((rows + TS_CHUNK - 1) / TS_CHUNK), nbatch);
     note_launch();
-    k_trsm<<<grid, TS_ROWS, smem, s>>>(Q, bs, rs, cs, rows, l, R, act);
+    k_trsm<<<grid, nt, smem, s>>>(Q, bs, rs, cs, rows, l, R, act);
     return cudaGetLastError();
 }
 
@@ -742,8 +780,198 @@ __global__ void __launch_bounds__(EX_THREADS) k_expand(Expand a)
     }
 }
 
+// Wide variant (S >= 16): CTA tile 64 rows x 64 sources, each thread 4 x 4
+// outputs; U tile stored transposed so 4 rows are one 32-B smem read.
+constexpr int EW_ROWS = 64;
+constexpr int EW_SRC = 64;
+
+__global__ void __launch_bounds__(256) k_expand_wide(Expand a)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int b = blockIdx.y, t = blockIdx.x;
+    const int k = a.k, S = a.S;
+    const int UST = EW_ROWS + 2;              // Ut[r][row], row stride (16-B aligned)
+    double *Ut = sm;                          // k x UST
+    double *Es = sm + (size_t)k * UST;        // k x EW_SRC (one source tile)
+    double *red = Es + (size_t)k * EW_SRC;    // 16 x 64
+    const int tr = threadIdx.x / 16, ts = threadIdx.x % 16;
+    const long r0 = (long)t * a.chunk_rows;
+    long r1 = r0 + a.chunk_rows;
+    if (r1 > a.rows) r1 = a.rows;
+    const double *__restrict__ Ub = a.U + (long)b * a.Ubs;
+    const double *__restrict__ base = a.base;
+    double *__restrict__ out = a.out;
+    const bool norms = a.normpart != nullptr;
+    const double *eb = a.e + (long)b * k * S;
+    for (int sb = 0; sb < S; sb += EW_SRC) {                  // source tiles
+        const int ns = min(EW_SRC, S - sb);
+        __syncthreads();
+        for (int i = threadIdx.x; i < k * EW_SRC; i += 256) {
+            const int r = i / EW_SRC, c = i % EW_SRC;
+            Es[i] = (c < ns) ? eb[(long)r * S + sb + c] : 0.0;
+        }
+        double nrm[4] = {0.0, 0.0, 0.0, 0.0};
+        const int s0 = 4 * ts;
+        const int nj = max(0, min(4, ns - s0));
+        const long v0 = (long)b * S + sb + s0;
+        for (long rt = r0; rt < r1; rt += EW_ROWS) {
+            const int nr = (int)min((long)EW_ROWS, r1 - rt);
+            __syncthreads();
+            const double *ut = Ub + rt * k;
+            for (int i = threadIdx.x; i < nr * k; i += 256) {
+                const int row = i / k, r = i % k;
+                Ut[r * UST + row] = ut[i];
+            }
+            for (int i = threadIdx.x; i < (EW_ROWS - nr) * k; i += 256) {
+                const int row = nr + i / k, r = i % k;
+                Ut[r * UST + row] = 0.0;
+            }
+            // global loads of base / old values first (memory-level parallelism)
+            double bv[4][4], ov[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int rl = 4 * tr + q;
+                const long row = rt + rl;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const bool ok = (rl < nr) && (j < nj);
+                    bv[q][j] = (ok && base) ? base[row * a.brs + (v0 + j) * a.bvs] : 0.0;
+                    ov[q][j] = (ok && norms) ? out[row * a.ors + (v0 + j) * a.ovs] : 0.0;
+                }
+            }
+            __syncthreads();
+            double acc[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[q][j] = bv[q][j];
+#pragma unroll 4
+            for (int r = 0; r < k; ++r) {
+                const double2 u01 = *reinterpret_cast<const double2 *>(Ut + r * UST + 4 * tr);
+                const double2 u23 = *reinterpret_cast<const double2 *>(Ut + r * UST + 4 * tr + 2);
+                const double2 e01 = *reinterpret_cast<const double2 *>(Es + r * EW_SRC + s0);
+                const double2 e23 = *reinterpret_cast<const double2 *>(Es + r * EW_SRC + s0 + 2);
+                const double uu[4] = {u01.x, u01.y, u23.x, u23.y};
+                const double ee[4] = {e01.x, e01.y, e23.x, e23.y};
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[q][j] = fma(uu[q], ee[j], acc[q][j]);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int rl = 4 * tr + q;
+                if (rl >= nr) break;
+                const long row = rt + rl;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (j < nj) {
+                        if (norms) {
+                            const double dl = acc[q][j] - ov[q][j];
+                            nrm[j] = fma(dl, dl, nrm[j]);
+                        }
+                        out[row * a.ors + (v0 + j) * a.ovs] = acc[q][j];
+                    }
+                }
+            }
+        }
+        if (norms) {
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < 4; ++j) red[tr * EW_SRC + s0 + j] = nrm[j];
+            __syncthreads();
+            if (tr == 0) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (j >= nj) break;
+                    double sum = 0.0;
+                    for (int y = 0; y < 16; ++y) sum += red[y * EW_SRC + s0 + j];
+                    a.normpart[((long)b * S + sb + s0 + j) * a.nchunk + t] = sum;
+                }
+            }
+        }
+    }
+}
+
+// Narrow variant (S < 16): one row per thread, the row of U_b read straight
+// from global memory (contiguous k doubles, 16-B loads), e_b broadcast from
+// shared memory, four independent partial sums per output.
+__global__ void __launch_bounds__(256) k_expand_narrow(Expand a)
+{
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double red[256];
+    const int b = blockIdx.y, t = blockIdx.x;
+    const int k = a.k, S = a.S;
+    double *es = sm;   // k x S
+    const double *eb = a.e + (long)b * k * S;
+    for (int i = threadIdx.x; i < k * S; i += 256) es[i] = eb[i];
+    __syncthreads();
+    const long r0 = (long)t * a.chunk_rows;
+    long r1 = r0 + a.chunk_rows;
+    if (r1 > a.rows) r1 = a.rows;
+    const double *__restrict__ Ub = a.U + (long)b * a.Ubs;
+    const bool norms = a.normpart != nullptr;
+    const bool vec = (k % 2 == 0);
+    for (int s = 0; s < S; ++s) {
+        const long v = (long)b * S + s;
+        double nrm = 0.0;
+        for (long row = r0 + threadIdx.x; row < r1; row += 256) {
+            const double *ur = Ub + row * k;
+            double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+            int r = 0;
+            if (vec) {
+                for (; r + 3 < k; r += 4) {
+                    const double2 u01 = *reinterpret_cast<const double2 *>(ur + r);
+                    const double2 u23 = *reinterpret_cast<const double2 *>(ur + r + 2);
+                    c0 = fma(u01.x, es[r * S + s], c0);
+                    c1 = fma(u01.y, es[(r + 1) * S + s], c1);
+                    c2 = fma(u23.x, es[(r + 2) * S + s], c2);
+                    c3 = fma(u23.y, es[(r + 3) * S + s], c3);
+                }
+            }
+            for (; r < k; ++r) c0 = fma(ur[r], es[r * S + s], c0);
+            double val = (c0 + c1) + (c2 + c3);
+            if (a.base) val += a.base[row * a.brs + v * a.bvs];
+            double *o = a.out + row * a.ors + v * a.ovs;
+            if (norms) {
+                const double dl = val - *o;
+                nrm = fma(dl, dl, nrm);
+            }
+            *o = val;
+        }
+        if (norms) {
+            red[threadIdx.x] = nrm;
+            __syncthreads();
+            for (int w = 128; w > 0; w >>= 1) {
+                if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+                __syncthreads();
+            }
+            if (threadIdx.x == 0) a.normpart[v * a.nchunk + t] = red[0];
+            __syncthreads();
+        }
+    }
+}
+
 cudaError_t launch_expand(const Expand &a, cudaStream_t s)
 {
+    if (a.S < 16 && ((uintptr_t)a.U & 15) == 0 && a.k % 2 == 0) {
+        size_t smem = (size_t)a.k * a.S * sizeof(double);
+        cudaError_t e = cudaFuncSetAttribute(k_expand_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        dim3 grid(a.nchunk, a.nbatch);
+        note_launch();
+        k_expand_narrow<<<grid, 256, smem, s>>>(a);
+        return cudaGetLastError();
+    }
+    if (a.S >= 16 && a.k <= 128) {
+        size_t smem = ((size_t)a.k * (EW_ROWS + 2) + (size_t)a.k * EW_SRC + 16 * EW_SRC) * sizeof(double);
+        cudaError_t e = cudaFuncSetAttribute(k_expand_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        dim3 grid(a.nchunk, a.nbatch);
+        note_launch();
+        k_expand_wide<<<grid, 256, smem, s>>>(a);
+        return cudaGetLastError();
+    }
     if (a.S > 128 || a.k > 128) return cudaErrorInvalidValue;
     const int S4 = (a.S + 3) & ~3;
     const int NS4 = S4 / 4;

@@ -180,33 +180,39 @@ static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double 
     PR_ALLOC(state, int, nb, S);
     PR_ALLOC(act, int, nb, S);
     PR_ALLOC(active, int, 1, S);
-    int *h_active = nullptr;
-    PR_CUDA(cudaMallocHost(&h_active, sizeof(int)));
-    struct HostFree { int *p; ~HostFree() { cudaFreeHost(p); } } hf{h_active};
+    // pinned landing slot for the device "active" counter (allocated once per thread)
+    static thread_local int *h_active = nullptr;
+    if (!h_active) PR_CUDA(cudaMallocHost(&h_active, sizeof(int)));
     PR_CUDA(cudaMemsetAsync(state, 0, nb * sizeof(int), s));
     if (Rtot) PR_CUDA(launch_eye(Rtot, nb, l, s));
-    int pass = 0;
+    // Passes are enqueued in groups before the host reads the counter: blocks
+    // that are done skip every kernel of later passes, so a speculative pass
+    // costs only its launches, while each host read costs a stream sync.
+    int pass = 0, done_at = 0;
+    const int group = 3;
     for (;;) {
-        ++pass;
-        XtY x{state, Q, xbs, L.rs, L.vs, l, Q, xbs, L.rs, L.vs, l, rows, nb, nchunk, chunk_rows, part};
-        PR_CUDA(launch_xty(x, s));
-        stage("qr gram", s);
-        PR_CUDA(cudaMemsetAsync(active, 0, sizeof(int), s));
-        CholArgs c{part, nchunk, nb, l, rows, state, act, R, Rtot, active, fail};
-        PR_CUDA(launch_chol(c, s));
-        stage("qr chol", s);
-        PR_CUDA(launch_trsm(Q, xbs, L.rs, L.vs, rows, l, nb, R, act, s));
-        stage("qr trsm", s);
+        for (int g = 0; g < group; ++g) {
+            ++pass;
+            XtY x{state, Q, xbs, L.rs, L.vs, l, Q, xbs, L.rs, L.vs, l, rows, nb, nchunk, chunk_rows, part};
+            PR_CUDA(launch_xty(x, s));
+            stage("qr gram", s);
+            PR_CUDA(cudaMemsetAsync(active, 0, sizeof(int), s));
+            CholArgs c{part, nchunk, nb, l, rows, state, act, R, Rtot, active, fail};
+            PR_CUDA(launch_chol(c, s));
+            stage("qr chol", s);
+            PR_CUDA(launch_trsm(Q, xbs, L.rs, L.vs, rows, l, nb, R, act, s));
+            stage("qr trsm", s);
+        }
         PR_CUDA(cudaMemcpyAsync(h_active, active, sizeof(int), cudaMemcpyDeviceToHost, s));
         PR_CUDA(cudaStreamSynchronize(s));
-        if (*h_active == 0) break;
+        if (*h_active == 0) { done_at = pass; break; }
         if (pass >= 24) {
             set_error("CholeskyQR did not converge in 24 passes");
             if (passes_out) *passes_out = pass;
             return PR_ENOCONV;
         }
     }
-    if (passes_out) *passes_out = pass;
+    if (passes_out) *passes_out = done_at;
     return PR_OK;
 }
 
