@@ -183,19 +183,19 @@ cudaError_t launch_sketch(int dim, int n, long rows, int q0, int nint, int l,
     return cudaGetLastError();
 }
 
-__global__ void k_transpose(const double *in, int R, int n, double *out)
+__global__ void k_transpose(const double *in, int R, int n, double *out, int ldo)
 {
     long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= (long)R * n) return;
-    int r = (int)(t / n), i = (int)(t % n);
-    out[(long)i * R + r] = in[t];
+    if (t >= (long)ldo * n) return;
+    int i = (int)(t / ldo), r = (int)(t % ldo);
+    out[t] = (r < R) ? in[(long)r * n + i] : 0.0;     // zero-padded columns
 }
 
-cudaError_t launch_transpose(const double *in, int R, int n, double *out, cudaStream_t s)
+cudaError_t launch_transpose(const double *in, int R, int n, double *out, int ldo, cudaStream_t s)
 {
-    long total = (long)R * n;
+    long total = (long)ldo * n;
     note_launch();
-    k_transpose<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(in, R, n, out);
+    k_transpose<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(in, R, n, out, ldo);
     return cudaGetLastError();
 }
 
@@ -274,7 +274,7 @@ struct WarpSmem {
 // One pass over all rows.  DOWN: rows ascending.  FIN: finish the previous
 // step (back substitution).  START: start step `step` (forward elimination).
 // LOAD: read the state (else zero).  AFF: source term.  OFF: add offset.
-template <int VPT, bool DOWN, bool FIN, bool START, bool LOAD, bool AFF, bool OFF>
+template <int VPT, bool DOWN, bool FIN, bool START, bool LOAD, int RS, bool OFF>
 __device__ __forceinline__ void run_pass(const StepArgs &a, const WarpSmem &w, const Coef *coefs,
                                          const double *src, long lds, long c0, bool valid,
                                          int lane, const double (*alpha)[VPT])
@@ -284,7 +284,7 @@ __device__ __forceinline__ void run_pass(const StepArgs &a, const WarpSmem &w, c
     const long step_src = DOWN ? lds : -lds;
     const long step_dst = DOWN ? a.ld_out : -a.ld_out;
     const long step_off = DOWN ? a.ld_off : -a.ld_off;
-    const int R = AFF ? a.R : 0;
+    constexpr bool AFF = RS > 0;
 
     auto row_of = [&](int g, int r) -> int {
         int t = g * GR + r;
@@ -314,9 +314,14 @@ __device__ __forceinline__ void run_pass(const StepArgs &a, const WarpSmem &w, c
                 double *cr = w.cring + (size_t)(slot0 + lane) * w.CW;
                 cp_async_16(cr, &coefs[i].a);
                 cp_async_16(cr + 2, &coefs[i].c);
-                if (AFF) {
-                    const double *spc = a.spaceT + (long)i * a.R;
-                    for (int t = 0; t < R; ++t) cp_async_8(cr + 4 + t, spc + t);
+                if constexpr (AFF) {
+                    const double *spc = a.spaceT + (long)i * RS;    // zero-padded to RS columns
+                    if constexpr (RS == 1) {
+                        cp_async_8(cr + 4, spc);
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < RS; t += 2) cp_async_16(cr + 4 + t, spc + t);
+                    }
                 }
             }
         }
@@ -348,14 +353,26 @@ __device__ __forceinline__ void run_pass(const StepArgs &a, const WarpSmem &w, c
             double fs[VPT];
 #pragma unroll
             for (int v = 0; v < VPT; ++v) fs[v] = 0.0;
-            if (AFF) {
+            if constexpr (AFF) {
+                const double *spr = cr + (size_t)r * w.CW + 4;
+                if constexpr (RS == 1) {
 #pragma unroll
-                for (int t = 0; t < 8; ++t) {
-                    if (t < R) {
-                        const double sp = cr[(size_t)r * w.CW + 4 + t];
+                    for (int v = 0; v < VPT; ++v) fs[v] = alpha[0][v] * spr[0];
+                } else {
+                    double fa[VPT];
 #pragma unroll
-                        for (int v = 0; v < VPT; ++v) fs[v] = fma(alpha[t][v], sp, fs[v]);
+                    for (int v = 0; v < VPT; ++v) fa[v] = 0.0;
+#pragma unroll
+                    for (int t = 0; t < RS; t += 2) {
+                        const double2 sp = *reinterpret_cast<const double2 *>(spr + t);
+#pragma unroll
+                        for (int v = 0; v < VPT; ++v) {
+                            fs[v] = fma(alpha[t][v], sp.x, fs[v]);          // two independent
+                            fa[v] = fma(alpha[t + 1][v], sp.y, fa[v]);      // partial sums
+                        }
                     }
+#pragma unroll
+                    for (int v = 0; v < VPT; ++v) fs[v] += fa[v];
                 }
             }
             double res[VPT];
@@ -393,7 +410,7 @@ __device__ __forceinline__ void run_pass(const StepArgs &a, const WarpSmem &w, c
     __syncwarp();
 }
 
-template <int VPT, bool AFF>
+template <int VPT, int RS>
 __global__ void __launch_bounds__(32) k_stepper(StepArgs a)
 {
     extern __shared__ __align__(16) double smem_dyn[];
@@ -402,8 +419,8 @@ __global__ void __launch_bounds__(32) k_stepper(StepArgs a)
     const bool valid = c0 < a.B;      // B % VPT == 0 when VPT > 1
     const bool have_off = a.off != nullptr;
     WarpSmem w;
-    const int Rp = AFF ? ((a.R + 1) & ~1) : 0;
-    w.CW = 4 + Rp;
+    constexpr bool AFF = RS > 0;
+    w.CW = AFF ? 4 + (RS < 2 ? 2 : RS) : 4;
     w.vring = smem_dyn;
     w.oring = smem_dyn + (size_t)RING * GR * 32 * VPT;
     w.cring = smem_dyn + (size_t)(have_off ? 2 : 1) * RING * GR * 32 * VPT;
@@ -417,11 +434,11 @@ __global__ void __launch_bounds__(32) k_stepper(StepArgs a)
         qv[v] = a.q0 + (int)(c / a.vpi);
         srcv[v] = AFF ? (int)(c % a.nsrc) : 0;
     }
-    double alpha[AFF ? 8 : 1][VPT];
+    double alpha[AFF ? RS : 1][VPT];
     auto set_alpha = [&](int step) {      // alpha_r = dt amp[s, r] time[r, g-1] of step `step`
         if constexpr (AFF) {
 #pragma unroll
-            for (int r = 0; r < 8; ++r)
+            for (int r = 0; r < RS; ++r)
 #pragma unroll
                 for (int v = 0; v < VPT; ++v) {
                     double al = 0.0;
@@ -440,21 +457,21 @@ __global__ void __launch_bounds__(32) k_stepper(StepArgs a)
         const Coef *coefs = down ? a.DN : a.UP;
         if (p == 1) {
             if (a.in)
-                run_pass<VPT, true, false, true, true, AFF, false>(a, w, coefs, a.in, a.ld_in, c0, valid, lane, alpha);
+                run_pass<VPT, true, false, true, true, RS, false>(a, w, coefs, a.in, a.ld_in, c0, valid, lane, alpha);
             else
-                run_pass<VPT, true, false, true, false, AFF, false>(a, w, coefs, nullptr, a.ld_out, c0, valid, lane, alpha);
+                run_pass<VPT, true, false, true, false, RS, false>(a, w, coefs, nullptr, a.ld_out, c0, valid, lane, alpha);
         } else if (p <= m) {
             if (down)
-                run_pass<VPT, true, true, true, true, AFF, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                run_pass<VPT, true, true, true, true, RS, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
             else
-                run_pass<VPT, false, true, true, true, AFF, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                run_pass<VPT, false, true, true, true, RS, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
         } else {   // p == m + 1: finish the last step (+ offset)
             if (down) {
-                if (have_off) run_pass<VPT, true, true, false, true, false, true>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
-                else run_pass<VPT, true, true, false, true, false, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                if (have_off) run_pass<VPT, true, true, false, true, 0, true>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                else run_pass<VPT, true, true, false, true, 0, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
             } else {
-                if (have_off) run_pass<VPT, false, true, false, true, false, true>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
-                else run_pass<VPT, false, true, false, true, false, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                if (have_off) run_pass<VPT, false, true, false, true, 0, true>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                else run_pass<VPT, false, true, false, true, 0, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
             }
         }
     }
@@ -472,16 +489,16 @@ __global__ void k_copy_off(const double *in, long ld_in, double *out, long ld_ou
     out[i * ld_out + c] = v;
 }
 
-template <int VPT, bool AFF>
+template <int VPT, int RS>
 static cudaError_t launch_stepper_t(const StepArgs &a, cudaStream_t s)
 {
     long nthreads = (a.B + VPT - 1) / VPT;
     long blocks = (nthreads + 31) / 32;
     if (blocks == 0) return cudaSuccess;
-    const int Rp = AFF ? ((a.R + 1) & ~1) : 0;
+    const int CW = RS > 0 ? 4 + (RS < 2 ? 2 : RS) : 4;
     size_t ring = (size_t)RING * GR * 32 * VPT * sizeof(double);
-    size_t smem = ring * (a.off ? 2 : 1) + (size_t)RING * GR * (4 + Rp) * sizeof(double);
-    auto kern = k_stepper<VPT, AFF>;
+    size_t smem = ring * (a.off ? 2 : 1) + (size_t)RING * GR * CW * sizeof(double);
+    auto kern = k_stepper<VPT, RS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const bool prof = profiling();
@@ -491,6 +508,15 @@ static cudaError_t launch_stepper_t(const StepArgs &a, cudaStream_t s)
     e = cudaGetLastError();
     if (prof) stepper_timed_end(s, (double)a.n * (double)a.B * (double)a.m, 0.0);
     return e;
+}
+
+int stepper_rs(int R)
+{
+    if (R <= 0) return 0;
+    if (R == 1) return 1;
+    if (R == 2) return 2;
+    if (R <= 4) return 4;
+    return 8;
 }
 
 cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s)
@@ -521,12 +547,22 @@ cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s)
         int f = atoi(e);
         if ((f == 1) || (f == 2 && fits(2)) || (f == 4 && fits(4))) vpt = f;
     }
-    const bool aff = a.R > 0;
-    switch (vpt) {
-    case 4: return aff ? launch_stepper_t<4, true>(a, s) : launch_stepper_t<4, false>(a, s);
-    case 2: return aff ? launch_stepper_t<2, true>(a, s) : launch_stepper_t<2, false>(a, s);
-    default: return aff ? launch_stepper_t<1, true>(a, s) : launch_stepper_t<1, false>(a, s);
+    // source terms padded to RS in {1, 2, 4, 8} (spaceT is zero-padded to RS columns)
+    const int rs = stepper_rs(a.R);
+#define STEP_RS(V)                                                  \
+    switch (rs) {                                                   \
+    case 0: return launch_stepper_t<V, 0>(a, s);                    \
+    case 1: return launch_stepper_t<V, 1>(a, s);                    \
+    case 2: return launch_stepper_t<V, 2>(a, s);                    \
+    case 4: return launch_stepper_t<V, 4>(a, s);                    \
+    default: return launch_stepper_t<V, 8>(a, s);                   \
     }
+    switch (vpt) {
+    case 4: STEP_RS(4)
+    case 2: STEP_RS(2)
+    default: STEP_RS(1)
+    }
+#undef STEP_RS
 }
 
 }  // namespace pr

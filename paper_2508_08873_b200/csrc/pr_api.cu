@@ -260,8 +260,9 @@ static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi
     a.dt = op.dt;
     if (mode == PR_AFFINE && f && f->kind == PR_SRC_SEP1D && f->nterms > 0) {
         double *spT;
-        PR_ALLOC(spT, double, (size_t)op.n * f->nterms, S);
-        PR_CUDA(launch_transpose(f->space, f->nterms, op.n, spT, s));
+        const int rsp = stepper_rs(f->nterms);
+        PR_ALLOC(spT, double, (size_t)op.n * rsp, S);
+        PR_CUDA(launch_transpose(f->space, f->nterms, op.n, spT, rsp, s));
         a.R = f->nterms;
         a.spaceT = spT;
         a.time = f->time;

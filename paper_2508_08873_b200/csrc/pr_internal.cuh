@@ -85,7 +85,7 @@ struct StepArgs {
     int vpi;                           // vectors per interval
     // source (PR_SRC_SEP1D) -- R == 0: none
     int R;
-    const double *spaceT;              // (n x R) row-major (transposed copy)
+    const double *spaceT;              // (n x stepper_rs(R)) row-major, zero-padded transpose
     const double *time;                // (R x nsteps)
     const double *amp;                 // (S x R)
     int nsteps;
@@ -99,7 +99,8 @@ cudaError_t launch_factor_1d(int n, const double *subA, const double *supA, cons
 cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s);
 cudaError_t launch_sketch(int dim, int n, long rows, int q0, int nint, int l,
                           unsigned long long seed, double *out, long rs, long vs, cudaStream_t s);
-cudaError_t launch_transpose(const double *in, int R, int n, double *out, cudaStream_t s);
+cudaError_t launch_transpose(const double *in, int R, int n, double *out, int ldo, cudaStream_t s);
+int stepper_rs(int R);   // source-term count padded to 1, 2, 4 or 8
 
 // Tall-skinny cross products: for batch b, chunk t of rows,
 //   part[((b*nchunk + t)*a + i)*c + j] = sum_{rows in chunk} X_b[row, i] * Y_b[row, j]
