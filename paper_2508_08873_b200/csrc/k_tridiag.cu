@@ -209,8 +209,8 @@ cudaError_t launch_transpose(const double *in, int R, int n, double *out, int ld
 // The coefficient row {-a', w, -g, 0} (+ the source's space values) is read
 // from shared memory as a warp-wide broadcast.
 constexpr int GR = 32;     // rows per group
-constexpr int PD = 2;      // groups in flight ahead of the one being computed
-constexpr int RING = PD + 1;
+// PD (groups in flight ahead of the one being computed) is a template
+// parameter: 2 or 4; the ring holds PD + 1 groups.
 
 __device__ __forceinline__ void cp_async_8(void *smem, const void *gmem)
 {
@@ -274,7 +274,7 @@ struct WarpSmem {
 // One pass over all rows.  DOWN: rows ascending.  FIN: finish the previous
 // step (back substitution).  START: start step `step` (forward elimination).
 // LOAD: read the state (else zero).  AFF: source term.  OFF: add offset.
-template <int VPT, bool DOWN, bool FIN, bool START, bool LOAD, int RS, bool OFF>
+template <int VPT, int PD, bool DOWN, bool FIN, bool START, bool LOAD, int RS, bool OFF>
 __device__ __forceinline__ void run_pass(const StepArgs &a, const WarpSmem &w, const Coef *coefs,
                                          const double *src, long lds, long c0, bool valid,
                                          int lane, const double (*alpha)[VPT])
@@ -285,6 +285,7 @@ __device__ __forceinline__ void run_pass(const StepArgs &a, const WarpSmem &w, c
     const long step_dst = DOWN ? a.ld_out : -a.ld_out;
     const long step_off = DOWN ? a.ld_off : -a.ld_off;
     constexpr bool AFF = RS > 0;
+    constexpr int RING = PD + 1;
 
     auto row_of = [&](int g, int r) -> int {
         int t = g * GR + r;
@@ -410,7 +411,7 @@ __device__ __forceinline__ void run_pass(const StepArgs &a, const WarpSmem &w, c
     __syncwarp();
 }
 
-template <int VPT, int RS>
+template <int VPT, int RS, int PD>
 __global__ void __launch_bounds__(32) k_stepper(StepArgs a)
 {
     extern __shared__ __align__(16) double smem_dyn[];
@@ -420,6 +421,7 @@ __global__ void __launch_bounds__(32) k_stepper(StepArgs a)
     const bool have_off = a.off != nullptr;
     WarpSmem w;
     constexpr bool AFF = RS > 0;
+    constexpr int RING = PD + 1;
     w.CW = AFF ? 4 + (RS < 2 ? 2 : RS) : 4;
     w.vring = smem_dyn;
     w.oring = smem_dyn + (size_t)RING * GR * 32 * VPT;
@@ -457,21 +459,21 @@ __global__ void __launch_bounds__(32) k_stepper(StepArgs a)
         const Coef *coefs = down ? a.DN : a.UP;
         if (p == 1) {
             if (a.in)
-                run_pass<VPT, true, false, true, true, RS, false>(a, w, coefs, a.in, a.ld_in, c0, valid, lane, alpha);
+                run_pass<VPT, PD, true, false, true, true, RS, false>(a, w, coefs, a.in, a.ld_in, c0, valid, lane, alpha);
             else
-                run_pass<VPT, true, false, true, false, RS, false>(a, w, coefs, nullptr, a.ld_out, c0, valid, lane, alpha);
+                run_pass<VPT, PD, true, false, true, false, RS, false>(a, w, coefs, nullptr, a.ld_out, c0, valid, lane, alpha);
         } else if (p <= m) {
             if (down)
-                run_pass<VPT, true, true, true, true, RS, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                run_pass<VPT, PD, true, true, true, true, RS, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
             else
-                run_pass<VPT, false, true, true, true, RS, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                run_pass<VPT, PD, false, true, true, true, RS, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
         } else {   // p == m + 1: finish the last step (+ offset)
             if (down) {
-                if (have_off) run_pass<VPT, true, true, false, true, 0, true>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
-                else run_pass<VPT, true, true, false, true, 0, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                if (have_off) run_pass<VPT, PD, true, true, false, true, 0, true>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                else run_pass<VPT, PD, true, true, false, true, 0, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
             } else {
-                if (have_off) run_pass<VPT, false, true, false, true, 0, true>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
-                else run_pass<VPT, false, true, false, true, 0, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                if (have_off) run_pass<VPT, PD, false, true, false, true, 0, true>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
+                else run_pass<VPT, PD, false, true, false, true, 0, false>(a, w, coefs, a.out, a.ld_out, c0, valid, lane, alpha);
             }
         }
     }
@@ -489,16 +491,22 @@ __global__ void k_copy_off(const double *in, long ld_in, double *out, long ld_ou
     out[i * ld_out + c] = v;
 }
 
-template <int VPT, int RS>
-static cudaError_t launch_stepper_t(const StepArgs &a, cudaStream_t s)
+static size_t stepper_smem(int VPT, int PD, int RS, bool off)
+{
+    const int RING = PD + 1;
+    const int CW = RS > 0 ? 4 + (RS < 2 ? 2 : RS) : 4;
+    size_t ring = (size_t)RING * GR * 32 * VPT * sizeof(double);
+    return ring * (off ? 2 : 1) + (size_t)RING * GR * CW * sizeof(double);
+}
+
+template <int VPT, int RS, int PD>
+static cudaError_t launch_stepper_pd(const StepArgs &a, cudaStream_t s)
 {
     long nthreads = (a.B + VPT - 1) / VPT;
     long blocks = (nthreads + 31) / 32;
     if (blocks == 0) return cudaSuccess;
-    const int CW = RS > 0 ? 4 + (RS < 2 ? 2 : RS) : 4;
-    size_t ring = (size_t)RING * GR * 32 * VPT * sizeof(double);
-    size_t smem = ring * (a.off ? 2 : 1) + (size_t)RING * GR * CW * sizeof(double);
-    auto kern = k_stepper<VPT, RS>;
+    const size_t smem = stepper_smem(VPT, PD, RS, a.off != nullptr);
+    auto kern = k_stepper<VPT, RS, PD>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const bool prof = profiling();
@@ -508,6 +516,21 @@ static cudaError_t launch_stepper_t(const StepArgs &a, cudaStream_t s)
     e = cudaGetLastError();
     if (prof) stepper_timed_end(s, (double)a.n * (double)a.B * (double)a.m, 0.0);
     return e;
+}
+
+// Prefetch depth: PD = 2 groups of 32 rows.  Measured on B200 (C4 build batch):
+// PD = 2 94 ms, PD = 4 99 ms (the bigger ring halves CTA residency and the
+// HBM pipe is already full).  PR_STEPPER_PD=4 selects the deeper ring.
+template <int VPT, int RS>
+static cudaError_t launch_stepper_t(const StepArgs &a, cudaStream_t s)
+{
+    int pd = 2;
+    if (const char *e = getenv("PR_STEPPER_PD")) {
+        int f = atoi(e);
+        if (f == 2 || (f == 4 && stepper_smem(VPT, 4, RS, a.off != nullptr) <= 227 * 1024)) pd = f;
+    }
+    if (pd == 4) return launch_stepper_pd<VPT, RS, 4>(a, s);
+    return launch_stepper_pd<VPT, RS, 2>(a, s);
 }
 
 int stepper_rs(int R)
