@@ -393,6 +393,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol(CholArgs a)
         __syncthreads();
     }
     const double offI = sqrt(red[0]);
+    if (a.offI && threadIdx.x == 0) a.offI[b] = offI;
     __syncthreads();
 
     const bool plain = (st == 1) || (offI < 0.5);
@@ -438,6 +439,10 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol(CholArgs a)
         }
         load_G();
         shift = (shift > 0.0 ? shift * 100.0 : DBL_EPSILON * (normG > 0 ? normG : 1.0));
+    }
+    if (a.shift_dbg && threadIdx.x == 0) {
+        a.shift_dbg[2 * b] = (normG > 0.0) ? shift / normG : shift;
+        a.shift_dbg[2 * b + 1] = attempt;
     }
     // write R (upper, zero below)
     double *Rb = a.R + (long)b * per;

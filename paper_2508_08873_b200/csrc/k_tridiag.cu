@@ -126,9 +126,9 @@ __device__ __forceinline__ void philox4x64_10(unsigned long long c[4], unsigned 
 
 // Four N(0,1) values for rows 4*blk .. 4*blk+3 of column col of interval q.
 __device__ __forceinline__ void gauss4(unsigned long long seed, unsigned long long blk, int col,
-                                       int q, double z[4])
+                                       int q, double z[4], unsigned long long ctr3 = 0ULL)
 {
-    unsigned long long c[4] = {blk, (unsigned long long)col, (unsigned long long)q, 0ULL};
+    unsigned long long c[4] = {blk, (unsigned long long)col, (unsigned long long)q, ctr3};
     philox4x64_10(c, seed, 0ULL);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -143,7 +143,8 @@ __device__ __forceinline__ void gauss4(unsigned long long seed, unsigned long lo
 }
 
 __global__ void k_sketch(int dim, int n, long rows, int q0, int nint, int l,
-                         unsigned long long seed, double *out, long rs, long vs)
+                         unsigned long long seed, double *out, long rs, long vs, double scale,
+                         unsigned long long ctr3)
 {
     // one thread = 4 consecutive interior DOFs of one column
     long ndof = (dim == 1) ? n : (long)n * n;
@@ -156,7 +157,7 @@ __global__ void k_sketch(int dim, int n, long rows, int q0, int nint, int l,
     int q = q0 + (int)(v / l);
     int col = (int)(v % l);
     double z[4];
-    gauss4(seed, (unsigned long long)blk, col, q, z);
+    gauss4(seed, (unsigned long long)blk, col, q, z, ctr3);
     for (int h = 0; h < 4; ++h) {
         long dof = blk * 4 + h;
         if (dof >= ndof) break;
@@ -165,13 +166,15 @@ __global__ void k_sketch(int dim, int n, long rows, int q0, int nint, int l,
             long ix = dof / n, iy = dof % n;
             row = (ix + 1) * (n + 1) + (iy + 1);
         }
-        out[row * rs + v * vs] = z[h];
+        if (scale == 0.0) out[row * rs + v * vs] = z[h];       // Omega itself
+        else out[row * rs + v * vs] += scale * z[h];           // rounding-level perturbation
     }
     (void)rows;
 }
 
 cudaError_t launch_sketch(int dim, int n, long rows, int q0, int nint, int l,
-                          unsigned long long seed, double *out, long rs, long vs, cudaStream_t s)
+                          unsigned long long seed, double *out, long rs, long vs, cudaStream_t s,
+                          double scale, unsigned long long ctr3)
 {
     long ndof = (dim == 1) ? n : (long)n * n;
     long total = ((ndof + 3) / 4) * (long)nint * l;
@@ -179,7 +182,7 @@ cudaError_t launch_sketch(int dim, int n, long rows, int q0, int nint, int l,
     int th = 256;
     long bl = (total + th - 1) / th;
     note_launch();
-    k_sketch<<<(unsigned)bl, th, 0, s>>>(dim, n, rows, q0, nint, l, seed, out, rs, vs);
+    k_sketch<<<(unsigned)bl, th, 0, s>>>(dim, n, rows, q0, nint, l, seed, out, rs, vs, scale, ctr3);
     return cudaGetLastError();
 }
 

@@ -198,13 +198,35 @@ static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double 
             stage("qr gram", s);
             PR_CUDA(cudaMemsetAsync(active, 0, sizeof(int), s));
             CholArgs c{part, nchunk, nb, l, rows, state, act, R, Rtot, active, fail};
+            double *offI = nullptr;
+            if (debug_sync()) {
+                offI = S.get<double>(3 * nb);
+                if (offI) PR_CUDA(cudaMemsetAsync(offI, 0, 3 * nb * sizeof(double), s));
+                c.offI = offI;
+                c.shift_dbg = offI + nb;
+            }
             PR_CUDA(launch_chol(c, s));
             stage("qr chol", s);
+            if (offI) {
+                std::vector<double> h(3 * nb);
+                std::vector<int> hs(nb);
+                PR_CUDA(cudaMemcpy(h.data(), offI, 3 * nb * sizeof(double), cudaMemcpyDeviceToHost));
+                double smax = 0, amax = 0;
+                for (int i = 0; i < nb; ++i) { smax = std::max(smax, h[nb + 2 * i]); amax = std::max(amax, h[nb + 2 * i + 1]); }
+                fprintf(stderr, "[pr]   shift/||G||_F max %.3e, Cholesky retries max %.0f\n", smax, amax);
+                PR_CUDA(cudaMemcpy(hs.data(), state, nb * sizeof(int), cudaMemcpyDeviceToHost));
+                double mn = 1e300, mx = 0;
+                int cnt[3] = {0, 0, 0};
+                for (int i = 0; i < nb; ++i) { mn = std::min(mn, h[i]); mx = std::max(mx, h[i]); cnt[hs[i]]++; }
+                fprintf(stderr, "[pr] qr pass %d: ||G-I||_F min %.3e max %.3e; states after: shift %d plain1 %d done %d\n",
+                        pass, mn, mx, cnt[0], cnt[1], cnt[2]);
+            }
             PR_CUDA(launch_trsm(Q, xbs, L.rs, L.vs, rows, l, nb, R, act, s));
             stage("qr trsm", s);
         }
         PR_CUDA(cudaMemcpyAsync(h_active, active, sizeof(int), cudaMemcpyDeviceToHost, s));
         PR_CUDA(cudaStreamSynchronize(s));
+        if (getenv("PR_QR_TRACE")) fprintf(stderr, "[pr] qr after pass %d: active %d of %d\n", pass, *h_active, nb);
         if (*h_active == 0) { done_at = pass; break; }
         if (pass >= 24) {
             set_error("CholeskyQR did not converge in 24 passes");
@@ -505,6 +527,18 @@ pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local,
                        nullptr, 0, 0, 0, s);
         if (st != PR_OK) return bail(st);
         stage("build step 3", s);
+        // Rounding-level regularisation of Z (reading R-QRF): the
+        // stepper damps its own rounding errors, so F'^* W has singular values
+        // far below u ||F'|| in the directions W does not resolve; lifting them
+        // to ~u with ||delta_c|| ~ 2^-52 (within the floating-point error of
+        // evaluating F'^* w_c, ||w_c|| = 1) saves the shifted CholeskyQR passes
+        // that would only amplify noise.  G changes by O(u sigma_1).
+        {
+            const double ndof = (op.dim == 1) ? (double)op.n : (double)op.n * op.n;
+            const double scale = ldexp(1.0, -52) / sqrt(ndof);
+            PR_CUDA(launch_sketch(op.dim, op.n, op.rows, first_interval, nl, l, seed, Z,
+                                  (op.dim == 1) ? ld : 1, (op.dim == 1) ? 1 : ld, s, scale, 1ULL));
+        }
         // step 4: V R_Z = Z
         st = cholqr(op, Z, ld, nl, l, Rtot, G->fail, &G->qr_passes[1], s);
         if (st != PR_OK) return bail(st);

@@ -97,8 +97,10 @@ cudaError_t launch_factor_1d(int n, const double *subA, const double *supA, cons
                              const double *diagA, double dt, int transpose, Coef *DN, Coef *UP,
                              int *bad, cudaStream_t s);
 cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s);
+// scale == 0: out = Omega; else out += scale * (independent N(0,1) field, counter word 3 = ctr3)
 cudaError_t launch_sketch(int dim, int n, long rows, int q0, int nint, int l,
-                          unsigned long long seed, double *out, long rs, long vs, cudaStream_t s);
+                          unsigned long long seed, double *out, long rs, long vs, cudaStream_t s,
+                          double scale = 0.0, unsigned long long ctr3 = 0ULL);
 cudaError_t launch_transpose(const double *in, int R, int n, double *out, int ldo, cudaStream_t s);
 int stepper_rs(int R);   // source-term count padded to 1, 2, 4 or 8
 
@@ -135,6 +137,8 @@ struct CholArgs {
     double *Rtot;                     // per batch l x l accumulated product (nullable)
     int *active;                      // device counter of batches still active
     int *fail;                        // device flag: Cholesky broke down
+    double *offI = nullptr;           // optional per-batch ||G - I||_F of this pass (debug)
+    double *shift_dbg = nullptr;      // optional per-batch final shift / ||G||_F and attempts (debug)
 };
 cudaError_t launch_chol(const CholArgs &a, cudaStream_t s);
 cudaError_t launch_trsm(double *Q, long bs, long rs, long cs, long rows, int l, int nbatch,

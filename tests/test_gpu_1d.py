@@ -211,3 +211,29 @@ def test_parareal_full_size_against_fine_solution(name):
     scale = np.max(np.linalg.norm(ref, axis=-1))
     err = np.max(np.linalg.norm(got - ref, axis=-1))
     assert err <= TAU_1D * scale, err / scale
+
+
+@pytest.mark.parametrize("name", ["C1", "T4", "C4"])
+def test_lifted_factors_orthonormal_and_deterministic(name):
+    """U_q = W Psi_k and V_q = V Phi_k have orthonormal columns (steps 2, 4, 5
+    of P:258-299 produce orthonormal bases; Psi, Phi orthogonal), and a rebuild
+    with the same seed is bit-identical (counter-based sketch, fixed-order
+    reductions)."""
+    import torch
+    from paper_2508_08873_b200 import Coarse
+    cfg = get(name)
+    op = gpu_op(cfg)
+    G1 = Coarse.build(op, cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega)
+    G2 = Coarse.build(op, cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega)
+    i1, i2 = G1.info(), G2.info()
+    np.testing.assert_array_equal(i1["sigma"], i2["sigma"])
+    U = torch.empty((op.rows, cfg.k), dtype=torch.float64, device="cuda")
+    V = torch.empty_like(U)
+    U2, V2 = torch.empty_like(U), torch.empty_like(U)
+    I = torch.eye(cfg.k, dtype=torch.float64, device="cuda")
+    for q in sorted({0, cfg.N // 2, cfg.N - 1}):
+        G1.export_interval(q, U_q=U, V_q=V)
+        G2.export_interval(q, U_q=U2, V_q=V2)
+        assert float((U.T @ U - I).abs().max()) < 1e-13
+        assert float((V.T @ V - I).abs().max()) < 1e-13
+        assert torch.equal(U, U2) and torch.equal(V, V2)

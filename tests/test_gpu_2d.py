@@ -188,3 +188,20 @@ def test_build_c5_shard_sampled_intervals():
         ref = tr.apply_linear(X.reshape(2, -1))
         for v in range(2):
             assert np.linalg.norm(got[v] - ref[v]) <= TAU_2D * s1 * np.linalg.norm(X[v])
+
+
+def test_lifted_factors_orthonormal_2d():
+    import torch
+    from paper_2508_08873_b200 import Coarse
+    cfg = C3
+    op = gpu_op(cfg)
+    Gc = Coarse.build(op, cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega)
+    U = torch.empty((op.rows, cfg.k), dtype=torch.float64, device="cuda")
+    V = torch.empty_like(U)
+    I = torch.eye(cfg.k, dtype=torch.float64, device="cuda")
+    for q in (0, cfg.N - 1):
+        Gc.export_interval(q, U_q=U, V_q=V)
+        assert float((U.T @ U - I).abs().max()) < 1e-13
+        assert float((V.T @ V - I).abs().max()) < 1e-13
+        P = cfg.n + 1
+        assert float(U.view(P, P, cfg.k)[0].abs().max()) == 0.0      # ghosts stay zero
