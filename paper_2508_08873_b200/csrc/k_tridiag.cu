@@ -402,11 +402,70 @@ __device__ __forceinline__ void run_pass(const StepArgs &a, const WarpSmem &w, c
             if (valid) stg_vec<VPT>(dst, res);
             dst += step_dst;
         };
-        if (nr == GR) {
+        if constexpr (!AFF) {
+            if (nr == GR) {
+                // Software-pipelined full group: the shared-memory operands of
+                // sub-batch k+1 (4 rows) are loaded into registers while sub-batch
+                // k is computed, so a lone warp (small batches) is not serialised
+                // on shared-memory latency row by row.
+                constexpr int SB = 4;
+                struct Ops {
+                    double2 c01[SB];
+                    double cc[SB];
+                    double val[SB][VPT];
+                    double off[SB][VPT];
+                };
+                auto load = [&](int r0, Ops &o) {
 #pragma unroll
-            for (int r = 0; r < GR; ++r) body(r);
+                    for (int k = 0; k < SB; ++k) {
+                        const double *crow = cr + (size_t)(r0 + k) * 4;      // CW == 4
+                        o.c01[k] = *reinterpret_cast<const double2 *>(crow);
+                        o.cc[k] = reinterpret_cast<const double2 *>(crow)[1].x;
+                        if (LOAD) lds_vec<VPT>(o.val[k], vr + (size_t)(r0 + k) * 32 * VPT);
+                        if (OFF) lds_vec<VPT>(o.off[k], orr + (size_t)(r0 + k) * 32 * VPT);
+                    }
+                };
+                auto compute = [&](const Ops &o) {
+#pragma unroll
+                    for (int k = 0; k < SB; ++k) {
+                        double res[VPT];
+#pragma unroll
+                        for (int v = 0; v < VPT; ++v) {
+                            const double in = LOAD ? o.val[k][v] : 0.0;
+                            const double x = FIN ? fma(o.c01[k].x, xprev[v], in) : in;
+                            xprev[v] = x;
+                            if (START) {
+                                const double y = fma(o.cc[k], yprev[v], o.c01[k].y * x);
+                                yprev[v] = y;
+                                res[v] = y;
+                            } else {
+                                res[v] = x;
+                            }
+                            if (OFF) res[v] += o.off[k][v];
+                        }
+                        if (valid) stg_vec<VPT>(dst, res);
+                        dst += step_dst;
+                    }
+                };
+                Ops A, B;
+                load(0, A);
+#pragma unroll
+                for (int sb = 0; sb < GR / SB; sb += 2) {
+                    load((sb + 1) * SB, B);
+                    compute(A);
+                    if (sb + 2 < GR / SB) load((sb + 2) * SB, A);
+                    compute(B);
+                }
+            } else {
+                for (int r = 0; r < nr; ++r) body(r);
+            }
         } else {
-            for (int r = 0; r < nr; ++r) body(r);
+            if (nr == GR) {
+#pragma unroll
+                for (int r = 0; r < GR; ++r) body(r);
+            } else {
+                for (int r = 0; r < nr; ++r) body(r);
+            }
         }
         __syncwarp();   // all lanes done with this ring slot before it is refilled
     }
