@@ -262,9 +262,76 @@ __global__ void __launch_bounds__(XM_THREADS) k_xty_mma(XtY p)
     }
 }
 
+// ---- skinny X^T Y (few right-hand columns, e.g. the Parareal projections with
+// one source): warp lanes run over the a columns of a row of X (row-major, one
+// coalesced load per row), the <= 8 values of Y's row are warp broadcasts; each
+// warp accumulates its rows, the 8 warps are summed in fixed order at the end.
+constexpr int XS_WARPS = 8;
+
+template <int CT>
+__global__ void __launch_bounds__(32 * XS_WARPS) k_xty_skinny(XtY p)
+{
+    __shared__ double red[XS_WARPS][128 * CT];
+    const int b = blockIdx.y, t = blockIdx.x;
+    if (p.skip && p.skip[b] == 2) return;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ctot = p.c + p.c2;
+    const long r0 = (long)t * p.chunk_rows;
+    long r1 = r0 + p.chunk_rows;
+    if (r1 > p.rows) r1 = p.rows;
+    const double *Xb = p.X + (long)b * p.xbs;
+    const double *Yb = p.Y + (long)b * p.ybs;
+    const double *Y2b = p.Y2 ? p.Y2 + (long)b * p.ybs : nullptr;
+    constexpr int AJ = 4;                    // a <= 128: lane owns columns lane + 32 j
+    double acc[AJ][CT];
+#pragma unroll
+    for (int j = 0; j < AJ; ++j)
+#pragma unroll
+        for (int c = 0; c < CT; ++c) acc[j][c] = 0.0;
+    for (long row = r0 + w; row < r1; row += XS_WARPS) {
+        double y[CT];
+#pragma unroll
+        for (int c = 0; c < CT; ++c) {
+            y[c] = 0.0;
+            if (c < ctot) {
+                const double *src = (c < p.c) ? Yb + row * p.yrs + (long)c * p.ycs
+                                              : Y2b + row * p.yrs + (long)(c - p.c) * p.ycs;
+                y[c] = __ldg(src);
+            }
+        }
+        const double *xr = Xb + row * p.xrs;
+#pragma unroll
+        for (int j = 0; j < AJ; ++j) {
+            const int i = lane + 32 * j;
+            const double xv = (i < p.a) ? xr[i] : 0.0;
+#pragma unroll
+            for (int c = 0; c < CT; ++c) acc[j][c] = fma(xv, y[c], acc[j][c]);
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < AJ; ++j)
+#pragma unroll
+        for (int c = 0; c < CT; ++c) red[w][(lane + 32 * j) * CT + c] = acc[j][c];
+    __syncthreads();
+    double *out = p.part + ((long)b * p.nchunk + t) * p.a * ctot;
+    for (int e = threadIdx.x; e < p.a * ctot; e += 32 * XS_WARPS) {
+        const int i = e / ctot, c = e % ctot;
+        double sum = 0.0;
+        for (int ww = 0; ww < XS_WARPS; ++ww) sum += red[ww][i * CT + c];
+        out[e] = sum;
+    }
+}
+
 cudaError_t launch_xty(const XtY &p, cudaStream_t s)
 {
     const int ctot = p.c + p.c2;
+    if (ctot <= 4 && p.a <= 128 && p.xcs == 1) {
+        dim3 grid(p.nchunk, p.nbatch);
+        note_launch();
+        if (ctot <= 2) k_xty_skinny<2><<<grid, 32 * XS_WARPS, 0, s>>>(p);
+        else k_xty_skinny<4><<<grid, 32 * XS_WARPS, 0, s>>>(p);
+        return cudaGetLastError();
+    }
     // DMMA path for the 2D (column-contiguous) layout only: measured on B200 it
     // is faster there (C3 Gram 7.9 vs 9.3 ms), while the register-blocked FMA
     // kernel is faster for the 1D row-major layout (C4 build 296 vs 356 ms).

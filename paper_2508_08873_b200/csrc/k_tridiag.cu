@@ -418,7 +418,7 @@ __device__ __forceinline__ void run_pass(const StepArgs &a, const WarpSmem &w, c
                 auto load = [&](int r0, Ops &o) {
 #pragma unroll
                     for (int k = 0; k < SB; ++k) {
-                        const double *crow = cr + (size_t)(r0 + k) * 4;      // CW == 4
+                        const double *crow = cr + (size_t)(r0 + k) * w.CW;   // CW even: 16-B rows
                         o.c01[k] = *reinterpret_cast<const double2 *>(crow);
                         o.cc[k] = reinterpret_cast<const double2 *>(crow)[1].x;
                         if (LOAD) lds_vec<VPT>(o.val[k], vr + (size_t)(r0 + k) * 32 * VPT);
