@@ -804,6 +804,9 @@ cudaError_t launch_lift(const double *X, long xbs, long xrs, long xcs, long rows
     return cudaGetLastError();
 }
 
+cudaError_t launch_sweep_seq(const double *C, const double *d, int N, int k, int S, double *e,
+                             cudaStream_t s);
+
 // ----------------------------------------------------------------- sweep
 // e_j = C_j e_{j-1} + d_j, e_{-1} = 0: the only sequential part of a Parareal
 // iteration, in k-dimensional reduced coordinates.  C_{j+1} and d_{j+1} are
@@ -858,8 +861,130 @@ __global__ void __launch_bounds__(SW_THREADS) k_sweep(const double *C, const dou
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
+// ---- blocked sweep: blocks of SWB consecutive intervals.
+//  A (one CTA per block): zero-start local solution f and transfer Phi = C_last..C_first
+//  B (one CTA): E_b = Phi_b E_{b-1} + f_b over the NB block ends (sequential, short)
+//  C (one CTA per block): e_j = C_j e_{j-1} + d_j from e_{first-1} = E_{b-1}
+// Exact algebra; only the association of the block-boundary products differs
+// from the sequential recurrence.
+constexpr int SWB = 16;
+
+// y (r x S) = M (r x r) x (r x S) + add  (shared-memory operands, block-wide)
+__device__ __forceinline__ void sw_gemm(const double *M, const double *x, const double *add,
+                                        double *y, int r, int S)
+{
+    for (int o = threadIdx.x; o < r * S; o += blockDim.x) {
+        const int i = o / S, c = o % S;
+        double acc = add ? add[o] : 0.0;
+        for (int t = 0; t < r; ++t) acc = fma(M[i * r + t], x[t * S + c], acc);
+        y[o] = acc;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_sweep_A(const double *C, const double *d, int N, int k, int S,
+                                                  double *fend, double *Phi)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int kS = k * S, kk = k * k;
+    double *f0 = sm, *f1 = sm + kS, *Cs = sm + 2 * kS, *P0 = Cs + kk, *P1 = P0 + kk;
+    const int b = blockIdx.x;
+    const int j0 = b * SWB, j1 = min(N, j0 + SWB);
+    for (int i = threadIdx.x; i < kS; i += blockDim.x) f0[i] = 0.0;
+    for (int i = threadIdx.x; i < kk; i += blockDim.x) P0[i] = (i / k == i % k) ? 1.0 : 0.0;
+    __syncthreads();
+    for (int j = j0; j < j1; ++j) {
+        if (j == 0) {                       // e_{-1} = 0: f = d_0, Phi irrelevant (block 0)
+            for (int i = threadIdx.x; i < kS; i += blockDim.x) f1[i] = d[i];
+            for (int i = threadIdx.x; i < kk; i += blockDim.x) P1[i] = 0.0;
+        } else {
+            for (int i = threadIdx.x; i < kk; i += blockDim.x) Cs[i] = C[(long)j * kk + i];
+            __syncthreads();
+            sw_gemm(Cs, f0, d + (long)j * kS, f1, k, S);
+            sw_gemm(Cs, P0, nullptr, P1, k, k);
+        }
+        __syncthreads();
+        double *t = f0; f0 = f1; f1 = t;
+        t = P0; P0 = P1; P1 = t;
+    }
+    for (int i = threadIdx.x; i < kS; i += blockDim.x) fend[(long)b * kS + i] = f0[i];
+    for (int i = threadIdx.x; i < kk; i += blockDim.x) Phi[(long)b * kk + i] = P0[i];
+}
+
+__global__ void __launch_bounds__(1024) k_sweep_B(const double *fend, const double *Phi, int NB, int k,
+                                                  int S, double *E)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int kS = k * S, kk = k * k;
+    double *e0 = sm, *e1 = sm + kS, *Ps = sm + 2 * kS;
+    for (int i = threadIdx.x; i < kS; i += blockDim.x) e0[i] = 0.0;
+    __syncthreads();
+    for (int b = 0; b < NB; ++b) {
+        for (int i = threadIdx.x; i < kk; i += blockDim.x) Ps[i] = Phi[(long)b * kk + i];
+        __syncthreads();
+        sw_gemm(Ps, e0, fend + (long)b * kS, e1, k, S);
+        __syncthreads();
+        for (int i = threadIdx.x; i < kS; i += blockDim.x) E[(long)b * kS + i] = e1[i];
+        double *t = e0; e0 = e1; e1 = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_sweep_C(const double *C, const double *d, const double *E,
+                                                  int N, int k, int S, double *e)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int kS = k * S, kk = k * k;
+    double *e0 = sm, *e1 = sm + kS, *Cs = sm + 2 * kS;
+    const int b = blockIdx.x;
+    const int j0 = b * SWB, j1 = min(N, j0 + SWB);
+    for (int i = threadIdx.x; i < kS; i += blockDim.x) e0[i] = (b > 0) ? E[(long)(b - 1) * kS + i] : 0.0;
+    __syncthreads();
+    for (int j = j0; j < j1; ++j) {
+        if (j == 0) {
+            for (int i = threadIdx.x; i < kS; i += blockDim.x) e1[i] = d[i];
+        } else {
+            for (int i = threadIdx.x; i < kk; i += blockDim.x) Cs[i] = C[(long)j * kk + i];
+            __syncthreads();
+            sw_gemm(Cs, e0, d + (long)j * kS, e1, k, S);
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < kS; i += blockDim.x) e[(long)j * kS + i] = e1[i];
+        double *t = e0; e0 = e1; e1 = t;
+    }
+}
+
 cudaError_t launch_sweep(const double *C, const double *d, int N, int k, int S, double *e,
                          cudaStream_t s)
+{
+    const int NB = (N + SWB - 1) / SWB;
+    const size_t kS = (size_t)k * S, kk = (size_t)k * k;
+    const size_t smA = (2 * kS + 3 * kk) * sizeof(double);
+    if (NB >= 4 && smA <= 200 * 1024) {
+        double *tmp = (double *)ws_alloc((size_t)NB * (2 * kS + kk) * sizeof(double));
+        if (tmp) {
+            double *fend = tmp, *E = tmp + NB * kS, *Phi = tmp + 2 * NB * kS;
+            const size_t smB = (2 * kS + kk) * sizeof(double);
+            cudaError_t er;
+            er = cudaFuncSetAttribute(k_sweep_A, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
+            if (er == cudaSuccess) er = cudaFuncSetAttribute(k_sweep_B, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
+            if (er == cudaSuccess) er = cudaFuncSetAttribute(k_sweep_C, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
+            if (er != cudaSuccess) { ws_free(tmp); return er; }
+            const int th = (kS > 512 || kk > 512) ? 1024 : 256;
+            note_launch();
+            k_sweep_A<<<NB, th, smA, s>>>(C, d, N, k, S, fend, Phi);
+            note_launch();
+            k_sweep_B<<<1, th, smB, s>>>(fend, Phi, NB, k, S, E);
+            note_launch();
+            k_sweep_C<<<NB, th, smB, s>>>(C, d, E, N, k, S, e);
+            er = cudaGetLastError();
+            ws_free(tmp);                    // stream-ordered reuse
+            return er;
+        }
+    }
+    return launch_sweep_seq(C, d, N, k, S, e, s);
+}
+
+cudaError_t launch_sweep_seq(const double *C, const double *d, int N, int k, int S, double *e,
+                             cudaStream_t s)
 {
     size_t smem = ((size_t)4 * k * S + (size_t)2 * k * k) * sizeof(double);
     cudaError_t er = cudaFuncSetAttribute(k_sweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
