@@ -531,10 +531,26 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol(CholArgs a)
             }
         }
     }
+    // Unshifted passes: ||G - I|| < 1/2 gives cond(R) <= sqrt(3), so applying
+    // an explicit R^{-1} is as stable as substitution and runs as a GEMM on the
+    // tensor cores.  Column j of R^{-1} by back substitution (one thread each).
+    const bool use_inv = plain && a.Rinv;
+    if (use_inv) {
+        double *Xb = a.Rinv + (long)b * per;
+        __syncthreads();
+        for (int j = threadIdx.x; j < l; j += CH_THREADS) {
+            for (int i = l - 1; i > j; --i) Xb[(long)i * l + j] = 0.0;
+            for (int i = j; i >= 0; --i) {
+                double t = (i == j) ? 1.0 : 0.0;
+                for (int k = i + 1; k <= j; ++k) t -= G[i * l + k] * Xb[(long)k * l + j];
+                Xb[(long)i * l + j] = t / G[i * l + i];
+            }
+        }
+    }
     if (threadIdx.x == 0) {
         int ns = plain ? (st == 1 ? 2 : 1) : 0;
         a.state[b] = ns;
-        a.act[b] = 1;
+        a.act[b] = use_inv ? 2 : 1;
         if (ns != 2) atomicAdd(a.active, 1);
     }
 }
@@ -565,7 +581,7 @@ __global__ void __launch_bounds__(128) k_trsm(double *Q, long bs, long rs, long 
 {
     extern __shared__ __align__(16) double sm[];
     const int b = blockIdx.y;
-    if (!act[b]) return;
+    if (act[b] != 1) return;
     const int nt = blockDim.x;
     const int LP = (l + TB - 1) / TB * TB;   // padded width
     double *Rs = sm;                          // LP x LP, diag = 1/R_jj, zero padded
@@ -634,6 +650,104 @@ cudaError_t launch_trsm(double *Q, long bs, long rs, long cs, long rows, int l, 
     dim3 grid((unsigned)((rows + TS_CHUNK - 1) / TS_CHUNK), nbatch);
     note_launch();
     k_trsm<<<grid, nt, smem, s>>>(Q, bs, rs, cs, rows, l, R, act);
+    return cudaGetLastError();
+}
+
+// ---- Q <- Q Rinv on FP64 tensor cores (unshifted CholeskyQR passes).  A CTA
+// loads Rinv once and sweeps TS_CHUNK rows in tiles of 64; warp w computes rows
+// 16w .. 16w+15 of the tile times Rinv (m8n8k4 DMMA), in place.
+constexpr int RA_ROWS = 64;
+
+template <bool CM>
+__global__ void __launch_bounds__(128) k_rinv_apply(double *Q, long bs, long rs, long cs, long rows,
+                                                    int l, const double *Rinv, const int *act)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int b = blockIdx.y;
+    if (act[b] != 2) return;
+    const int LP = (l + 15) / 16 * 16;
+    const int ST = LP + 4;                    // stride = 4 (mod 16): conflict-free fragments
+    double *Rs = sm;                          // LP x ST
+    double *Ys = sm + (size_t)LP * ST;        // RA_ROWS x ST
+    const double *Rb = Rinv + (long)b * l * l;
+    for (int e = threadIdx.x; e < LP * LP; e += 128) {
+        const int i = e / LP, j = e % LP;
+        Rs[i * ST + j] = (i < l && j < l) ? Rb[(long)i * l + j] : 0.0;
+    }
+    double *Qb = Q + (long)b * bs;
+    const long c0 = (long)blockIdx.x * TS_CHUNK;
+    const long c1 = min(rows, c0 + TS_CHUNK);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int NT = LP / 8;                    // <= 16 output column tiles
+    for (long r0 = c0; r0 < c1; r0 += RA_ROWS) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < RA_ROWS * LP; e += 128) {
+            int r, j;
+            if (CM) { j = e / RA_ROWS; r = e % RA_ROWS; } else { r = e / LP; j = e % LP; }
+            const long row = r0 + r;
+            Ys[r * ST + j] = (row < c1 && j < l) ? Qb[row * rs + (long)j * cs] : 0.0;
+        }
+        __syncthreads();
+        double acc[2][16][2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < 16; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+        for (int k0 = 0; k0 < LP; k0 += 4) {
+            double af[2];
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi) af[mi] = Ys[(w * 16 + mi * 8 + gq) * ST + k0 + tq];
+#pragma unroll
+            for (int nj = 0; nj < 16; ++nj) {
+                if (nj < NT) {
+                    const double bf = Rs[(k0 + tq) * ST + nj * 8 + gq];
+#pragma unroll
+                    for (int mi = 0; mi < 2; ++mi) dmma_f64(acc[mi][nj][0], acc[mi][nj][1], af[mi], bf);
+                }
+            }
+        }
+        __syncwarp();      // this warp's rows of Ys are only read by this warp
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < 16; ++nj) {
+                if (nj < NT) {
+                    const int r = w * 16 + mi * 8 + gq, j = nj * 8 + 2 * tq;
+                    Ys[r * ST + j] = acc[mi][nj][0];
+                    Ys[r * ST + j + 1] = acc[mi][nj][1];
+                }
+            }
+        __syncthreads();
+        for (int e = threadIdx.x; e < RA_ROWS * LP; e += 128) {
+            int r, j;
+            if (CM) { j = e / RA_ROWS; r = e % RA_ROWS; } else { r = e / LP; j = e % LP; }
+            const long row = r0 + r;
+            if (row < c1 && j < l) Qb[row * rs + (long)j * cs] = Ys[r * ST + j];
+        }
+    }
+}
+
+cudaError_t launch_rinv_apply(double *Q, long bs, long rs, long cs, long rows, int l, int nbatch,
+                              const double *Rinv, const int *act, cudaStream_t s)
+{
+    if (l > 128) return cudaErrorInvalidValue;
+    const int LP = (l + 15) / 16 * 16;
+    const size_t smem = ((size_t)LP + RA_ROWS) * (LP + 4) * sizeof(double);
+    const bool cm = (cs != 1);
+    dim3 grid((unsigned)((rows + TS_CHUNK - 1) / TS_CHUNK), nbatch);
+    cudaError_t e;
+    if (cm) {
+        e = cudaFuncSetAttribute(k_rinv_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        note_launch();
+        k_rinv_apply<true><<<grid, 128, smem, s>>>(Q, bs, rs, cs, rows, l, Rinv, act);
+    } else {
+        e = cudaFuncSetAttribute(k_rinv_apply<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        note_launch();
+        k_rinv_apply<false><<<grid, 128, smem, s>>>(Q, bs, rs, cs, rows, l, Rinv, act);
+    }
     return cudaGetLastError();
 }
 

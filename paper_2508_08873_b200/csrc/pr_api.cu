@@ -177,6 +177,8 @@ static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double 
     int *state, *act, *active;
     PR_ALLOC(part, double, (size_t)nb * nchunk * l * l, S);
     PR_ALLOC(R, double, (size_t)nb * l * l, S);
+    double *Rinv;
+    PR_ALLOC(Rinv, double, (size_t)nb * l * l, S);
     PR_ALLOC(state, int, nb, S);
     PR_ALLOC(act, int, nb, S);
     PR_ALLOC(active, int, 1, S);
@@ -198,6 +200,7 @@ static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double 
             stage("qr gram", s);
             PR_CUDA(cudaMemsetAsync(active, 0, sizeof(int), s));
             CholArgs c{part, nchunk, nb, l, rows, state, act, R, Rtot, active, fail};
+            c.Rinv = Rinv;
             double *offI = nullptr;
             if (debug_sync()) {
                 offI = S.get<double>(3 * nb);
@@ -222,7 +225,8 @@ static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double 
                         pass, mn, mx, cnt[0], cnt[1], cnt[2]);
             }
             PR_CUDA(launch_trsm(Q, xbs, L.rs, L.vs, rows, l, nb, R, act, s));
-            stage("qr trsm", s);
+            PR_CUDA(launch_rinv_apply(Q, xbs, L.rs, L.vs, rows, l, nb, Rinv, act, s));
+            stage("qr apply", s);
         }
         PR_CUDA(cudaMemcpyAsync(h_active, active, sizeof(int), cudaMemcpyDeviceToHost, s));
         PR_CUDA(cudaStreamSynchronize(s));

@@ -132,17 +132,21 @@ struct CholArgs {
     const double *part; int nchunk;   // Gram partials
     int nbatch; int l; long nrows;    // nrows: rows of the block (shift formula)
     int *state;                       // per batch: 0 shift phase, 1 one plain pass done, 2 done
-    int *act;                         // per batch: 1 if this pass applies R (written)
+    int *act;                         // per batch: 0 nothing, 1 apply R by substitution, 2 apply Rinv (GEMM)
     double *R;                        // per batch l x l (upper) for this pass
     double *Rtot;                     // per batch l x l accumulated product (nullable)
     int *active;                      // device counter of batches still active
     int *fail;                        // device flag: Cholesky broke down
     double *offI = nullptr;           // optional per-batch ||G - I||_F of this pass (debug)
     double *shift_dbg = nullptr;      // optional per-batch final shift / ||G||_F and attempts (debug)
+    double *Rinv = nullptr;           // per batch l x l: R^{-1} written for unshifted passes (act = 2)
 };
 cudaError_t launch_chol(const CholArgs &a, cudaStream_t s);
 cudaError_t launch_trsm(double *Q, long bs, long rs, long cs, long rows, int l, int nbatch,
                         const double *R, const int *act, cudaStream_t s);
+// Q <- Q Rinv (upper triangular) for batches with act == 2, DMMA tiles
+cudaError_t launch_rinv_apply(double *Q, long bs, long rs, long cs, long rows, int l, int nbatch,
+                              const double *Rinv, const int *act, cudaStream_t s);
 
 cudaError_t launch_jacobi(const double *Rtot, int nbatch, int l, double *Psi, double *sigma,
                           double *Phi, int *fail, cudaStream_t s);
