@@ -296,7 +296,8 @@ static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi
         a.nsteps = f->nsteps;
         a.nsrc = f->nsrc;
     }
-    PR_CUDA(launch_stepper_1d(a, s));
+    if (part_preferred(op, B, m)) PR_CUDA(launch_stepper_part(op, a, mode == PR_ADJOINT, s));
+    else PR_CUDA(launch_stepper_1d(a, s));
     return PR_OK;
 }
 
@@ -362,6 +363,7 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
         cudaFree(d_in);
         cudaFree(d_bad);
         cudaFree(op.dn_fw); cudaFree(op.up_fw); cudaFree(op.dn_tr); cudaFree(op.up_tr);
+        cudaFree(op.part_rowc_fw); cudaFree(op.part_fac_fw); cudaFree(op.part_rowc_tr); cudaFree(op.part_fac_tr);
         delete h;
         return st;
     };
@@ -383,8 +385,26 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
         e = launch_factor_1d(n, dsub, dsup, rowsum ? drs : nullptr, ddiag, dt, 0, op.dn_fw, op.up_fw, d_bad, 0);
     if (e == cudaSuccess)
         e = launch_factor_1d(n, dsub, dsup, colsum ? dcs : nullptr, ddiag, dt, 1, op.dn_tr, op.up_tr, d_bad, 0);
+    // partitioned-stepper factors (small batches), both orientations
+    const int P = part_chunks(n);
+    double *d_ends = nullptr;
+    if (e == cudaSuccess && P > 0) {
+        op.part_P = P;
+        e = cudaMalloc(&op.part_rowc_fw, 5 * nb);
+        if (e == cudaSuccess) e = cudaMalloc(&op.part_rowc_tr, 5 * nb);
+        if (e == cudaSuccess) e = cudaMalloc(&op.part_fac_fw, (size_t)10 * P * sizeof(double));
+        if (e == cudaSuccess) e = cudaMalloc(&op.part_fac_tr, (size_t)10 * P * sizeof(double));
+        if (e == cudaSuccess) e = cudaMalloc(&d_ends, (size_t)8 * P * sizeof(double));
+        if (e == cudaSuccess)
+            e = launch_part_setup(n, P, dsub, dsup, rowsum ? drs : nullptr, ddiag, dt, 0, op.part_rowc_fw,
+                                  op.part_fac_fw, d_ends, d_bad, 0);
+        if (e == cudaSuccess)
+            e = launch_part_setup(n, P, dsub, dsup, colsum ? dcs : nullptr, ddiag, dt, 1, op.part_rowc_tr,
+                                  op.part_fac_tr, d_ends, d_bad, 0);
+    }
     int bad = 0;
     if (e == cudaSuccess) e = cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost);
+    cudaFree(d_ends);
     if (e != cudaSuccess) return fail(cuda_fail(e, "pr_op_create_tridiag factor"));
     if (bad) {
         set_error("non-positive or non-finite pivot in the factorisation of I + dt A");
@@ -401,6 +421,7 @@ pr_status pr_op_destroy(pr_op h)
     if (!h) return PR_OK;
     Op &op = h->op;
     cudaFree(op.dn_fw); cudaFree(op.up_fw); cudaFree(op.dn_tr); cudaFree(op.up_tr);
+    cudaFree(op.part_rowc_fw); cudaFree(op.part_fac_fw); cudaFree(op.part_rowc_tr); cudaFree(op.part_fac_tr);
     cudaFree(op.S); cudaFree(op.lam);
     delete h;
     return PR_OK;

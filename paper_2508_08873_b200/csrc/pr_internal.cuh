@@ -63,6 +63,11 @@ struct Op {
     //   DN[i] = {ap_i, w_i, ga_i, 0}: down pass = UL back-substitution then LU forward
     //   UP[i] = {cp_i, wt_i, gc_i, 0}: up pass   = LU back-substitution then UL forward
     Coef *dn_fw = nullptr, *up_fw = nullptr, *dn_tr = nullptr, *up_tr = nullptr;
+    // 1D partitioned stepper (k_part.cu, small batches): P chunks per vector,
+    // per-row {w, -ga, -cp, V, W} (n x 5) and interface factors (2P x 5).
+    int part_P = 0;
+    double *part_rowc_fw = nullptr, *part_fac_fw = nullptr;
+    double *part_rowc_tr = nullptr, *part_fac_tr = nullptr;
     // 2D: P = n+1; S (P x P) sine matrix with zero row/col 0; lam[P] eigenvalues of T.
     int P = 0;
     double *S = nullptr;
@@ -97,6 +102,16 @@ cudaError_t launch_factor_1d(int n, const double *subA, const double *supA, cons
                              const double *diagA, double dt, int transpose, Coef *DN, Coef *UP,
                              int *bad, cudaStream_t s);
 cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s);
+
+// partitioned stepper (k_part.cu): chunk count for n (0: not supported), setup
+// (ends: P x 8 scratch), selection and launch
+constexpr int PART_LMAX = 512;
+int part_chunks(int n);
+cudaError_t launch_part_setup(int n, int P, const double *subA, const double *supA, const double *rsA,
+                              const double *diagA, double dt, int transpose, double *rowc, double *fac,
+                              double *ends, int *bad, cudaStream_t s);
+bool part_preferred(const Op &op, long B, int m);
+cudaError_t launch_stepper_part(const Op &op, const StepArgs &a, int transpose, cudaStream_t s);
 // scale == 0: out = Omega; else out += scale * (independent N(0,1) field, counter word 3 = ctr3)
 cudaError_t launch_sketch(int dim, int n, long rows, int q0, int nint, int l,
                           unsigned long long seed, double *out, long rs, long vs, cudaStream_t s,

@@ -40,11 +40,23 @@ def test_gaussian_sketch_matches_oracle(n, nint, l, q0):
 
 
 # -------------------------------------------------------------- fine solver
+def _stepper_path(monkeypatch, path):
+    """Select the 1D stepper: the fused one-vector-per-thread kernel (K1) or the
+    cluster-partitioned small-batch kernel (K1P, k_part.cu; used for every n it
+    supports)."""
+    monkeypatch.delenv("PR_NO_PART", raising=False)
+    monkeypatch.delenv("PR_FORCE_PART", raising=False)
+    monkeypatch.setenv("PR_NO_PART" if path == "fused" else "PR_FORCE_PART", "1")
+
+
 @pytest.mark.parametrize("name,n,m,B", [("C1", 127, 64, 12), ("C1", 127, 1, 6), ("C1", 127, 2, 5),
-                                        ("T4", 301, 16, 33), ("T4", 37, 7, 64), ("C2", 4095, 256, 10),
+                                        ("T4", 301, 16, 33), ("T4", 37, 7, 64), ("T1", 200, 12, 70),
+                                        ("C2", 4095, 256, 10), ("C2", 8192, 20, 3),
                                         ("C4", 16383, 128, 6)])
 @pytest.mark.parametrize("mode", ["linear", "adjoint"])
-def test_fine_linear_adjoint(name, n, m, B, mode):
+@pytest.mark.parametrize("path", ["fused", "part"])
+def test_fine_linear_adjoint(name, n, m, B, mode, path, monkeypatch):
+    _stepper_path(monkeypatch, path)
     from paper_2508_08873_b200 import PR_ADJOINT, PR_LINEAR
     cfg = replace(get(name), n=n, m=m)
     op_o = make_op(cfg)
@@ -61,7 +73,9 @@ def test_fine_linear_adjoint(name, n, m, B, mode):
 
 
 @pytest.mark.parametrize("name,B,ld", [("T4", 5 * 4, 20), ("T4", 5 * 3, 17), ("C1", 8, 8)])
-def test_fine_affine_offset_and_inplace(name, B, ld):
+@pytest.mark.parametrize("path", ["fused", "part"])
+def test_fine_affine_offset_and_inplace(name, B, ld, path, monkeypatch):
+    _stepper_path(monkeypatch, path)
     from paper_2508_08873_b200 import PR_AFFINE, PR_LINEAR
     cfg = get(name)
     op_o, op_g = make_op(cfg), gpu_op(cfg)
