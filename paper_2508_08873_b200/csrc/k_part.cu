@@ -3,24 +3,37 @@
 // The fused stepper (k_tridiag.cu) runs one vector per thread, so a batch of
 // B vectors keeps only B/32 warps busy; with few vectors (Parareal fine solves
 // of C1/C2: 16-64 vectors) each warp's row recurrence is latency-bound.  Here
-// every vector's n rows are split into P chunks, one chunk per CTA of a
-// P-CTA thread-block cluster, and the chunk state stays in shared memory for
-// all m steps.  One step (I + dt A) x = r by the partition method:
-//   g_c  = T_c^{-1} r_c                         (local LU, row-sum pivots)
-//   x_c  = g_c + V_c b_{c-1} + W_c t_{c+1}      (spikes V_c = T_c^{-1}(-a e_1),
-//                                                W_c = T_c^{-1}(-c e_L), fixed)
-//   (t_c, b_c) = first / last unknown of chunk c, solved from the 2P x 2P
-//   interface system  z_i - V b - W t = g_i,  a banded M-matrix factored once
-//   with row-sum (GTH-type) elimination: its row sums 1 - V - W = T_c^{-1} s_c
-//   are computed directly, so the pivots keep O(u) relative accuracy whatever
-//   dt/h^2 (reading R-ACC).
-// Per step a CTA sweeps its chunk down (forward elimination, after applying the
-// previous step's spike correction and the source) and up (back substitution)
-// in shared memory, publishes its two end values to the cluster leader through
-// distributed shared memory, the leader solves the interface system (one lane
-// per vector) and scatters (b_{c-1}, t_{c+1}) back.  Two cluster barriers per
-// step; HBM is touched only to read the input and write the result.
+// every vector's rows are split into P = CL * W chunks of L rows (one warp per
+// chunk, W warps per CTA, CL CTAs per thread-block cluster, rows >= n are
+// decoupled identity rows) and each chunk's state lives in REGISTERS for all m
+// steps (L <= 64 doubles per lane).  One step (I + dt A) x = r by
+// the partition method:
+//   x_c = T_c^{-1} r_c + V_c b_{c-1} + W_c t_{c+1}
+//   V_c = T_c^{-1}(-a e_1), W_c = T_c^{-1}(-c e_L)     (spikes, fixed)
+//   (t_c, b_c) = first / last unknown of chunk c, from the 2P x 2P interface
+//   system z - V b - W t = g (rows at the chunk ends): a banded M-matrix.
+// The interface system is solved in two levels: the W chunks of a CTA form a
+// super-chunk whose local 2W x 2W system is inverted once (its inverse, and the
+// super-chunk spikes alpha = Minv_C e_left, beta = Minv_C e_right), and the
+// CL super-chunks form a 2CL x 2CL system of the same shape, inverted once; a
+// CTA keeps the two rows of that inverse giving its neighbours' boundary
+// values.  All factorizations use row-sum (GTH-type) elimination of the
+// M-matrices with row sums propagated exactly (reading R-ACC), so the inverses
+// are entrywise accurate and non-negative.
+//
+// Pipelining.  Write the chunk solution of step j as
+//   x_j = S_j + a_j V2 + c_j W2 + b_j V + t_j W,   V2 = T_c^{-1} V, W2 = T_c^{-1} W,
+// with (a_j, c_j) = (b_{j-1}, t_{j-1}).  Then S_{j+1} = T_c^{-1}(S_j + a_j V2 + c_j W2
+// + dt f_{j+1}) needs only the PREVIOUS step's interface values, so the sweep of
+// step j+1 runs while the interface exchange of step j is in flight: after its
+// sweep a CTA combines its chunks' end values (shared memory), sends its
+// super-chunk's two reduced values to every CTA of the cluster with st.async
+// (distributed shared memory, completion counted on the receiver's mbarrier),
+// and only after the next sweep waits for the gathered values.  HBM is touched
+// only to read the input and write the result.
 #include <cooperative_groups.h>
+#include <stdio.h>
+#include <stdlib.h>
 
 #include "pr_internal.cuh"
 
@@ -28,9 +41,17 @@ namespace cg = cooperative_groups;
 
 namespace pr {
 
+// per-CTA interface data (PART_CTAD doubles): Minv_C (2W x 2W, row-major) |
+// alpha (2W) | beta (2W) | rows of the global inverse for B_{C-1} (2CL) and T_{C+1} (2CL)
+constexpr int CTAD_A = 4 * PART_WMAX * PART_WMAX;
+constexpr int CTAD_B = CTAD_A + 2 * PART_WMAX;
+constexpr int CTAD_GB = CTAD_B + 2 * PART_WMAX;
+constexpr int CTAD_GT = CTAD_GB + 2 * PART_CLMAX;
+
 // ------------------------------------------------------------------ setup
-// One thread per chunk c (rows s0..e0-1): local LU of T_c in row-sum form and
-// the three local solves V_c, W_c, rho_c.  rowc row i: {w_i, -ga_i, -cp_i, V_i, W_i};
+// One thread per chunk c (rows s0..s0+L-1): local LU of T_c in row-sum form and
+// the local solves V, W (spikes), V2 = T_c^{-1} V, W2 = T_c^{-1} W and rho = T_c^{-1} s.
+// rowc row i: {w_i, -ga_i, -cp_i, V_i, W_i, V2_i, W2_i, 0};
 // ends[c] = {rho_top, rho_bot, V_top, V_bot, W_top, W_bot, 0, 0}.
 __global__ void k_part_setup(int n, int P, int L, const double *subA, const double *supA,
                              const double *rsA, const double *diagA, double dt, int transpose,
@@ -38,22 +59,22 @@ __global__ void k_part_setup(int n, int P, int L, const double *subA, const doub
 {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= P) return;
-    const int s0 = c * L, e0 = min(n, s0 + L);
-    if (s0 >= e0 || e0 - s0 > PART_LMAX) { atomicExch(bad, 1); return; }
+    const int s0 = c * L, e0 = s0 + L;
     auto a_of = [&](int i) -> double {              // (I + dt A)[i, i-1] (or of the transpose)
-        if (i <= 0) return 0.0;
+        if (i <= 0 || i >= n) return 0.0;
         return dt * (transpose ? supA[i - 1] : subA[i]);
     };
     auto c_of = [&](int i) -> double {              // (I + dt A)[i, i+1]
         if (i >= n - 1) return 0.0;
         return dt * (transpose ? subA[i + 1] : supA[i]);
     };
-    auto s_of = [&](int i) -> double {              // row sums of I + dt A
+    auto s_of = [&](int i) -> double {              // row sums of I + dt A (1 on padding rows)
+        if (i >= n) return 1.0;
         if (rsA) return 1.0 + dt * rsA[i];
         return a_of(i) + (1.0 + dt * diagA[i]) + c_of(i);
     };
     // local LU: T_c drops a_{s0} and c_{e0-1}; its row sums are s_i minus the
-    // dropped (non-positive) entries, so they stay exact sums of the stencil
+    // dropped (non-positive) entries
     double r = 0.0, den = 1.0;
     for (int i = s0; i < e0; ++i) {
         const double ai = (i == s0) ? 0.0 : a_of(i);
@@ -65,78 +86,65 @@ __global__ void k_part_setup(int n, int P, int L, const double *subA, const doub
         den = r - ci;
         if (!(den > 0.0) || !isfinite(den)) atomicExch(bad, 1);
         const double w = 1.0 / den;
-        double *R = rowc + (size_t)i * 5;
+        double *R = rowc + (size_t)i * 8;
         R[0] = w;
         R[1] = -(w * ai);
         R[2] = -(w * ci);
+        R[7] = 0.0;
     }
     // T_c x = rhs: forward y_i = w_i rhs_i - ga_i y_{i-1}, back x_i = y_i - cp_i x_{i+1}
-    double y[PART_LMAX];
+    double y[64];                                   // L <= 64
     double *E = ends + (size_t)c * 8;
-    for (int which = 0; which < 3; ++which) {       // 0: V, 1: W, 2: rho
+    for (int which = 0; which < 5; ++which) {       // 0: V, 1: W, 2: rho, 3: V2, 4: W2
         double yp = 0.0;
         for (int i = s0; i < e0; ++i) {
+            const double *R = rowc + (size_t)i * 8;
             double rhs = 0.0;
             if (which == 0 && i == s0) rhs = -a_of(s0);
             if (which == 1 && i == e0 - 1) rhs = -c_of(e0 - 1);
             if (which == 2) rhs = s_of(i);
-            const double *R = rowc + (size_t)i * 5;
+            if (which == 3) rhs = R[3];
+            if (which == 4) rhs = R[4];
             yp = fma(R[1], yp, R[0] * rhs);
             y[i - s0] = yp;
         }
         double xn = 0.0;
         for (int i = e0 - 1; i >= s0; --i) {
-            double *R = rowc + (size_t)i * 5;
+            double *R = rowc + (size_t)i * 8;
             const double x = fma(R[2], xn, y[i - s0]);
-            if (which < 2) R[3 + which] = x;
-            if (i == s0) E[which == 0 ? 2 : which == 1 ? 4 : 0] = x;
-            if (i == e0 - 1) E[which == 0 ? 3 : which == 1 ? 5 : 1] = x;
+            if (which == 0) R[3] = x;
+            if (which == 1) R[4] = x;
+            if (which == 3) R[5] = x;
+            if (which == 4) R[6] = x;
+            if (which < 3) {
+                if (i == s0) E[which == 0 ? 2 : which == 1 ? 4 : 0] = x;
+                if (i == e0 - 1) E[which == 0 ? 3 : which == 1 ? 5 : 1] = x;
+            }
             xn = x;
         }
     }
     E[6] = E[7] = 0.0;
 }
 
-// Interface system of 2P unknowns z = (t_0, b_0, ..., t_{P-1}, b_{P-1}):
-//   row 2c   : t_c - V_c[top] b_{c-1} - W_c[top] t_{c+1} = g_c[top]
-//   row 2c+1 : b_c - V_c[bot] b_{c-1} - W_c[bot] t_{c+1} = g_c[bot]
-// Banded M-matrix (offsets -2..+2), factored without pivoting; off-diagonals
-// are updated with same-sign products, row sums with positive terms, and each
-// pivot is (row sum) - (remaining off-diagonals): no cancellation.
-// fac (per row i, 5 doubles): {l_{i,i-2}, l_{i,i-1}, 1/u_ii, u_{i,i+1}, u_{i,i+2}}.
-__global__ void k_part_reduced(int P, const double *ends, double *fac, int *bad)
+// Banded M-matrix of order M <= 32 with offsets -2..+2 (A[i][d] at column
+// i + d - 2, off-diagonals <= 0) and exact row sums rs[i] > 0, factored without
+// pivoting: off-diagonals are updated with same-sign products, row sums with
+// positive terms, and each pivot is (row sum) - (remaining off-diagonals).
+// F[i] = {l_{i,i-2}, l_{i,i-1}, 1/u_ii, u_{i,i+1}, u_{i,i+2}}.
+__device__ bool band_factor(int M, double (*A)[5], double *rs, double (*F)[5])
 {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const int M = 2 * P;
-    double A[64][5];          // band: A[i][d], column i + d - 2
-    double rs[64];
-    for (int i = 0; i < M; ++i) {
-        for (int d = 0; d < 5; ++d) A[i][d] = 0.0;
-        const int c = i / 2;
-        const bool top = (i % 2 == 0);
-        const double *E = ends + (size_t)c * 8;
-        const double V = top ? E[2] : E[3];
-        const double W = top ? E[4] : E[5];
-        A[i][2] = 1.0;
-        // b_{c-1} is column 2c-1: offset (2c-1) - i + 2
-        if (c > 0) A[i][(2 * c - 1) - i + 2] = -V;
-        // t_{c+1} is column 2c+2
-        if (c < P - 1) A[i][(2 * c + 2) - i + 2] = -W;
-        rs[i] = top ? E[0] : E[1];
-    }
+    bool ok = true;
     for (int i = 0; i < M; ++i) {
         double l2 = 0.0, l1 = 0.0;
-        for (int dj = 2; dj >= 1; --dj) {              // eliminate columns i-2, i-1
+        for (int dj = 2; dj >= 1; --dj) {
             const int j = i - dj;
             if (j < 0) continue;
             const double aij = A[i][2 - dj];
             if (aij == 0.0) continue;
-            const double mult = aij * fac[(size_t)j * 5 + 2];     // a_ij / u_jj  (<= 0)
-            // row_i -= mult * row_j (columns > j): u_{j,j+1}, u_{j,j+2}
+            const double mult = aij * F[j][2];                 // a_ij / u_jj (<= 0)
             for (int e = 1; e <= 2; ++e) {
-                const int col = j + e;
-                const int di = col - i + 2;
-                if (di >= 0 && di < 5) A[i][di] -= mult * fac[(size_t)j * 5 + 2 + e];
+                const int di = j + e - i + 2;
+                if (di >= 0 && di < 5) A[i][di] -= mult * F[j][2 + e];
             }
             rs[i] -= mult * rs[j];
             if (dj == 2) l2 = mult; else l1 = mult;
@@ -145,212 +153,449 @@ __global__ void k_part_reduced(int P, const double *ends, double *fac, int *bad)
         double off = 0.0;
         for (int e = 1; e <= 2; ++e)
             if (i + e < M) off += A[i][2 + e];
-        const double piv = rs[i] - off;               // accurate diagonal
-        if (!(piv > 0.0) || !isfinite(piv)) atomicExch(bad, 1);
-        double *F = fac + (size_t)i * 5;
-        F[0] = l2;
-        F[1] = l1;
-        F[2] = 1.0 / piv;
-        F[3] = (i + 1 < M) ? A[i][3] : 0.0;
-        F[4] = (i + 2 < M) ? A[i][4] : 0.0;
+        const double piv = rs[i] - off;
+        if (!(piv > 0.0) || !isfinite(piv)) ok = false;
+        F[i][0] = l2;
+        F[i][1] = l1;
+        F[i][2] = 1.0 / piv;
+        F[i][3] = (i + 1 < M) ? A[i][3] : 0.0;
+        F[i][4] = (i + 2 < M) ? A[i][4] : 0.0;
     }
+    return ok;
+}
+
+// x <- M^{-1} x with the factors (for x >= 0 every term is non-negative)
+__device__ void band_solve(int M, const double (*F)[5], double *x)
+{
+    for (int i = 0; i < M; ++i) {
+        if (i >= 2) x[i] -= F[i][0] * x[i - 2];
+        if (i >= 1) x[i] -= F[i][1] * x[i - 1];
+    }
+    for (int i = M - 1; i >= 0; --i) {
+        if (i + 1 < M) x[i] -= F[i][3] * x[i + 1];
+        if (i + 2 < M) x[i] -= F[i][4] * x[i + 2];
+        x[i] *= F[i][2];
+    }
+}
+
+// Interface data (one thread).  Chunk-level rows of chunk c: row 2c (t_c) and
+// 2c+1 (b_c):  z - V_c[end] b_{c-1} - W_c[end] t_{c+1} = g_c[end].
+// Super-chunk C = chunks C*W .. C*W+W-1: local matrix M_C (couplings inside C),
+// Minv_C, alpha_C = Minv_C e_left (V of the first chunk), beta_C = Minv_C e_right
+// (W of the last chunk), rho_C = Minv_C rho (row sums of the full rows).  Global
+// rows of C: T_C - alpha_C[0] B_{C-1} - beta_C[0] T_{C+1} = zloc_C[0] and
+// B_C - alpha_C[2W-1] B_{C-1} - beta_C[2W-1] T_{C+1} = zloc_C[2W-1].
+__global__ void k_part_iface(int CL, int W, const double *ends, double *ctad, int *bad)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double A[2 * PART_CLMAX][5], rs[2 * PART_CLMAX], F[2 * PART_CLMAX][5], x[2 * PART_CLMAX];
+    double gA[2 * PART_CLMAX][5], grs[2 * PART_CLMAX];
+    const int M = 2 * W;
+    bool ok = true;
+    for (int C = 0; C < CL; ++C) {
+        double *D = ctad + (size_t)C * PART_CTAD;
+        for (int i = 0; i < PART_CTAD; ++i) D[i] = 0.0;
+        for (int r = 0; r < M; ++r) {
+            const int w = r / 2, e = r % 2;
+            const double *E = ends + (size_t)(C * W + w) * 8;
+            for (int d = 0; d < 5; ++d) A[r][d] = 0.0;
+            A[r][2] = 1.0;
+            if (w > 0) A[r][(2 * w - 1) - r + 2] = -E[2 + e];
+            if (w < W - 1) A[r][(2 * w + 2) - r + 2] = -E[4 + e];
+            rs[r] = E[e] + (w == 0 ? E[2 + e] : 0.0) + (w == W - 1 ? E[4 + e] : 0.0);
+        }
+        ok = band_factor(M, A, rs, F) && ok;
+        for (int col = 0; col < M; ++col) {
+            for (int r = 0; r < M; ++r) x[r] = (r == col) ? 1.0 : 0.0;
+            band_solve(M, F, x);
+            for (int r = 0; r < M; ++r) D[r * M + col] = x[r];
+        }
+        const double *E0 = ends + (size_t)(C * W) * 8, *E1 = ends + (size_t)(C * W + W - 1) * 8;
+        for (int r = 0; r < M; ++r) x[r] = 0.0;
+        x[0] = E0[2];
+        x[1] = E0[3];
+        band_solve(M, F, x);
+        for (int r = 0; r < M; ++r) D[CTAD_A + r] = x[r];
+        const double aT = x[0], aB = x[M - 1];
+        for (int r = 0; r < M; ++r) x[r] = 0.0;
+        x[M - 2] = E1[4];
+        x[M - 1] = E1[5];
+        band_solve(M, F, x);
+        for (int r = 0; r < M; ++r) D[CTAD_B + r] = x[r];
+        const double bT = x[0], bB = x[M - 1];
+        for (int r = 0; r < M; ++r) x[r] = ends[(size_t)(C * W + r / 2) * 8 + r % 2];
+        band_solve(M, F, x);
+        // global rows 2C (T_C) and 2C+1 (B_C)
+        for (int e = 0; e < 2; ++e) {
+            const int r = 2 * C + e;
+            for (int d = 0; d < 5; ++d) gA[r][d] = 0.0;
+            gA[r][2] = 1.0;
+            if (C > 0) gA[r][(2 * C - 1) - r + 2] = -(e ? aB : aT);
+            if (C < CL - 1) gA[r][(2 * C + 2) - r + 2] = -(e ? bB : bT);
+            grs[r] = e ? x[M - 1] : x[0];
+        }
+    }
+    const int MG = 2 * CL;
+    ok = band_factor(MG, gA, grs, F) && ok;
+    for (int col = 0; col < MG; ++col) {
+        for (int r = 0; r < MG; ++r) x[r] = (r == col) ? 1.0 : 0.0;
+        band_solve(MG, F, x);
+        for (int C = 0; C < CL; ++C) {
+            double *D = ctad + (size_t)C * PART_CTAD;
+            D[CTAD_GB + col] = (C > 0) ? x[2 * C - 1] : 0.0;
+            D[CTAD_GT + col] = (C < CL - 1) ? x[2 * C + 2] : 0.0;
+        }
+    }
+    if (!ok) atomicExch(bad, 1);
 }
 
 // ------------------------------------------------------------------ stepper
 struct PartArgs {
-    int n, L, m;
+    int n, m;
     long B;
-    const double *rowc;                // n x 5
-    const double *fac;                 // 2P x 5
+    const double *rowc;                // (P*L) x 8
+    const double *ctad;                // CL x PART_CTAD
     const double *in; long ld_in;      // null -> zero
     double *out; long ld_out;
     const double *off; long ld_off;
     // source (same convention as StepArgs): R == 0 none
-    int R, RS;
+    int R;
     const double *spaceT;              // n x RS (zero padded)
     const double *time;
     const double *amp;
     int nsteps, nsrc, q0, vpi;
     double dt;
+    unsigned long long *prof;          // dev aid (PR_PART_PROF): per-phase clock sums, or null
 };
 
-// Shared memory of one CTA (chunk): state [L][32] | coefficients [L][5] |
-// source rows [L][RS] | interface factors [2P][5] | interface rhs [2P][32]
-// (used in the leader) | this chunk's (b_{c-1}, t_{c+1}) [2][32].
-static size_t part_smem(int L, int P, int RS)
+// CTA shared memory (doubles): 6 mbarriers | gathered super-chunk values [2][CL][32]
+// (double2) | raw chunk ends [2][W][32] (double2) | interface values (b_{c-1}, t_{c+1})
+// [2][W][32] (double2) | interface data | per compute warp: {w, -ga, V2, W2} [L] |
+// -cp [L] | source rows [L][RS] | cluster addresses [2][CL] (u32)
+template <int CL, int W, int L, int RS>
+constexpr size_t part_smem_t()
 {
-    return ((size_t)L * 32 + (size_t)L * 5 + (size_t)L * RS + (size_t)2 * P * 5 + (size_t)2 * P * 32 + 64) *
+    return (6 + (size_t)4 * CL * 32 + (size_t)8 * W * 32 + PART_CTAD + (size_t)W * L * (5 + RS) + CL) *
            sizeof(double);
 }
 
-template <int P, int RS>
-__global__ void __launch_bounds__(32) k_part_step(PartArgs a)
+__device__ __forceinline__ unsigned smem_u32(const void *p)
 {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ unsigned cluster_map(unsigned addr, unsigned rank)
+{
+    unsigned r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void st_async_v2(unsigned raddr, double x, double y, unsigned rbar)
+{
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+                 :: "r"(raddr), "d"(x), "d"(y), "r"(rbar) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity)
+{
+    unsigned done = 0;
+    while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    }
+}
+
+__device__ __forceinline__ void mbar_arrive(unsigned bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
+
+// Warps 0..W-1 each own a chunk (state in registers) and only sweep; warp W is
+// the interface warp: it turns the chunks' raw end values into super-chunk
+// values, exchanges them across the cluster, and hands each compute warp its
+// (b_{c-1}, t_{c+1}) -- all while the compute warps run the next sweep.
+// Local hand-offs use mbarriers: ebar[p] (W compute warps arrive: raw ends of a
+// step of parity p written), cbar[p] (interface warp arrives: interface values
+// of a step of parity p written); gbar[p] counts the cluster gather bytes.
+template <int CL, int W, int L, int RS>
+__global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
+{
+    constexpr int M = 2 * W;
     extern __shared__ __align__(16) double sm[];
     cg::cluster_group cluster = cg::this_cluster();
-    const int c = (int)cluster.block_rank();             // chunk
-    const long grp = blockIdx.x / P;                     // group of 32 vectors
-    const int lane = threadIdx.x;
-    const long v = grp * 32 + lane;
+    const int C = (int)cluster.block_rank();
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long v = (long)(blockIdx.x / CL) * 32 + lane;  // vector
     const bool valid = v < a.B;
-    const int L = a.L;
-    const int s0 = c * L, nr = max(0, min(a.n, s0 + L) - s0);
-    double *st = sm;
-    double *co = st + (size_t)L * 32;
-    double *sp = co + (size_t)L * 5;
-    double *fac = sp + (size_t)L * RS;
-    double *xg = fac + 2 * P * 5;
-    double *mine = xg + 2 * P * 32;
-    for (int i = lane; i < nr * 5; i += 32) co[i] = a.rowc[(size_t)s0 * 5 + i];
-    if constexpr (RS > 0)
-        for (int i = lane; i < nr * RS; i += 32) sp[i] = a.spaceT[(size_t)s0 * RS + i];
-    if (c == 0)
-        for (int i = lane; i < 2 * P * 5; i += 32) fac[i] = a.fac[i];
-    for (int i = 0; i < nr; ++i)
-        st[i * 32 + lane] = (a.in && valid) ? a.in[(long)(s0 + i) * a.ld_in + v] : 0.0;
-    double bL = 0.0, tR = 0.0;
-    const int q = valid ? a.q0 + (int)(v / a.vpi) : a.q0;
-    const int src = (RS > 0 && valid) ? (int)(v % a.nsrc) : 0;
-    double *lead = cluster.map_shared_rank(xg, 0);
-    __syncwarp();
-    for (int j = 1; j <= a.m; ++j) {
-        double alpha[RS > 0 ? RS : 1];
-        if constexpr (RS > 0) {
-#pragma unroll
-            for (int r = 0; r < RS; ++r) {
-                double al = 0.0;
-                if (r < a.R && valid)
-                    al = a.dt * a.amp[(long)src * a.R + r] * a.time[(long)r * a.nsteps + (long)q * a.m + j - 1];
-                alpha[r] = al;
-            }
+    unsigned long long *bar = reinterpret_cast<unsigned long long *>(sm);   // gbar[2] ebar[2] cbar[2]
+    double2 *gth = reinterpret_cast<double2 *>(sm + 6);              // [2][CL][32]
+    double2 *rawE = gth + 2 * CL * 32;                               // [2][W][32]
+    double2 *coef = rawE + 2 * W * 32;                               // [2][W][32]
+    double *ctad = reinterpret_cast<double *>(coef + 2 * W * 32);
+    double *regions = ctad + PART_CTAD;
+    unsigned *rmap = reinterpret_cast<unsigned *>(regions + (size_t)W * L * (5 + RS));  // [2][CL]
+    auto cd_of = [&](int u) { return reinterpret_cast<double4 *>(regions + (size_t)u * L * (5 + RS)); };
+    const unsigned bar0 = smem_u32(bar), gth0 = smem_u32(gth);
+    const unsigned gbar = bar0, ebar = bar0 + 16, cbar = bar0 + 32;
+
+    for (int i = threadIdx.x; i < PART_CTAD; i += blockDim.x) ctad[i] = a.ctad[(size_t)C * PART_CTAD + i];
+    if (threadIdx.x < CL) {        // cluster addresses of every CTA's gather buffer and barriers
+        rmap[threadIdx.x] = cluster_map(gth0, threadIdx.x);
+        rmap[CL + threadIdx.x] = cluster_map(bar0, threadIdx.x);
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(gbar) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(gbar + 8) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(ebar), "r"(W) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(ebar + 8), "r"(W) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(cbar) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(cbar + 8) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+
+    if (w < W) {
+        // ------------------------------------------------ compute warp: chunk c
+        const int c = C * W + w;
+        const int s0 = c * L;
+        double4 *cd = cd_of(w);
+        double *cu = reinterpret_cast<double *>(cd) + 4 * L;
+        double *sp = cu + L;
+        for (int i = lane; i < L; i += 32) {
+            const double *R = a.rowc + (size_t)(s0 + i) * 8;
+            cd[i] = make_double4(R[0], R[1], R[5], R[6]);
+            cu[i] = R[2];
         }
-        // down: x = g + V bL + W tR (previous step's solution), r = x + dt f_j,
-        //       y_i = w_i r_i - ga_i y_{i-1}
-        double yp = 0.0;
-        const bool corr = j > 1;
-#pragma unroll 4
-        for (int i = 0; i < nr; ++i) {
-            const double *C = co + i * 5;
-            double x = st[i * 32 + lane];
-            if (corr) x = fma(C[3], bL, fma(C[4], tR, x));
+        if constexpr (RS > 0)
+            for (int i = lane; i < L * RS; i += 32) {
+                const int row = s0 + i / RS;
+                sp[i] = (row < a.n) ? a.spaceT[(size_t)row * RS + i % RS] : 0.0;
+            }
+        double S[L];
+#pragma unroll
+        for (int i = 0; i < L; ++i)
+            S[i] = (a.in && valid && s0 + i < a.n) ? a.in[(long)(s0 + i) * a.ld_in + v] : 0.0;
+        cluster.sync();
+        const int q = valid ? a.q0 + (int)(v / a.vpi) : a.q0;
+        const int src = (RS > 0 && valid) ? (int)(v % a.nsrc) : 0;
+        double ca = 0.0, cc = 0.0;     // (b_{c-1}, t_{c+1}) of step j-1: coefficients of V2, W2
+        for (int j = 1; j <= a.m; ++j) {
+            long long t0 = a.prof ? clock64() : 0;
+            double alpha[RS > 0 ? RS : 1];
             if constexpr (RS > 0) {
 #pragma unroll
-                for (int r = 0; r < RS; ++r) x = fma(alpha[r], sp[i * RS + r], x);
+                for (int r = 0; r < RS; ++r) {
+                    double al = 0.0;
+                    if (r < a.R && valid)
+                        al = a.dt * a.amp[(long)src * a.R + r] * a.time[(long)r * a.nsteps + (long)q * a.m + j - 1];
+                    alpha[r] = al;
+                }
             }
-            yp = fma(C[1], yp, C[0] * x);
-            st[i * 32 + lane] = yp;
+            // S_j = T_c^{-1}(S_{j-1} + ca V2 + cc W2 + dt f_j); down: y_i = w_i x_i - ga_i y_{i-1}
+            double yp = 0.0;
+#pragma unroll
+            for (int i = 0; i < L; ++i) {
+                const double4 q4 = cd[i];
+                double x = fma(q4.z, ca, fma(q4.w, cc, S[i]));
+                if constexpr (RS > 0) {
+#pragma unroll
+                    for (int r = 0; r < RS; ++r) x = fma(alpha[r], sp[i * RS + r], x);
+                }
+                yp = fma(q4.y, yp, q4.x * x);
+                S[i] = yp;
+            }
+            // up: S_i = y_i - cp_i S_{i+1}
+            double gn = 0.0;
+#pragma unroll
+            for (int i = L - 1; i >= 0; --i) {
+                gn = fma(cu[i], gn, S[i]);
+                S[i] = gn;
+            }
+            long long t1 = a.prof ? clock64() : 0;
+            const int p = j & 1;
+            rawE[(p * W + w) * 32 + lane] = make_double2(S[0], S[L - 1]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ebar + 8 * p);
+            if (j >= 2) {              // interface values of step j-1 (formed during this sweep)
+                const int pp = (j - 1) & 1;
+                mbar_wait(cbar + 8 * pp, ((j - 2) >> 1) & 1);
+                const double2 e = coef[(pp * W + w) * 32 + lane];
+                ca = e.x;
+                cc = e.y;
+            }
+            if (a.prof && lane == 0) {
+                long long t2 = clock64();
+                unsigned long long *pr = a.prof + (size_t)c * 4;
+                atomicAdd(pr + 0, (unsigned long long)(t1 - t0));
+                atomicAdd(pr + 1, (unsigned long long)(t2 - t1));
+            }
         }
-        // up: g_i = y_i - cp_i g_{i+1}
-        double gn = 0.0;
-#pragma unroll 4
-        for (int i = nr - 1; i >= 0; --i) {
-            const double g = fma(co[i * 5 + 2], gn, st[i * 32 + lane]);
-            st[i * 32 + lane] = g;
-            gn = g;
+        const int pm = a.m & 1;
+        mbar_wait(cbar + 8 * pm, ((a.m - 1) >> 1) & 1);
+        const double2 e = coef[(pm * W + w) * 32 + lane];       // (b_m, t_m) of the neighbours
+        if (valid) {
+#pragma unroll
+            for (int i = 0; i < L; ++i) {
+                if (s0 + i < a.n) {
+                    const double4 q4 = cd[i];
+                    const double *R = a.rowc + (size_t)(s0 + i) * 8;
+                    double x = fma(q4.z, ca, fma(q4.w, cc, S[i]));
+                    x = fma(R[3], e.x, fma(R[4], e.y, x));
+                    if (a.off) x += a.off[(long)(s0 + i) * a.ld_off + v];
+                    a.out[(long)(s0 + i) * a.ld_out + v] = x;
+                }
+            }
         }
-        lead[(2 * c) * 32 + lane] = st[lane];
-        lead[(2 * c + 1) * 32 + lane] = st[(nr - 1) * 32 + lane];
+    } else {
+        // ------------------------------------------------ interface warp
         cluster.sync();
-        if (c == 0) {
-            // banded forward / back substitution of the interface system
-            constexpr int M = 2 * P;
-            double z[M];
+        double hb[W], ht[W], zb[W], zt[W];          // (b, t) of step j-1 per chunk; local parts
 #pragma unroll
-            for (int i = 0; i < M; ++i) {
-                double zi = xg[i * 32 + lane];
-                if (i >= 2) zi = fma(-fac[i * 5 + 0], z[i - 2], zi);
-                if (i >= 1) zi = fma(-fac[i * 5 + 1], z[i - 1], zi);
-                z[i] = zi;
+        for (int u = 0; u < W; ++u) hb[u] = ht[u] = zb[u] = zt[u] = 0.0;
+        // step j's values from every super-chunk -> (b_{c-1}, t_{c+1}) of step j per chunk
+        auto gather = [&](int j) {
+            const int p = j & 1;
+            if (lane == 0)
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                             :: "r"(gbar + 8 * p), "r"((unsigned)(CL * 32 * sizeof(double2))) : "memory");
+            mbar_wait(gbar + 8 * p, ((j - 1) >> 1) & 1);
+            const double2 *G = gth + (size_t)p * CL * 32 + lane;
+            double b0 = 0.0, b1 = 0.0, t0 = 0.0, t1 = 0.0;
+#pragma unroll
+            for (int u = 0; u < CL; ++u) {
+                const double2 e = G[u * 32];
+                b0 = fma(ctad[CTAD_GB + 2 * u], e.x, b0);
+                b1 = fma(ctad[CTAD_GB + 2 * u + 1], e.y, b1);
+                t0 = fma(ctad[CTAD_GT + 2 * u], e.x, t0);
+                t1 = fma(ctad[CTAD_GT + 2 * u + 1], e.y, t1);
+            }
+            const double Bx = b0 + b1, Tx = t0 + t1;       // B_{C-1}, T_{C+1}
+#pragma unroll
+            for (int u = 0; u < W; ++u) {
+                hb[u] = (u == 0) ? Bx : fma(ctad[CTAD_A + 2 * u - 1], Bx, fma(ctad[CTAD_B + 2 * u - 1], Tx, zb[u]));
+                ht[u] = (u == W - 1) ? Tx : fma(ctad[CTAD_A + 2 * u + 2], Bx, fma(ctad[CTAD_B + 2 * u + 2], Tx, zt[u]));
+                coef[(p * W + u) * 32 + lane] = make_double2(hb[u], ht[u]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(cbar + 8 * p);
+        };
+        // chunk ends of g_j = S_j + b V2 + c W2 -> super-chunk values -> every CTA
+        auto publish = [&](int j) {
+            const int p = j & 1;
+            mbar_wait(ebar + 8 * p, ((j - 1) >> 1) & 1);
+            double E[M];
+#pragma unroll
+            for (int u = 0; u < W; ++u) {
+                const double2 r = rawE[(p * W + u) * 32 + lane];
+                const double4 q0 = cd_of(u)[0], q1 = cd_of(u)[L - 1];
+                E[2 * u] = fma(q0.z, hb[u], fma(q0.w, ht[u], r.x));
+                E[2 * u + 1] = fma(q1.z, hb[u], fma(q1.w, ht[u], r.y));
+            }
+            double T = 0.0, Bv = 0.0;
+#pragma unroll
+            for (int k = 0; k < M; ++k) {
+                T = fma(ctad[k], E[k], T);
+                Bv = fma(ctad[(M - 1) * M + k], E[k], Bv);
             }
 #pragma unroll
-            for (int i = M - 1; i >= 0; --i) {
-                double zi = z[i];
-                if (i + 1 < M) zi = fma(-fac[i * 5 + 3], z[i + 1], zi);
-                if (i + 2 < M) zi = fma(-fac[i * 5 + 4], z[i + 2], zi);
-                z[i] = zi * fac[i * 5 + 2];
-            }
+            for (int u = 0; u < W; ++u) {
+                double sb = 0.0, st = 0.0;
 #pragma unroll
-            for (int cc = 0; cc < P; ++cc) {
-                double *dst = cluster.map_shared_rank(mine, cc);
-                dst[lane] = (cc > 0) ? z[2 * cc - 1] : 0.0;
-                dst[32 + lane] = (cc < P - 1) ? z[2 * cc + 2] : 0.0;
+                for (int k = 0; k < M; ++k) {
+                    if (u > 0) sb = fma(ctad[(2 * u - 1) * M + k], E[k], sb);
+                    if (u < W - 1) st = fma(ctad[(2 * u + 2) * M + k], E[k], st);
+                }
+                zb[u] = sb;
+                zt[u] = st;
             }
+            const unsigned off = (unsigned)(((p * CL + C) * 32 + lane) * sizeof(double2));
+#pragma unroll
+            for (int r = 0; r < CL; ++r)
+                st_async_v2(rmap[r] + off, T, Bv, rmap[CL + r] + 8 * p);
+        };
+        for (int j = 1; j <= a.m; ++j) {
+            if (j >= 2) gather(j - 1);
+            publish(j);
         }
-        cluster.sync();
-        bL = mine[lane];
-        tR = mine[32 + lane];
+        gather(a.m);
     }
-    if (valid) {
-        for (int i = 0; i < nr; ++i) {
-            const double *C = co + i * 5;
-            double x = fma(C[3], bL, fma(C[4], tR, st[i * 32 + lane]));
-            if (a.off) x += a.off[(long)(s0 + i) * a.ld_off + v];
-            a.out[(long)(s0 + i) * a.ld_out + v] = x;
-        }
-    }
+    cluster.sync();                // no CTA leaves while cluster peers may still target it
 }
 
 // ---------------------------------------------------------------- driver
-int part_chunks(int n)
+bool part_config(int n, int &P, int &L, int &CL, int &W)
 {
-    // largest P in {16, 8, 4, 2} with chunks of >= 32 rows; chunks hold <= PART_LMAX rows
-    for (int P = 16; P >= 2; P /= 2)
-        if (n / P >= 32 && (n + P - 1) / P <= PART_LMAX) return P;
-    return 0;
+    // chunks of L = 32 rows up to n = 512, else 64 (measured on B200, C2 B=64:
+    // 0.41 ms at L=64, 4 warps/CTA vs 0.50 ms at L=32, 8 warps/CTA): P (a power
+    // of two) chunks cover P*L >= n rows, the rest identity padding; up to 16
+    // CTAs per cluster, then 2..8 warps per CTA.  PR_PART_L=32 forces 32-row
+    // chunks (measurements).
+    if (n < 64 || n > 16 * PART_WMAX * 64) return false;
+    L = (n <= 512) ? 32 : 64;
+    if (const char *e = getenv("PR_PART_L"))
+        if (atoi(e) == 32 && n <= 16 * PART_WMAX * 32) L = 32;
+    const int need = (n + L - 1) / L;
+    P = 2;
+    while (P < need) P *= 2;
+    CL = P < PART_CLMAX ? P : PART_CLMAX;
+    W = P / CL;
+    return W <= PART_WMAX;
 }
 
-cudaError_t launch_part_setup(int n, int P, const double *subA, const double *supA, const double *rsA,
-                              const double *diagA, double dt, int transpose, double *rowc, double *fac,
-                              double *ends, int *bad, cudaStream_t s)
+cudaError_t launch_part_setup(int n, int P, int L, int CL, int W, const double *subA, const double *supA,
+                              const double *rsA, const double *diagA, double dt, int transpose, double *rowc,
+                              double *ctad, double *ends, int *bad, cudaStream_t s)
 {
-    const int L = (n + P - 1) / P;
     note_launch();
-    k_part_setup<<<1, 32, 0, s>>>(n, P, L, subA, supA, rsA, diagA, dt, transpose, rowc, ends, bad);
+    k_part_setup<<<(P + 63) / 64, 64, 0, s>>>(n, P, L, subA, supA, rsA, diagA, dt, transpose, rowc, ends, bad);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     note_launch();
-    k_part_reduced<<<1, 1, 0, s>>>(P, ends, fac, bad);
+    k_part_iface<<<1, 32, 0, s>>>(CL, W, ends, ctad, bad);
     return cudaGetLastError();
 }
 
-template <int P, int RS>
+template <int CL, int W, int L, int RS>
 static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
 {
-    const size_t smem = part_smem(a.L, P, RS);
+    constexpr size_t smem = part_smem_t<CL, W, L, RS>();
+    static_assert(smem <= 227 * 1024, "partitioned stepper shared memory");
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(k_part_step<P, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)part_smem(PART_LMAX, P, RS));
-        if (e == cudaSuccess && P > 8)
-            e = cudaFuncSetAttribute(k_part_step<P, RS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaError_t e = cudaFuncSetAttribute(k_part_step<CL, W, L, RS>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess && CL > 8)
+            e = cudaFuncSetAttribute(k_part_step<CL, W, L, RS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(groups * P));
-    cfg.blockDim = dim3(32);
+    cfg.gridDim = dim3((unsigned)(groups * CL));
+    cfg.blockDim = dim3(32 * (W + 1));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = P;
+    attr[0].val.clusterDim.x = CL;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     note_launch();
-    return cudaLaunchKernelEx(&cfg, k_part_step<P, RS>, a);
+    return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, L, RS>, a);
 }
 
-template <int P>
-static cudaError_t part_launch_rs(const PartArgs &a, long groups, cudaStream_t s)
+template <int CL, int W, int L>
+static cudaError_t part_launch_rs(const PartArgs &a, int RS, long groups, cudaStream_t s)
 {
-    switch (a.RS) {
-    case 0: return part_launch<P, 0>(a, groups, s);
-    case 1: return part_launch<P, 1>(a, groups, s);
-    case 2: return part_launch<P, 2>(a, groups, s);
-    case 4: return part_launch<P, 4>(a, groups, s);
-    default: return part_launch<P, 8>(a, groups, s);
+    switch (RS) {
+    case 0: return part_launch<CL, W, L, 0>(a, groups, s);
+    case 1: return part_launch<CL, W, L, 1>(a, groups, s);
+    case 2: return part_launch<CL, W, L, 2>(a, groups, s);
+    case 4: return part_launch<CL, W, L, 4>(a, groups, s);
+    default: return part_launch<CL, W, L, 8>(a, groups, s);
     }
 }
 
@@ -365,28 +610,59 @@ bool part_preferred(const Op &op, long B, int m)
 
 cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose, cudaStream_t s)
 {
-    const int P = op.part_P;
     PartArgs a{};
-    a.n = sa.n; a.L = (sa.n + P - 1) / P; a.m = sa.m; a.B = sa.B;
+    a.n = sa.n; a.m = sa.m; a.B = sa.B;
     a.rowc = transpose ? op.part_rowc_tr : op.part_rowc_fw;
-    a.fac = transpose ? op.part_fac_tr : op.part_fac_fw;
+    a.ctad = transpose ? op.part_ctad_tr : op.part_ctad_fw;
     a.in = sa.in; a.ld_in = sa.ld_in; a.out = sa.out; a.ld_out = sa.ld_out;
     a.off = sa.off; a.ld_off = sa.ld_off;
-    a.R = sa.R; a.RS = sa.R > 0 ? stepper_rs(sa.R) : 0;
+    a.R = sa.R;
+    const int RS = sa.R > 0 ? stepper_rs(sa.R) : 0;
     a.spaceT = sa.spaceT; a.time = sa.time; a.amp = sa.amp;
     a.nsteps = sa.nsteps; a.nsrc = sa.nsrc; a.q0 = sa.q0; a.vpi = sa.vpi; a.dt = sa.dt;
     const long groups = (sa.B + 31) / 32;
     if (groups == 0) return cudaSuccess;
+    static unsigned long long *dprof = nullptr;
+    const int P = op.part_P;
+    const bool want_prof = getenv("PR_PART_PROF") != nullptr;
+    if (want_prof) {
+        if (!dprof) cudaMalloc(&dprof, 16 * PART_WMAX * 4 * sizeof(unsigned long long));
+        cudaMemsetAsync(dprof, 0, 16 * PART_WMAX * 4 * sizeof(unsigned long long), s);
+        a.prof = dprof;
+    }
     const bool prof = profiling();
     if (prof) stepper_timed_begin(s);
-    cudaError_t e;
-    switch (P) {
-    case 16: e = part_launch_rs<16>(a, groups, s); break;
-    case 8: e = part_launch_rs<8>(a, groups, s); break;
-    case 4: e = part_launch_rs<4>(a, groups, s); break;
-    default: e = part_launch_rs<2>(a, groups, s); break;
+    cudaError_t e = cudaErrorInvalidValue;
+    if (op.part_L == 32 && op.part_W == 1) {
+        switch (op.part_CL) {
+        case 2: e = part_launch_rs<2, 1, 32>(a, RS, groups, s); break;
+        case 4: e = part_launch_rs<4, 1, 32>(a, RS, groups, s); break;
+        case 8: e = part_launch_rs<8, 1, 32>(a, RS, groups, s); break;
+        case 16: e = part_launch_rs<16, 1, 32>(a, RS, groups, s); break;
+        }
+    } else if (op.part_L == 32 && op.part_CL == 16) {
+        switch (op.part_W) {
+        case 2: e = part_launch_rs<16, 2, 32>(a, RS, groups, s); break;
+        case 4: e = part_launch_rs<16, 4, 32>(a, RS, groups, s); break;
+        case 8: e = part_launch_rs<16, 8, 32>(a, RS, groups, s); break;
+        }
+    } else if (op.part_L == 64 && op.part_CL == 16) {
+        switch (op.part_W) {
+        case 4: e = part_launch_rs<16, 4, 64>(a, RS, groups, s); break;
+        case 8: e = part_launch_rs<16, 8, 64>(a, RS, groups, s); break;
+        }
     }
     if (prof) stepper_timed_end(s, (double)sa.n * (double)sa.B * (double)sa.m, 0.0);
+    if (want_prof && e == cudaSuccess) {
+        unsigned long long h[16 * PART_WMAX * 4];
+        cudaMemcpyAsync(h, dprof, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        const double norm = (double)groups * sa.m;
+        fprintf(stderr, "part P=%d L=%d CL=%d W=%d m=%d groups=%ld  cycles/step [sweep hand-off]:\n", P,
+                op.part_L, op.part_CL, op.part_W, sa.m, groups);
+        for (int c = 0; c < P; c += (P > 16 ? P / 16 : 1))
+            fprintf(stderr, "  chunk %3d: %8.0f %8.0f\n", c, h[c * 4] / norm, h[c * 4 + 1] / norm);
+    }
     return e;
 }
 

@@ -363,7 +363,7 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
         cudaFree(d_in);
         cudaFree(d_bad);
         cudaFree(op.dn_fw); cudaFree(op.up_fw); cudaFree(op.dn_tr); cudaFree(op.up_tr);
-        cudaFree(op.part_rowc_fw); cudaFree(op.part_fac_fw); cudaFree(op.part_rowc_tr); cudaFree(op.part_fac_tr);
+        cudaFree(op.part_rowc_fw); cudaFree(op.part_ctad_fw); cudaFree(op.part_rowc_tr); cudaFree(op.part_ctad_tr);
         delete h;
         return st;
     };
@@ -386,21 +386,22 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
     if (e == cudaSuccess)
         e = launch_factor_1d(n, dsub, dsup, colsum ? dcs : nullptr, ddiag, dt, 1, op.dn_tr, op.up_tr, d_bad, 0);
     // partitioned-stepper factors (small batches), both orientations
-    const int P = part_chunks(n);
+    int pP = 0, pL = 0, pCL = 0, pW = 0;
     double *d_ends = nullptr;
-    if (e == cudaSuccess && P > 0) {
-        op.part_P = P;
-        e = cudaMalloc(&op.part_rowc_fw, 5 * nb);
-        if (e == cudaSuccess) e = cudaMalloc(&op.part_rowc_tr, 5 * nb);
-        if (e == cudaSuccess) e = cudaMalloc(&op.part_fac_fw, (size_t)10 * P * sizeof(double));
-        if (e == cudaSuccess) e = cudaMalloc(&op.part_fac_tr, (size_t)10 * P * sizeof(double));
-        if (e == cudaSuccess) e = cudaMalloc(&d_ends, (size_t)8 * P * sizeof(double));
+    if (e == cudaSuccess && part_config(n, pP, pL, pCL, pW)) {
+        op.part_P = pP; op.part_L = pL; op.part_CL = pCL; op.part_W = pW;
+        const size_t rb = (size_t)pP * pL * 8 * sizeof(double), cb = (size_t)pCL * PART_CTAD * sizeof(double);
+        e = cudaMalloc(&op.part_rowc_fw, rb);
+        if (e == cudaSuccess) e = cudaMalloc(&op.part_rowc_tr, rb);
+        if (e == cudaSuccess) e = cudaMalloc(&op.part_ctad_fw, cb);
+        if (e == cudaSuccess) e = cudaMalloc(&op.part_ctad_tr, cb);
+        if (e == cudaSuccess) e = cudaMalloc(&d_ends, (size_t)8 * pP * sizeof(double));
         if (e == cudaSuccess)
-            e = launch_part_setup(n, P, dsub, dsup, rowsum ? drs : nullptr, ddiag, dt, 0, op.part_rowc_fw,
-                                  op.part_fac_fw, d_ends, d_bad, 0);
+            e = launch_part_setup(n, pP, pL, pCL, pW, dsub, dsup, rowsum ? drs : nullptr, ddiag, dt, 0,
+                                  op.part_rowc_fw, op.part_ctad_fw, d_ends, d_bad, 0);
         if (e == cudaSuccess)
-            e = launch_part_setup(n, P, dsub, dsup, colsum ? dcs : nullptr, ddiag, dt, 1, op.part_rowc_tr,
-                                  op.part_fac_tr, d_ends, d_bad, 0);
+            e = launch_part_setup(n, pP, pL, pCL, pW, dsub, dsup, colsum ? dcs : nullptr, ddiag, dt, 1,
+                                  op.part_rowc_tr, op.part_ctad_tr, d_ends, d_bad, 0);
     }
     int bad = 0;
     if (e == cudaSuccess) e = cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost);
@@ -421,7 +422,7 @@ pr_status pr_op_destroy(pr_op h)
     if (!h) return PR_OK;
     Op &op = h->op;
     cudaFree(op.dn_fw); cudaFree(op.up_fw); cudaFree(op.dn_tr); cudaFree(op.up_tr);
-    cudaFree(op.part_rowc_fw); cudaFree(op.part_fac_fw); cudaFree(op.part_rowc_tr); cudaFree(op.part_fac_tr);
+    cudaFree(op.part_rowc_fw); cudaFree(op.part_ctad_fw); cudaFree(op.part_rowc_tr); cudaFree(op.part_ctad_tr);
     cudaFree(op.S); cudaFree(op.lam);
     delete h;
     return PR_OK;

@@ -63,11 +63,12 @@ struct Op {
     //   DN[i] = {ap_i, w_i, ga_i, 0}: down pass = UL back-substitution then LU forward
     //   UP[i] = {cp_i, wt_i, gc_i, 0}: up pass   = LU back-substitution then UL forward
     Coef *dn_fw = nullptr, *up_fw = nullptr, *dn_tr = nullptr, *up_tr = nullptr;
-    // 1D partitioned stepper (k_part.cu, small batches): P chunks per vector,
-    // per-row {w, -ga, -cp, V, W} (n x 5) and interface factors (2P x 5).
-    int part_P = 0;
-    double *part_rowc_fw = nullptr, *part_fac_fw = nullptr;
-    double *part_rowc_tr = nullptr, *part_fac_tr = nullptr;
+    // 1D partitioned stepper (k_part.cu, small batches): P = CL * W chunks of
+    // L rows (rows >= n: identity padding).  rowc: (P*L) x 8 per-row
+    // {w, -ga, -cp, V, W, V2, W2, 0}; ctad: CL x PART_CTAD per-CTA interface data.
+    int part_P = 0, part_L = 0, part_CL = 0, part_W = 0;
+    double *part_rowc_fw = nullptr, *part_ctad_fw = nullptr;
+    double *part_rowc_tr = nullptr, *part_ctad_tr = nullptr;
     // 2D: P = n+1; S (P x P) sine matrix with zero row/col 0; lam[P] eigenvalues of T.
     int P = 0;
     double *S = nullptr;
@@ -103,13 +104,15 @@ cudaError_t launch_factor_1d(int n, const double *subA, const double *supA, cons
                              int *bad, cudaStream_t s);
 cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s);
 
-// partitioned stepper (k_part.cu): chunk count for n (0: not supported), setup
-// (ends: P x 8 scratch), selection and launch
-constexpr int PART_LMAX = 512;
-int part_chunks(int n);
-cudaError_t launch_part_setup(int n, int P, const double *subA, const double *supA, const double *rsA,
-                              const double *diagA, double dt, int transpose, double *rowc, double *fac,
-                              double *ends, int *bad, cudaStream_t s);
+// partitioned stepper (k_part.cu): configuration for n (false: not supported),
+// setup (ends: P x 8 scratch), selection and launch
+constexpr int PART_WMAX = 8;                   // warps (chunks) per CTA
+constexpr int PART_CLMAX = 16;                 // CTAs per cluster
+constexpr int PART_CTAD = 4 * PART_WMAX * PART_WMAX + 4 * PART_WMAX + 4 * PART_CLMAX;
+bool part_config(int n, int &P, int &L, int &CL, int &W);
+cudaError_t launch_part_setup(int n, int P, int L, int CL, int W, const double *subA, const double *supA,
+                              const double *rsA, const double *diagA, double dt, int transpose, double *rowc,
+                              double *ctad, double *ends, int *bad, cudaStream_t s);
 bool part_preferred(const Op &op, long B, int m);
 cudaError_t launch_stepper_part(const Op &op, const StepArgs &a, int transpose, cudaStream_t s);
 // scale == 0: out = Omega; else out += scale * (independent N(0,1) field, counter word 3 = ctr3)
