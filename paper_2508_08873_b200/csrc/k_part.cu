@@ -41,11 +41,12 @@ namespace cg = cooperative_groups;
 
 namespace pr {
 
-// per-CTA interface data (PART_CTAD doubles): Minv_C (2W x 2W, row-major) |
-// alpha (2W) | beta (2W) | rows of the global inverse for B_{C-1} (2CL) and T_{C+1} (2CL)
-constexpr int CTAD_A = 4 * PART_WMAX * PART_WMAX;
-constexpr int CTAD_B = CTAD_A + 2 * PART_WMAX;
-constexpr int CTAD_GB = CTAD_B + 2 * PART_WMAX;
+// per-CTA interface data (PART_CTAD doubles): band factors of the local
+// interface matrix M_C (2K rows x 5) | alpha (2K) | beta (2K) | rows of the
+// global inverse for B_{C-1} (2CL) and T_{C+1} (2CL)
+constexpr int CTAD_A = 5 * 2 * PART_KMAX;
+constexpr int CTAD_B = CTAD_A + 2 * PART_KMAX;
+constexpr int CTAD_GB = CTAD_B + 2 * PART_KMAX;
 constexpr int CTAD_GT = CTAD_GB + 2 * PART_CLMAX;
 
 // ------------------------------------------------------------------ setup
@@ -180,37 +181,36 @@ __device__ void band_solve(int M, const double (*F)[5], double *x)
 
 // Interface data (one thread).  Chunk-level rows of chunk c: row 2c (t_c) and
 // 2c+1 (b_c):  z - V_c[end] b_{c-1} - W_c[end] t_{c+1} = g_c[end].
-// Super-chunk C = chunks C*W .. C*W+W-1: local matrix M_C (couplings inside C),
-// Minv_C, alpha_C = Minv_C e_left (V of the first chunk), beta_C = Minv_C e_right
-// (W of the last chunk), rho_C = Minv_C rho (row sums of the full rows).  Global
-// rows of C: T_C - alpha_C[0] B_{C-1} - beta_C[0] T_{C+1} = zloc_C[0] and
-// B_C - alpha_C[2W-1] B_{C-1} - beta_C[2W-1] T_{C+1} = zloc_C[2W-1].
-__global__ void k_part_iface(int CL, int W, const double *ends, double *ctad, int *bad)
+// Super-chunk C = chunks C*K .. C*K+K-1: local matrix M_C (couplings inside C)
+// and its band factors, alpha_C = M_C^{-1} e_left (V of the first chunk),
+// beta_C = M_C^{-1} e_right (W of the last chunk), rho_C = M_C^{-1} rho (row sums
+// of the full rows).  Global rows of C:
+//   T_C - alpha_C[0] B_{C-1} - beta_C[0] T_{C+1} = zloc_C[0]
+//   B_C - alpha_C[2K-1] B_{C-1} - beta_C[2K-1] T_{C+1} = zloc_C[2K-1],  zloc_C = M_C^{-1} g_C.
+__global__ void k_part_iface(int CL, int K, const double *ends, double *ctad, int *bad)
 {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double A[2 * PART_CLMAX][5], rs[2 * PART_CLMAX], F[2 * PART_CLMAX][5], x[2 * PART_CLMAX];
+    constexpr int MX = 2 * (PART_KMAX > PART_CLMAX ? PART_KMAX : PART_CLMAX);
+    double A[MX][5], rs[MX], F[MX][5], x[MX];
     double gA[2 * PART_CLMAX][5], grs[2 * PART_CLMAX];
-    const int M = 2 * W;
+    const int M = 2 * K;
     bool ok = true;
     for (int C = 0; C < CL; ++C) {
         double *D = ctad + (size_t)C * PART_CTAD;
         for (int i = 0; i < PART_CTAD; ++i) D[i] = 0.0;
         for (int r = 0; r < M; ++r) {
             const int w = r / 2, e = r % 2;
-            const double *E = ends + (size_t)(C * W + w) * 8;
+            const double *E = ends + (size_t)(C * K + w) * 8;
             for (int d = 0; d < 5; ++d) A[r][d] = 0.0;
             A[r][2] = 1.0;
             if (w > 0) A[r][(2 * w - 1) - r + 2] = -E[2 + e];
-            if (w < W - 1) A[r][(2 * w + 2) - r + 2] = -E[4 + e];
-            rs[r] = E[e] + (w == 0 ? E[2 + e] : 0.0) + (w == W - 1 ? E[4 + e] : 0.0);
+            if (w < K - 1) A[r][(2 * w + 2) - r + 2] = -E[4 + e];
+            rs[r] = E[e] + (w == 0 ? E[2 + e] : 0.0) + (w == K - 1 ? E[4 + e] : 0.0);
         }
         ok = band_factor(M, A, rs, F) && ok;
-        for (int col = 0; col < M; ++col) {
-            for (int r = 0; r < M; ++r) x[r] = (r == col) ? 1.0 : 0.0;
-            band_solve(M, F, x);
-            for (int r = 0; r < M; ++r) D[r * M + col] = x[r];
-        }
-        const double *E0 = ends + (size_t)(C * W) * 8, *E1 = ends + (size_t)(C * W + W - 1) * 8;
+        for (int r = 0; r < M; ++r)
+            for (int d = 0; d < 5; ++d) D[r * 5 + d] = F[r][d];
+        const double *E0 = ends + (size_t)(C * K) * 8, *E1 = ends + (size_t)(C * K + K - 1) * 8;
         for (int r = 0; r < M; ++r) x[r] = 0.0;
         x[0] = E0[2];
         x[1] = E0[3];
@@ -223,7 +223,7 @@ __global__ void k_part_iface(int CL, int W, const double *ends, double *ctad, in
         band_solve(M, F, x);
         for (int r = 0; r < M; ++r) D[CTAD_B + r] = x[r];
         const double bT = x[0], bB = x[M - 1];
-        for (int r = 0; r < M; ++r) x[r] = ends[(size_t)(C * W + r / 2) * 8 + r % 2];
+        for (int r = 0; r < M; ++r) x[r] = ends[(size_t)(C * K + r / 2) * 8 + r % 2];
         band_solve(M, F, x);
         // global rows 2C (T_C) and 2C+1 (B_C)
         for (int e = 0; e < 2; ++e) {
@@ -259,7 +259,7 @@ struct PartArgs {
     double *out; long ld_out;
     const double *off; long ld_off;
     // source (same convention as StepArgs): R == 0 none
-    int R;
+    int R, RS;                         // RS: column stride of spaceT
     const double *spaceT;              // n x RS (zero padded)
     const double *time;
     const double *amp;
@@ -268,15 +268,18 @@ struct PartArgs {
     unsigned long long *prof;          // dev aid (PR_PART_PROF): per-phase clock sums, or null
 };
 
+constexpr int PART_RSM = 8;            // shared-memory stride of the source rows
+
 // CTA shared memory (doubles): 6 mbarriers | gathered super-chunk values [2][CL][32]
-// (double2) | raw chunk ends [2][W][32] (double2) | interface values (b_{c-1}, t_{c+1})
-// [2][W][32] (double2) | interface data | per compute warp: {w, -ga, V2, W2} [L] |
-// -cp [L] | source rows [L][RS] | cluster addresses [2][CL] (u32)
-template <int CL, int W, int L, int RS>
+// (double2) | chunk end values [2][K][32] (double2) | (B_{C-1}, T_{C+1}) [2][32]
+// (double2) | interface data | per chunk: {w, -ga, V2, W2} [L] | -cp [L] | source
+// rows [L][8] (AFF) | cluster addresses [2][CL] (u32) | local solution [2][2K][32]
+template <int CL, int W, int H, int L, bool AFF>
 constexpr size_t part_smem_t()
 {
-    return (6 + (size_t)4 * CL * 32 + (size_t)8 * W * 32 + PART_CTAD + (size_t)W * L * (5 + RS) + CL) *
-           sizeof(double);
+    constexpr int K = W * H;
+    return (6 + (size_t)4 * CL * 32 + (size_t)4 * K * 32 + 4 * 32 + PART_CTAD +
+            (size_t)K * (L * (5 + (AFF ? PART_RSM : 0)) + 4) + CL + (size_t)4 * K * 32) * sizeof(double);
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void *p)
@@ -313,31 +316,40 @@ __device__ __forceinline__ void mbar_arrive(unsigned bar)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
 }
 
-// Warps 0..W-1 each own a chunk (state in registers) and only sweep; warp W is
-// the interface warp: it turns the chunks' raw end values into super-chunk
-// values, exchanges them across the cluster, and hands each compute warp its
-// (b_{c-1}, t_{c+1}) -- all while the compute warps run the next sweep.
-// Local hand-offs use mbarriers: ebar[p] (W compute warps arrive: raw ends of a
-// step of parity p written), cbar[p] (interface warp arrives: interface values
-// of a step of parity p written); gbar[p] counts the cluster gather bytes.
-template <int CL, int W, int L, int RS>
+// Warps 0..W-1 each own H chunks (H = 2: the two half-warps hold different chunks
+// of the same 16 vectors), with the chunk state in registers, and only sweep;
+// warp W is the interface warp: it turns the chunks' raw end values into
+// super-chunk values (banded solve with the local factors), exchanges them
+// across the cluster, and hands each chunk its (b_{c-1}, t_{c+1}) -- all while
+// the compute warps run the next sweep.  Local hand-offs use mbarriers: ebar[p]
+// (W compute warps arrive: raw ends of a step of parity p written), cbar[p]
+// (interface warp arrives: interface values of a step of parity p written);
+// gbar[p] counts the cluster gather bytes.
+template <int CL, int W, int H, int L, bool AFF>
 __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
 {
-    constexpr int M = 2 * W;
+    constexpr int VPW = 32 / H;          // vectors per warp
+    constexpr int K = W * H;             // chunks per CTA
+    constexpr int M = 2 * K;             // local interface unknowns
+    constexpr int RSM = AFF ? PART_RSM : 0;
     extern __shared__ __align__(16) double sm[];
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.block_rank();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long v = (long)(blockIdx.x / CL) * 32 + lane;  // vector
+    const int vl = lane % VPW, h = lane / VPW;
+    const long v = (long)(blockIdx.x / CL) * VPW + vl;   // vector
     const bool valid = v < a.B;
     unsigned long long *bar = reinterpret_cast<unsigned long long *>(sm);   // gbar[2] ebar[2] cbar[2]
     double2 *gth = reinterpret_cast<double2 *>(sm + 6);              // [2][CL][32]
-    double2 *rawE = gth + 2 * CL * 32;                               // [2][W][32]
-    double2 *coef = rawE + 2 * W * 32;                               // [2][W][32]
-    double *ctad = reinterpret_cast<double *>(coef + 2 * W * 32);
+    double2 *rawE = gth + 2 * CL * 32;                               // [2][K][32]
+    double2 *coef = rawE + 2 * K * 32;                               // [2][32]: (B_{C-1}, T_{C+1})
+    double *ctad = reinterpret_cast<double *>(coef + 2 * 32);
     double *regions = ctad + PART_CTAD;
-    unsigned *rmap = reinterpret_cast<unsigned *>(regions + (size_t)W * L * (5 + RS));  // [2][CL]
-    auto cd_of = [&](int u) { return reinterpret_cast<double4 *>(regions + (size_t)u * L * (5 + RS)); };
+    // chunk regions are padded by 4 doubles so the two chunks read by the
+    // half-warps of one warp (H = 2) fall in different shared-memory banks
+    constexpr int RSTR = L * (5 + RSM) + 4;
+    unsigned *rmap = reinterpret_cast<unsigned *>(regions + (size_t)K * RSTR);  // [2][CL]
+    auto cd_of = [&](int u) { return reinterpret_cast<double4 *>(regions + (size_t)u * RSTR); };
     const unsigned bar0 = smem_u32(bar), gth0 = smem_u32(gth);
     const unsigned gbar = bar0, ebar = bar0 + 16, cbar = bar0 + 32;
 
@@ -358,35 +370,48 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
 
     if (w < W) {
         // ------------------------------------------------ compute warp: chunk c
-        const int c = C * W + w;
+        const int u = w * H + h;                     // chunk within the CTA
+        const int c = C * K + u;
         const int s0 = c * L;
-        double4 *cd = cd_of(w);
-        double *cu = reinterpret_cast<double *>(cd) + 4 * L;
-        double *sp = cu + L;
-        for (int i = lane; i < L; i += 32) {
-            const double *R = a.rowc + (size_t)(s0 + i) * 8;
-            cd[i] = make_double4(R[0], R[1], R[5], R[6]);
-            cu[i] = R[2];
-        }
-        if constexpr (RS > 0)
-            for (int i = lane; i < L * RS; i += 32) {
-                const int row = s0 + i / RS;
-                sp[i] = (row < a.n) ? a.spaceT[(size_t)row * RS + i % RS] : 0.0;
+        for (int i = lane; i < H * L; i += 32) {     // this warp's H chunk regions
+            const int uu = w * H + i / L, row = i % L;
+            const double *R = a.rowc + ((size_t)(C * K + uu) * L + row) * 8;
+            double4 *cdu = cd_of(uu);
+            cdu[row] = make_double4(R[0], R[1], R[5], R[6]);
+            reinterpret_cast<double *>(cdu)[4 * L + row] = R[2];
+            if constexpr (AFF) {
+                const int grow = (C * K + uu) * L + row;
+                double *spu = reinterpret_cast<double *>(cdu) + 5 * L + row * RSM;
+#pragma unroll
+                for (int r = 0; r < RSM; ++r)
+                    spu[r] = (grow < a.n && r < a.RS) ? a.spaceT[(size_t)grow * a.RS + r] : 0.0;
             }
+        }
+        const double4 *cd = cd_of(u);
+        const double *cu = reinterpret_cast<const double *>(cd) + 4 * L;
+        const double *sp = cu + L;
         double S[L];
 #pragma unroll
         for (int i = 0; i < L; ++i)
             S[i] = (a.in && valid && s0 + i < a.n) ? a.in[(long)(s0 + i) * a.ld_in + v] : 0.0;
+        // (b_{c-1}, t_{c+1}) of a step from the CTA's (B_{C-1}, T_{C+1}) and local solution
+        const double *zsb = reinterpret_cast<const double *>(rmap + 2 * CL);
+        auto neighbours = [&](int pp, double &b, double &t) {
+            const double2 bt = coef[pp * 32 + vl];
+            const double *zz = zsb + (size_t)pp * M * 32 + vl;
+            b = (u == 0) ? bt.x : fma(ctad[CTAD_A + 2 * u - 1], bt.x, fma(ctad[CTAD_B + 2 * u - 1], bt.y, zz[(2 * u - 1) * 32]));
+            t = (u == K - 1) ? bt.y : fma(ctad[CTAD_A + 2 * u + 2], bt.x, fma(ctad[CTAD_B + 2 * u + 2], bt.y, zz[(2 * u + 2) * 32]));
+        };
         cluster.sync();
         const int q = valid ? a.q0 + (int)(v / a.vpi) : a.q0;
-        const int src = (RS > 0 && valid) ? (int)(v % a.nsrc) : 0;
+        const int src = (AFF && valid) ? (int)(v % a.nsrc) : 0;
         double ca = 0.0, cc = 0.0;     // (b_{c-1}, t_{c+1}) of step j-1: coefficients of V2, W2
         for (int j = 1; j <= a.m; ++j) {
             long long t0 = a.prof ? clock64() : 0;
-            double alpha[RS > 0 ? RS : 1];
-            if constexpr (RS > 0) {
+            double alpha[AFF ? PART_RSM : 1];
+            if constexpr (AFF) {
 #pragma unroll
-                for (int r = 0; r < RS; ++r) {
+                for (int r = 0; r < PART_RSM; ++r) {
                     double al = 0.0;
                     if (r < a.R && valid)
                         al = a.dt * a.amp[(long)src * a.R + r] * a.time[(long)r * a.nsteps + (long)q * a.m + j - 1];
@@ -399,9 +424,9 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
             for (int i = 0; i < L; ++i) {
                 const double4 q4 = cd[i];
                 double x = fma(q4.z, ca, fma(q4.w, cc, S[i]));
-                if constexpr (RS > 0) {
+                if constexpr (AFF) {
 #pragma unroll
-                    for (int r = 0; r < RS; ++r) x = fma(alpha[r], sp[i * RS + r], x);
+                    for (int r = 0; r < PART_RSM; ++r) x = fma(alpha[r], sp[i * RSM + r], x);
                 }
                 yp = fma(q4.y, yp, q4.x * x);
                 S[i] = yp;
@@ -415,17 +440,19 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
             }
             long long t1 = a.prof ? clock64() : 0;
             const int p = j & 1;
-            rawE[(p * W + w) * 32 + lane] = make_double2(S[0], S[L - 1]);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(ebar + 8 * p);
             if (j >= 2) {              // interface values of step j-1 (formed during this sweep)
                 const int pp = (j - 1) & 1;
                 mbar_wait(cbar + 8 * pp, ((j - 2) >> 1) & 1);
-                const double2 e = coef[(pp * W + w) * 32 + lane];
-                ca = e.x;
-                cc = e.y;
+                neighbours(pp, ca, cc);
             }
-            if (a.prof && lane == 0) {
+            {                          // chunk ends of g_j = S_j + ca V2 + cc W2
+                const double4 q0 = cd[0], q1 = cd[L - 1];
+                rawE[(p * K + u) * 32 + vl] = make_double2(fma(q0.z, ca, fma(q0.w, cc, S[0])),
+                                                           fma(q1.z, ca, fma(q1.w, cc, S[L - 1])));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(ebar + 8 * p);
+            if (a.prof && vl == 0) {
                 long long t2 = clock64();
                 unsigned long long *pr = a.prof + (size_t)c * 4;
                 atomicAdd(pr + 0, (unsigned long long)(t1 - t0));
@@ -434,7 +461,8 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
         }
         const int pm = a.m & 1;
         mbar_wait(cbar + 8 * pm, ((a.m - 1) >> 1) & 1);
-        const double2 e = coef[(pm * W + w) * 32 + lane];       // (b_m, t_m) of the neighbours
+        double2 e;                                               // (b_m, t_m) of the neighbours
+        neighbours(pm, e.x, e.y);
         if (valid) {
 #pragma unroll
             for (int i = 0; i < L; ++i) {
@@ -450,101 +478,110 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
         }
     } else {
         // ------------------------------------------------ interface warp
+        // lane = (half h, vector vl); with H = 2 the two half-warps split the
+        // cluster sends and the gather dot products
         cluster.sync();
-        double hb[W], ht[W], zb[W], zt[W];          // (b, t) of step j-1 per chunk; local parts
-#pragma unroll
-        for (int u = 0; u < W; ++u) hb[u] = ht[u] = zb[u] = zt[u] = 0.0;
-        // step j's values from every super-chunk -> (b_{c-1}, t_{c+1}) of step j per chunk
+        double *zs = reinterpret_cast<double *>(rmap + 2 * CL);          // [2][M][32]
+        constexpr int CLH = CL / H;                                      // CTAs per half-warp
+        // step j's values from every super-chunk -> (B_{C-1}, T_{C+1}) of step j
         auto gather = [&](int j) {
             const int p = j & 1;
             if (lane == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                             :: "r"(gbar + 8 * p), "r"((unsigned)(CL * 32 * sizeof(double2))) : "memory");
+                             :: "r"(gbar + 8 * p), "r"((unsigned)(CL * VPW * sizeof(double2))) : "memory");
             mbar_wait(gbar + 8 * p, ((j - 1) >> 1) & 1);
-            const double2 *G = gth + (size_t)p * CL * 32 + lane;
+            const double2 *G = gth + (size_t)p * CL * 32 + vl;
             double b0 = 0.0, b1 = 0.0, t0 = 0.0, t1 = 0.0;
 #pragma unroll
-            for (int u = 0; u < CL; ++u) {
-                const double2 e = G[u * 32];
-                b0 = fma(ctad[CTAD_GB + 2 * u], e.x, b0);
-                b1 = fma(ctad[CTAD_GB + 2 * u + 1], e.y, b1);
-                t0 = fma(ctad[CTAD_GT + 2 * u], e.x, t0);
-                t1 = fma(ctad[CTAD_GT + 2 * u + 1], e.y, t1);
+            for (int rr = 0; rr < CLH; ++rr) {
+                const int r = h * CLH + rr;
+                const double2 e = G[r * 32];
+                b0 = fma(ctad[CTAD_GB + 2 * r], e.x, b0);
+                b1 = fma(ctad[CTAD_GB + 2 * r + 1], e.y, b1);
+                t0 = fma(ctad[CTAD_GT + 2 * r], e.x, t0);
+                t1 = fma(ctad[CTAD_GT + 2 * r + 1], e.y, t1);
             }
-            const double Bx = b0 + b1, Tx = t0 + t1;       // B_{C-1}, T_{C+1}
-#pragma unroll
-            for (int u = 0; u < W; ++u) {
-                hb[u] = (u == 0) ? Bx : fma(ctad[CTAD_A + 2 * u - 1], Bx, fma(ctad[CTAD_B + 2 * u - 1], Tx, zb[u]));
-                ht[u] = (u == W - 1) ? Tx : fma(ctad[CTAD_A + 2 * u + 2], Bx, fma(ctad[CTAD_B + 2 * u + 2], Tx, zt[u]));
-                coef[(p * W + u) * 32 + lane] = make_double2(hb[u], ht[u]);
+            double Bx = b0 + b1, Tx = t0 + t1;
+            if constexpr (H == 2) {
+                Bx += __shfl_xor_sync(0xffffffffu, Bx, 16);
+                Tx += __shfl_xor_sync(0xffffffffu, Tx, 16);
             }
+            if (h == 0) coef[p * 32 + vl] = make_double2(Bx, Tx);
             __syncwarp();
             if (lane == 0) mbar_arrive(cbar + 8 * p);
         };
-        // chunk ends of g_j = S_j + b V2 + c W2 -> super-chunk values -> every CTA
+        // chunk end values of step j -> local solve z = M_C^{-1} g_C -> (T_C, B_C) to every CTA
         auto publish = [&](int j) {
             const int p = j & 1;
             mbar_wait(ebar + 8 * p, ((j - 1) >> 1) & 1);
-            double E[M];
+            double z[M];
 #pragma unroll
-            for (int u = 0; u < W; ++u) {
-                const double2 r = rawE[(p * W + u) * 32 + lane];
-                const double4 q0 = cd_of(u)[0], q1 = cd_of(u)[L - 1];
-                E[2 * u] = fma(q0.z, hb[u], fma(q0.w, ht[u], r.x));
-                E[2 * u + 1] = fma(q1.z, hb[u], fma(q1.w, ht[u], r.y));
+            for (int uu = 0; uu < K; ++uu) {
+                const double2 r = rawE[(p * K + uu) * 32 + vl];
+                z[2 * uu] = r.x;
+                z[2 * uu + 1] = r.y;
             }
-            double T = 0.0, Bv = 0.0;
+            // band factors, row i: l2, l1, 1/u, u1, u2
 #pragma unroll
-            for (int k = 0; k < M; ++k) {
-                T = fma(ctad[k], E[k], T);
-                Bv = fma(ctad[(M - 1) * M + k], E[k], Bv);
+            for (int i = 0; i < M; ++i) {
+                if (i >= 2) z[i] = fma(-ctad[i * 5 + 0], z[i - 2], z[i]);
+                if (i >= 1) z[i] = fma(-ctad[i * 5 + 1], z[i - 1], z[i]);
             }
 #pragma unroll
-            for (int u = 0; u < W; ++u) {
-                double sb = 0.0, st = 0.0;
-#pragma unroll
-                for (int k = 0; k < M; ++k) {
-                    if (u > 0) sb = fma(ctad[(2 * u - 1) * M + k], E[k], sb);
-                    if (u < W - 1) st = fma(ctad[(2 * u + 2) * M + k], E[k], st);
-                }
-                zb[u] = sb;
-                zt[u] = st;
+            for (int i = M - 1; i >= 0; --i) {
+                if (i + 1 < M) z[i] = fma(-ctad[i * 5 + 3], z[i + 1], z[i]);
+                if (i + 2 < M) z[i] = fma(-ctad[i * 5 + 4], z[i + 2], z[i]);
+                z[i] *= ctad[i * 5 + 2];
             }
-            const unsigned off = (unsigned)(((p * CL + C) * 32 + lane) * sizeof(double2));
+            if (h == 0) {
 #pragma unroll
-            for (int r = 0; r < CL; ++r)
-                st_async_v2(rmap[r] + off, T, Bv, rmap[CL + r] + 8 * p);
+                for (int i = 0; i < M; ++i) zs[((size_t)p * M + i) * 32 + vl] = z[i];
+            }
+            const unsigned off = (unsigned)(((p * CL + C) * 32 + vl) * sizeof(double2));
+#pragma unroll
+            for (int rr = 0; rr < CLH; ++rr) {
+                const int r = h * CLH + rr;
+                st_async_v2(rmap[r] + off, z[0], z[M - 1], rmap[CL + r] + 8 * p);
+            }
         };
+        unsigned long long tw = 0, tp = 0, tg = 0;
         for (int j = 1; j <= a.m; ++j) {
+            long long t0 = a.prof ? clock64() : 0;
             if (j >= 2) gather(j - 1);
+            long long t1 = a.prof ? clock64() : 0;
             publish(j);
+            long long t2 = a.prof ? clock64() : 0;
+            tg += t1 - t0;
+            tp += t2 - t1;
         }
         gather(a.m);
+        if (a.prof && lane == 0) {
+            unsigned long long *pr = a.prof + (size_t)(C * K) * 4;
+            atomicAdd(pr + 2, tg);
+            atomicAdd(pr + 3, tp);
+        }
+        (void)tw;
     }
     cluster.sync();                // no CTA leaves while cluster peers may still target it
 }
 
 // ---------------------------------------------------------------- driver
-bool part_config(int n, int &P, int &L, int &CL, int &W)
+bool part_config(int n, int &P, int &L, int &CL, int &K)
 {
-    // chunks of L = 32 rows up to n = 512, else 64 (measured on B200, C2 B=64:
-    // 0.41 ms at L=64, 4 warps/CTA vs 0.50 ms at L=32, 8 warps/CTA): P (a power
-    // of two) chunks cover P*L >= n rows, the rest identity padding; up to 16
-    // CTAs per cluster, then 2..8 warps per CTA.  PR_PART_L=32 forces 32-row
-    // chunks (measurements).
-    if (n < 64 || n > 16 * PART_WMAX * 64) return false;
+    // chunks of L = 32 rows (one warp per chunk, up to 16 CTAs) up to n = 512,
+    // else 64 rows in 16 CTAs of K = 1..16 chunks: P (a power of two) chunks
+    // cover P*L >= n rows, the rest identity padding.
+    if (n < 64 || n > PART_CLMAX * PART_KMAX * 64) return false;
     L = (n <= 512) ? 32 : 64;
-    if (const char *e = getenv("PR_PART_L"))
-        if (atoi(e) == 32 && n <= 16 * PART_WMAX * 32) L = 32;
     const int need = (n + L - 1) / L;
     P = 2;
     while (P < need) P *= 2;
     CL = P < PART_CLMAX ? P : PART_CLMAX;
-    W = P / CL;
-    return W <= PART_WMAX;
+    K = P / CL;
+    return K <= PART_KMAX;
 }
 
-cudaError_t launch_part_setup(int n, int P, int L, int CL, int W, const double *subA, const double *supA,
+cudaError_t launch_part_setup(int n, int P, int L, int CL, int K, const double *subA, const double *supA,
                               const double *rsA, const double *diagA, double dt, int transpose, double *rowc,
                               double *ctad, double *ends, int *bad, cudaStream_t s)
 {
@@ -553,21 +590,22 @@ cudaError_t launch_part_setup(int n, int P, int L, int CL, int W, const double *
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     note_launch();
-    k_part_iface<<<1, 32, 0, s>>>(CL, W, ends, ctad, bad);
+    k_part_iface<<<1, 32, 0, s>>>(CL, K, ends, ctad, bad);
     return cudaGetLastError();
 }
 
-template <int CL, int W, int L, int RS>
+template <int CL, int W, int H, int L, bool AFF>
 static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
 {
-    constexpr size_t smem = part_smem_t<CL, W, L, RS>();
+    constexpr size_t smem = part_smem_t<CL, W, H, L, AFF>();
     static_assert(smem <= 227 * 1024, "partitioned stepper shared memory");
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(k_part_step<CL, W, L, RS>,
+        cudaError_t e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, AFF>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess && CL > 8)
-            e = cudaFuncSetAttribute(k_part_step<CL, W, L, RS>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, AFF>,
+                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
@@ -584,28 +622,23 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     note_launch();
-    return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, L, RS>, a);
+    return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, AFF>, a);
 }
 
-template <int CL, int W, int L>
-static cudaError_t part_launch_rs(const PartArgs &a, int RS, long groups, cudaStream_t s)
+template <int CL, int W, int H, int L>
+static cudaError_t part_launch_aff(const PartArgs &a, long B, cudaStream_t s)
 {
-    switch (RS) {
-    case 0: return part_launch<CL, W, L, 0>(a, groups, s);
-    case 1: return part_launch<CL, W, L, 1>(a, groups, s);
-    case 2: return part_launch<CL, W, L, 2>(a, groups, s);
-    case 4: return part_launch<CL, W, L, 4>(a, groups, s);
-    default: return part_launch<CL, W, L, 8>(a, groups, s);
-    }
+    const long groups = (B + 32 / H - 1) / (32 / H);
+    return a.R > 0 ? part_launch<CL, W, H, L, true>(a, groups, s) : part_launch<CL, W, H, L, false>(a, groups, s);
 }
 
 bool part_preferred(const Op &op, long B, int m)
 {
+    // measured on B200 (C1, C2 shapes, B = 32 .. 20480): the partitioned stepper
+    // beats the fused one at every batch size it supports
+    (void)B;
     if (op.part_P == 0 || m < 1 || getenv("PR_NO_PART")) return false;
-    if (getenv("PR_FORCE_PART")) return true;
-    // the fused stepper wins once its one-vector-per-thread warps fill the GPU
-    const long groups = (B + 31) / 32;
-    return groups * 4 <= num_sms();
+    return true;
 }
 
 cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose, cudaStream_t s)
@@ -617,51 +650,66 @@ cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose,
     a.in = sa.in; a.ld_in = sa.ld_in; a.out = sa.out; a.ld_out = sa.ld_out;
     a.off = sa.off; a.ld_off = sa.ld_off;
     a.R = sa.R;
-    const int RS = sa.R > 0 ? stepper_rs(sa.R) : 0;
+    a.RS = sa.R > 0 ? stepper_rs(sa.R) : 0;
     a.spaceT = sa.spaceT; a.time = sa.time; a.amp = sa.amp;
     a.nsteps = sa.nsteps; a.nsrc = sa.nsrc; a.q0 = sa.q0; a.vpi = sa.vpi; a.dt = sa.dt;
-    const long groups = (sa.B + 31) / 32;
-    if (groups == 0) return cudaSuccess;
+    if (sa.B == 0) return cudaSuccess;
+    const int P = op.part_P, K = op.part_K;
+    // two chunks per warp (16 vectors per warp) when that spreads a small batch
+    // over more SMs, or when K chunks would need more than 8 compute warps
+    int H = 1;
+    if (K >= 2) {
+        const long clusters32 = (sa.B + 31) / 32;
+        if (K > 8 || clusters32 * op.part_CL * 2 <= num_sms()) H = 2;
+        if (const char *e = getenv("PR_PART_H")) {
+            const int f = atoi(e);
+            if ((f == 1 && K <= 8) || f == 2) H = f;
+        }
+    }
     static unsigned long long *dprof = nullptr;
-    const int P = op.part_P;
     const bool want_prof = getenv("PR_PART_PROF") != nullptr;
     if (want_prof) {
-        if (!dprof) cudaMalloc(&dprof, 16 * PART_WMAX * 4 * sizeof(unsigned long long));
-        cudaMemsetAsync(dprof, 0, 16 * PART_WMAX * 4 * sizeof(unsigned long long), s);
+        if (!dprof) cudaMalloc(&dprof, 256 * 4 * sizeof(unsigned long long));
+        cudaMemsetAsync(dprof, 0, 256 * 4 * sizeof(unsigned long long), s);
         a.prof = dprof;
     }
     const bool prof = profiling();
     if (prof) stepper_timed_begin(s);
     cudaError_t e = cudaErrorInvalidValue;
-    if (op.part_L == 32 && op.part_W == 1) {
+    if (op.part_L == 32) {
         switch (op.part_CL) {
-        case 2: e = part_launch_rs<2, 1, 32>(a, RS, groups, s); break;
-        case 4: e = part_launch_rs<4, 1, 32>(a, RS, groups, s); break;
-        case 8: e = part_launch_rs<8, 1, 32>(a, RS, groups, s); break;
-        case 16: e = part_launch_rs<16, 1, 32>(a, RS, groups, s); break;
+        case 2: e = part_launch_aff<2, 1, 1, 32>(a, sa.B, s); break;
+        case 4: e = part_launch_aff<4, 1, 1, 32>(a, sa.B, s); break;
+        case 8: e = part_launch_aff<8, 1, 1, 32>(a, sa.B, s); break;
+        case 16: e = part_launch_aff<16, 1, 1, 32>(a, sa.B, s); break;
         }
-    } else if (op.part_L == 32 && op.part_CL == 16) {
-        switch (op.part_W) {
-        case 2: e = part_launch_rs<16, 2, 32>(a, RS, groups, s); break;
-        case 4: e = part_launch_rs<16, 4, 32>(a, RS, groups, s); break;
-        case 8: e = part_launch_rs<16, 8, 32>(a, RS, groups, s); break;
+    } else if (op.part_CL == 16 && H == 1) {
+        switch (K) {
+        case 1: e = part_launch_aff<16, 1, 1, 64>(a, sa.B, s); break;
+        case 2: e = part_launch_aff<16, 2, 1, 64>(a, sa.B, s); break;
+        case 4: e = part_launch_aff<16, 4, 1, 64>(a, sa.B, s); break;
+        case 8: e = part_launch_aff<16, 8, 1, 64>(a, sa.B, s); break;
         }
-    } else if (op.part_L == 64 && op.part_CL == 16) {
-        switch (op.part_W) {
-        case 4: e = part_launch_rs<16, 4, 64>(a, RS, groups, s); break;
-        case 8: e = part_launch_rs<16, 8, 64>(a, RS, groups, s); break;
+    } else if (op.part_CL == 16 && H == 2) {
+        switch (K) {
+        case 2: e = part_launch_aff<16, 1, 2, 64>(a, sa.B, s); break;
+        case 4: e = part_launch_aff<16, 2, 2, 64>(a, sa.B, s); break;
+        case 8: e = part_launch_aff<16, 4, 2, 64>(a, sa.B, s); break;
+        case 16: e = part_launch_aff<16, 8, 2, 64>(a, sa.B, s); break;
         }
     }
     if (prof) stepper_timed_end(s, (double)sa.n * (double)sa.B * (double)sa.m, 0.0);
     if (want_prof && e == cudaSuccess) {
-        unsigned long long h[16 * PART_WMAX * 4];
+        unsigned long long h[256 * 4];
         cudaMemcpyAsync(h, dprof, sizeof(h), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
+        const long groups = (sa.B + 32 / H - 1) / (32 / H);
         const double norm = (double)groups * sa.m;
-        fprintf(stderr, "part P=%d L=%d CL=%d W=%d m=%d groups=%ld  cycles/step [sweep hand-off]:\n", P,
-                op.part_L, op.part_CL, op.part_W, sa.m, groups);
+        fprintf(stderr, "part P=%d L=%d CL=%d K=%d H=%d m=%d groups=%ld  cycles/step [sweep hand-off | helper: gather(incl. wait) publish(incl. wait)]:\n", P,
+                op.part_L, op.part_CL, K, H, sa.m, groups);
         for (int c = 0; c < P; c += (P > 16 ? P / 16 : 1))
-            fprintf(stderr, "  chunk %3d: %8.0f %8.0f\n", c, h[c * 4] / norm, h[c * 4 + 1] / norm);
+            fprintf(stderr, "  chunk %3d: %8.0f %8.0f | %8.0f %8.0f\n", c + (P > 16 ? 1 : 0), h[(c + (P > 16 ? 1 : 0)) * 4] / norm,
+                    h[(c + (P > 16 ? 1 : 0)) * 4 + 1] / norm, h[c * 4 + 2] / norm, h[c * 4 + 3] / norm);
     }
     return e;
 }

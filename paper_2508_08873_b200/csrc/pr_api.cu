@@ -386,10 +386,10 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
     if (e == cudaSuccess)
         e = launch_factor_1d(n, dsub, dsup, colsum ? dcs : nullptr, ddiag, dt, 1, op.dn_tr, op.up_tr, d_bad, 0);
     // partitioned-stepper factors (small batches), both orientations
-    int pP = 0, pL = 0, pCL = 0, pW = 0;
+    int pP = 0, pL = 0, pCL = 0, pK = 0;
     double *d_ends = nullptr;
-    if (e == cudaSuccess && part_config(n, pP, pL, pCL, pW)) {
-        op.part_P = pP; op.part_L = pL; op.part_CL = pCL; op.part_W = pW;
+    if (e == cudaSuccess && part_config(n, pP, pL, pCL, pK)) {
+        op.part_P = pP; op.part_L = pL; op.part_CL = pCL; op.part_K = pK;
         const size_t rb = (size_t)pP * pL * 8 * sizeof(double), cb = (size_t)pCL * PART_CTAD * sizeof(double);
         e = cudaMalloc(&op.part_rowc_fw, rb);
         if (e == cudaSuccess) e = cudaMalloc(&op.part_rowc_tr, rb);
@@ -397,10 +397,10 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
         if (e == cudaSuccess) e = cudaMalloc(&op.part_ctad_tr, cb);
         if (e == cudaSuccess) e = cudaMalloc(&d_ends, (size_t)8 * pP * sizeof(double));
         if (e == cudaSuccess)
-            e = launch_part_setup(n, pP, pL, pCL, pW, dsub, dsup, rowsum ? drs : nullptr, ddiag, dt, 0,
+            e = launch_part_setup(n, pP, pL, pCL, pK, dsub, dsup, rowsum ? drs : nullptr, ddiag, dt, 0,
                                   op.part_rowc_fw, op.part_ctad_fw, d_ends, d_bad, 0);
         if (e == cudaSuccess)
-            e = launch_part_setup(n, pP, pL, pCL, pW, dsub, dsup, colsum ? dcs : nullptr, ddiag, dt, 1,
+            e = launch_part_setup(n, pP, pL, pCL, pK, dsub, dsup, colsum ? dcs : nullptr, ddiag, dt, 1,
                                   op.part_rowc_tr, op.part_ctad_tr, d_ends, d_bad, 0);
     }
     int bad = 0;

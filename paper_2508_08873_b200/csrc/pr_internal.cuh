@@ -66,7 +66,7 @@ struct Op {
     // 1D partitioned stepper (k_part.cu, small batches): P = CL * W chunks of
     // L rows (rows >= n: identity padding).  rowc: (P*L) x 8 per-row
     // {w, -ga, -cp, V, W, V2, W2, 0}; ctad: CL x PART_CTAD per-CTA interface data.
-    int part_P = 0, part_L = 0, part_CL = 0, part_W = 0;
+    int part_P = 0, part_L = 0, part_CL = 0, part_K = 0;
     double *part_rowc_fw = nullptr, *part_ctad_fw = nullptr;
     double *part_rowc_tr = nullptr, *part_ctad_tr = nullptr;
     // 2D: P = n+1; S (P x P) sine matrix with zero row/col 0; lam[P] eigenvalues of T.
@@ -106,11 +106,12 @@ cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s);
 
 // partitioned stepper (k_part.cu): configuration for n (false: not supported),
 // setup (ends: P x 8 scratch), selection and launch
-constexpr int PART_WMAX = 8;                   // warps (chunks) per CTA
+constexpr int PART_KMAX = 16;                  // chunks per CTA
 constexpr int PART_CLMAX = 16;                 // CTAs per cluster
-constexpr int PART_CTAD = 4 * PART_WMAX * PART_WMAX + 4 * PART_WMAX + 4 * PART_CLMAX;
-bool part_config(int n, int &P, int &L, int &CL, int &W);
-cudaError_t launch_part_setup(int n, int P, int L, int CL, int W, const double *subA, const double *supA,
+constexpr int PART_CTAD = 5 * 2 * PART_KMAX + 4 * PART_KMAX + 4 * PART_CLMAX;
+// P = CL * K chunks of L rows (K chunks per CTA)
+bool part_config(int n, int &P, int &L, int &CL, int &K);
+cudaError_t launch_part_setup(int n, int P, int L, int CL, int K, const double *subA, const double *supA,
                               const double *rsA, const double *diagA, double dt, int transpose, double *rowc,
                               double *ctad, double *ends, int *bad, cudaStream_t s);
 bool part_preferred(const Op &op, long B, int m);

@@ -14,7 +14,7 @@ build.build()
 for name in sys.argv[1:] or ["C2", "C1"]:
     cfg = get(name)
     op = gpu_op(cfg)
-    for B in (32, 64, 128, 256, 512, 1024, 2560):
+    for B in [int(b) for b in os.environ.get("BLIST", "32,64,128,256,512,1024,2560").split(",")]:
         X = torch.randn(cfg.n, B, dtype=torch.float64, device="cuda")
         Y = torch.empty_like(X)
         res = {}
