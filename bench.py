@@ -174,6 +174,22 @@ class Workload:
         return self.U
 
 
+def _fp64_alu_peak(dev):
+    """FP64 vector (DFMA) ceiling from unit counts and the clock: SMs x 4 sub-
+    partitions x 16 DFMA lanes/clk (measured: 2.1 cycles per DFMA warp-
+    instruction per sub-partition) x 2 flops x max SM clock (MEASURED_PEAKS.json)."""
+    import torch
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f)["sm_max_mhz"])
+        src = "derived: SMs x 64 DFMA/clk x 2 flops x sm_max_mhz (MEASURED_PEAKS.json)"
+    except Exception:
+        mhz = 1965.0
+        src = "derived: SMs x 64 DFMA/clk x 2 flops x 1965 MHz (fallback clock)"
+    return sms * 64 * 2 * mhz * 1e6 / 1e12, src
+
+
 def _fp64_peak(dev):
     """Measured FP64 ceiling on this GPU: cuBLAS DGEMM 8192^3 (best of 5, CUDA
     events).  MEASURED_PEAKS.json carries no FP64 figure."""
@@ -343,7 +359,20 @@ def main():
     st_ms = ctr["stepper_ms"] / max(ctr["stepper_launches"], 1)
     st_dof = ctr["stepper_dof_steps"] / max(ctr["stepper_launches"], 1)
     st_fl = ctr["stepper_flops"] / max(ctr["stepper_launches"], 1)
-    if cfg.dim == 1:
+    if cfg.dim == 1 and st_fl > 0:
+        # K1P (partitioned stepper): the state stays on chip for all m steps, so
+        # HBM carries only the input and output (16 B per DOF per launch); the
+        # bound is the FP64 pipe, 5 algorithmic flops per DOF-step
+        peak, src = _fp64_alu_peak(dev)
+        achieved = st_fl / (st_ms / 1e3) / 1e12 if st_ms > 0 else None
+        roofline = {"kernel": "k_part_step (K1P, cluster-partitioned implicit Euler, state in registers)",
+                    "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": (achieved / peak) if achieved else None,
+                    "traffic": _ncu_traffic(cfg.name),
+                    "algorithmic_flops_per_launch": st_fl,
+                    "algorithmic_bytes_per_launch": 16.0 * st_dof / cfg.m,
+                    "peak_source": src}
+    elif cfg.dim == 1:
         peak, peak_kind = _peaks()
         achieved = 16.0 * st_dof / (st_ms / 1e3) / 1e9 if st_ms > 0 else None
         roofline = {"kernel": "k_stepper (K1, batched tridiagonal implicit Euler)", "bound": "hbm",

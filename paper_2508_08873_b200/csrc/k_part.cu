@@ -698,7 +698,9 @@ cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose,
         case 16: e = part_launch_aff<16, 8, 2, 64>(a, sa.B, s); break;
         }
     }
-    if (prof) stepper_timed_end(s, (double)sa.n * (double)sa.B * (double)sa.m, 0.0);
+    // algorithmic FP64 flops per DOF-step: Thomas with precomputed factors,
+    // y = w r - ga y' (3) and x = y - cp x' (2)  (bench.py roofline)
+    if (prof) stepper_timed_end(s, (double)sa.n * (double)sa.B * (double)sa.m, 5.0 * (double)sa.n * (double)sa.B * (double)sa.m);
     if (want_prof && e == cudaSuccess) {
         unsigned long long h[256 * 4];
         cudaMemcpyAsync(h, dprof, sizeof(h), cudaMemcpyDeviceToHost, s);
