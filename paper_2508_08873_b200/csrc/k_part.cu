@@ -272,14 +272,14 @@ constexpr int PART_RSM = 8;            // shared-memory stride of the source row
 
 // CTA shared memory (doubles): 6 mbarriers | gathered super-chunk values [2][CL][32]
 // (double2) | chunk end values [2][K][32] (double2) | (B_{C-1}, T_{C+1}) [2][32]
-// (double2) | interface data | per chunk: {w, -ga, V2, W2} [L] | -cp [L] | source
-// rows [L][8] (AFF) | cluster addresses [2][CL] (u32) | local solution [2][2K][32]
+// (double2) | interface data | per chunk: {w, -ga, V2, W2} [L] | -cp [L] | {V, W} [L] |
+// source rows [L][8] (AFF) | cluster addresses [2][CL] (u32) | local solution [2][2K][32]
 template <int CL, int W, int H, int L, bool AFF>
 constexpr size_t part_smem_t()
 {
     constexpr int K = W * H;
     return (6 + (size_t)4 * CL * 32 + (size_t)4 * K * 32 + 4 * 32 + PART_CTAD +
-            (size_t)K * (L * (5 + (AFF ? PART_RSM : 0)) + 4) + CL + (size_t)4 * K * 32) * sizeof(double);
+            (size_t)K * (L * (7 + (AFF ? PART_RSM : 0)) + 4) + CL + (size_t)4 * K * 32) * sizeof(double);
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void *p)
@@ -333,6 +333,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
     constexpr int M = 2 * K;             // local interface unknowns
     constexpr int RSM = AFF ? PART_RSM : 0;
     extern __shared__ __align__(16) double sm[];
+    const long long tk0 = a.prof ? clock64() : 0;
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.block_rank();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -347,7 +348,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
     double *regions = ctad + PART_CTAD;
     // chunk regions are padded by 4 doubles so the two chunks read by the
     // half-warps of one warp (H = 2) fall in different shared-memory banks
-    constexpr int RSTR = L * (5 + RSM) + 4;
+    constexpr int RSTR = L * (7 + RSM) + 4;
     unsigned *rmap = reinterpret_cast<unsigned *>(regions + (size_t)K * RSTR);  // [2][CL]
     auto cd_of = [&](int u) { return reinterpret_cast<double4 *>(regions + (size_t)u * RSTR); };
     const unsigned bar0 = smem_u32(bar), gth0 = smem_u32(gth);
@@ -373,15 +374,18 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
         const int u = w * H + h;                     // chunk within the CTA
         const int c = C * K + u;
         const int s0 = c * L;
+#pragma unroll 4
         for (int i = lane; i < H * L; i += 32) {     // this warp's H chunk regions
             const int uu = w * H + i / L, row = i % L;
-            const double *R = a.rowc + ((size_t)(C * K + uu) * L + row) * 8;
+            const double2 *R = reinterpret_cast<const double2 *>(a.rowc + ((size_t)(C * K + uu) * L + row) * 8);
+            const double2 r01 = R[0], r23 = R[1], r45 = R[2], r67 = R[3];
             double4 *cdu = cd_of(uu);
-            cdu[row] = make_double4(R[0], R[1], R[5], R[6]);
-            reinterpret_cast<double *>(cdu)[4 * L + row] = R[2];
+            cdu[row] = make_double4(r01.x, r01.y, r45.y, r67.x);
+            reinterpret_cast<double *>(cdu)[4 * L + row] = r23.x;
+            reinterpret_cast<double2 *>(reinterpret_cast<double *>(cdu) + 5 * L)[row] = make_double2(r23.y, r45.x);
             if constexpr (AFF) {
                 const int grow = (C * K + uu) * L + row;
-                double *spu = reinterpret_cast<double *>(cdu) + 5 * L + row * RSM;
+                double *spu = reinterpret_cast<double *>(cdu) + 7 * L + row * RSM;
 #pragma unroll
                 for (int r = 0; r < RSM; ++r)
                     spu[r] = (grow < a.n && r < a.RS) ? a.spaceT[(size_t)grow * a.RS + r] : 0.0;
@@ -389,7 +393,8 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
         }
         const double4 *cd = cd_of(u);
         const double *cu = reinterpret_cast<const double *>(cd) + 4 * L;
-        const double *sp = cu + L;
+        const double2 *vw = reinterpret_cast<const double2 *>(cu + L);
+        const double *sp = cu + 3 * L;
         double S[L];
 #pragma unroll
         for (int i = 0; i < L; ++i)
@@ -403,6 +408,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
             t = (u == K - 1) ? bt.y : fma(ctad[CTAD_A + 2 * u + 2], bt.x, fma(ctad[CTAD_B + 2 * u + 2], bt.y, zz[(2 * u + 2) * 32]));
         };
         cluster.sync();
+        const long long tk1 = a.prof ? clock64() : 0;
         const int q = valid ? a.q0 + (int)(v / a.vpi) : a.q0;
         const int src = (AFF && valid) ? (int)(v % a.nsrc) : 0;
         double ca = 0.0, cc = 0.0;     // (b_{c-1}, t_{c+1}) of step j-1: coefficients of V2, W2
@@ -459,6 +465,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
                 atomicAdd(pr + 1, (unsigned long long)(t2 - t1));
             }
         }
+        const long long tl = a.prof ? clock64() : 0;
         const int pm = a.m & 1;
         mbar_wait(cbar + 8 * pm, ((a.m - 1) >> 1) & 1);
         double2 e;                                               // (b_m, t_m) of the neighbours
@@ -468,13 +475,18 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
             for (int i = 0; i < L; ++i) {
                 if (s0 + i < a.n) {
                     const double4 q4 = cd[i];
-                    const double *R = a.rowc + (size_t)(s0 + i) * 8;
+                    const double2 VW = vw[i];
                     double x = fma(q4.z, ca, fma(q4.w, cc, S[i]));
-                    x = fma(R[3], e.x, fma(R[4], e.y, x));
+                    x = fma(VW.x, e.x, fma(VW.y, e.y, x));
                     if (a.off) x += a.off[(long)(s0 + i) * a.ld_off + v];
                     a.out[(long)(s0 + i) * a.ld_out + v] = x;
                 }
             }
+        }
+        if (a.prof && threadIdx.x == 0) {
+            const long long tk2 = clock64();
+            atomicAdd(a.prof + (size_t)(512 + C) * 4 + 0, (unsigned long long)(tk1 - tk0));
+            atomicAdd(a.prof + (size_t)(512 + C) * 4 + 1, (unsigned long long)(tk2 - tl));
         }
     } else {
         // ------------------------------------------------ interface warp
@@ -621,6 +633,13 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (getenv("PR_PART_PROF")) {
+        int nc = -1;
+        cudaError_t eo = cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, AFF>, &cfg);
+        fprintf(stderr, "part: max active clusters %d (%s), smem %zu B, groups %ld\n", nc,
+                eo == cudaSuccess ? "ok" : cudaGetErrorString(eo), smem, groups);
+        (void)cudaGetLastError();
+    }
     note_launch();
     return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, AFF>, a);
 }
@@ -669,8 +688,8 @@ cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose,
     static unsigned long long *dprof = nullptr;
     const bool want_prof = getenv("PR_PART_PROF") != nullptr;
     if (want_prof) {
-        if (!dprof) cudaMalloc(&dprof, 256 * 4 * sizeof(unsigned long long));
-        cudaMemsetAsync(dprof, 0, 256 * 4 * sizeof(unsigned long long), s);
+        if (!dprof) cudaMalloc(&dprof, 1024 * 4 * sizeof(unsigned long long));
+        cudaMemsetAsync(dprof, 0, 1024 * 4 * sizeof(unsigned long long), s);
         a.prof = dprof;
     }
     const bool prof = profiling();
@@ -702,13 +721,15 @@ cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose,
     // y = w r - ga y' (3) and x = y - cp x' (2)  (bench.py roofline)
     if (prof) stepper_timed_end(s, (double)sa.n * (double)sa.B * (double)sa.m, 5.0 * (double)sa.n * (double)sa.B * (double)sa.m);
     if (want_prof && e == cudaSuccess) {
-        unsigned long long h[256 * 4];
+        unsigned long long h[1024 * 4];
         cudaMemcpyAsync(h, dprof, sizeof(h), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
         const long groups = (sa.B + 32 / H - 1) / (32 / H);
         const double norm = (double)groups * sa.m;
         fprintf(stderr, "part P=%d L=%d CL=%d K=%d H=%d m=%d groups=%ld  cycles/step [sweep hand-off | helper: gather(incl. wait) publish(incl. wait)]:\n", P,
                 op.part_L, op.part_CL, K, H, sa.m, groups);
+        fprintf(stderr, "  CTA 0 per group: prologue %.0f epilogue %.0f cycles\n", (double)h[512 * 4] / groups,
+                (double)h[512 * 4 + 1] / groups);
         for (int c = 0; c < P; c += (P > 16 ? P / 16 : 1))
             fprintf(stderr, "  chunk %3d: %8.0f %8.0f | %8.0f %8.0f\n", c + (P > 16 ? 1 : 0), h[(c + (P > 16 ? 1 : 0)) * 4] / norm,
                     h[(c + (P > 16 ? 1 : 0)) * 4 + 1] / norm, h[c * 4 + 2] / norm, h[c * 4 + 3] / norm);

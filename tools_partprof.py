@@ -15,7 +15,7 @@ build.build()
 for name in sys.argv[1:] or ["C2", "C1"]:
     cfg = get(name)
     op = gpu_op(cfg)
-    X = torch.randn(cfg.n, 64, dtype=torch.float64, device="cuda")
+    X = torch.randn(cfg.n, int(os.environ.get("PB", "64")), dtype=torch.float64, device="cuda")
     Y = torch.empty_like(X)
     op.fine_propagate(PR_LINEAR, 0, cfg.m, X, Y)
     torch.cuda.synchronize()
