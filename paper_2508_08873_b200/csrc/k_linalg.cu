@@ -11,6 +11,7 @@
 //   K8/K9 sweep, expand   : reduced Parareal correction (eq. def_Parareal,
 //                           P:144-151) and update norms
 #include <float.h>
+#include <stdlib.h>
 
 #include "pr_internal.cuh"
 
@@ -262,6 +263,120 @@ __global__ void __launch_bounds__(XM_THREADS) k_xty_mma(XtY p)
     }
 }
 
+// ---- X^T Y on FP64 tensor cores for the 1D row-major layout (a row's a resp.
+// c values contiguous and 16-byte aligned): rows stream through a 2-stage ring
+// of 16-byte cp.async copies (XR_TR rows per stage); warp w owns output
+// tile-columns w and w + 8 and every tile-row.  diff: the right operand is
+// Y2 - Y (the Parareal projection V^T (F u - u)), formed on the fly.
+constexpr int XR_TR = 32;
+
+__device__ __forceinline__ void cpa16_zfill(double *smem, const double *gmem, bool valid)
+{
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    int n = valid ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+
+template <bool DIFF>
+__global__ void __launch_bounds__(XM_THREADS) k_xty_rm(XtY p)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int b = blockIdx.y, t = blockIdx.x;
+    if (p.skip && p.skip[b] == 2) return;
+    const int ctot = DIFF ? p.c : p.c + p.c2;
+    const int MT = (p.a + 7) / 8, NT = (ctot + 7) / 8;
+    const int SX = xm_stride(p.a), SY = xm_stride(ctot);
+    const int xsz = XR_TR * SX, ysz = XR_TR * SY;
+    const int nY = DIFF ? 2 : 1;
+    double *Xs = sm, *Ys = sm + 2 * xsz;                 // Ys: [stage][nY][XR_TR][SY]
+    const long r0 = (long)t * p.chunk_rows;
+    long r1 = r0 + p.chunk_rows;
+    if (r1 > p.rows) r1 = p.rows;
+    const double *Xb = p.X + (long)b * p.xbs;
+    const double *Yb = p.Y + (long)b * p.ybs;
+    const double *Y2b = p.Y2 ? p.Y2 + (long)b * p.ybs : nullptr;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int ax2 = (p.a + 1) / 2, cy2 = (ctot + 1) / 2;   // 16-byte pieces per row (a, c even)
+
+    auto stage = [&](long rt, int buf) {
+        double *xs = Xs + buf * xsz, *ys = Ys + buf * nY * ysz;
+        for (int e = threadIdx.x; e < XR_TR * ax2; e += XM_THREADS) {
+            const int r = e / ax2, i = 2 * (e % ax2);
+            const long row = rt + r;
+            const bool ok = row < r1;
+            cpa16_zfill(xs + r * SX + i, ok ? Xb + row * p.xrs + i : Xb, ok);
+        }
+        for (int e = threadIdx.x; e < XR_TR * cy2; e += XM_THREADS) {
+            const int r = e / cy2, j = 2 * (e % cy2);
+            const long row = rt + r;
+            const bool ok = row < r1;
+            if (DIFF) {
+                cpa16_zfill(ys + r * SY + j, ok ? Yb + row * p.yrs + j : Yb, ok);
+                cpa16_zfill(ys + ysz + r * SY + j, ok ? Y2b + row * p.yrs + j : Y2b, ok);
+            } else {
+                const double *src = Yb;
+                if (ok) src = (j < p.c) ? Yb + row * p.yrs + j : Y2b + row * p.yrs + (j - p.c);
+                cpa16_zfill(ys + r * SY + j, src, ok);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+
+    double acc[2][8][2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[q][i][0] = acc[q][i][1] = 0.0;
+
+    const int ntiles = (int)((r1 - r0 + XR_TR - 1) / XR_TR);
+    if (ntiles > 0) stage(r0, 0);
+    for (int it = 0; it < ntiles; ++it) {
+        if (it + 1 < ntiles) {
+            stage(r0 + (long)(it + 1) * XR_TR, (it + 1) & 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+        const double *xs = Xs + (it & 1) * xsz, *ys = Ys + (it & 1) * nY * ysz;
+#pragma unroll
+        for (int ks = 0; ks < XR_TR / 4; ++ks) {
+            const int k = ks * 4 + tq;
+            double af[8];
+#pragma unroll
+            for (int mi = 0; mi < 8; ++mi) af[mi] = (mi < MT) ? xs[k * SX + mi * 8 + gq] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int nj = w + 8 * q;
+                if (nj < NT) {
+                    double bf = ys[k * SY + nj * 8 + gq];
+                    if (DIFF) bf = ys[ysz + k * SY + nj * 8 + gq] - bf;
+#pragma unroll
+                    for (int mi = 0; mi < 8; ++mi)
+                        if (mi < MT) dmma_f64(acc[q][mi][0], acc[q][mi][1], af[mi], bf);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    double *out = p.part + ((long)b * p.nchunk + t) * p.a * ctot;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        const int nj = w + 8 * q;
+        if (nj >= NT) continue;
+#pragma unroll
+        for (int mi = 0; mi < 8; ++mi) {
+            if (mi >= MT) continue;
+            const int i = mi * 8 + gq, j = nj * 8 + 2 * tq;
+            if (i < p.a) {
+                if (j < ctot) out[(long)i * ctot + j] = acc[q][mi][0];
+                if (j + 1 < ctot) out[(long)i * ctot + j + 1] = acc[q][mi][1];
+            }
+        }
+    }
+}
+
 // ---- skinny X^T Y (few right-hand columns, e.g. the Parareal projections with
 // one source): warp lanes run over the a columns of a row of X (row-major, one
 // coalesced load per row), the <= 8 values of Y's row are warp broadcasts; each
@@ -322,9 +437,41 @@ __global__ void __launch_bounds__(32 * XS_WARPS) k_xty_skinny(XtY p)
     }
 }
 
+// row-major 1D operands that the 16-byte staging of k_xty_rm can take
+static bool xty_rm_ok(const XtY &p, int ctot)
+{
+    auto al16 = [](const void *q) { return ((uintptr_t)q & 15) == 0; };
+    if (getenv("PR_NO_XTY_RM")) return false;
+    if (p.xcs != 1 || p.ycs != 1 || p.a > 64 || ctot > 128 || p.a % 2 || ctot % 2) return false;
+    if (p.diff ? (p.c % 2) : (p.c % 2 || p.c2 % 2)) return false;
+    if (p.xrs % 2 || p.yrs % 2 || p.xbs % 2 || p.ybs % 2) return false;
+    return al16(p.X) && al16(p.Y) && (!p.Y2 || al16(p.Y2));
+}
+
 cudaError_t launch_xty(const XtY &p, cudaStream_t s)
 {
-    const int ctot = p.c + p.c2;
+    const int ctot = p.diff ? p.c : p.c + p.c2;
+    if (p.diff || ctot > 4) {
+        if (xty_rm_ok(p, ctot)) {
+            const int SX = xm_stride(p.a), SY = xm_stride(ctot);
+            const size_t smem = (size_t)2 * XR_TR * (SX + (p.diff ? 2 : 1) * SY) * sizeof(double);
+            dim3 grid(p.nchunk, p.nbatch);
+            cudaError_t e;
+            if (p.diff) {
+                e = cudaFuncSetAttribute(k_xty_rm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return e;
+                note_launch();
+                k_xty_rm<true><<<grid, XM_THREADS, smem, s>>>(p);
+            } else {
+                e = cudaFuncSetAttribute(k_xty_rm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return e;
+                note_launch();
+                k_xty_rm<false><<<grid, XM_THREADS, smem, s>>>(p);
+            }
+            return cudaGetLastError();
+        }
+        if (p.diff) return cudaErrorInvalidValue;    // callers fall back to the [Y | Y2] form
+    }
     if (ctot <= 4 && p.a <= 128 && p.xcs == 1) {
         dim3 grid(p.nchunk, p.nbatch);
         note_launch();
@@ -357,6 +504,22 @@ cudaError_t launch_xty(const XtY &p, cudaStream_t s)
         return cudaGetLastError();
     }
     return launch_xty_fma(p, s);
+}
+
+cudaError_t launch_xty_diff(XtY p, const double *Y2, int c, int &pcols, cudaStream_t s)
+{
+    p.Y2 = Y2;
+    p.c = c;
+    p.c2 = 0;
+    p.diff = 1;
+    if (xty_rm_ok(p, c)) {
+        pcols = 0;
+        return launch_xty(p, s);
+    }
+    p.diff = 0;
+    p.c2 = c;
+    pcols = c;
+    return launch_xty(p, s);
 }
 
 cudaError_t launch_xty_fma(const XtY &p, cudaStream_t s)
@@ -1362,6 +1525,149 @@ __global__ void __launch_bounds__(256) k_expand_wide(Expand a)
     }
 }
 
+// DMMA variant for the 1D layout (sources contiguous in a row, S % 8 == 0,
+// k <= 64): out_b = base_b + U_b e_b as an (rows x k) x (k x S) product on the
+// FP64 tensor cores.  e_b's B fragments stay in registers for the whole chunk
+// (warp w: source tiles w, w + 8); the U rows, the base rows and (for the norm
+// partials) the old rows of each 32-row stage stream through a 2-stage ring of
+// 16-byte cp.async copies, so HBM requests stay in flight while the tensor
+// cores work on the previous stage.  Norm partials as in k_expand_wide.
+constexpr int EM_TR = 32;
+
+__host__ __device__ inline int em_sy(int S) { return S + 4; }   // conflict-light row stride
+
+__global__ void __launch_bounds__(256) k_expand_mma(Expand a)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int b = blockIdx.y, t = blockIdx.x;
+    const int k = a.k, S = a.S;
+    const int KS = (k + 3) / 4, NT = S / 8;
+    const int SU = xm_stride(k), SY = em_sy(S);
+    const bool norms = a.normpart != nullptr;
+    const bool hasb = a.base != nullptr;
+    const int ustage = EM_TR * SU, ystage = EM_TR * SY;
+    const int stage_sz = ustage + (hasb ? ystage : 0) + (norms ? ystage : 0);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const long r0 = (long)t * a.chunk_rows;
+    long r1 = r0 + a.chunk_rows;
+    if (r1 > a.rows) r1 = a.rows;
+    const double *Ub = a.U + (long)b * a.Ubs;
+    const double *eb = a.e + (long)b * k * S;
+    const long col0 = (long)b * S;
+    // B fragments: B[kk][n] = e_b[kk, n], kk = 4 ks + tq, n = 8 nj + gq
+    double bf[2][16];
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+            const int nj = w + 8 * q, kk = 4 * ks + tq;
+            bf[q][ks] = (nj < NT && ks < KS && kk < k) ? eb[(long)kk * S + nj * 8 + gq] : 0.0;
+        }
+    const int k2 = k / 2, s2 = S / 2;
+    auto stage = [&](long rt, int buf) {
+        double *us = sm + buf * stage_sz;
+        double *bs = us + ustage;
+        double *os = bs + (hasb ? ystage : 0);
+        for (int e = threadIdx.x; e < EM_TR * k2; e += 256) {
+            const int r = e / k2, i = 2 * (e % k2);
+            const long row = rt + r;
+            const bool ok = row < r1;
+            cpa16_zfill(us + r * SU + i, ok ? Ub + row * k + i : Ub, ok);
+        }
+        if (hasb)
+            for (int e = threadIdx.x; e < EM_TR * s2; e += 256) {
+                const int r = e / s2, j = 2 * (e % s2);
+                const long row = rt + r;
+                const bool ok = row < r1;
+                cpa16_zfill(bs + r * SY + j, ok ? a.base + row * a.brs + col0 + j : a.base, ok);
+            }
+        if (norms)
+            for (int e = threadIdx.x; e < EM_TR * s2; e += 256) {
+                const int r = e / s2, j = 2 * (e % s2);
+                const long row = rt + r;
+                const bool ok = row < r1;
+                cpa16_zfill(os + r * SY + j, ok ? a.out + row * a.ors + col0 + j : a.out, ok);
+            }
+        for (int e = threadIdx.x; e < EM_TR * (4 * KS - k); e += 256) {   // k-step padding
+            const int r = e / (4 * KS - k), i = k + e % (4 * KS - k);
+            us[r * SU + i] = 0.0;
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    double nrm[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const int ntiles = (int)((r1 - r0 + EM_TR - 1) / EM_TR);
+    if (ntiles > 0) stage(r0, 0);
+    for (int it = 0; it < ntiles; ++it) {
+        if (it + 1 < ntiles) {
+            stage(r0 + (long)(it + 1) * EM_TR, (it + 1) & 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+        const double *us = sm + (it & 1) * stage_sz;
+        const double *bs = us + ustage;
+        const double *os = bs + (hasb ? ystage : 0);
+        const long rt = r0 + (long)it * EM_TR;
+#pragma unroll
+        for (int mi = 0; mi < EM_TR / 8; ++mi) {
+            const int rl = mi * 8 + gq;
+            const long row = rt + rl;
+            double acc[2][2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                const int nj = w + 8 * q;
+                double2 bv = make_double2(0.0, 0.0);
+                if (hasb && nj < NT) bv = *reinterpret_cast<const double2 *>(bs + rl * SY + nj * 8 + 2 * tq);
+                acc[q][0] = bv.x;
+                acc[q][1] = bv.y;
+            }
+#pragma unroll
+            for (int ks = 0; ks < 16; ++ks) {
+                if (ks < KS) {
+                    const double af = us[rl * SU + 4 * ks + tq];
+#pragma unroll
+                    for (int q = 0; q < 2; ++q)
+                        if (w + 8 * q < NT) dmma_f64(acc[q][0], acc[q][1], af, bf[q][ks]);
+                }
+            }
+            if (row < r1) {
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const int nj = w + 8 * q;
+                    if (nj < NT) {
+                        const long col = col0 + nj * 8 + 2 * tq;
+                        *reinterpret_cast<double2 *>(a.out + row * a.ors + col) = make_double2(acc[q][0], acc[q][1]);
+                        if (norms) {
+                            const double2 ov = *reinterpret_cast<const double2 *>(os + rl * SY + nj * 8 + 2 * tq);
+                            const double d0 = acc[q][0] - ov.x, d1 = acc[q][1] - ov.y;
+                            nrm[q][0] = fma(d0, d0, nrm[q][0]);
+                            nrm[q][1] = fma(d1, d1, nrm[q][1]);
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (norms) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int nj = w + 8 * q;
+            if (nj >= NT) continue;                   // warp-uniform
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                double v = nrm[q][c];
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 8);
+                v += __shfl_xor_sync(0xffffffffu, v, 16);
+                if (gq == 0) a.normpart[((long)b * S + nj * 8 + 2 * tq + c) * a.nchunk + t] = v;
+            }
+        }
+    }
+}
+
 // Narrow variant (S < 16): one row per thread, the row of U_b read straight
 // from global memory (contiguous k doubles, 16-B loads), e_b broadcast from
 // shared memory, four independent partial sums per output.
@@ -1431,6 +1737,22 @@ cudaError_t launch_expand(const Expand &a, cudaStream_t s)
         note_launch();
         k_expand_narrow<<<grid, 256, smem, s>>>(a);
         return cudaGetLastError();
+    }
+    {
+        auto al16 = [](const void *q) { return ((uintptr_t)q & 15) == 0; };
+        if (!getenv("PR_NO_EXPAND_MMA") && a.ovs == 1 && (a.base == nullptr || a.bvs == 1) && a.S % 8 == 0 &&
+            a.S <= 128 && a.k <= 64 && a.k % 2 == 0 && a.ors % 2 == 0 && (a.base == nullptr || a.brs % 2 == 0) &&
+            a.Ubs % 2 == 0 && al16(a.out) && al16(a.U) && (a.base == nullptr || al16(a.base))) {
+            const size_t smem = (size_t)2 * EM_TR *
+                                (xm_stride(a.k) + (a.base ? em_sy(a.S) : 0) + (a.normpart ? em_sy(a.S) : 0)) *
+                                sizeof(double);
+            cudaError_t e = cudaFuncSetAttribute(k_expand_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            dim3 grid(a.nchunk, a.nbatch);
+            note_launch();
+            k_expand_mma<<<grid, 256, smem, s>>>(a);
+            return cudaGetLastError();
+        }
     }
     if (a.S >= 16 && a.k <= 128) {
         size_t smem = ((size_t)a.k * (EW_ROWS + 2) + (size_t)a.k * EW_SRC + 16 * EW_SRC) * sizeof(double);

@@ -742,9 +742,10 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
     auto project = [&](bool with_p) -> pr_status {
         XtY x{nullptr, G->V, rows * k, k, 1, k, with_p ? U_out : Fu, blk, L.rs, L.vs, S, rows, N,
               nchunk, cr, part};
-        if (with_p) { x.Y2 = Fu; x.c2 = S; }
-        PR_CUDA(launch_xty(x, s));
-        PR_CUDA(launch_reduce_pq(part, N, nchunk, k, S, with_p ? S : 0, sig, G->l, qv, s));
+        int pcols = 0;
+        if (with_p) PR_CUDA(launch_xty_diff(x, Fu, S, pcols, s));
+        else PR_CUDA(launch_xty(x, s));
+        PR_CUDA(launch_reduce_pq(part, N, nchunk, k, S, pcols, sig, G->l, qv, s));
         return PR_OK;
     };
     auto expand = [&](bool norms) -> pr_status {
@@ -852,9 +853,10 @@ pr_status pr_coarse_project(pr_coarse G, int nsrc, const double *Y1, const doubl
     double *part;
     PR_ALLOC(part, double, (size_t)N * nchunk * k * 2 * S, Sc);
     XtY x{nullptr, G->V, rows * k, k, 1, k, Y1 ? Y1 : Y2, blk, L.rs, L.vs, S, rows, N, nchunk, cr, part};
-    if (Y1) { x.Y2 = Y2; x.c2 = S; }
-    PR_CUDA(launch_xty(x, s));
-    PR_CUDA(launch_reduce_pq(part, N, nchunk, k, S, Y1 ? S : 0, G->sigma, G->l, d, s));
+    int pcols = 0;
+    if (Y1) PR_CUDA(launch_xty_diff(x, Y2, S, pcols, s));
+    else PR_CUDA(launch_xty(x, s));
+    PR_CUDA(launch_reduce_pq(part, N, nchunk, k, S, pcols, G->sigma, G->l, d, s));
     return PR_OK;
 }
 

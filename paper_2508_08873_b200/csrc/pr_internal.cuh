@@ -137,8 +137,11 @@ struct XtY {
     double *part;                     // (nbatch, nchunk, a, c + c2)
     const double *Y2 = nullptr;       // optional: columns [c, c + c2) from Y2 (Y's strides)
     int c2 = 0;
+    int diff = 0;                     // 1: the right operand is Y2 - Y (c columns, c2 == 0)
 };
 cudaError_t launch_xty(const XtY &p, cudaStream_t s);
+// partials of X^T (Y2 - Y) (pcols = 0) on the row-major DMMA path, else of X^T [Y | Y2] (pcols = c)
+cudaError_t launch_xty_diff(XtY p, const double *Y2, int c, int &pcols, cudaStream_t s);
 int xty_chunks(long rows, int nbatch);
 
 // out[(b*a + i)*c + j] = scale_i(b) * sum_t part[...]  (fixed order over t)
