@@ -87,7 +87,9 @@ typedef struct pr_coarse_s *pr_coarse;
  * given, the LU and UL pivots of I + dt A are computed from them (DESIGN.md
  * reading R-ACC: relative accuracy independent of dt/h^2 for diagonally
  * dominant M-matrices); when NULL they are formed as sub+diag+sup.  The
- * factorization runs once, in a device kernel.  Synchronizing.
+ * factorizations (the whole-vector LU/UL pair and, for 64 <= n <= 16384, the
+ * partitioned-stepper chunk LUs, spikes and interface factors, both built
+ * from row sums) run once, in device kernels.  Synchronizing.
  * Errors: EINVAL (n < 2, dt <= 0, null arrays), ESINGULAR (pivot <= 0 or
  * non-finite), EOOM, ECUDA. */
 pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, const double *sup,
@@ -138,6 +140,10 @@ enum { PR_LINEAR = 0, PR_ADJOINT = 1, PR_AFFINE = 2 };
  * U_in == NULL means a zero input (so PR_AFFINE gives b_q).  offset (nullable,
  * op layout, stride ld_off) is added to the result: F' u + b_q from a stored
  * b_q.  U_in may equal U_out (in place) when ld_in == ld_out.
+ * Each step (I + dt A) x = r is solved exactly (up to rounding order): for a
+ * 1D op with 64 <= n <= 16384 by the partition method over a thread-block
+ * cluster with the state in registers (k_part.cu, reading R-PART),
+ * otherwise by the fused LU/UL stepper; 2D ops in the sine eigenbasis.
  * Errors: EINVAL (mode, m < 0, B < 0, vecs_per_interval < 1, missing source
  * for PR_AFFINE with f->kind mismatched to the op), EDIM (ld too small). */
 pr_status pr_fine_propagate(pr_op op, int mode, int first_interval, int m, int B,
