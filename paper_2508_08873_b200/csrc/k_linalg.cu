@@ -1526,9 +1526,9 @@ __global__ void __launch_bounds__(256) k_expand_wide(Expand a)
 }
 
 // DMMA variant for the 1D layout (sources contiguous in a row, S % 8 == 0,
-// k <= 64): out_b = base_b + U_b e_b as an (rows x k) x (k x S) product on the
-// FP64 tensor cores.  e_b's B fragments stay in registers for the whole chunk
-// (warp w: source tiles w, w + 8); the U rows, the base rows and (for the norm
+// S <= 64, k <= 64): out_b = base_b + U_b e_b as an (rows x k) x (k x S) product
+// on the FP64 tensor cores.  e_b's B fragments stay in registers for the whole
+// chunk (warp w: source tile w); the U rows, the base rows and (for the norm
 // partials) the old rows of each 32-row stage stream through a 2-stage ring of
 // 16-byte cp.async copies, so HBM requests stay in flight while the tensor
 // cores work on the previous stage.  Norm partials as in k_expand_wide.
@@ -1536,7 +1536,7 @@ constexpr int EM_TR = 32;
 
 __host__ __device__ inline int em_sy(int S) { return S + 4; }   // conflict-light row stride
 
-__global__ void __launch_bounds__(256) k_expand_mma(Expand a)
+__global__ void __launch_bounds__(256, 2) k_expand_mma(Expand a)
 {
     extern __shared__ __align__(16) double sm[];
     const int b = blockIdx.y, t = blockIdx.x;
@@ -1555,15 +1555,14 @@ __global__ void __launch_bounds__(256) k_expand_mma(Expand a)
     const double *Ub = a.U + (long)b * a.Ubs;
     const double *eb = a.e + (long)b * k * S;
     const long col0 = (long)b * S;
-    // B fragments: B[kk][n] = e_b[kk, n], kk = 4 ks + tq, n = 8 nj + gq
-    double bf[2][16];
+    // B fragments: B[kk][n] = e_b[kk, n], kk = 4 ks + tq, n = 8 w + gq (warp w: source tile w)
+    const bool act = w < NT;
+    double bf[16];
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
-#pragma unroll
-        for (int ks = 0; ks < 16; ++ks) {
-            const int nj = w + 8 * q, kk = 4 * ks + tq;
-            bf[q][ks] = (nj < NT && ks < KS && kk < k) ? eb[(long)kk * S + nj * 8 + gq] : 0.0;
-        }
+    for (int ks = 0; ks < 16; ++ks) {
+        const int kk = 4 * ks + tq;
+        bf[ks] = (act && ks < KS && kk < k) ? eb[(long)kk * S + w * 8 + gq] : 0.0;
+    }
     const int k2 = k / 2, s2 = S / 2;
     auto stage = [&](long rt, int buf) {
         double *us = sm + buf * stage_sz;
@@ -1595,7 +1594,7 @@ __global__ void __launch_bounds__(256) k_expand_mma(Expand a)
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    double nrm[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    double nrm[2] = {0.0, 0.0};
     const int ntiles = (int)((r1 - r0 + EM_TR - 1) / EM_TR);
     if (ntiles > 0) stage(r0, 0);
     for (int it = 0; it < ntiles; ++it) {
@@ -1610,60 +1609,51 @@ __global__ void __launch_bounds__(256) k_expand_mma(Expand a)
         const double *bs = us + ustage;
         const double *os = bs + (hasb ? ystage : 0);
         const long rt = r0 + (long)it * EM_TR;
+        // the stage's 4 m-tiles run as independent accumulator chains over k
+        constexpr int MTS = EM_TR / 8;
+        if (act) {
+            double acc[MTS][2];
 #pragma unroll
-        for (int mi = 0; mi < EM_TR / 8; ++mi) {
-            const int rl = mi * 8 + gq;
-            const long row = rt + rl;
-            double acc[2][2];
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int nj = w + 8 * q;
+            for (int mi = 0; mi < MTS; ++mi) {
                 double2 bv = make_double2(0.0, 0.0);
-                if (hasb && nj < NT) bv = *reinterpret_cast<const double2 *>(bs + rl * SY + nj * 8 + 2 * tq);
-                acc[q][0] = bv.x;
-                acc[q][1] = bv.y;
+                if (hasb) bv = *reinterpret_cast<const double2 *>(bs + (mi * 8 + gq) * SY + w * 8 + 2 * tq);
+                acc[mi][0] = bv.x;
+                acc[mi][1] = bv.y;
             }
 #pragma unroll
             for (int ks = 0; ks < 16; ++ks) {
                 if (ks < KS) {
-                    const double af = us[rl * SU + 4 * ks + tq];
 #pragma unroll
-                    for (int q = 0; q < 2; ++q)
-                        if (w + 8 * q < NT) dmma_f64(acc[q][0], acc[q][1], af, bf[q][ks]);
+                    for (int mi = 0; mi < MTS; ++mi)
+                        dmma_f64(acc[mi][0], acc[mi][1], us[(mi * 8 + gq) * SU + 4 * ks + tq], bf[ks]);
                 }
             }
-            if (row < r1) {
 #pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    const int nj = w + 8 * q;
-                    if (nj < NT) {
-                        const long col = col0 + nj * 8 + 2 * tq;
-                        *reinterpret_cast<double2 *>(a.out + row * a.ors + col) = make_double2(acc[q][0], acc[q][1]);
-                        if (norms) {
-                            const double2 ov = *reinterpret_cast<const double2 *>(os + rl * SY + nj * 8 + 2 * tq);
-                            const double d0 = acc[q][0] - ov.x, d1 = acc[q][1] - ov.y;
-                            nrm[q][0] = fma(d0, d0, nrm[q][0]);
-                            nrm[q][1] = fma(d1, d1, nrm[q][1]);
-                        }
+            for (int mi = 0; mi < MTS; ++mi) {
+                const int rl = mi * 8 + gq;
+                const long row = rt + rl;
+                if (row < r1) {
+                    const long col = col0 + w * 8 + 2 * tq;
+                    *reinterpret_cast<double2 *>(a.out + row * a.ors + col) = make_double2(acc[mi][0], acc[mi][1]);
+                    if (norms) {
+                        const double2 ov = *reinterpret_cast<const double2 *>(os + rl * SY + w * 8 + 2 * tq);
+                        const double d0 = acc[mi][0] - ov.x, d1 = acc[mi][1] - ov.y;
+                        nrm[0] = fma(d0, d0, nrm[0]);
+                        nrm[1] = fma(d1, d1, nrm[1]);
                     }
                 }
             }
         }
         __syncthreads();
     }
-    if (norms) {
+    if (norms && act) {
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            const int nj = w + 8 * q;
-            if (nj >= NT) continue;                   // warp-uniform
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                double v = nrm[q][c];
-                v += __shfl_xor_sync(0xffffffffu, v, 4);
-                v += __shfl_xor_sync(0xffffffffu, v, 8);
-                v += __shfl_xor_sync(0xffffffffu, v, 16);
-                if (gq == 0) a.normpart[((long)b * S + nj * 8 + 2 * tq + c) * a.nchunk + t] = v;
-            }
+        for (int c = 0; c < 2; ++c) {
+            double v = nrm[c];
+            v += __shfl_xor_sync(0xffffffffu, v, 4);
+            v += __shfl_xor_sync(0xffffffffu, v, 8);
+            v += __shfl_xor_sync(0xffffffffu, v, 16);
+            if (gq == 0) a.normpart[((long)b * S + w * 8 + 2 * tq + c) * a.nchunk + t] = v;
         }
     }
 }
@@ -1741,7 +1731,7 @@ cudaError_t launch_expand(const Expand &a, cudaStream_t s)
     {
         auto al16 = [](const void *q) { return ((uintptr_t)q & 15) == 0; };
         if (!getenv("PR_NO_EXPAND_MMA") && a.ovs == 1 && (a.base == nullptr || a.bvs == 1) && a.S % 8 == 0 &&
-            a.S <= 128 && a.k <= 64 && a.k % 2 == 0 && a.ors % 2 == 0 && (a.base == nullptr || a.brs % 2 == 0) &&
+            a.S <= 64 && a.k <= 64 && a.k % 2 == 0 && a.ors % 2 == 0 && (a.base == nullptr || a.brs % 2 == 0) &&
             a.Ubs % 2 == 0 && al16(a.out) && al16(a.U) && (a.base == nullptr || al16(a.base))) {
             const size_t smem = (size_t)2 * EM_TR *
                                 (xm_stride(a.k) + (a.base ? em_sy(a.S) : 0) + (a.normpart ? em_sy(a.S) : 0)) *
