@@ -25,8 +25,10 @@ cudaError_t launch_xty_fma(const XtY &p, cudaStream_t s);
 
 int xty_chunks(long rows, int nbatch)
 {
-    // enough CTAs to fill the machine twice, at least 64 rows per chunk
-    long want = (2L * num_sms() + nbatch - 1) / nbatch;
+    // enough CTAs to fill the machine four times (the DMMA kernels run one or
+    // two CTAs per SM; more, shorter CTAs shrink the last-wave tail), at least
+    // 64 rows per chunk
+    long want = (4L * num_sms() + nbatch - 1) / nbatch;
     long maxc = (rows + 63) / 64;
     long c = want < maxc ? want : maxc;
     if (c < 1) c = 1;
@@ -163,9 +165,11 @@ __device__ __forceinline__ void cpa8_zfill(double *smem, const double *gmem, boo
 
 __host__ __device__ inline int xm_stride(int w) { return ((w + 15) / 16) * 16 + 4; }
 
-template <bool CM>
-__global__ void __launch_bounds__(XM_THREADS) k_xty_mma(XtY p)
+// NQ n-tiles per warp: 16 / NQ warps (NQ = 1: 512 threads, one tile-column each)
+template <bool CM, int MTM, int NQ>
+__global__ void __launch_bounds__(512 / NQ) k_xty_mma(XtY p)
 {
+    constexpr int NWARP = 16 / NQ, NTH = 32 * NWARP;
     extern __shared__ __align__(16) double sm[];
     const int b = blockIdx.y, t = blockIdx.x;
     if (p.skip && p.skip[b] == 2) return;
@@ -186,17 +190,42 @@ __global__ void __launch_bounds__(XM_THREADS) k_xty_mma(XtY p)
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gq = lane >> 2, tq = lane & 3;
 
+    // column-major tiles (2D layout): rows of a column are contiguous, so the
+    // tile is staged in 16-byte pieces (2 rows) when the strides allow it
+    const bool v16 = CM && (p.xcs % 2 == 0) && (p.ycs % 2 == 0) && (p.xbs % 2 == 0) && (p.ybs % 2 == 0) &&
+                     (r0 % 2 == 0) && ((uintptr_t)p.X % 16 == 0) && ((uintptr_t)p.Y % 16 == 0) &&
+                     (p.Y2 == nullptr || (uintptr_t)p.Y2 % 16 == 0);
     auto stage = [&](long rt, int buf) {
         double *xs = Xs + buf * xsz, *ys = Ys + buf * ysz;
         const int ax = MT * 8, cy = NT * 8;
-        for (int e = threadIdx.x; e < XM_TR * ax; e += XM_THREADS) {
+        if (v16) {
+            constexpr int HR = XM_TR / 2;
+            for (int e = threadIdx.x; e < HR * ax; e += NTH) {
+                const int i = e / HR, r = 2 * (e % HR);
+                const long row = rt + r;
+                const int nb = (i < p.a) ? (row + 1 < r1 ? 16 : (row < r1 ? 8 : 0)) : 0;
+                const double *src = nb ? Xb + row + (long)i * p.xcs : Xb;
+                unsigned sd = (unsigned)__cvta_generic_to_shared(xs + i * SC + r);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sd), "l"(src), "r"(nb) : "memory");
+            }
+            for (int e = threadIdx.x; e < HR * cy; e += NTH) {
+                const int j = e / HR, r = 2 * (e % HR);
+                const long row = rt + r;
+                const int nb = (j < ctot) ? (row + 1 < r1 ? 16 : (row < r1 ? 8 : 0)) : 0;
+                const double *src = Yb;
+                if (nb) src = (j < p.c) ? Yb + row + (long)j * p.ycs : Y2b + row + (long)(j - p.c) * p.ycs;
+                unsigned sd = (unsigned)__cvta_generic_to_shared(ys + j * SC + r);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sd), "l"(src), "r"(nb) : "memory");
+            }
+        } else {
+        for (int e = threadIdx.x; e < XM_TR * ax; e += NTH) {
             int r, i;
             if (CM) { i = e / XM_TR; r = e % XM_TR; } else { r = e / ax; i = e % ax; }
             const long row = rt + r;
             const bool ok = row < r1 && i < p.a;
             cpa8_zfill(xs + (CM ? i * SC + r : r * SXr + i), ok ? Xb + row * p.xrs + (long)i * p.xcs : Xb, ok);
         }
-        for (int e = threadIdx.x; e < XM_TR * cy; e += XM_THREADS) {
+        for (int e = threadIdx.x; e < XM_TR * cy; e += NTH) {
             int r, j;
             if (CM) { j = e / XM_TR; r = e % XM_TR; } else { r = e / cy; j = e % cy; }
             const long row = rt + r;
@@ -206,14 +235,15 @@ __global__ void __launch_bounds__(XM_THREADS) k_xty_mma(XtY p)
                                     : Y2b + row * p.yrs + (long)(j - p.c) * p.ycs;
             cpa8_zfill(ys + (CM ? j * SC + r : r * SYr + j), src, ok);
         }
+        }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
 
-    double acc[2][16][2];
+    double acc[NQ][MTM][2];
 #pragma unroll
-    for (int q = 0; q < 2; ++q)
+    for (int q = 0; q < NQ; ++q)
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[q][i][0] = acc[q][i][1] = 0.0;
+        for (int i = 0; i < MTM; ++i) acc[q][i][0] = acc[q][i][1] = 0.0;
 
     const int ntiles = (int)((r1 - r0 + XM_TR - 1) / XM_TR);
     if (ntiles > 0) stage(r0, 0);
@@ -229,17 +259,17 @@ __global__ void __launch_bounds__(XM_THREADS) k_xty_mma(XtY p)
 #pragma unroll
         for (int ks = 0; ks < XM_TR / 4; ++ks) {
             const int k = ks * 4 + tq;
-            double af[16];
+            double af[MTM];
 #pragma unroll
-            for (int mi = 0; mi < 16; ++mi)
+            for (int mi = 0; mi < MTM; ++mi)
                 af[mi] = (mi < MT) ? (CM ? xs[(mi * 8 + gq) * SC + k] : xs[k * SXr + mi * 8 + gq]) : 0.0;
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-                const int nj = w + 8 * q;
+            for (int q = 0; q < NQ; ++q) {
+                const int nj = w + NWARP * q;
                 if (nj < NT) {
                     const double bf = CM ? ys[(nj * 8 + gq) * SC + k] : ys[k * SYr + nj * 8 + gq];
 #pragma unroll
-                    for (int mi = 0; mi < 16; ++mi)
+                    for (int mi = 0; mi < MTM; ++mi)
                         if (mi < MT) dmma_f64(acc[q][mi][0], acc[q][mi][1], af[mi], bf);
                 }
             }
@@ -248,11 +278,11 @@ __global__ void __launch_bounds__(XM_THREADS) k_xty_mma(XtY p)
     }
     double *out = p.part + ((long)b * p.nchunk + t) * p.a * ctot;
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-        const int nj = w + 8 * q;
+    for (int q = 0; q < NQ; ++q) {
+        const int nj = w + NWARP * q;
         if (nj >= NT) continue;
 #pragma unroll
-        for (int mi = 0; mi < 16; ++mi) {
+        for (int mi = 0; mi < MTM; ++mi) {
             if (mi >= MT) continue;
             const int i = mi * 8 + gq, j = nj * 8 + 2 * tq;
             if (i < p.a) {
@@ -479,9 +509,8 @@ cudaError_t launch_xty(const XtY &p, cudaStream_t s)
         else k_xty_skinny<4><<<grid, 32 * XS_WARPS, 0, s>>>(p);
         return cudaGetLastError();
     }
-    // DMMA path for the 2D (column-contiguous) layout only: measured on B200 it
-    // is faster there (C3 Gram 7.9 vs 9.3 ms), while the register-blocked FMA
-    // kernel is faster for the 1D row-major layout (C4 build 296 vs 356 ms).
+    // DMMA path for the 2D (column-contiguous) layout (the 1D row-major layout
+    // takes k_xty_rm above when its strides allow 16-byte staging)
     if (p.a <= 128 && ctot <= 128 && p.xrs == 1 && p.yrs == 1 && p.xcs != 1 && p.ycs != 1) {
         const bool cm = (p.xcs != 1);
         const int MT = (p.a + 7) / 8, NT = (ctot + 7) / 8;
@@ -490,17 +519,18 @@ cudaError_t launch_xty(const XtY &p, cudaStream_t s)
         const size_t smem = (size_t)2 * (xsz + ysz) * sizeof(double);
         dim3 grid(p.nchunk, p.nbatch);
         cudaError_t e;
-        if (cm) {
-            e = cudaFuncSetAttribute(k_xty_mma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
+        auto go = [&](auto kern, int threads) -> cudaError_t {
+            cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e2 != cudaSuccess) return e2;
             note_launch();
-            k_xty_mma<true><<<grid, XM_THREADS, smem, s>>>(p);
-        } else {
-            e = cudaFuncSetAttribute(k_xty_mma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            note_launch();
-            k_xty_mma<false><<<grid, XM_THREADS, smem, s>>>(p);
-        }
+            kern<<<grid, threads, smem, s>>>(p);
+            return cudaSuccess;
+        };
+        // MT <= 8 (a <= 64): 8 warps with 2 tile-columns each and half the
+        // accumulators (two CTAs per SM); else 16 warps with one tile-column each
+        if (cm) e = (MT <= 8) ? go(k_xty_mma<true, 8, 2>, 256) : go(k_xty_mma<true, 16, 1>, 512);
+        else e = (MT <= 8) ? go(k_xty_mma<false, 8, 2>, 256) : go(k_xty_mma<false, 16, 1>, 512);
+        if (e != cudaSuccess) return e;
         return cudaGetLastError();
     }
     return launch_xty_fma(p, s);
