@@ -51,6 +51,7 @@ def _stepper_path(monkeypatch, path):
 
 @pytest.mark.parametrize("name,n,m,B", [("C1", 127, 64, 12), ("C1", 127, 1, 6), ("C1", 127, 2, 5),
                                         ("T4", 301, 16, 33), ("T4", 37, 7, 64), ("T1", 200, 12, 70),
+                                        ("C1", 64, 5, 33), ("C2", 513, 7, 9), ("C4", 16384, 3, 17),
                                         ("C2", 4095, 256, 10), ("C2", 8192, 20, 3),
                                         ("C4", 16383, 128, 6)])
 @pytest.mark.parametrize("mode", ["linear", "adjoint"])
