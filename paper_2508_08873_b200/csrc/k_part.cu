@@ -43,11 +43,14 @@ namespace pr {
 
 // per-CTA interface data (PART_CTAD doubles): band factors of the local
 // interface matrix M_C (2K rows x 5) | alpha (2K) | beta (2K) | rows of the
-// global inverse for B_{C-1} (2CL) and T_{C+1} (2CL)
+// global inverse for B_{C-1} (2CL) and T_{C+1} (2CL) | rows 0 and 2K-1 of
+// M_C^{-1} (2K each: the two values a CTA sends, off the band solve's chain)
 constexpr int CTAD_A = 5 * 2 * PART_KMAX;
 constexpr int CTAD_B = CTAD_A + 2 * PART_KMAX;
 constexpr int CTAD_GB = CTAD_B + 2 * PART_KMAX;
 constexpr int CTAD_GT = CTAD_GB + 2 * PART_CLMAX;
+constexpr int CTAD_R0 = CTAD_GT + 2 * PART_CLMAX;     // row 0 of M_C^{-1} (T_C)
+constexpr int CTAD_RM = CTAD_R0 + 2 * PART_KMAX;      // row 2K-1 of M_C^{-1} (B_C)
 
 // ------------------------------------------------------------------ setup
 // One thread per chunk c (rows s0..s0+L-1): local LU of T_c in row-sum form and
@@ -210,6 +213,12 @@ __global__ void k_part_iface(int CL, int K, const double *ends, double *ctad, in
         ok = band_factor(M, A, rs, F) && ok;
         for (int r = 0; r < M; ++r)
             for (int d = 0; d < 5; ++d) D[r * 5 + d] = F[r][d];
+        for (int col = 0; col < M; ++col) {          // rows 0 and M-1 of M_C^{-1}
+            for (int r = 0; r < M; ++r) x[r] = (r == col) ? 1.0 : 0.0;
+            band_solve(M, F, x);
+            D[CTAD_R0 + col] = x[0];
+            D[CTAD_RM + col] = x[M - 1];
+        }
         const double *E0 = ends + (size_t)(C * K) * 8, *E1 = ends + (size_t)(C * K + K - 1) * 8;
         for (int r = 0; r < M; ++r) x[r] = 0.0;
         x[0] = E0[2];
@@ -496,12 +505,16 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
         double *zs = reinterpret_cast<double *>(rmap + 2 * CL);          // [2][M][32]
         constexpr int CLH = CL / H;                                      // CTAs per half-warp
         // step j's values from every super-chunk -> (B_{C-1}, T_{C+1}) of step j
+        unsigned long long hx1 = 0, hx2 = 0, hw = 0, hg = 0;
         auto gather = [&](int j) {
             const int p = j & 1;
             if (lane == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                              :: "r"(gbar + 8 * p), "r"((unsigned)(CL * VPW * sizeof(double2))) : "memory");
+            long long ga = a.prof ? clock64() : 0;
             mbar_wait(gbar + 8 * p, ((j - 1) >> 1) & 1);
+            long long gb = a.prof ? clock64() : 0;
+            hw += gb - ga;
             const double2 *G = gth + (size_t)p * CL * 32 + vl;
             double b0 = 0.0, b1 = 0.0, t0 = 0.0, t1 = 0.0;
 #pragma unroll
@@ -521,11 +534,13 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
             if (h == 0) coef[p * 32 + vl] = make_double2(Bx, Tx);
             __syncwarp();
             if (lane == 0) mbar_arrive(cbar + 8 * p);
+            if (a.prof) hg += clock64() - gb;
         };
         // chunk end values of step j -> local solve z = M_C^{-1} g_C -> (T_C, B_C) to every CTA
         auto publish = [&](int j) {
             const int p = j & 1;
             mbar_wait(ebar + 8 * p, ((j - 1) >> 1) & 1);
+            long long pa = a.prof ? clock64() : 0;
             double z[M];
 #pragma unroll
             for (int uu = 0; uu < K; ++uu) {
@@ -533,6 +548,26 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
                 z[2 * uu] = r.x;
                 z[2 * uu + 1] = r.y;
             }
+            // (T_C, B_C) from the two stored rows of M_C^{-1} (independent FMAs),
+            // sent first; the full local solution follows with the band factors
+            // while the cluster exchange is in flight
+            double T0 = 0.0, T1 = 0.0, B0 = 0.0, B1 = 0.0;
+#pragma unroll
+            for (int i = 0; i < M; i += 2) {
+                T0 = fma(ctad[CTAD_R0 + i], z[i], T0);
+                T1 = fma(ctad[CTAD_R0 + i + 1], z[i + 1], T1);
+                B0 = fma(ctad[CTAD_RM + i], z[i], B0);
+                B1 = fma(ctad[CTAD_RM + i + 1], z[i + 1], B1);
+            }
+            const double Tv = T0 + T1, Bv = B0 + B1;
+            const unsigned off = (unsigned)(((p * CL + C) * 32 + vl) * sizeof(double2));
+#pragma unroll
+            for (int rr = 0; rr < CLH; ++rr) {
+                const int r = h * CLH + rr;
+                st_async_v2(rmap[r] + off, Tv, Bv, rmap[CL + r] + 8 * p);
+            }
+            long long pb = a.prof ? clock64() : 0;
+            hx1 += pb - pa;
             // band factors, row i: l2, l1, 1/u, u1, u2
 #pragma unroll
             for (int i = 0; i < M; ++i) {
@@ -549,12 +584,8 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
 #pragma unroll
                 for (int i = 0; i < M; ++i) zs[((size_t)p * M + i) * 32 + vl] = z[i];
             }
-            const unsigned off = (unsigned)(((p * CL + C) * 32 + vl) * sizeof(double2));
-#pragma unroll
-            for (int rr = 0; rr < CLH; ++rr) {
-                const int r = h * CLH + rr;
-                st_async_v2(rmap[r] + off, z[0], z[M - 1], rmap[CL + r] + 8 * p);
-            }
+            __syncwarp();
+            if (a.prof) hx2 += clock64() - pb;
         };
         unsigned long long tw = 0, tp = 0, tg = 0;
         for (int j = 1; j <= a.m; ++j) {
@@ -571,6 +602,11 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
             unsigned long long *pr = a.prof + (size_t)(C * K) * 4;
             atomicAdd(pr + 2, tg);
             atomicAdd(pr + 3, tp);
+            unsigned long long *px = a.prof + (size_t)(600 + C) * 4;
+            atomicAdd(px + 0, hx1);
+            atomicAdd(px + 1, hx2);
+            atomicAdd(px + 2, hw);
+            atomicAdd(px + 3, hg);
         }
         (void)tw;
     }
@@ -730,6 +766,9 @@ cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose,
                 op.part_L, op.part_CL, K, H, sa.m, groups);
         fprintf(stderr, "  CTA 0 per group: prologue %.0f epilogue %.0f cycles\n", (double)h[512 * 4] / groups,
                 (double)h[512 * 4 + 1] / groups);
+        fprintf(stderr, "  interface warp of CTA 0 per step: to-send %.0f band-solve %.0f gather-wait %.0f gather %.0f\n",
+                (double)h[600 * 4] / norm, (double)h[600 * 4 + 1] / norm, (double)h[600 * 4 + 2] / norm,
+                (double)h[600 * 4 + 3] / norm);
         for (int c = 0; c < P; c += (P > 16 ? P / 16 : 1))
             fprintf(stderr, "  chunk %3d: %8.0f %8.0f | %8.0f %8.0f\n", c + (P > 16 ? 1 : 0), h[(c + (P > 16 ? 1 : 0)) * 4] / norm,
                     h[(c + (P > 16 ? 1 : 0)) * 4 + 1] / norm, h[c * 4 + 2] / norm, h[c * 4 + 3] / norm);

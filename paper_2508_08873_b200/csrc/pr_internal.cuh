@@ -108,7 +108,7 @@ cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s);
 // setup (ends: P x 8 scratch), selection and launch
 constexpr int PART_KMAX = 16;                  // chunks per CTA
 constexpr int PART_CLMAX = 16;                 // CTAs per cluster
-constexpr int PART_CTAD = 5 * 2 * PART_KMAX + 4 * PART_KMAX + 4 * PART_CLMAX;
+constexpr int PART_CTAD = 5 * 2 * PART_KMAX + 8 * PART_KMAX + 4 * PART_CLMAX;
 // P = CL * K chunks of L rows (K chunks per CTA)
 bool part_config(int n, int &P, int &L, int &CL, int &K);
 cudaError_t launch_part_setup(int n, int P, int L, int CL, int K, const double *subA, const double *supA,
