@@ -1102,6 +1102,18 @@ __global__ void __launch_bounds__(LF_THREADS) k_lift(const double *X, long xbs, 
 cudaError_t launch_lift(const double *X, long xbs, long xrs, long xcs, long rows, int l,
                         const double *Cm, int ldc, int k, int nbatch, double *out, cudaStream_t s)
 {
+    // 1D layout (a row's l values contiguous): out_b = X_b C_b on the DMMA expand kernel
+    if (xcs == 1 && l <= 64 && l % 2 == 0 && xrs % 2 == 0 && xbs % 2 == 0 && k % 8 == 0 && k <= 64 &&
+        ((uintptr_t)X & 15) == 0 && ((uintptr_t)out & 15) == 0 && !getenv("PR_NO_EXPAND_MMA")) {
+        const int nchunk = xty_chunks(rows, nbatch);
+        Expand ex{out, k, 1, nullptr, 0, 0, X, xbs, Cm, l, k, nbatch, rows, nchunk, (rows + nchunk - 1) / nchunk,
+                  nullptr};
+        ex.Urs = xrs;
+        ex.ers = ldc;
+        ex.ebs = (long)l * ldc;
+        ex.obs = rows * k;
+        return launch_expand(ex, s);
+    }
     size_t smem = ((size_t)l * k + (size_t)LF_ROWS * (l + 1)) * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(k_lift, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1583,15 +1595,16 @@ __global__ void __launch_bounds__(256, 2) k_expand_mma(Expand a)
     long r1 = r0 + a.chunk_rows;
     if (r1 > a.rows) r1 = a.rows;
     const double *Ub = a.U + (long)b * a.Ubs;
-    const double *eb = a.e + (long)b * k * S;
-    const long col0 = (long)b * S;
+    const long urs = a.Urs ? a.Urs : k, ers = a.ers ? a.ers : S;
+    const double *eb = a.e + (long)b * (a.ebs ? a.ebs : (long)k * S);
+    const long col0 = (long)b * (a.obs ? a.obs : S);
     // B fragments: B[kk][n] = e_b[kk, n], kk = 4 ks + tq, n = 8 w + gq (warp w: source tile w)
     const bool act = w < NT;
     double bf[16];
 #pragma unroll
     for (int ks = 0; ks < 16; ++ks) {
         const int kk = 4 * ks + tq;
-        bf[ks] = (act && ks < KS && kk < k) ? eb[(long)kk * S + w * 8 + gq] : 0.0;
+        bf[ks] = (act && ks < KS && kk < k) ? eb[(long)kk * ers + w * 8 + gq] : 0.0;
     }
     const int k2 = k / 2, s2 = S / 2;
     auto stage = [&](long rt, int buf) {
@@ -1602,7 +1615,7 @@ __global__ void __launch_bounds__(256, 2) k_expand_mma(Expand a)
             const int r = e / k2, i = 2 * (e % k2);
             const long row = rt + r;
             const bool ok = row < r1;
-            cpa16_zfill(us + r * SU + i, ok ? Ub + row * k + i : Ub, ok);
+            cpa16_zfill(us + r * SU + i, ok ? Ub + row * urs + i : Ub, ok);
         }
         if (hasb)
             for (int e = threadIdx.x; e < EM_TR * s2; e += 256) {
@@ -1749,7 +1762,8 @@ __global__ void __launch_bounds__(256) k_expand_narrow(Expand a)
 
 cudaError_t launch_expand(const Expand &a, cudaStream_t s)
 {
-    if (a.S < 16 && ((uintptr_t)a.U & 15) == 0 && a.k % 2 == 0) {
+    const bool general = a.Urs || a.ers || a.ebs || a.obs;     // only k_expand_mma takes these
+    if (!general && a.S < 16 && ((uintptr_t)a.U & 15) == 0 && a.k % 2 == 0) {
         size_t smem = (size_t)a.k * a.S * sizeof(double);
         cudaError_t e = cudaFuncSetAttribute(k_expand_narrow, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -1762,7 +1776,8 @@ cudaError_t launch_expand(const Expand &a, cudaStream_t s)
         auto al16 = [](const void *q) { return ((uintptr_t)q & 15) == 0; };
         if (!getenv("PR_NO_EXPAND_MMA") && a.ovs == 1 && (a.base == nullptr || a.bvs == 1) && a.S % 8 == 0 &&
             a.S <= 64 && a.k <= 64 && a.k % 2 == 0 && a.ors % 2 == 0 && (a.base == nullptr || a.brs % 2 == 0) &&
-            a.Ubs % 2 == 0 && al16(a.out) && al16(a.U) && (a.base == nullptr || al16(a.base))) {
+            a.Ubs % 2 == 0 && a.Urs % 2 == 0 && a.obs % 2 == 0 && al16(a.out) && al16(a.U) &&
+            (a.base == nullptr || al16(a.base))) {
             const size_t smem = (size_t)2 * EM_TR *
                                 (xm_stride(a.k) + (a.base ? em_sy(a.S) : 0) + (a.normpart ? em_sy(a.S) : 0)) *
                                 sizeof(double);
@@ -1774,6 +1789,7 @@ cudaError_t launch_expand(const Expand &a, cudaStream_t s)
             return cudaGetLastError();
         }
     }
+    if (general) return cudaErrorInvalidValue;
     if (a.S >= 16 && a.k <= 128) {
         size_t smem = ((size_t)a.k * (EW_ROWS + 2) + (size_t)a.k * EW_SRC + 16 * EW_SRC) * sizeof(double);
         cudaError_t e = cudaFuncSetAttribute(k_expand_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

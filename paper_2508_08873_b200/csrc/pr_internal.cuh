@@ -198,6 +198,9 @@ struct Expand {
     long rows;
     int nchunk; long chunk_rows;
     double *normpart;                 // nullable: (nbatch*S, nchunk)
+    // general strides (k_expand_mma only; 0 = the defaults above): U row stride,
+    // e row / batch strides, per-batch element offset of out (default b*S*ovs)
+    long Urs = 0, ers = 0, ebs = 0, obs = 0;
 };
 cudaError_t launch_expand(const Expand &a, cudaStream_t s);
 // out[v] = sqrt(sum_t part[v*nchunk + t])
