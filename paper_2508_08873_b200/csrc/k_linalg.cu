@@ -1099,6 +1099,10 @@ __global__ void __launch_bounds__(LF_THREADS) k_lift(const double *X, long xbs, 
     }
 }
 
+constexpr int EM_TR = 32;   // rows per stage of k_expand_mma
+template <bool ACM, int KSM>
+__global__ void __launch_bounds__(256, 2) k_expand_mma(Expand a);
+
 cudaError_t launch_lift(const double *X, long xbs, long xrs, long xcs, long rows, int l,
                         const double *Cm, int ldc, int k, int nbatch, double *out, cudaStream_t s)
 {
@@ -1113,6 +1117,25 @@ cudaError_t launch_lift(const double *X, long xbs, long xrs, long xcs, long rows
         ex.ebs = (long)l * ldc;
         ex.obs = rows * k;
         return launch_expand(ex, s);
+    }
+    // 2D layout (a column's rows contiguous): same product with column-major staging
+    if (xrs == 1 && l <= 80 && xcs % 2 == 0 && xbs % 2 == 0 && k % 8 == 0 && k <= 64 &&
+        ((uintptr_t)X & 15) == 0 && ((uintptr_t)out & 15) == 0 && !getenv("PR_NO_EXPAND_MMA")) {
+        const int nchunk = xty_chunks(rows, nbatch);
+        Expand ex{out, k, 1, nullptr, 0, 0, X, xbs, Cm, l, k, nbatch, rows, nchunk, (rows + nchunk - 1) / nchunk,
+                  nullptr};
+        ex.Urs = xcs;
+        ex.ers = ldc;
+        ex.ebs = (long)l * ldc;
+        ex.obs = rows * k;
+        const int KS = (l + 3) / 4;
+        const size_t smem = (size_t)2 * 4 * KS * (EM_TR + 4) * sizeof(double);
+        cudaError_t e = cudaFuncSetAttribute(k_expand_mma<true, 20>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        dim3 grid(nchunk, nbatch);
+        note_launch();
+        k_expand_mma<true, 20><<<grid, 256, smem, s>>>(ex);
+        return cudaGetLastError();
     }
     size_t smem = ((size_t)l * k + (size_t)LF_ROWS * (l + 1)) * sizeof(double);
     cudaError_t e = cudaFuncSetAttribute(k_lift, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1574,20 +1597,21 @@ __global__ void __launch_bounds__(256) k_expand_wide(Expand a)
 // partials) the old rows of each 32-row stage stream through a 2-stage ring of
 // 16-byte cp.async copies, so HBM requests stay in flight while the tensor
 // cores work on the previous stage.  Norm partials as in k_expand_wide.
-constexpr int EM_TR = 32;
-
 __host__ __device__ inline int em_sy(int S) { return S + 4; }   // conflict-light row stride
 
+// ACM: U_b column-major (U_b[row, i] at U[b*Ubs + i*Urs + row], the 2D layout),
+// staged column-major in shared memory
+template <bool ACM, int KSM>
 __global__ void __launch_bounds__(256, 2) k_expand_mma(Expand a)
 {
     extern __shared__ __align__(16) double sm[];
     const int b = blockIdx.y, t = blockIdx.x;
     const int k = a.k, S = a.S;
     const int KS = (k + 3) / 4, NT = S / 8;
-    const int SU = xm_stride(k), SY = em_sy(S);
+    const int SU = xm_stride(k), SY = em_sy(S), SC = EM_TR + 4;
     const bool norms = a.normpart != nullptr;
     const bool hasb = a.base != nullptr;
-    const int ustage = EM_TR * SU, ystage = EM_TR * SY;
+    const int ustage = ACM ? 4 * KS * SC : EM_TR * SU, ystage = EM_TR * SY;
     const int stage_sz = ustage + (hasb ? ystage : 0) + (norms ? ystage : 0);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gq = lane >> 2, tq = lane & 3;
@@ -1600,9 +1624,9 @@ __global__ void __launch_bounds__(256, 2) k_expand_mma(Expand a)
     const long col0 = (long)b * (a.obs ? a.obs : S);
     // B fragments: B[kk][n] = e_b[kk, n], kk = 4 ks + tq, n = 8 w + gq (warp w: source tile w)
     const bool act = w < NT;
-    double bf[16];
+    double bf[KSM];
 #pragma unroll
-    for (int ks = 0; ks < 16; ++ks) {
+    for (int ks = 0; ks < KSM; ++ks) {
         const int kk = 4 * ks + tq;
         bf[ks] = (act && ks < KS && kk < k) ? eb[(long)kk * ers + w * 8 + gq] : 0.0;
     }
@@ -1611,11 +1635,23 @@ __global__ void __launch_bounds__(256, 2) k_expand_mma(Expand a)
         double *us = sm + buf * stage_sz;
         double *bs = us + ustage;
         double *os = bs + (hasb ? ystage : 0);
-        for (int e = threadIdx.x; e < EM_TR * k2; e += 256) {
-            const int r = e / k2, i = 2 * (e % k2);
-            const long row = rt + r;
-            const bool ok = row < r1;
-            cpa16_zfill(us + r * SU + i, ok ? Ub + row * urs + i : Ub, ok);
+        if (ACM) {
+            constexpr int HR = EM_TR / 2;
+            for (int e = threadIdx.x; e < HR * k; e += 256) {
+                const int i = e / HR, r = 2 * (e % HR);
+                const long row = rt + r;
+                const int nb = row + 1 < r1 ? 16 : (row < r1 ? 8 : 0);
+                const double *src = nb ? Ub + (long)i * urs + row : Ub;
+                unsigned sd = (unsigned)__cvta_generic_to_shared(us + i * SC + r);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sd), "l"(src), "r"(nb) : "memory");
+            }
+        } else {
+            for (int e = threadIdx.x; e < EM_TR * k2; e += 256) {
+                const int r = e / k2, i = 2 * (e % k2);
+                const long row = rt + r;
+                const bool ok = row < r1;
+                cpa16_zfill(us + r * SU + i, ok ? Ub + row * urs + i : Ub, ok);
+            }
         }
         if (hasb)
             for (int e = threadIdx.x; e < EM_TR * s2; e += 256) {
@@ -1633,7 +1669,7 @@ __global__ void __launch_bounds__(256, 2) k_expand_mma(Expand a)
             }
         for (int e = threadIdx.x; e < EM_TR * (4 * KS - k); e += 256) {   // k-step padding
             const int r = e / (4 * KS - k), i = k + e % (4 * KS - k);
-            us[r * SU + i] = 0.0;
+            us[ACM ? i * SC + r : r * SU + i] = 0.0;
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
@@ -1664,11 +1700,13 @@ __global__ void __launch_bounds__(256, 2) k_expand_mma(Expand a)
                 acc[mi][1] = bv.y;
             }
 #pragma unroll
-            for (int ks = 0; ks < 16; ++ks) {
+            for (int ks = 0; ks < KSM; ++ks) {
                 if (ks < KS) {
 #pragma unroll
                     for (int mi = 0; mi < MTS; ++mi)
-                        dmma_f64(acc[mi][0], acc[mi][1], us[(mi * 8 + gq) * SU + 4 * ks + tq], bf[ks]);
+                        dmma_f64(acc[mi][0], acc[mi][1],
+                                 ACM ? us[(4 * ks + tq) * SC + mi * 8 + gq] : us[(mi * 8 + gq) * SU + 4 * ks + tq],
+                                 bf[ks]);
                 }
             }
 #pragma unroll
@@ -1781,11 +1819,12 @@ cudaError_t launch_expand(const Expand &a, cudaStream_t s)
             const size_t smem = (size_t)2 * EM_TR *
                                 (xm_stride(a.k) + (a.base ? em_sy(a.S) : 0) + (a.normpart ? em_sy(a.S) : 0)) *
                                 sizeof(double);
-            cudaError_t e = cudaFuncSetAttribute(k_expand_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaError_t e = cudaFuncSetAttribute(k_expand_mma<false, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
             if (e != cudaSuccess) return e;
             dim3 grid(a.nchunk, a.nbatch);
             note_launch();
-            k_expand_mma<<<grid, 256, smem, s>>>(a);
+            k_expand_mma<false, 16><<<grid, 256, smem, s>>>(a);
             return cudaGetLastError();
         }
     }
