@@ -337,12 +337,18 @@ __device__ __forceinline__ void mbar_arrive(unsigned bar)
 template <int CL, int W, int H, int L, bool AFF>
 __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
 {
+    // clock64 probes (PR_PART_PROF) exist only in builds with -DPR_PART_PROBES
+#ifdef PR_PART_PROBES
+    const bool PROBE = a.prof != nullptr;
+#else
+    constexpr bool PROBE = false;
+#endif
     constexpr int VPW = 32 / H;          // vectors per warp
     constexpr int K = W * H;             // chunks per CTA
     constexpr int M = 2 * K;             // local interface unknowns
     constexpr int RSM = AFF ? PART_RSM : 0;
     extern __shared__ __align__(16) double sm[];
-    const long long tk0 = a.prof ? clock64() : 0;
+    const long long tk0 = PROBE ? clock64() : 0;
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.block_rank();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -417,12 +423,12 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
             t = (u == K - 1) ? bt.y : fma(ctad[CTAD_A + 2 * u + 2], bt.x, fma(ctad[CTAD_B + 2 * u + 2], bt.y, zz[(2 * u + 2) * 32]));
         };
         cluster.sync();
-        const long long tk1 = a.prof ? clock64() : 0;
+        const long long tk1 = PROBE ? clock64() : 0;
         const int q = valid ? a.q0 + (int)(v / a.vpi) : a.q0;
         const int src = (AFF && valid) ? (int)(v % a.nsrc) : 0;
         double ca = 0.0, cc = 0.0;     // (b_{c-1}, t_{c+1}) of step j-1: coefficients of V2, W2
         for (int j = 1; j <= a.m; ++j) {
-            long long t0 = a.prof ? clock64() : 0;
+            long long t0 = PROBE ? clock64() : 0;
             double alpha[AFF ? PART_RSM : 1];
             if constexpr (AFF) {
 #pragma unroll
@@ -453,7 +459,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
                 gn = fma(cu[i], gn, S[i]);
                 S[i] = gn;
             }
-            long long t1 = a.prof ? clock64() : 0;
+            long long t1 = PROBE ? clock64() : 0;
             const int p = j & 1;
             if (j >= 2) {              // interface values of step j-1 (formed during this sweep)
                 const int pp = (j - 1) & 1;
@@ -467,14 +473,14 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(ebar + 8 * p);
-            if (a.prof && vl == 0) {
+            if (PROBE && vl == 0) {
                 long long t2 = clock64();
                 unsigned long long *pr = a.prof + (size_t)c * 4;
                 atomicAdd(pr + 0, (unsigned long long)(t1 - t0));
                 atomicAdd(pr + 1, (unsigned long long)(t2 - t1));
             }
         }
-        const long long tl = a.prof ? clock64() : 0;
+        const long long tl = PROBE ? clock64() : 0;
         const int pm = a.m & 1;
         mbar_wait(cbar + 8 * pm, ((a.m - 1) >> 1) & 1);
         double2 e;                                               // (b_m, t_m) of the neighbours
@@ -492,7 +498,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
                 }
             }
         }
-        if (a.prof && threadIdx.x == 0) {
+        if (PROBE && threadIdx.x == 0) {
             const long long tk2 = clock64();
             atomicAdd(a.prof + (size_t)(512 + C) * 4 + 0, (unsigned long long)(tk1 - tk0));
             atomicAdd(a.prof + (size_t)(512 + C) * 4 + 1, (unsigned long long)(tk2 - tl));
@@ -511,9 +517,9 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
             if (lane == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                              :: "r"(gbar + 8 * p), "r"((unsigned)(CL * VPW * sizeof(double2))) : "memory");
-            long long ga = a.prof ? clock64() : 0;
+            long long ga = PROBE ? clock64() : 0;
             mbar_wait(gbar + 8 * p, ((j - 1) >> 1) & 1);
-            long long gb = a.prof ? clock64() : 0;
+            long long gb = PROBE ? clock64() : 0;
             hw += gb - ga;
             const double2 *G = gth + (size_t)p * CL * 32 + vl;
             double b0 = 0.0, b1 = 0.0, t0 = 0.0, t1 = 0.0;
@@ -534,13 +540,13 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
             if (h == 0) coef[p * 32 + vl] = make_double2(Bx, Tx);
             __syncwarp();
             if (lane == 0) mbar_arrive(cbar + 8 * p);
-            if (a.prof) hg += clock64() - gb;
+            if (PROBE) hg += clock64() - gb;
         };
         // chunk end values of step j -> local solve z = M_C^{-1} g_C -> (T_C, B_C) to every CTA
         auto publish = [&](int j) {
             const int p = j & 1;
             mbar_wait(ebar + 8 * p, ((j - 1) >> 1) & 1);
-            long long pa = a.prof ? clock64() : 0;
+            long long pa = PROBE ? clock64() : 0;
             double z[M];
 #pragma unroll
             for (int uu = 0; uu < K; ++uu) {
@@ -566,7 +572,7 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
                 const int r = h * CLH + rr;
                 st_async_v2(rmap[r] + off, Tv, Bv, rmap[CL + r] + 8 * p);
             }
-            long long pb = a.prof ? clock64() : 0;
+            long long pb = PROBE ? clock64() : 0;
             hx1 += pb - pa;
             // band factors, row i: l2, l1, 1/u, u1, u2
 #pragma unroll
@@ -585,20 +591,20 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
                 for (int i = 0; i < M; ++i) zs[((size_t)p * M + i) * 32 + vl] = z[i];
             }
             __syncwarp();
-            if (a.prof) hx2 += clock64() - pb;
+            if (PROBE) hx2 += clock64() - pb;
         };
         unsigned long long tw = 0, tp = 0, tg = 0;
         for (int j = 1; j <= a.m; ++j) {
-            long long t0 = a.prof ? clock64() : 0;
+            long long t0 = PROBE ? clock64() : 0;
             if (j >= 2) gather(j - 1);
-            long long t1 = a.prof ? clock64() : 0;
+            long long t1 = PROBE ? clock64() : 0;
             publish(j);
-            long long t2 = a.prof ? clock64() : 0;
+            long long t2 = PROBE ? clock64() : 0;
             tg += t1 - t0;
             tp += t2 - t1;
         }
         gather(a.m);
-        if (a.prof && lane == 0) {
+        if (PROBE && lane == 0) {
             unsigned long long *pr = a.prof + (size_t)(C * K) * 4;
             atomicAdd(pr + 2, tg);
             atomicAdd(pr + 3, tp);
