@@ -921,6 +921,101 @@ __global__ void __launch_bounds__(128) k_rinv_apply(double *Q, long bs, long rs,
     }
 }
 
+// 2D layout variant (a column's rows contiguous): the 64-row tiles are staged
+// column-major through a 2-stage ring of 16-byte cp.async copies (the next tile
+// loads while the tensor cores work on the current one), and the result goes
+// back through the same shared buffer as 16-byte column stores.
+constexpr int RC_S = RA_ROWS + 4;          // column stride of a staged tile
+
+__global__ void __launch_bounds__(128) k_rinv_apply_cm(double *Q, long bs, long cs, long rows, int l,
+                                                       const double *Rinv, const int *act)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int b = blockIdx.y;
+    if (act[b] != 2) return;
+    const int LP = (l + 15) / 16 * 16;
+    const int ST = LP + 4;
+    double *Rs = sm;                          // LP x ST (row-major R^{-1})
+    double *Ys = sm + (size_t)LP * ST;        // [2][LP][RC_S] column-major tiles
+    const double *Rb = Rinv + (long)b * l * l;
+    for (int e = threadIdx.x; e < LP * LP; e += 128) {
+        const int i = e / LP, j = e % LP;
+        Rs[i * ST + j] = (i < l && j < l) ? Rb[(long)i * l + j] : 0.0;
+    }
+    double *Qb = Q + (long)b * bs;
+    const long c0 = (long)blockIdx.x * TS_CHUNK;
+    const long c1 = min(rows, c0 + TS_CHUNK);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int NT = LP / 8;
+    constexpr int HR = RA_ROWS / 2;
+    auto stage = [&](long r0, int buf) {
+        double *ys = Ys + (size_t)buf * LP * RC_S;
+        for (int e = threadIdx.x; e < LP * HR; e += 128) {
+            const int j = e / HR, r = 2 * (e % HR);
+            const long row = r0 + r;
+            const int nb = (j < l) ? (row + 1 < c1 ? 16 : (row < c1 ? 8 : 0)) : 0;
+            const double *src = nb ? Qb + row + (long)j * cs : Qb;
+            unsigned sd = (unsigned)__cvta_generic_to_shared(ys + j * RC_S + r);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sd), "l"(src), "r"(nb) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    const int ntiles = (int)((c1 - c0 + RA_ROWS - 1) / RA_ROWS);
+    if (ntiles > 0) stage(c0, 0);
+    for (int it = 0; it < ntiles; ++it) {
+        const long r0 = c0 + (long)it * RA_ROWS;
+        if (it + 1 < ntiles) {
+            stage(r0 + RA_ROWS, (it + 1) & 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+        double *ys = Ys + (size_t)(it & 1) * LP * RC_S;
+        double acc[2][16][2];
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < 16; ++nj) acc[mi][nj][0] = acc[mi][nj][1] = 0.0;
+        for (int k0 = 0; k0 < LP; k0 += 4) {
+            double af[2];
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi) af[mi] = ys[(k0 + tq) * RC_S + w * 16 + mi * 8 + gq];
+#pragma unroll
+            for (int nj = 0; nj < 16; ++nj) {
+                if (nj < NT) {
+                    const double bf = Rs[(k0 + tq) * ST + nj * 8 + gq];
+#pragma unroll
+                    for (int mi = 0; mi < 2; ++mi) dmma_f64(acc[mi][nj][0], acc[mi][nj][1], af[mi], bf);
+                }
+            }
+        }
+        __syncthreads();                      // every warp has read the tile
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int nj = 0; nj < 16; ++nj) {
+                if (nj < NT) {
+                    const int r = w * 16 + mi * 8 + gq, j = nj * 8 + 2 * tq;
+                    ys[j * RC_S + r] = acc[mi][nj][0];
+                    ys[(j + 1) * RC_S + r] = acc[mi][nj][1];
+                }
+            }
+        __syncthreads();
+        for (int e = threadIdx.x; e < l * HR; e += 128) {
+            const int j = e / HR, r = 2 * (e % HR);
+            const long row = r0 + r;
+            if (row + 1 < c1) {
+                *reinterpret_cast<double2 *>(Qb + row + (long)j * cs) = *reinterpret_cast<const double2 *>(ys + j * RC_S + r);
+            } else if (row < c1) {
+                Qb[row + (long)j * cs] = ys[j * RC_S + r];
+            }
+        }
+        __syncthreads();                      // the buffer is refilled two tiles later
+    }
+}
+
 cudaError_t launch_rinv_apply(double *Q, long bs, long rs, long cs, long rows, int l, int nbatch,
                               const double *Rinv, const int *act, cudaStream_t s)
 {
@@ -930,7 +1025,13 @@ cudaError_t launch_rinv_apply(double *Q, long bs, long rs, long cs, long rows, i
     const bool cm = (cs != 1);
     dim3 grid((unsigned)((rows + TS_CHUNK - 1) / TS_CHUNK), nbatch);
     cudaError_t e;
-    if (cm) {
+    if (cm && rs == 1 && cs % 2 == 0 && bs % 2 == 0 && ((uintptr_t)Q & 15) == 0 && !getenv("PR_NO_RINV_CM")) {
+        const size_t smem2 = ((size_t)LP * (LP + 4) + (size_t)2 * LP * RC_S) * sizeof(double);
+        e = cudaFuncSetAttribute(k_rinv_apply_cm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+        if (e != cudaSuccess) return e;
+        note_launch();
+        k_rinv_apply_cm<<<grid, 128, smem2, s>>>(Q, bs, cs, rows, l, Rinv, act);
+    } else if (cm) {
         e = cudaFuncSetAttribute(k_rinv_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         note_launch();
