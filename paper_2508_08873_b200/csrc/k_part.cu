@@ -416,11 +416,15 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
             S[i] = (a.in && valid && s0 + i < a.n) ? a.in[(long)(s0 + i) * a.ld_in + v] : 0.0;
         // (b_{c-1}, t_{c+1}) of a step from the CTA's (B_{C-1}, T_{C+1}) and local solution
         const double *zsb = reinterpret_cast<const double *>(rmap + 2 * CL);
+        // this chunk's super-spike entries, held in registers for the hand-off
+        const double sA1 = (u == 0) ? 0.0 : ctad[CTAD_A + 2 * u - 1], sB1 = (u == 0) ? 0.0 : ctad[CTAD_B + 2 * u - 1];
+        const double sA2 = (u == K - 1) ? 0.0 : ctad[CTAD_A + 2 * u + 2];
+        const double sB2 = (u == K - 1) ? 0.0 : ctad[CTAD_B + 2 * u + 2];
         auto neighbours = [&](int pp, double &b, double &t) {
             const double2 bt = coef[pp * 32 + vl];
             const double *zz = zsb + (size_t)pp * M * 32 + vl;
-            b = (u == 0) ? bt.x : fma(ctad[CTAD_A + 2 * u - 1], bt.x, fma(ctad[CTAD_B + 2 * u - 1], bt.y, zz[(2 * u - 1) * 32]));
-            t = (u == K - 1) ? bt.y : fma(ctad[CTAD_A + 2 * u + 2], bt.x, fma(ctad[CTAD_B + 2 * u + 2], bt.y, zz[(2 * u + 2) * 32]));
+            b = (u == 0) ? bt.x : fma(sA1, bt.x, fma(sB1, bt.y, zz[(2 * u - 1) * 32]));
+            t = (u == K - 1) ? bt.y : fma(sA2, bt.x, fma(sB2, bt.y, zz[(2 * u + 2) * 32]));
         };
         cluster.sync();
         const long long tk1 = PROBE ? clock64() : 0;
