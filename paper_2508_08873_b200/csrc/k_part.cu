@@ -1,36 +1,37 @@
-// k_part.cu -- K1P: partitioned 1D backward-Euler stepper for small batches.
+// k_part.cu -- K1P: the cluster-partitioned 1D backward-Euler stepper (used
+// for every 1D operator with 64 <= n <= 16384).
 //
-// The fused stepper (k_tridiag.cu) runs one vector per thread, so a batch of
-// B vectors keeps only B/32 warps busy; with few vectors (Parareal fine solves
-// of C1/C2: 16-64 vectors) each warp's row recurrence is latency-bound.  Here
-// every vector's rows are split into P = CL * W chunks of L rows (one warp per
-// chunk, W warps per CTA, CL CTAs per thread-block cluster, rows >= n are
-// decoupled identity rows) and each chunk's state lives in REGISTERS for all m
-// steps (L <= 64 doubles per lane).  One step (I + dt A) x = r by
-// the partition method:
+// The fused stepper (k_tridiag.cu) runs one vector per thread and streams the
+// state through HBM once per step.  Here every vector's rows are split into
+// P = CL * K chunks of L rows (rows >= n are decoupled identity rows): a
+// thread-block cluster of CL CTAs owns a group of vectors, each CTA K chunks,
+// each compute warp one chunk (H = 1, 32 vectors) or two adjacent chunks in its
+// half-warps (H = 2, 16 vectors), and each lane keeps its chunk's L <= 64 state
+// values in REGISTERS for all m steps.  One step (I + dt A) x = r
+// by the partition method (reading R-PART):
 //   x_c = T_c^{-1} r_c + V_c b_{c-1} + W_c t_{c+1}
 //   V_c = T_c^{-1}(-a e_1), W_c = T_c^{-1}(-c e_L)     (spikes, fixed)
 //   (t_c, b_c) = first / last unknown of chunk c, from the 2P x 2P interface
 //   system z - V b - W t = g (rows at the chunk ends): a banded M-matrix.
-// The interface system is solved in two levels: the W chunks of a CTA form a
-// super-chunk whose local 2W x 2W system is inverted once (its inverse, and the
-// super-chunk spikes alpha = Minv_C e_left, beta = Minv_C e_right), and the
-// CL super-chunks form a 2CL x 2CL system of the same shape, inverted once; a
-// CTA keeps the two rows of that inverse giving its neighbours' boundary
-// values.  All factorizations use row-sum (GTH-type) elimination of the
-// M-matrices with row sums propagated exactly (reading R-ACC), so the inverses
-// are entrywise accurate and non-negative.
+// The interface system is solved in two levels: the K chunks of a CTA form a
+// super-chunk with a local 2K x 2K system (band factors, two rows of its
+// inverse, super-chunk spikes alpha = M_C^{-1} e_left, beta = M_C^{-1} e_right),
+// and the CL super-chunks form a 2CL x 2CL system of the same shape whose
+// inverse rows for each CTA's neighbours are stored.  All factorizations use
+// row-sum (GTH-type) elimination of the M-matrices with row sums propagated
+// exactly (reading R-ACC), so the inverses are entrywise accurate and
+// non-negative.
 //
 // Pipelining.  Write the chunk solution of step j as
 //   x_j = S_j + a_j V2 + c_j W2 + b_j V + t_j W,   V2 = T_c^{-1} V, W2 = T_c^{-1} W,
 // with (a_j, c_j) = (b_{j-1}, t_{j-1}).  Then S_{j+1} = T_c^{-1}(S_j + a_j V2 + c_j W2
 // + dt f_{j+1}) needs only the PREVIOUS step's interface values, so the sweep of
-// step j+1 runs while the interface exchange of step j is in flight: after its
-// sweep a CTA combines its chunks' end values (shared memory), sends its
-// super-chunk's two reduced values to every CTA of the cluster with st.async
-// (distributed shared memory, completion counted on the receiver's mbarrier),
-// and only after the next sweep waits for the gathered values.  HBM is touched
-// only to read the input and write the result.
+// step j+1 runs while the interface exchange of step j is in flight.  A
+// dedicated interface warp per CTA forms the super-chunk values, sends them to
+// every CTA of the cluster with st.async (distributed shared memory, completion
+// counted on the receiver's mbarrier), gathers, and hands each chunk its
+// neighbours' values through shared memory + mbarriers.  HBM is touched only
+// to read the input and write the result.
 #include <cooperative_groups.h>
 #include <stdio.h>
 #include <stdlib.h>
