@@ -23,12 +23,30 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every .cu to an object in parallel (one nvcc per file), then link
+    the shared library.  PR_EXTRA_NVCC_FLAGS adds flags (e.g. -DPR_PART_PROBES)."""
     if force or _stale():
         nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-        cmd = [nvcc] + NVCC_FLAGS + ["-o", SO + ".tmp"] + SRC
+        extra = os.environ.get("PR_EXTRA_NVCC_FLAGS", "").split()
+        cflags = [f for f in NVCC_FLAGS if f != "-shared"] + extra
+        objdir = os.path.join(HERE, "build_obj")
+        os.makedirs(objdir, exist_ok=True)
+        objs, procs = [], []
+        for src in SRC:
+            obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+            cmd = [nvcc] + cflags + ["-c", "-o", obj, src]
+            if verbose:
+                print(" ".join(cmd))
+            procs.append((subprocess.Popen(cmd, cwd=os.path.join(HERE, "csrc")), cmd))
+            objs.append(obj)
+        failed = [cmd for p, cmd in procs if p.wait() != 0]
+        if failed:
+            raise subprocess.CalledProcessError(1, failed[0])
+        cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+               "-o", SO + ".tmp"] + objs
         if verbose:
             print(" ".join(cmd))
-        subprocess.check_call(cmd, cwd=os.path.join(HERE, "csrc"))
+        subprocess.check_call(cmd)
         os.replace(SO + ".tmp", SO)
     return SO
 
