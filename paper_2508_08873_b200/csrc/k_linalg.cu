@@ -165,11 +165,13 @@ __device__ __forceinline__ void cpa8_zfill(double *smem, const double *gmem, boo
 
 __host__ __device__ inline int xm_stride(int w) { return ((w + 15) / 16) * 16 + 4; }
 
-// NQ n-tiles per warp: 16 / NQ warps (NQ = 1: 512 threads, one tile-column each)
-template <bool CM, int MTM, int NQ>
-__global__ void __launch_bounds__(512 / NQ) k_xty_mma(XtY p)
+// Warp layout: NGR = 16 / NQ groups of MS warps; warp (group wn, member ms)
+// owns tile-columns wn, wn + NGR, ... (NQ of them) and a contiguous 1/MS share
+// of the tile-rows (at most MTM).
+template <bool CM, int MTM, int NQ, int MS>
+__global__ void __launch_bounds__(512 / NQ * MS) k_xty_mma(XtY p)
 {
-    constexpr int NWARP = 16 / NQ, NTH = 32 * NWARP;
+    constexpr int NGR = 16 / NQ, NWARP = NGR * MS, NTH = 32 * NWARP;
     extern __shared__ __align__(16) double sm[];
     const int b = blockIdx.y, t = blockIdx.x;
     if (p.skip && p.skip[b] == 2) return;
@@ -187,8 +189,13 @@ __global__ void __launch_bounds__(512 / NQ) k_xty_mma(XtY p)
     const double *Xb = p.X + (long)b * p.xbs;
     const double *Yb = p.Y + (long)b * p.ybs;
     const double *Y2b = p.Y2 ? p.Y2 + (long)b * p.ybs : nullptr;
+    // a Gram matrix (Y == X) stages its operand once
+    const bool same = (p.X == p.Y) && (p.xbs == p.ybs) && (p.xrs == p.yrs) && (p.xcs == p.ycs) && (p.a == p.c) &&
+                      p.c2 == 0;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gq = lane >> 2, tq = lane & 3;
+    const int wn = w / MS, ms = w % MS;
+    const int mtm = (MT + MS - 1) / MS, m0 = ms * mtm;      // this warp's tile-rows m0 + i, i < mtm
 
     // column-major tiles (2D layout): rows of a column are contiguous, so the
     // tile is staged in 16-byte pieces (2 rows) when the strides allow it
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(512 / NQ) k_xty_mma(XtY p)
                 unsigned sd = (unsigned)__cvta_generic_to_shared(xs + i * SC + r);
                 asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sd), "l"(src), "r"(nb) : "memory");
             }
-            for (int e = threadIdx.x; e < HR * cy; e += NTH) {
+            for (int e = threadIdx.x; e < (same ? 0 : HR * cy); e += NTH) {
                 const int j = e / HR, r = 2 * (e % HR);
                 const long row = rt + r;
                 const int nb = (j < ctot) ? (row + 1 < r1 ? 16 : (row < r1 ? 8 : 0)) : 0;
@@ -225,7 +232,7 @@ __global__ void __launch_bounds__(512 / NQ) k_xty_mma(XtY p)
             const bool ok = row < r1 && i < p.a;
             cpa8_zfill(xs + (CM ? i * SC + r : r * SXr + i), ok ? Xb + row * p.xrs + (long)i * p.xcs : Xb, ok);
         }
-        for (int e = threadIdx.x; e < XM_TR * cy; e += NTH) {
+        for (int e = threadIdx.x; e < (same ? 0 : XM_TR * cy); e += NTH) {
             int r, j;
             if (CM) { j = e / XM_TR; r = e % XM_TR; } else { r = e / cy; j = e % cy; }
             const long row = rt + r;
@@ -255,22 +262,24 @@ __global__ void __launch_bounds__(512 / NQ) k_xty_mma(XtY p)
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
         __syncthreads();
-        const double *xs = Xs + (it & 1) * xsz, *ys = Ys + (it & 1) * ysz;
+        const double *xs = Xs + (it & 1) * xsz, *ys = same ? xs : Ys + (it & 1) * ysz;
 #pragma unroll
         for (int ks = 0; ks < XM_TR / 4; ++ks) {
             const int k = ks * 4 + tq;
             double af[MTM];
 #pragma unroll
-            for (int mi = 0; mi < MTM; ++mi)
-                af[mi] = (mi < MT) ? (CM ? xs[(mi * 8 + gq) * SC + k] : xs[k * SXr + mi * 8 + gq]) : 0.0;
+            for (int i = 0; i < MTM; ++i) {
+                const int mi = m0 + i;
+                af[i] = (i < mtm && mi < MT) ? (CM ? xs[(mi * 8 + gq) * SC + k] : xs[k * SXr + mi * 8 + gq]) : 0.0;
+            }
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
-                const int nj = w + NWARP * q;
+                const int nj = wn + NGR * q;
                 if (nj < NT) {
                     const double bf = CM ? ys[(nj * 8 + gq) * SC + k] : ys[k * SYr + nj * 8 + gq];
 #pragma unroll
-                    for (int mi = 0; mi < MTM; ++mi)
-                        if (mi < MT) dmma_f64(acc[q][mi][0], acc[q][mi][1], af[mi], bf);
+                    for (int i = 0; i < MTM; ++i)
+                        if (i < mtm && m0 + i < MT) dmma_f64(acc[q][i][0], acc[q][i][1], af[i], bf);
                 }
             }
         }
@@ -279,15 +288,16 @@ __global__ void __launch_bounds__(512 / NQ) k_xty_mma(XtY p)
     double *out = p.part + ((long)b * p.nchunk + t) * p.a * ctot;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-        const int nj = w + NWARP * q;
+        const int nj = wn + NGR * q;
         if (nj >= NT) continue;
 #pragma unroll
-        for (int mi = 0; mi < MTM; ++mi) {
-            if (mi >= MT) continue;
+        for (int ii = 0; ii < MTM; ++ii) {
+            const int mi = m0 + ii;
+            if (ii >= mtm || mi >= MT) continue;
             const int i = mi * 8 + gq, j = nj * 8 + 2 * tq;
             if (i < p.a) {
-                if (j < ctot) out[(long)i * ctot + j] = acc[q][mi][0];
-                if (j + 1 < ctot) out[(long)i * ctot + j + 1] = acc[q][mi][1];
+                if (j < ctot) out[(long)i * ctot + j] = acc[q][ii][0];
+                if (j + 1 < ctot) out[(long)i * ctot + j + 1] = acc[q][ii][1];
             }
         }
     }
@@ -325,6 +335,8 @@ __global__ void __launch_bounds__(XM_THREADS) k_xty_rm(XtY p)
     const double *Xb = p.X + (long)b * p.xbs;
     const double *Yb = p.Y + (long)b * p.ybs;
     const double *Y2b = p.Y2 ? p.Y2 + (long)b * p.ybs : nullptr;
+    // a Gram matrix (Y == X) stages its operand once
+    const bool same = !DIFF && (p.X == p.Y) && (p.xbs == p.ybs) && (p.xrs == p.yrs) && (p.a == p.c) && p.c2 == 0;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int gq = lane >> 2, tq = lane & 3;
     const int ax2 = (p.a + 1) / 2, cy2 = (ctot + 1) / 2;   // 16-byte pieces per row (a, c even)
@@ -337,7 +349,7 @@ __global__ void __launch_bounds__(XM_THREADS) k_xty_rm(XtY p)
             const bool ok = row < r1;
             cpa16_zfill(xs + r * SX + i, ok ? Xb + row * p.xrs + i : Xb, ok);
         }
-        for (int e = threadIdx.x; e < XR_TR * cy2; e += XM_THREADS) {
+        for (int e = threadIdx.x; e < (same ? 0 : XR_TR * cy2); e += XM_THREADS) {
             const int r = e / cy2, j = 2 * (e % cy2);
             const long row = rt + r;
             const bool ok = row < r1;
@@ -369,7 +381,7 @@ __global__ void __launch_bounds__(XM_THREADS) k_xty_rm(XtY p)
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
         __syncthreads();
-        const double *xs = Xs + (it & 1) * xsz, *ys = Ys + (it & 1) * nY * ysz;
+        const double *xs = Xs + (it & 1) * xsz, *ys = same ? xs : Ys + (it & 1) * nY * ysz;
 #pragma unroll
         for (int ks = 0; ks < XR_TR / 4; ++ks) {
             const int k = ks * 4 + tq;
@@ -527,9 +539,11 @@ cudaError_t launch_xty(const XtY &p, cudaStream_t s)
             return cudaSuccess;
         };
         // MT <= 8 (a <= 64): 8 warps with 2 tile-columns each and half the
-        // accumulators (two CTAs per SM); else 16 warps with one tile-column each
-        if (cm) e = (MT <= 8) ? go(k_xty_mma<true, 8, 2>, 256) : go(k_xty_mma<true, 16, 1>, 512);
-        else e = (MT <= 8) ? go(k_xty_mma<false, 8, 2>, 256) : go(k_xty_mma<false, 16, 1>, 512);
+        // accumulators (two CTAs per SM)
+        // MT <= 16, NT <= 16 otherwise: 16 warps as 8 groups of 2 (each warp two
+        // tile-columns and half the tile-rows: every warp busy for a = c = 74)
+        if (cm) e = (MT <= 8) ? go(k_xty_mma<true, 8, 2, 1>, 256) : go(k_xty_mma<true, 8, 2, 2>, 512);
+        else e = (MT <= 8) ? go(k_xty_mma<false, 8, 2, 1>, 256) : go(k_xty_mma<false, 8, 2, 2>, 512);
         if (e != cudaSuccess) return e;
         return cudaGetLastError();
     }
