@@ -846,9 +846,116 @@ __global__ void __launch_bounds__(128) k_trsm(double *Q, long bs, long rs, long 
     }
 }
 
+// Blocked substitution on the FP64 tensor cores: Q <- Q R^{-1} for the shifted
+// passes (act == 1), row-wise backward stable like k_trsm.  A warp owns 16 rows
+// of a 64-row tile; per 16-column block B it first subtracts the solved
+// columns, Y[:, B] -= X[:, <B] R[<B, B] (DMMA, warp-local), then its lanes 0..15
+// solve the 16 x 16 triangular block of their row by substitution.
+constexpr int TK_TB = 16;
+constexpr int TK_ROWS = 64;                // rows per tile (4 warps x 16)
+
+__global__ void __launch_bounds__(128) k_trsm_dmma(double *Q, long bs, long rs, long cs, long rows, int l,
+                                                   const double *R, const int *act)
+{
+    extern __shared__ __align__(16) double sm[];
+    const int b = blockIdx.y;
+    if (act[b] != 1) return;
+    const int LP = (l + TK_TB - 1) / TK_TB * TK_TB;
+    const int ST = LP + 4;                    // stride = 4 (mod 16): conflict-free fragments
+    double *Rs = sm;                          // LP x ST: -R off the diagonal, 1/R_jj on it, identity padding
+    double *Ys = sm + (size_t)LP * ST;        // TK_ROWS x ST
+    const double *Rb = R + (long)b * l * l;
+    for (int e = threadIdx.x; e < LP * LP; e += 128) {
+        const int i = e / LP, j = e % LP;
+        double v = 0.0;
+        if (i < l && j < l) v = (i == j) ? 1.0 / Rb[(long)i * l + j] : -Rb[(long)i * l + j];
+        else if (i == j) v = 1.0;
+        Rs[i * ST + j] = v;
+    }
+    double *Qb = Q + (long)b * bs;
+    const long c0 = (long)blockIdx.x * TS_CHUNK;
+    const long c1 = min(rows, c0 + TS_CHUNK);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const bool cmaj = (cs != 1);
+    for (long r0 = c0; r0 < c1; r0 += TK_ROWS) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < TK_ROWS * LP; e += 128) {
+            int r, j;
+            if (cmaj) { j = e / TK_ROWS; r = e % TK_ROWS; } else { r = e / LP; j = e % LP; }
+            const long row = r0 + r;
+            Ys[r * ST + j] = (row < c1 && j < l) ? Qb[row * rs + (long)j * cs] : 0.0;
+        }
+        __syncthreads();
+        double *yw = Ys + (size_t)(w * 16) * ST;       // this warp's 16 rows
+        for (int B = 0; B < LP; B += TK_TB) {
+            if (B > 0) {
+                double acc[2][2][2];
+#pragma unroll
+                for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+                    for (int nj = 0; nj < 2; ++nj) {
+                        const double2 c = *reinterpret_cast<const double2 *>(yw + (mi * 8 + gq) * ST + B + nj * 8 + 2 * tq);
+                        acc[mi][nj][0] = c.x;
+                        acc[mi][nj][1] = c.y;
+                    }
+                for (int k0 = 0; k0 < B; k0 += 4) {
+                    double af[2], bf[2];
+#pragma unroll
+                    for (int mi = 0; mi < 2; ++mi) af[mi] = yw[(mi * 8 + gq) * ST + k0 + tq];
+#pragma unroll
+                    for (int nj = 0; nj < 2; ++nj) bf[nj] = Rs[(k0 + tq) * ST + B + nj * 8 + gq];
+#pragma unroll
+                    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+                        for (int nj = 0; nj < 2; ++nj) dmma_f64(acc[mi][nj][0], acc[mi][nj][1], af[mi], bf[nj]);
+                }
+#pragma unroll
+                for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+                    for (int nj = 0; nj < 2; ++nj)
+                        *reinterpret_cast<double2 *>(yw + (mi * 8 + gq) * ST + B + nj * 8 + 2 * tq) =
+                            make_double2(acc[mi][nj][0], acc[mi][nj][1]);
+            }
+            __syncwarp();
+            if (lane < 16) {                       // in-block substitution, one row per lane
+                double *yr = yw + lane * ST + B;
+                double x[TK_TB];
+#pragma unroll
+                for (int t = 0; t < TK_TB; ++t) {
+                    double y = yr[t];
+#pragma unroll
+                    for (int u = 0; u < t; ++u) y = fma(x[u], Rs[(B + u) * ST + B + t], y);   // Rs = -R
+                    x[t] = y * Rs[(B + t) * ST + B + t];
+                }
+#pragma unroll
+                for (int t = 0; t < TK_TB; ++t) yr[t] = x[t];
+            }
+            __syncwarp();
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < TK_ROWS * LP; e += 128) {
+            int r, j;
+            if (cmaj) { j = e / TK_ROWS; r = e % TK_ROWS; } else { r = e / LP; j = e % LP; }
+            const long row = r0 + r;
+            if (row < c1 && j < l) Qb[row * rs + (long)j * cs] = Ys[r * ST + j];
+        }
+    }
+}
+
 cudaError_t launch_trsm(double *Q, long bs, long rs, long cs, long rows, int l, int nbatch,
                         const double *R, const int *act, cudaStream_t s)
 {
+    if (l <= 128 && !getenv("PR_NO_TRSM_DMMA")) {
+        const int LPd = (l + TK_TB - 1) / TK_TB * TK_TB;
+        const size_t smem = ((size_t)LPd + TK_ROWS) * (LPd + 4) * sizeof(double);
+        cudaError_t e = cudaFuncSetAttribute(k_trsm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        dim3 grid((unsigned)((rows + TS_CHUNK - 1) / TS_CHUNK), nbatch);
+        note_launch();
+        k_trsm_dmma<<<grid, 128, smem, s>>>(Q, bs, rs, cs, rows, l, R, act);
+        return cudaGetLastError();
+    }
     const int LP = (l + TB - 1) / TB * TB;
     const int nt = (LP <= 96) ? 128 : 64;
     size_t smem = ((size_t)LP * LP + (size_t)nt * (LP + 1)) * sizeof(double);
