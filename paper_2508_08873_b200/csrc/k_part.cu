@@ -658,6 +658,7 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
 {
     constexpr size_t smem = part_smem_t<CL, W, H, L, AFF>();
     static_assert(smem <= 227 * 1024, "partitioned stepper shared memory");
+    // function attributes are set once per process (one process drives one GPU)
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, AFF>,
