@@ -63,6 +63,12 @@ typedef enum {
 const char *pr_last_error(void);
 int pr_version(void);
 
+/* Re-read the PR_* diagnostic environment switches (DESIGN.md "Diagnostic
+ * switches"; they select alternate kernels or print probes).  The library reads
+ * them once, at its first call; a test that changes them calls this.  Host
+ * only, never fails. */
+pr_status pr_reload_env(void);
+
 /* Instrumentation.  pr_profile(1) brackets every fine-propagation launch
  * (1D: the K1 stepper kernel; 2D: the K2 GEMM passes of one call) with CUDA
  * events on its stream.  pr_counters (host; synchronises on the recorded
@@ -164,8 +170,9 @@ pr_status pr_gaussian_sketch(pr_op op, int first_interval, int n_intervals, int 
 /* ------------------------------------------------------------ coarse solvers */
 
 /* Randomized SVD of F_q' for q = first_interval .. first_interval
- * + n_local - 1 of N_total intervals, rank k, oversampling p (l = k + p <= 128,
- * l <= rows):
+ * + n_local - 1 of N_total intervals, rank k, oversampling p (l = k + p <= 112,
+ * l <= rows; 112 because the one-CTA Jacobi SVD of step 5 keeps two l x l
+ * fp64 matrices in shared memory, 2 * 112^2 * 8 B = 196 KB of the 227 KB):
  *   1. Y = F_q' Omega_q, Omega generated in the stepper (pr_gaussian_sketch)
  *   2. W = orth(Y)      iterated shifted CholeskyQR (reading Z7)
  *   3. Z = F_q'^* W
@@ -177,7 +184,7 @@ pr_status pr_gaussian_sketch(pr_op op, int first_interval, int n_intervals, int 
  * intervals are sharded.  The handle also precomputes the reduced sweep
  * matrices C_q = Sigma_q V_q^T U_{q-1}.
  * Asynchronous; errors detected on the device (no convergence) are reported by
- * pr_coarse_info.  Errors: EINVAL, EDIM (l > 128 or l > rows), EOOM. */
+ * pr_coarse_info.  Errors: EINVAL, EDIM (l > 112 or l > rows), EOOM. */
 pr_status pr_build_coarse(pr_op op, int N_total, int first_interval, int n_local, int m,
                           int k, int p, uint64_t seed, void *stream, pr_coarse *out);
 

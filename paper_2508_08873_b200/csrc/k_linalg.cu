@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(32 * XS_WARPS) k_xty_skinny(XtY p)
 static bool xty_rm_ok(const XtY &p, int ctot)
 {
     auto al16 = [](const void *q) { return ((uintptr_t)q & 15) == 0; };
-    if (getenv("PR_NO_XTY_RM")) return false;
+    if (flags().no_xty_rm) return false;
     if (p.xcs != 1 || p.ycs != 1 || p.a > 64 || ctot > 128 || p.a % 2 || ctot % 2) return false;
     if (p.diff ? (p.c % 2) : (p.c % 2 || p.c2 % 2)) return false;
     if (p.xrs % 2 || p.yrs % 2 || p.xbs % 2 || p.ybs % 2) return false;
@@ -946,7 +946,7 @@ __global__ void __launch_bounds__(128) k_trsm_dmma(double *Q, long bs, long rs, 
 cudaError_t launch_trsm(double *Q, long bs, long rs, long cs, long rows, int l, int nbatch,
                         const double *R, const int *act, cudaStream_t s)
 {
-    if (l <= 128 && !getenv("PR_NO_TRSM_DMMA")) {
+    if (l <= 128 && !flags().no_trsm_dmma) {
         const int LPd = (l + TK_TB - 1) / TK_TB * TK_TB;
         const size_t smem = ((size_t)LPd + TK_ROWS) * (LPd + 4) * sizeof(double);
         cudaError_t e = cudaFuncSetAttribute(k_trsm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1146,7 +1146,7 @@ cudaError_t launch_rinv_apply(double *Q, long bs, long rs, long cs, long rows, i
     const bool cm = (cs != 1);
     dim3 grid((unsigned)((rows + TS_CHUNK - 1) / TS_CHUNK), nbatch);
     cudaError_t e;
-    if (cm && rs == 1 && cs % 2 == 0 && bs % 2 == 0 && ((uintptr_t)Q & 15) == 0 && !getenv("PR_NO_RINV_CM")) {
+    if (cm && rs == 1 && cs % 2 == 0 && bs % 2 == 0 && ((uintptr_t)Q & 15) == 0 && !flags().no_rinv_cm) {
         const size_t smem2 = ((size_t)LP * (LP + 4) + (size_t)2 * LP * RC_S) * sizeof(double);
         e = cudaFuncSetAttribute(k_rinv_apply_cm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
         if (e != cudaSuccess) return e;
@@ -1330,7 +1330,7 @@ cudaError_t launch_lift(const double *X, long xbs, long xrs, long xcs, long rows
 {
     // 1D layout (a row's l values contiguous): out_b = X_b C_b on the DMMA expand kernel
     if (xcs == 1 && l <= 64 && l % 2 == 0 && xrs % 2 == 0 && xbs % 2 == 0 && k % 8 == 0 && k <= 64 &&
-        ((uintptr_t)X & 15) == 0 && ((uintptr_t)out & 15) == 0 && !getenv("PR_NO_EXPAND_MMA")) {
+        ((uintptr_t)X & 15) == 0 && ((uintptr_t)out & 15) == 0 && !flags().no_expand_mma) {
         const int nchunk = xty_chunks(rows, nbatch);
         Expand ex{out, k, 1, nullptr, 0, 0, X, xbs, Cm, l, k, nbatch, rows, nchunk, (rows + nchunk - 1) / nchunk,
                   nullptr};
@@ -1342,7 +1342,7 @@ cudaError_t launch_lift(const double *X, long xbs, long xrs, long xcs, long rows
     }
     // 2D layout (a column's rows contiguous): same product with column-major staging
     if (xrs == 1 && l <= 80 && xcs % 2 == 0 && xbs % 2 == 0 && k % 8 == 0 && k <= 64 &&
-        ((uintptr_t)X & 15) == 0 && ((uintptr_t)out & 15) == 0 && !getenv("PR_NO_EXPAND_MMA")) {
+        ((uintptr_t)X & 15) == 0 && ((uintptr_t)out & 15) == 0 && !flags().no_expand_mma) {
         const int nchunk = xty_chunks(rows, nbatch);
         Expand ex{out, k, 1, nullptr, 0, 0, X, xbs, Cm, l, k, nbatch, rows, nchunk, (rows + nchunk - 1) / nchunk,
                   nullptr};
@@ -1523,7 +1523,7 @@ cudaError_t launch_sweep(const double *C, const double *d, int N, int k, int S, 
     const size_t kS = (size_t)k * S, kk = (size_t)k * k;
     const size_t smA = (2 * kS + 3 * kk) * sizeof(double);
     if (NB >= 4 && smA <= 200 * 1024) {
-        double *tmp = (double *)ws_alloc((size_t)NB * (2 * kS + kk) * sizeof(double));
+        double *tmp = (double *)ws_alloc((size_t)NB * (2 * kS + kk) * sizeof(double), s);
         if (tmp) {
             double *fend = tmp, *E = tmp + NB * kS, *Phi = tmp + 2 * NB * kS;
             const size_t smB = (2 * kS + kk) * sizeof(double);
@@ -1531,7 +1531,7 @@ cudaError_t launch_sweep(const double *C, const double *d, int N, int k, int S, 
             er = cudaFuncSetAttribute(k_sweep_A, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
             if (er == cudaSuccess) er = cudaFuncSetAttribute(k_sweep_B, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
             if (er == cudaSuccess) er = cudaFuncSetAttribute(k_sweep_C, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
-            if (er != cudaSuccess) { ws_free(tmp); return er; }
+            if (er != cudaSuccess) { ws_free(tmp, s); return er; }
             const int th = (kS > 512 || kk > 512) ? 1024 : 256;
             note_launch();
             k_sweep_A<<<NB, th, smA, s>>>(C, d, N, k, S, fend, Phi);
@@ -1540,7 +1540,7 @@ cudaError_t launch_sweep(const double *C, const double *d, int N, int k, int S, 
             note_launch();
             k_sweep_C<<<NB, th, smB, s>>>(C, d, E, N, k, S, e);
             er = cudaGetLastError();
-            ws_free(tmp);                    // stream-ordered reuse
+            ws_free(tmp, s);                 // stream-ordered reuse
             return er;
         }
     }
@@ -2034,7 +2034,7 @@ cudaError_t launch_expand(const Expand &a, cudaStream_t s)
     }
     {
         auto al16 = [](const void *q) { return ((uintptr_t)q & 15) == 0; };
-        if (!getenv("PR_NO_EXPAND_MMA") && a.ovs == 1 && (a.base == nullptr || a.bvs == 1) && a.S % 8 == 0 &&
+        if (!flags().no_expand_mma && a.ovs == 1 && (a.base == nullptr || a.bvs == 1) && a.S % 8 == 0 &&
             a.S <= 64 && a.k <= 64 && a.k % 2 == 0 && a.ors % 2 == 0 && (a.base == nullptr || a.brs % 2 == 0) &&
             a.Ubs % 2 == 0 && a.Urs % 2 == 0 && a.obs % 2 == 0 && al16(a.out) && al16(a.U) &&
             (a.base == nullptr || al16(a.base))) {

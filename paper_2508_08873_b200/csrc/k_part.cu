@@ -384,6 +384,9 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(cbar + 8) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    // ctad / rmap are written by all warps and read below (sA1..sB2, neighbours)
+    // by warps that may run ahead: make the copies visible before any use
+    __syncthreads();
 
     if (w < W) {
         // ------------------------------------------------ compute warp: chunk c
@@ -681,7 +684,7 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (getenv("PR_PART_PROF")) {
+    if (flags().part_prof) {
         int nc = -1;
         cudaError_t eo = cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, AFF>, &cfg);
         fprintf(stderr, "part: max active clusters %d (%s), smem %zu B, groups %ld\n", nc,
@@ -704,7 +707,7 @@ bool part_preferred(const Op &op, long B, int m)
     // measured on B200 (C1, C2 shapes, B = 32 .. 20480): the partitioned stepper
     // beats the fused one at every batch size it supports
     (void)B;
-    if (op.part_P == 0 || m < 1 || getenv("PR_NO_PART")) return false;
+    if (op.part_P == 0 || m < 1 || flags().no_part) return false;
     return true;
 }
 
@@ -728,13 +731,12 @@ cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose,
     if (K >= 2) {
         const long clusters32 = (sa.B + 31) / 32;
         if (K > 8 || clusters32 * op.part_CL * 2 <= num_sms()) H = 2;
-        if (const char *e = getenv("PR_PART_H")) {
-            const int f = atoi(e);
+        if (const int f = flags().part_h) {
             if ((f == 1 && K <= 8) || f == 2) H = f;
         }
     }
     static unsigned long long *dprof = nullptr;
-    const bool want_prof = getenv("PR_PART_PROF") != nullptr;
+    const bool want_prof = flags().part_prof;
     if (want_prof) {
         if (!dprof) cudaMalloc(&dprof, 1024 * 4 * sizeof(unsigned long long));
         cudaMemsetAsync(dprof, 0, 1024 * 4 * sizeof(unsigned long long), s);

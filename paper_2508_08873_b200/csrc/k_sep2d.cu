@@ -270,9 +270,9 @@ static pr_status run_sep2d_impl(const Sep2dArgs &a, cudaStream_t s, int *passes)
     const int P = op.P;
     const long per = (long)P * P;
     const long B = a.B;
-    double *T = (double *)ws_alloc((size_t)B * per * sizeof(double));
+    double *T = (double *)ws_alloc((size_t)B * per * sizeof(double), s);
     if (!T) { set_error("out of device memory"); return PR_EOOM; }
-    struct Free { void *p; ~Free() { ws_free(p); } } fT{T};
+    struct Free { void *p; cudaStream_t s; ~Free() { ws_free(p, s); } } fT{T, s};
     GemmArgs g{};
     g.S = op.S;
     g.P = P;
@@ -286,16 +286,16 @@ static pr_status run_sep2d_impl(const Sep2dArgs &a, cudaStream_t s, int *passes)
         return PR_EINVAL;
     }
     double *bvec = nullptr;
-    struct Free2 { void *p; ~Free2() { ws_free(p); } } fb{nullptr};
+    struct Free2 { void *p; cudaStream_t s; ~Free2() { ws_free(p, s); } } fb{nullptr, s};
     if (affine) {
         // b = F 0: eigenbasis offsets, then S b^ S (+ offset when there is no input)
         const int nint = (int)((B + a.vpi - 1) / a.vpi);
         const int g0 = a.q0 * a.m;
         const int nsl = nint * a.m;
         const int nb = a.f->nterms;
-        double *gh = (double *)ws_alloc((size_t)2 * nb * nsl * P * sizeof(double));
+        double *gh = (double *)ws_alloc((size_t)2 * nb * nsl * P * sizeof(double), s);
         if (!gh) { set_error("out of device memory"); return PR_EOOM; }
-        struct Free3 { void *p; ~Free3() { ws_free(p); } } fg{gh};
+        struct Free3 { void *p; cudaStream_t s; ~Free3() { ws_free(p, s); } } fg{gh, s};
         double *gxh = gh, *gyh = gh + (size_t)nb * nsl * P;
         long tot = (long)nb * nsl * P;
         note_launch();
@@ -303,7 +303,7 @@ static pr_status run_sep2d_impl(const Sep2dArgs &a, cudaStream_t s, int *passes)
         note_launch();
         k_src_hat<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(op.S, P, a.f->gy, a.f->nsteps, g0, nsl, nb, gyh);
         PR_CHECK_LAUNCH("k_src_hat");
-        bvec = a.in ? (double *)ws_alloc((size_t)B * per * sizeof(double)) : a.out;
+        bvec = a.in ? (double *)ws_alloc((size_t)B * per * sizeof(double), s) : a.out;
         if (!bvec) { set_error("out of device memory"); return PR_EOOM; }
         if (a.in) fb.p = bvec;
         const long ldb = a.in ? per : a.ld_out;

@@ -587,8 +587,7 @@ template <int VPT, int RS>
 static cudaError_t launch_stepper_t(const StepArgs &a, cudaStream_t s)
 {
     int pd = 2;
-    if (const char *e = getenv("PR_STEPPER_PD")) {
-        int f = atoi(e);
+    if (const int f = flags().stepper_pd) {
         if (f == 2 || (f == 4 && stepper_smem(VPT, 4, RS, a.off != nullptr) <= 227 * 1024)) pd = f;
     }
     if (pd == 4) return launch_stepper_pd<VPT, RS, 4>(a, s);
@@ -628,8 +627,7 @@ cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s)
     int vpt = 1;
     if (fits(4) && a.B / 128 >= 4 * sms) vpt = 4;
     else if (fits(2) && a.B / 64 >= (sms * 3) / 4) vpt = 2;
-    if (const char *e = getenv("PR_STEPPER_VPT")) {
-        int f = atoi(e);
+    if (const int f = flags().stepper_vpt) {
         if ((f == 1) || (f == 2 && fits(2)) || (f == 4 && fits(4))) vpt = f;
     }
     // source terms padded to RS in {1, 2, 4, 8} (spaceT is zero-padded to RS columns)

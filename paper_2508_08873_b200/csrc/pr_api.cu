@@ -31,46 +31,110 @@ pr_status cuda_fail(cudaError_t e, const char *where)
 }
 
 // --------------------------------------------------------------- workspace
+// Stream-ordered caching pool.  A freed block remembers the stream it was last
+// used on and an event recorded there at free time; reusing it on the same
+// stream needs nothing (stream order), reusing it on another stream first makes
+// that stream wait for the event (no host synchronisation in either case).
+// Free lists are per device.
+struct WsBlock {
+    size_t bytes;
+    int dev;
+    cudaStream_t last;
+    cudaEvent_t ev;
+};
 static std::mutex g_ws_mu;
-static std::multimap<size_t, void *> g_ws_free;
-static std::unordered_map<void *, size_t> g_ws_size;
+static std::multimap<std::pair<int, size_t>, void *> g_ws_free;   // (device, bytes) -> block
+static std::unordered_map<void *, WsBlock> g_ws_blk;
 
-void *ws_alloc(size_t bytes)
+static int cur_device()
+{
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+
+void *ws_alloc(size_t bytes, cudaStream_t s)
 {
     if (bytes == 0) bytes = 256;
     bytes = (bytes + 255) & ~(size_t)255;
+    const int dev = cur_device();
     std::lock_guard<std::mutex> lk(g_ws_mu);
-    auto it = g_ws_free.lower_bound(bytes);
-    if (it != g_ws_free.end() && it->first <= 2 * bytes + (64 << 20)) {
+    auto it = g_ws_free.lower_bound({dev, bytes});
+    if (it != g_ws_free.end() && it->first.first == dev && it->first.second <= 2 * bytes + (64 << 20)) {
         void *p = it->second;
         g_ws_free.erase(it);
+        WsBlock &b = g_ws_blk[p];
+        if (b.last != s && b.ev) cudaStreamWaitEvent(s, b.ev, 0);
+        b.last = s;
         return p;
     }
     void *p = nullptr;
     if (cudaMalloc(&p, bytes) != cudaSuccess) {
         cudaGetLastError();
-        // release cached blocks and retry once
-        for (auto &kv : g_ws_free) {
-            cudaFree(kv.second);
-            g_ws_size.erase(kv.second);
+        // release this device's cached blocks (cudaFree synchronises) and retry once
+        for (auto i = g_ws_free.begin(); i != g_ws_free.end();) {
+            if (i->first.first != dev) { ++i; continue; }
+            auto b = g_ws_blk.find(i->second);
+            if (b != g_ws_blk.end()) {
+                if (b->second.ev) cudaEventDestroy(b->second.ev);
+                g_ws_blk.erase(b);
+            }
+            cudaFree(i->second);
+            i = g_ws_free.erase(i);
         }
-        g_ws_free.clear();
         if (cudaMalloc(&p, bytes) != cudaSuccess) {
             cudaGetLastError();
             return nullptr;
         }
     }
-    g_ws_size[p] = bytes;
+    g_ws_blk[p] = WsBlock{bytes, dev, s, nullptr};
     return p;
 }
 
-void ws_free(void *p)
+void ws_free(void *p, cudaStream_t s)
 {
     if (!p) return;
     std::lock_guard<std::mutex> lk(g_ws_mu);
-    auto it = g_ws_size.find(p);
-    if (it == g_ws_size.end()) return;
-    g_ws_free.emplace(it->second, p);
+    auto it = g_ws_blk.find(p);
+    if (it == g_ws_blk.end()) return;
+    WsBlock &b = it->second;
+    if (!b.ev) cudaEventCreateWithFlags(&b.ev, cudaEventDisableTiming);
+    if (b.ev) cudaEventRecord(b.ev, s);
+    b.last = s;
+    g_ws_free.emplace(std::make_pair(b.dev, b.bytes), p);
+}
+
+// ------------------------------------------------------------------- flags
+static Flags g_flags;
+static std::atomic<int> g_flags_gen{-1};
+static std::mutex g_flags_mu;
+
+static void read_flags()
+{
+    auto on = [](const char *n) { const char *e = getenv(n); return e && *e && *e != '0'; };
+    auto num = [](const char *n) { const char *e = getenv(n); return e ? atoi(e) : 0; };
+    Flags f;
+    f.no_part = on("PR_NO_PART");
+    f.no_xty_rm = on("PR_NO_XTY_RM");
+    f.no_trsm_dmma = on("PR_NO_TRSM_DMMA");
+    f.no_rinv_cm = on("PR_NO_RINV_CM");
+    f.no_expand_mma = on("PR_NO_EXPAND_MMA");
+    f.part_prof = on("PR_PART_PROF");
+    f.qr_trace = on("PR_QR_TRACE");
+    f.debug_sync = on("PR_DEBUG_SYNC");
+    f.part_h = num("PR_PART_H");
+    f.stepper_pd = num("PR_STEPPER_PD");
+    f.stepper_vpt = num("PR_STEPPER_VPT");
+    g_flags = f;
+}
+
+const Flags &flags()
+{
+    if (g_flags_gen.load(std::memory_order_acquire) < 0) {
+        std::lock_guard<std::mutex> lk(g_flags_mu);
+        if (g_flags_gen.load() < 0) { read_flags(); g_flags_gen.store(0, std::memory_order_release); }
+    }
+    return g_flags;
 }
 
 // ---------------------------------------------------------------- counters
@@ -118,14 +182,16 @@ int num_sms()
     return sms;
 }
 
-// RAII set of workspace buffers, released in stream order at scope exit.
+// RAII set of workspace buffers of one stream, released in stream order at scope exit.
 struct Scratch {
+    cudaStream_t s;
     std::vector<void *> bufs;
-    ~Scratch() { for (void *p : bufs) ws_free(p); }
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    ~Scratch() { for (void *p : bufs) ws_free(p, s); }
     template <class T>
     T *get(size_t count)
     {
-        void *p = ws_alloc(count * sizeof(T));
+        void *p = ws_alloc(count * sizeof(T), s);
         if (p) bufs.push_back(p);
         return (T *)p;
     }
@@ -144,15 +210,7 @@ struct Lay {
 static inline Lay lay(const Op &op, long ld) { return op.dim == 1 ? Lay{ld, 1} : Lay{1, ld}; }
 
 // PR_DEBUG_SYNC=1: synchronise and log after every orchestration stage.
-static bool debug_sync()
-{
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("PR_DEBUG_SYNC");
-        v = (e && *e && *e != '0') ? 1 : 0;
-    }
-    return v == 1;
-}
+static bool debug_sync() { return flags().debug_sync; }
 
 static void stage(const char *what, cudaStream_t s)
 {
@@ -167,7 +225,7 @@ static void stage(const char *what, cudaStream_t s)
 static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double *Rtot, int *fail,
                         int *passes_out, cudaStream_t s)
 {
-    Scratch S;
+    Scratch S(s);
     Lay L = lay(op, ld);
     const long rows = op.rows;
     const long xbs = (op.dim == 1) ? (long)l : (long)l * ld;
@@ -230,7 +288,7 @@ static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double 
         }
         PR_CUDA(cudaMemcpyAsync(h_active, active, sizeof(int), cudaMemcpyDeviceToHost, s));
         PR_CUDA(cudaStreamSynchronize(s));
-        if (getenv("PR_QR_TRACE")) fprintf(stderr, "[pr] qr after pass %d: active %d of %d\n", pass, *h_active, nb);
+        if (flags().qr_trace) fprintf(stderr, "[pr] qr after pass %d: active %d of %d\n", pass, *h_active, nb);
         if (*h_active == 0) { done_at = pass; break; }
         if (pass >= 24) {
             set_error("CholeskyQR did not converge in 24 passes");
@@ -259,7 +317,7 @@ static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi
         }
         return run_sep2d(a, s);
     }
-    Scratch S;
+    Scratch S(s);
     if (sketch) {
         // Omega materialised by the fully parallel generator, then stepped in place
         // (a thread-serial Philox inside the stepper's first pass costs more than
@@ -309,6 +367,14 @@ using namespace pr;
 extern "C" {
 
 const char *pr_last_error(void) { return g_err.c_str(); }
+
+pr_status pr_reload_env(void)
+{
+    std::lock_guard<std::mutex> lk(g_flags_mu);
+    read_flags();
+    g_flags_gen.store(1, std::memory_order_release);
+    return PR_OK;
+}
 int pr_version(void) { return 1; }
 
 pr_status pr_profile(int enable)
@@ -512,13 +578,14 @@ pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local,
     pr_coarse G = new pr_coarse_s();
     G->N_total = N_total; G->first = first_interval; G->nloc = n_local; G->m = m;
     G->k = k; G->p = p; G->l = l; G->rows = op.rows; G->dim = op.dim;
+    G->stream = s;
     const long rows = op.rows;
     const int nl = n_local;
-    G->U = (double *)ws_alloc((size_t)nl * rows * k * sizeof(double));
-    G->V = (double *)ws_alloc((size_t)nl * rows * k * sizeof(double));
-    G->sigma = (double *)ws_alloc((size_t)nl * l * sizeof(double));
-    G->C = (double *)ws_alloc((size_t)nl * k * k * sizeof(double));
-    G->fail = (int *)ws_alloc(2 * sizeof(int));
+    G->U = (double *)ws_alloc((size_t)nl * rows * k * sizeof(double), s);
+    G->V = (double *)ws_alloc((size_t)nl * rows * k * sizeof(double), s);
+    G->sigma = (double *)ws_alloc((size_t)nl * l * sizeof(double), s);
+    G->C = (double *)ws_alloc((size_t)nl * k * k * sizeof(double), s);
+    G->fail = (int *)ws_alloc(2 * sizeof(int), s);
     if (!G->U || !G->V || !G->sigma || !G->C || !G->fail) {
         pr_coarse_destroy(G);
         set_error("out of device memory");
@@ -529,7 +596,7 @@ pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local,
     if (e == cudaSuccess) e = cudaMemsetAsync(G->C, 0, (size_t)nl * k * k * sizeof(double), s);
     if (e != cudaSuccess) return bail(cuda_fail(e, "build init"));
     {
-        Scratch S;
+        Scratch S(s);
         const long B = (long)nl * l;
         const long ld = (op.dim == 1) ? ((B + 1) & ~1L) : rows;   // even ld: 16-B rows
         double *Y = S.get<double>((size_t)rows * (op.dim == 1 ? ld : B));
@@ -648,7 +715,7 @@ pr_status pr_coarse_apply(pr_coarse G, int q_local, int nvec, const double *X, l
     long minld = (G->dim == 1) ? nvec : rows;
     PR_REQUIRE(ldx >= minld && ldy >= minld, PR_EDIM, "leading dimension too small");
     cudaStream_t s = (cudaStream_t)stream;
-    Scratch S;
+    Scratch S(s);
     Lay Lx = (G->dim == 1) ? Lay{ldx, 1} : Lay{1, ldx};
     Lay Ly = (G->dim == 1) ? Lay{ldy, 1} : Lay{1, ldy};
     int nchunk = xty_chunks(rows, 1);
@@ -669,7 +736,8 @@ pr_status pr_coarse_apply(pr_coarse G, int q_local, int nvec, const double *X, l
 pr_status pr_coarse_destroy(pr_coarse G)
 {
     if (!G) return PR_OK;
-    ws_free(G->U); ws_free(G->V); ws_free(G->sigma); ws_free(G->C); ws_free(G->fail);
+    cudaStream_t s = G->stream;   // ordered after the last call that used the handle
+    ws_free(G->U, s); ws_free(G->V, s); ws_free(G->sigma, s); ws_free(G->C, s); ws_free(G->fail, s);
     delete G;
     return PR_OK;
 }
@@ -698,7 +766,7 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
             PR_REQUIRE(f->nsrc == S, PR_EDIM, "source nsrc must equal nsrc");
     }
     cudaStream_t s = (cudaStream_t)stream;
-    Scratch Sc;
+    Scratch Sc(s);
     const long ld = ld_out;          // Fu and b share U_out's layout
     Lay L = lay(op, ld);
     Lay L0 = lay(op, ld_u0);
@@ -799,7 +867,7 @@ pr_status pr_coarse_sweep_matrices(pr_coarse G, const double *U_prev, void *stre
     cudaStream_t s = (cudaStream_t)stream;
     const long rows = G->rows;
     const int k = G->k;
-    Scratch S;
+    Scratch S(s);
     if (!U_prev) {
         PR_CUDA(cudaMemsetAsync(G->C, 0, (size_t)k * k * sizeof(double), s));
         return PR_OK;
@@ -845,7 +913,7 @@ pr_status pr_coarse_project(pr_coarse G, int nsrc, const double *Y1, const doubl
     const int k = G->k, N = G->nloc, S = nsrc;
     PR_REQUIRE(ld >= (G->dim == 1 ? (long)N * S : rows), PR_EDIM, "ld too small");
     cudaStream_t s = (cudaStream_t)stream;
-    Scratch Sc;
+    Scratch Sc(s);
     const Lay L = (G->dim == 1) ? Lay{ld, 1} : Lay{1, ld};
     const long blk = (G->dim == 1) ? (long)S : (long)S * ld;
     const int nchunk = xty_chunks(rows, N);
@@ -877,7 +945,7 @@ pr_status pr_coarse_expand(pr_coarse G, int nsrc, const double *Fu, const double
     const int k = G->k, N = G->nloc, S = nsrc;
     PR_REQUIRE(ld >= (G->dim == 1 ? (long)N * S : rows), PR_EDIM, "ld too small");
     cudaStream_t s = (cudaStream_t)stream;
-    Scratch Sc;
+    Scratch Sc(s);
     const Lay L = (G->dim == 1) ? Lay{ld, 1} : Lay{1, ld};
     const int nchunk = xty_chunks(rows, N);
     const long cr = (rows + nchunk - 1) / nchunk;

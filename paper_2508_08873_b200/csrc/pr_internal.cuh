@@ -36,8 +36,23 @@ pr_status cuda_fail(cudaError_t e, const char *where);
 // Grow-only caching allocator: buffers returned by ws_free go back to a
 // size-keyed free list and are reused (no cudaFree/cudaMalloc, hence no
 // implicit device synchronisation, in repeated builds / Parareal runs).
-void *ws_alloc(size_t bytes);
-void ws_free(void *p);
+// Stream-ordered: a block freed on stream s1 and reused on s2 makes s2 wait for
+// an event recorded at the free (no host synchronisation).
+void *ws_alloc(size_t bytes, cudaStream_t s);
+void ws_free(void *p, cudaStream_t s);
+
+// Diagnostic switches from the environment (PR_NO_PART, PR_NO_XTY_RM,
+// PR_NO_TRSM_DMMA, PR_NO_RINV_CM, PR_NO_EXPAND_MMA select the alternate
+// kernels that tests/test_gpu_alt_paths.py exercises; PR_PART_H, PR_STEPPER_PD,
+// PR_STEPPER_VPT force a launch shape; PR_PART_PROF, PR_QR_TRACE,
+// PR_DEBUG_SYNC print diagnostics).  Read once per process and again on
+// pr_reload_env(), never per launch.
+struct Flags {
+    bool no_part = false, no_xty_rm = false, no_trsm_dmma = false, no_rinv_cm = false,
+         no_expand_mma = false, part_prof = false, qr_trace = false, debug_sync = false;
+    int part_h = 0, stepper_pd = 0, stepper_vpt = 0;
+};
+const Flags &flags();
 
 // Number of SMs of the current device (cached).
 int num_sms();
@@ -242,4 +257,5 @@ struct pr_coarse_s {
     double *C = nullptr;       // (nloc, k, k): C_q = Sigma_q V_q^T U_{q-1} (q >= first+1)
     int *fail = nullptr;       // device flags [0]: qr, [1]: svd
     int qr_passes[2] = {0, 0};
+    cudaStream_t stream = nullptr;   // stream of the last call that used the handle (destroy is ordered on it)
 };

@@ -40,13 +40,11 @@ def test_gaussian_sketch_matches_oracle(n, nint, l, q0):
 
 
 # -------------------------------------------------------------- fine solver
-def _stepper_path(monkeypatch, path):
+def _stepper_path(pr_env, path):
     """Select the 1D stepper: the fused one-vector-per-thread kernel (K1) or the
-    cluster-partitioned small-batch kernel (K1P, k_part.cu; used for every n it
+    cluster-partitioned kernel (K1P, k_part.cu; the default for every n it
     supports)."""
-    monkeypatch.delenv("PR_NO_PART", raising=False)
-    monkeypatch.delenv("PR_FORCE_PART", raising=False)
-    monkeypatch.setenv("PR_NO_PART" if path == "fused" else "PR_FORCE_PART", "1")
+    pr_env(PR_NO_PART="1" if path == "fused" else None)
 
 
 @pytest.mark.parametrize("name,n,m,B", [("C1", 127, 64, 12), ("C1", 127, 1, 6), ("C1", 127, 2, 5),
@@ -56,8 +54,8 @@ def _stepper_path(monkeypatch, path):
                                         ("C4", 16383, 128, 6)])
 @pytest.mark.parametrize("mode", ["linear", "adjoint"])
 @pytest.mark.parametrize("path", ["fused", "part"])
-def test_fine_linear_adjoint(name, n, m, B, mode, path, monkeypatch):
-    _stepper_path(monkeypatch, path)
+def test_fine_linear_adjoint(name, n, m, B, mode, path, pr_env):
+    _stepper_path(pr_env, path)
     from paper_2508_08873_b200 import PR_ADJOINT, PR_LINEAR
     cfg = replace(get(name), n=n, m=m)
     op_o = make_op(cfg)
@@ -75,8 +73,8 @@ def test_fine_linear_adjoint(name, n, m, B, mode, path, monkeypatch):
 
 @pytest.mark.parametrize("name,B,ld", [("T4", 5 * 4, 20), ("T4", 5 * 3, 17), ("C1", 8, 8)])
 @pytest.mark.parametrize("path", ["fused", "part"])
-def test_fine_affine_offset_and_inplace(name, B, ld, path, monkeypatch):
-    _stepper_path(monkeypatch, path)
+def test_fine_affine_offset_and_inplace(name, B, ld, path, pr_env):
+    _stepper_path(pr_env, path)
     from paper_2508_08873_b200 import PR_AFFINE, PR_LINEAR
     cfg = get(name)
     op_o, op_g = make_op(cfg), gpu_op(cfg)

@@ -1,0 +1,79 @@
+"""The alternate kernels behind libpr's diagnostic switches (DESIGN.md
+"Diagnostic switches") still match the oracle.  Each switch replaces one
+kernel of the default path by its simpler fallback:
+
+  PR_NO_PART        fused LU/UL streaming stepper (K1) instead of K1P
+  PR_NO_XTY_RM      CUDA-core cross products instead of the row-major DMMA Gram
+  PR_NO_TRSM_DMMA   row-wise substitution instead of the blocked DMMA TRSM
+  PR_NO_RINV_CM     generic R^{-1} apply instead of the column-major DMMA one (2D)
+  PR_NO_EXPAND_MMA  CUDA-core lift / reconstruction instead of the DMMA ones
+
+A whole rSVD build + Parareal run (T4 in 1D, T2D in 2D) goes through the
+switched kernel and is compared with the oracle at
+the north-star tolerances.
+"""
+import functools
+
+import numpy as np
+import pytest
+
+from gpu_util import TAU_1D, TAU_2D, empty_batch, from_gpu, gpu_op, gpu_source, to_gpu
+from oracle.fine import make_op
+from oracle.parareal import parareal as oracle_parareal
+from oracle.rsvd import rsvd_interval
+from workloads import generators as G
+from workloads.configs import get
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    import torch
+    from paper_2508_08873_b200 import build as B
+    B.build()
+    assert torch.cuda.is_available()
+
+
+@functools.lru_cache(maxsize=None)
+def _oracle(name):
+    cfg = get(name)
+    op_o = make_op(cfg)
+    truncs = [rsvd_interval(op_o, n, cfg.k, cfg.p, cfg.seed_omega) for n in range(1, cfg.N + 1)]
+    S = cfg.nsrc
+    if cfg.dim == 1:
+        u0 = np.stack([G.initial_value(cfg)] * S)
+        res = oracle_parareal(op_o, truncs, u0, cfg.N, cfg.K, G.source_1d(cfg), np.arange(S))
+    else:
+        u0 = G.initial_value(cfg)[None]
+        res = oracle_parareal(op_o, truncs, u0, cfg.N, cfg.K, G.source_2d(cfg))
+    return np.stack([t.sigma for t in truncs]), res, u0
+
+
+def _run(name):
+    from paper_2508_08873_b200 import Coarse, parareal
+    cfg = get(name)
+    opg = gpu_op(cfg)
+    Gg = Coarse.build(opg, cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega)
+    info = Gg.info()
+    sig, res, u0 = _oracle(name)
+    S = cfg.nsrc if cfg.dim == 1 else 1
+    Uo = empty_batch(cfg, (cfg.N + 1) * S)
+    upd, bn = parareal(Gg, opg, to_gpu(cfg, u0), gpu_source(cfg), cfg.K, Uo, nsrc=S)
+    tau = TAU_1D if cfg.dim == 1 else TAU_2D
+    assert np.max(np.abs(info["sigma"] - sig)) <= tau * sig.max()
+    got = from_gpu(cfg, Uo).reshape((cfg.N + 1, S) + res.U.shape[3:])
+    scale = np.max(np.abs(res.U))
+    assert np.max(np.abs(got - res.U[cfg.K])) <= tau * scale
+
+
+SWITCHES = ["PR_NO_PART", "PR_NO_XTY_RM", "PR_NO_TRSM_DMMA", "PR_NO_RINV_CM", "PR_NO_EXPAND_MMA"]
+
+
+@pytest.mark.parametrize("switch", SWITCHES)
+@pytest.mark.parametrize("name", ["T4", "T2D"])
+def test_alternate_kernel_matches_oracle(name, switch, pr_env):
+    if switch == "PR_NO_PART" and name == "T2D":
+        pytest.skip("PR_NO_PART concerns the 1D stepper only")
+    pr_env(**{switch: "1"})
+    _run(name)
