@@ -1,6 +1,8 @@
 """A priori and a posteriori error bounds -- TEST INFRASTRUCTURE ONLY.
 
-Theorem general_convergence and the a posteriori theorem
+Theorem general_convergence (eqs. error_bound_initial,
+error_bound_eps_delta, error_bound_eps_delta2, error_bound_eps,
+error_bound_eps_inf_time) and the a posteriori theorem
 (P:599-612), written out term by term.  delta, eps as in eq. bounds_delta_eps
 (P:407-411); norms are Euclidean.  Index conventions follow the
 paper: n = 1..N, m the summation index, b_0 := u_0.
@@ -45,3 +47,19 @@ def a_posteriori_sup(delta, eps, upd_k):
 def spectral_contraction(sigma_next, e0max, k):
     """Corollary spectral_bound: sigma_{R+1}^k max_{n<=N-k} ||e^0_n||."""
     return sigma_next ** k * e0max
+
+
+def a_priori_eps(eps, N, k, e0):
+    """eq. error_bound_eps (delta <= 1): max_n ||e^k_n|| <= C(N, k) eps^k max_{1<=m<=N-k} ||e^0_m||."""
+    if N - k < 1:
+        return 0.0
+    return comb(N, k) * eps ** k * max(e0[m] for m in range(1, N - k + 1))
+
+
+def a_priori_eps_inf_time(delta, eps, N, k, e0):
+    """eq. error_bound_eps_inf_time (delta < 1):
+    max_n ||e^k_n|| <= (eps / (1 - delta))^k max_{1<=n<=N-k} ||e^0_n||."""
+    assert delta < 1
+    if N - k < 1:
+        return 0.0
+    return (eps / (1.0 - delta)) ** k * max(e0[n] for n in range(1, N - k + 1))

@@ -11,7 +11,10 @@ One step of interval n (1-based), j = 1..m, global index g = (n-1)*m + j:
 
 1D: each step is one Thomas solve (oracle/csrc/oracle_thomas.c), pivots from
     the exact row sums of I + dt A (reading R-ACC).
-2D: A = T(x)I + I(x)T (5-point, Dirichlet).  The step is solved exactly by
+2D, "oracle A" (fine_2d_banded): each step is one banded Cholesky solve of the
+    5-point system (oracle/csrc/oracle_band.c) -- no sine basis.  Used to
+    cross-validate oracle B below (tests/test_oracle_fine2d_banded.py).
+2D, "oracle B" (fine_2d): A = T(x)I + I(x)T (5-point, Dirichlet).  The step is solved exactly by
     the classical fast-Poisson partial diagonalisation: transform the x index
     with the orthogonal sine matrix S (T = S diag(lam) S), then for every
     x-mode i solve the tridiagonal system ((1 + dt lam_i) I + dt T) in y with
@@ -23,7 +26,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from ._clib import thomas_batch
+from ._clib import band_factor, band_solve, thomas_batch
 
 
 # --------------------------------------------------------------------- 1D
@@ -134,6 +137,34 @@ def fine_2d(op: Op2D, interval: int, X: np.ndarray, mode: str = "linear", src=No
             V += op.dt * (Sg @ gy[:, g - 1, :])[None]                  # S f_g
         thomas_batch(*op.Ty, V.reshape(nvec * n, n), shift, rowsum=op.Ty_rs)
     return np.einsum("ij,bjk->bik", S, V)
+
+
+class Op2DBanded:
+    """Oracle A: the n x n 5-point Dirichlet Laplacian with unit diffusion
+    (BJ C3/C5), I + dt A factored once by banded Cholesky."""
+
+    def __init__(self, n: int, dt: float, m: int):
+        self.n, self.dt, self.m = int(n), float(dt), int(m)
+        self.L = band_factor(self.n, self.dt)
+
+
+def fine_2d_banded(op: Op2DBanded, interval: int, X: np.ndarray, mode: str = "linear",
+                   src=None) -> np.ndarray:
+    """As fine_2d, by m banded solves per call (X: (nvec, n, n) [x, y]).  A is
+    symmetric and time independent, so the adjoint is the same product."""
+    X = np.array(X, dtype=np.float64, copy=True)
+    if X.ndim == 2:
+        return fine_2d_banded(op, interval, X[None], mode, src)[0]
+    nvec, n = X.shape[0], op.n
+    V = np.ascontiguousarray(X.reshape(nvec, n * n))
+    for j in range(1, op.m + 1):
+        if mode == "affine" and src is not None:
+            gx, gy = src
+            g = (interval - 1) * op.m + j
+            f = gx[:, g - 1, :].T @ gy[:, g - 1, :]              # f[ix, iy] = sum_b gx gy
+            V += op.dt * f.reshape(1, n * n)
+        band_solve(n, op.L, V)
+    return V.reshape(nvec, n, n)
 
 
 # ---------------------------------------------------------------- dispatch

@@ -106,6 +106,10 @@ def test_lemma1_and_a_priori_and_a_posteriori_bounds():
             assert e[k, n] <= bounds.a_priori_k(delta, eps, bnorm, n, k) + floor
         if k >= 1:
             assert np.max(e[k, 1:]) <= bounds.a_posteriori_sup(delta, eps, res.upd[k, :, 0]) + floor
+            # eqs. error_bound_eps (delta <= 1) and error_bound_eps_inf_time (delta < 1)
+            assert delta < 1
+            assert np.max(e[k, 1:]) <= bounds.a_priori_eps(eps, cfg.N, k, e[0]) + floor
+            assert np.max(e[k, 1:]) <= bounds.a_priori_eps_inf_time(delta, eps, cfg.N, k, e[0]) + floor
 
 
 def test_update_norms_are_iterate_differences():
