@@ -132,7 +132,7 @@ class Workload:
             rs, cs = self.host["sums"]
             self.op = Operator.tridiag(*self.host["op"], cfg.dt, rowsum=rs, colsum=cs)
             self.src = SourceTerm.sep1d(space, time_, self.host["amp"])
-            self.U = torch.empty((cfg.n, (cfg.N + 1) * self.ns), dtype=torch.float64, device=dev)
+            self.U = torch.empty((cfg.n, (self.nq + 1) * self.ns), dtype=torch.float64, device=dev)
         else:
             gx, gy = G.source_2d(cfg)
             P = cfg.n + 1
@@ -140,8 +140,13 @@ class Workload:
                              u0=G.pad2d(u0).reshape(1, P * P))
             self.op = Operator.sep2d(cfg.n, cfg.dt)
             self.src = SourceTerm.bump2d(self.host["gx"], self.host["gy"])
-            self.U = torch.empty(((cfg.N + 1) * self.ns, P * P), dtype=torch.float64, device=dev)
+            self.U = torch.empty(((self.nq + 1) * self.ns, P * P), dtype=torch.float64, device=dev)
         self.u0 = torch.tensor(self.host["u0"], dtype=torch.float64, device=dev)
+        # interval-sharded runs: one pr_comm (NCCL) over the torch.distributed group
+        self.comm = None
+        if world > 1:
+            from paper_2508_08873_b200.parallel import nccl_comm
+            self.comm = nccl_comm()
 
     def dof_steps(self) -> float:
         """Fine-solve DOF-steps this rank performs per step."""
@@ -151,25 +156,19 @@ class Workload:
         return float(build + par)
 
     def step(self, events=None, op=None, src=None, u0=None):
-        """rSVD build of the own intervals + Parareal (1 GPU: pr_parareal; N GPUs:
-        the interval-sharded orchestration of paper_2508_08873_b200.parallel)."""
+        """rSVD build of the own intervals + Parareal, through the C ABI only
+        (N GPUs: pr_build_coarse / pr_parareal with the NCCL pr_comm; libpr
+        moves the interval-boundary data itself)."""
         from paper_2508_08873_b200 import Coarse, parareal
         c = self.cfg
         op = op or self.op
         src = src or self.src
         u0 = self.u0 if u0 is None else u0
-        G = Coarse.build(op, c.N, c.m, c.k, c.p, c.seed_omega, first_interval=self.q0,
-                         n_local=self.nq)
+        G = Coarse.build(op, c.N, c.m, c.k, c.p, c.seed_omega, comm=self.comm)
         if events is not None:
             events.append(_event())
-        if self.world == 1:
-            upd, bn = parareal(G, op, u0, src, c.K, self.U, nsrc=self.ns)
-        else:
-            from paper_2508_08873_b200.parallel import Blocks, Comm, LibprBackend, parareal_sharded
-            be = LibprBackend(op, G, c.N, self.q0, self.nq, c.m, c.k, self.ns, src)
-            rows = op.rows
-            blocks = Blocks(c.dim, rows, self.ns, self.dev)
-            self.U, upd = parareal_sharded(be, blocks, u0, c.K, Comm())
+        upd, bn = parareal(G, op, u0 if self.rank == 0 else None, src, c.K, self.U, nsrc=self.ns)
+        self.last_upd = upd
         G.close()
         return self.U
 

@@ -57,7 +57,8 @@ typedef enum {
     PR_ENOCONV = 4,    /* CholeskyQR or Jacobi SVD did not converge               */
     PR_EUNAVAIL = 5,   /* quantity not available (e.g. eps needs p >= 1)          */
     PR_EOOM = 6,       /* device allocation failed                                */
-    PR_ECUDA = 7       /* CUDA runtime error (message in pr_last_error)           */
+    PR_ECUDA = 7,      /* CUDA runtime error (message in pr_last_error)           */
+    PR_ENCCL = 8       /* NCCL missing or failed (message in pr_last_error)       */
 } pr_status;
 
 const char *pr_last_error(void);
@@ -83,6 +84,35 @@ pr_status pr_counters(int reset, long *kernel_launches, long *stepper_launches, 
 
 typedef struct pr_op_s *pr_op;
 typedef struct pr_coarse_s *pr_coarse;
+typedef struct pr_comm_s *pr_comm;
+
+/* -------------------------------------------------------------- distribution
+ * The path shards by time interval (the paper runs one MPI rank
+ * per interval group): rank r of `world` owns the contiguous block
+ * of intervals shard(N, r, world) = (first, n_local), first = r*floor(N/world)
+ * + min(r, N % world).  Only interval-boundary data crosses ranks: one
+ * boundary block per sweep to the right neighbour, the
+ * k-dimensional reduced sweep data of all intervals (all-gather), and the
+ * max-reductions of delta and eps (eq. bounds_delta_eps).  A
+ * pr_comm carries them, stream-ordered on the caller's stream.
+ *
+ * pr_comm_nccl_unique_id: 128-byte NCCL id (host), made on rank 0 and handed to
+ *   every rank by the caller (e.g. a torch.distributed broadcast).
+ * pr_comm_create_nccl: one process per GPU (the current device); NCCL is loaded
+ *   at run time (libnccl.so.2 already in the process, else the system's).
+ *   Collective: every rank calls it.  Errors: EINVAL, ENCCL.
+ * pr_comm_create_local: `world` virtual ranks in ONE process on the current
+ *   GPU; out[r] (host array of world handles) is rank r.  Each rank must be
+ *   driven by its own host thread (calls on different ranks meet at host
+ *   barriers) with its own stream; data moves by device-to-device copies
+ *   ordered with CUDA events.  For running the sharded schedule with more
+ *   ranks than GPUs (tests).  Errors: EINVAL.
+ * A communicator must outlive every handle built with it. */
+pr_status pr_comm_nccl_unique_id(void *id);
+pr_status pr_comm_create_nccl(int rank, int world, const void *id, pr_comm *out);
+pr_status pr_comm_create_local(int world, pr_comm *out);
+pr_status pr_comm_info(pr_comm c, int *rank, int *world);
+pr_status pr_comm_destroy(pr_comm c);
 
 /* ------------------------------------------------------------------ operator */
 
@@ -173,28 +203,38 @@ pr_status pr_gaussian_sketch(pr_op op, int first_interval, int n_intervals, int 
  * + n_local - 1 of N_total intervals, rank k, oversampling p (l = k + p <= 112,
  * l <= rows; 112 because the one-CTA Jacobi SVD of step 5 keeps two l x l
  * fp64 matrices in shared memory, 2 * 112^2 * 8 B = 196 KB of the 227 KB):
- *   1. Y = F_q' Omega_q, Omega generated in the stepper (pr_gaussian_sketch)
+ *   1. Y = F_q' Omega_q, Omega as pr_gaussian_sketch
  *   2. W = orth(Y)      iterated shifted CholeskyQR (reading Z7)
  *   3. Z = F_q'^* W
  *   4. V R_Z = Z        (same orthonormalisation, R_Z accumulated)
  *   5. M = R_Z^T (= (F'^* w_i, v_j)), M = Psi Sigma Phi^T by one-sided Jacobi;
  *      psi_r = W Psi_r, phi_r = V Phi_r (swapped reading of P:293-294, Z5)
  *   6. keep r <= k.
- * Seeds depend only on (seed, q, column), so results do not depend on how the
- * intervals are sharded.  The handle also precomputes the reduced sweep
- * matrices C_q = Sigma_q V_q^T U_{q-1}.
- * Asynchronous; errors detected on the device (no convergence) are reported by
- * pr_coarse_info.  Errors: EINVAL, EDIM (l > 112 or l > rows), EOOM. */
+ * comm (nullable): with a communicator, first_interval / n_local are ignored
+ * and the rank's block shard(N_total, rank, world) is built; the handle keeps
+ * comm (which must outlive it), receives U_{first-1} from the left neighbour
+ * for its first sweep matrix, and holds delta / eps reduced over all ranks and
+ * the sweep matrices C_q of all intervals (for pr_parareal).
+ * Seeds depend only on (seed, q, column) and every reduction's chunking only
+ * on N_total, so results are bit-identical for any sharding.  The handle also
+ * holds the reduced sweep matrices C_q = Sigma_q V_q^T U_{q-1} (DESIGN.md
+ * "reduced sweep").  Intervals are processed in chunks whose scratch fits
+ * min(16 GiB, 40% of free memory), so scratch does not grow with n_local.
+ * Asynchronous (no host synchronisation: the CholeskyQR pass loop is
+ * controlled on the device, at most 24 passes); errors detected on the device
+ * (no convergence) are reported by pr_coarse_info and pr_parareal.
+ * Errors: EINVAL, EDIM (l > 112 or l > rows), EOOM, ENCCL. */
 pr_status pr_build_coarse(pr_op op, int N_total, int first_interval, int n_local, int m,
-                          int k, int p, uint64_t seed, void *stream, pr_coarse *out);
+                          int k, int p, uint64_t seed, pr_comm comm, void *stream, pr_coarse *out);
 
-/* Synchronizing.  k, l, n_local, first_interval, m; delta = max_q sigma_{q,1}
- * and eps = max_q sigma_{q,k+1} over the local intervals (eq.
+/* Synchronizes with the stream of the handle's last call.  k, l, n_local,
+ * first_interval, m; delta = max_q sigma_{q,1} and eps = max_q sigma_{q,k+1}
+ * over ALL intervals (all ranks when built with a communicator; eq.
  * bounds_delta_eps; eps uses the computed sigma_{k+1});
- * sigma_host (nullable, host, n_local*l) all computed singular values;
- * qr_passes (nullable, host, 2) the CholeskyQR pass counts of steps 2 and 4.
- * Returns PR_ENOCONV if a QR or SVD failed to converge on the device, and
- * PR_EUNAVAIL for eps when p == 0 (eps set to NaN). */
+ * sigma_host (nullable, host, n_local*l) the local computed singular values;
+ * qr_passes (nullable, host, 2) the CholeskyQR pass counts of steps 2 and 4
+ * (max over the local intervals).  Returns PR_ENOCONV if a QR or SVD failed to
+ * converge on the device, and PR_EUNAVAIL for eps when p == 0 (eps = NaN). */
 pr_status pr_coarse_info(pr_coarse G, int *k, int *l, int *n_local, int *first_interval, int *m,
                          double *delta, double *eps, double *sigma_host, int *qr_passes);
 
@@ -210,9 +250,8 @@ pr_status pr_coarse_destroy(pr_coarse G);
 
 /* ----------------------------------------------------------------- Parareal */
 
-/* Parareal (eq. def_Parareal) over all N intervals of G (which must
- * hold every interval, first_interval = 0), nsrc independent sources sharing
- * G' (Remark affine_g_n), with G_n = G_n' + b_n:
+/* Parareal (eq. def_Parareal) with nsrc independent sources
+ * sharing G' (Remark affine_g_n), G_n = G_n' + b_n:
  *   b_q = F_q 0                                    (PR_AFFINE from zero)
  *   u^0_0 = u0, u^0_{q+1} = G_{q+1} u^0_q           (initialisation)
  *   u^{k+1}_{q+1} = F_{q+1} u^k_q + G'_{q+1} u^{k+1}_q - G'_{q+1} u^k_q
@@ -220,15 +259,26 @@ pr_status pr_coarse_destroy(pr_coarse G);
  * stepper launch (F' u + b_q); the sequential part runs in the reduced
  * coordinates e_q = C_q e_{q-1} + (q_q - p_q) of dimension k (DESIGN.md
  * "reduced sweep"; exact algebra, no approximation).
- *   u0       device, nsrc vectors (op layout, stride ld_u0)
- *   U_out    device, (N+1)*nsrc vectors, vector j*nsrc + s = u^K_j of source s
- *            (op layout, stride ld_out); also used as the iteration state.
- *   upd_host host, nullable, K_iter x (N+1) x nsrc: ||u^k_j - u^{k-1}_j||, k = 1..K
+ * G either covers all intervals (built without a communicator) or is one
+ * rank's shard (built with one): then this is a collective call of all ranks,
+ * each computing its own intervals q0 .. q0+nq-1 (q0 = first_interval,
+ * nq = n_local of pr_coarse_info), with one boundary block per half-iteration
+ * sent to the right neighbour and the k x nsrc sweep data all-gathered.  The
+ * result is bit-identical to the unsharded run.
+ *   u0       device, nsrc vectors (op layout, stride ld_u0); read on rank 0
+ *            only (may be NULL elsewhere)
+ *   U_out    device, (nq+1)*nsrc vectors, vector i*nsrc + s = u^K_{q0+i} of
+ *            source s (op layout, stride ld_out); block 0 is u_{q0} (u0 on
+ *            rank 0); also the iteration state.
+ *   upd_host host, nullable, K_iter x (N+1) x nsrc: ||u^k_j - u^{k-1}_j||,
+ *            k = 1..K, all boundaries j (gathered from every rank)
  *   bnorm_host host, nullable, (N+1) x nsrc: ||b_j|| with b_0 := u0
- *   hist     device, nullable: if given, u^k (all (N+1)*nsrc vectors, same
- *            layout as U_out) is stored at hist + k*hist_stride, k = 0..K.
- * Synchronizing (at the end, to fill the host arrays).
- * Errors: EINVAL, EDIM (G not covering all intervals, source/op mismatch). */
+ *   hist     device, nullable: if given, u^k (the (nq+1)*nsrc local vectors,
+ *            same layout as U_out) is stored at hist + k*hist_stride, k = 0..K.
+ * Synchronizing (at the end, to fill the host arrays).  Returns PR_ENOCONV
+ * (outputs undefined) if the rSVD of G failed on the device.
+ * Errors: EINVAL, EDIM (G not covering all intervals without a communicator,
+ * source/op mismatch), ENOCONV, EOOM, ENCCL. */
 pr_status pr_parareal(pr_coarse G, pr_op op, int nsrc, const double *u0, long ld_u0,
                       const pr_source *f, int K_iter, double *U_out, long ld_out,
                       double *upd_host, double *bnorm_host, double *hist, long hist_stride,

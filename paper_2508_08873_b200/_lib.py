@@ -12,9 +12,9 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(_HERE, "libpr.so")
 
-PR_OK, PR_EINVAL, PR_EDIM, PR_ESINGULAR, PR_ENOCONV, PR_EUNAVAIL, PR_EOOM, PR_ECUDA = range(8)
+PR_OK, PR_EINVAL, PR_EDIM, PR_ESINGULAR, PR_ENOCONV, PR_EUNAVAIL, PR_EOOM, PR_ECUDA, PR_ENCCL = range(9)
 STATUS_NAMES = ["PR_OK", "PR_EINVAL", "PR_EDIM", "PR_ESINGULAR", "PR_ENOCONV", "PR_EUNAVAIL",
-                "PR_EOOM", "PR_ECUDA"]
+                "PR_EOOM", "PR_ECUDA", "PR_ENCCL"]
 PR_LINEAR, PR_ADJOINT, PR_AFFINE = 0, 1, 2
 PR_SRC_NONE, PR_SRC_SEP1D, PR_SRC_BUMP2D = 0, 1, 2
 
@@ -23,7 +23,9 @@ EXPORTS = ["pr_last_error", "pr_version", "pr_reload_env", "pr_profile", "pr_cou
            "pr_op_destroy", "pr_op_info", "pr_fine_propagate", "pr_gaussian_sketch",
            "pr_build_coarse", "pr_coarse_info", "pr_coarse_factors", "pr_coarse_apply",
            "pr_coarse_destroy", "pr_parareal", "pr_bounds", "pr_coarse_sweep_matrices",
-           "pr_coarse_export", "pr_coarse_export_interval", "pr_coarse_project", "pr_reduced_sweep", "pr_coarse_expand"]
+           "pr_coarse_export", "pr_coarse_export_interval", "pr_coarse_project", "pr_reduced_sweep", "pr_coarse_expand",
+           "pr_comm_nccl_unique_id", "pr_comm_create_nccl", "pr_comm_create_local", "pr_comm_info",
+           "pr_comm_destroy"]
 
 
 class PrError(RuntimeError):
@@ -65,7 +67,7 @@ def lib():
             "pr_op_info": ([vp, ctypes.POINTER(lg), ip, ip], I),
             "pr_fine_propagate": ([vp, I, I, I, I, I, ctypes.POINTER(Source), vp, lg, vp, lg, vp, lg, vp], I),
             "pr_gaussian_sketch": ([vp, I, I, I, U64, vp, lg, vp], I),
-            "pr_build_coarse": ([vp, I, I, I, I, I, I, U64, vp, ctypes.POINTER(vp)], I),
+            "pr_build_coarse": ([vp, I, I, I, I, I, I, U64, vp, vp, ctypes.POINTER(vp)], I),
             "pr_coarse_info": ([vp, ip, ip, ip, ip, ip, dp, dp, dp, ip], I),
             "pr_coarse_factors": ([vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)], I),
             "pr_coarse_apply": ([vp, I, I, vp, lg, vp, lg, vp], I),
@@ -78,6 +80,11 @@ def lib():
             "pr_coarse_project": ([vp, I, vp, vp, lg, vp, vp], I),
             "pr_reduced_sweep": ([vp, vp, I, I, I, vp, vp], I),
             "pr_coarse_expand": ([vp, I, vp, vp, vp, lg, vp, vp], I),
+            "pr_comm_nccl_unique_id": ([vp], I),
+            "pr_comm_create_nccl": ([I, I, vp, ctypes.POINTER(vp)], I),
+            "pr_comm_create_local": ([I, ctypes.POINTER(vp)], I),
+            "pr_comm_info": ([vp, ip, ip], I),
+            "pr_comm_destroy": ([vp], I),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)

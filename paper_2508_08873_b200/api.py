@@ -134,22 +134,69 @@ class SourceTerm:
         return cls(L.PR_SRC_NONE, 0, 1, 0, {})
 
 
+class Comm:
+    """A pr_comm (include/pr.h "distribution"): NCCL over one process per GPU,
+    or `world` in-process virtual ranks on one GPU (one host thread each)."""
+
+    def __init__(self, handle, keep=None):
+        self._h = handle
+        self._keep = keep            # the local group: destroyed with its last rank
+        r, w = ctypes.c_int(), ctypes.c_int()
+        check(L.lib().pr_comm_info(self._h, ctypes.byref(r), ctypes.byref(w)), "pr_comm_info")
+        self.rank, self.world = r.value, w.value
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        check(L.lib().pr_comm_nccl_unique_id(buf), "pr_comm_nccl_unique_id")
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, rank: int, world: int, uid: bytes) -> "Comm":
+        assert len(uid) == 128
+        h = ctypes.c_void_p()
+        check(L.lib().pr_comm_create_nccl(int(rank), int(world), ctypes.create_string_buffer(uid, 128),
+                                          ctypes.byref(h)), "pr_comm_create_nccl")
+        return cls(h)
+
+    @classmethod
+    def local(cls, world: int) -> list:
+        hs = (ctypes.c_void_p * world)()
+        check(L.lib().pr_comm_create_local(int(world), hs), "pr_comm_create_local")
+        return [cls(ctypes.c_void_p(hs[r])) for r in range(world)]
+
+    def close(self):
+        if self._h:
+            L.lib().pr_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Coarse:
     """Spectral coarse solvers G_q' = U_q Sigma_q V_q^T of the owned intervals."""
 
-    def __init__(self, handle):
+    def __init__(self, handle, comm=None, N_total: int = None):
         self._h = handle
+        self._comm = comm            # keeps the communicator alive as long as the handle
+        self.N_total = N_total
 
     @classmethod
     def build(cls, op: Operator, N_total: int, m: int, k: int, p: int, seed: int,
-              first_interval: int = 0, n_local: int = None, stream=None) -> "Coarse":
+              first_interval: int = 0, n_local: int = None, comm: "Comm" = None,
+              stream=None) -> "Coarse":
         if n_local is None:
             n_local = N_total - first_interval
         h = ctypes.c_void_p()
         check(L.lib().pr_build_coarse(op._h, int(N_total), int(first_interval), int(n_local),
                                       int(m), int(k), int(p), ctypes.c_uint64(int(seed)),
+                                      comm._h if comm is not None else None,
                                       _stream(stream), ctypes.byref(h)), "pr_build_coarse")
-        return cls(h)
+        return cls(h, comm, int(N_total))
 
     def info(self, raise_on_error: bool = True) -> dict:
         k, l, nl, first, m = (ctypes.c_int() for _ in range(5))
@@ -165,6 +212,7 @@ class Coarse:
         if raise_on_error and st not in (L.PR_OK, L.PR_EUNAVAIL):
             check(st, "pr_coarse_info")
         return dict(k=k.value, l=l.value, n_local=nl.value, first_interval=first.value, m=m.value,
+                    N_total=self.N_total,
                     delta=delta.value, eps=eps.value, sigma=sig.reshape(nl.value, l.value),
                     qr_passes=(passes[0], passes[1]), status=st)
 
@@ -209,13 +257,15 @@ class Coarse:
 
 def parareal(G: Coarse, op: Operator, u0, source: SourceTerm, K: int, U_out, nsrc: int = 1,
              hist=None, stream=None):
-    """Returns (upd[K, N+1, nsrc], bnorm[N+1, nsrc]) host arrays; U_out holds u^K."""
-    nvec = (U_out.shape[1] if op.dim == 1 else U_out.shape[0])
-    Np1 = nvec // nsrc
+    """Returns (upd[K, N+1, nsrc], bnorm[N+1, nsrc]) host arrays (all
+    boundaries); U_out holds u^K of the handle's boundaries (all of them, or
+    the rank's shard + halo block when G was built with a communicator)."""
+    Np1 = G.N_total + 1
     upd = np.zeros((max(K, 0), Np1, nsrc))
     bn = np.zeros((Np1, nsrc))
     hs = int(hist.stride(0)) if hist is not None else 0
-    check(L.lib().pr_parareal(G._h, op._h, int(nsrc), _ptr(u0), _ld(u0, op.dim),
+    check(L.lib().pr_parareal(G._h, op._h, int(nsrc), _ptr(u0),
+                              _ld(u0, op.dim) if u0 is not None else 0,
                               ctypes.byref(source.struct), int(K), _ptr(U_out), _ld(U_out, op.dim),
                               _hptr(upd) if K > 0 else None, _hptr(bn),
                               _ptr(hist) if hist is not None else None, hs, _stream(stream)),

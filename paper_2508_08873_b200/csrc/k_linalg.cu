@@ -633,6 +633,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol(CholArgs a)
         if (threadIdx.x == 0) a.act[b] = 0;
         return;
     }
+    if (a.passes && threadIdx.x == 0) atomicMax(a.passes, a.pass);   // last pass that did work
     const long per = (long)l * l;
     auto load_G = [&]() {
         for (int e = threadIdx.x; e < l * l; e += CH_THREADS) {
@@ -758,7 +759,8 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol(CholArgs a)
         int ns = plain ? (st == 1 ? 2 : 1) : 0;
         a.state[b] = ns;
         a.act[b] = use_inv ? 2 : 1;
-        if (ns != 2) atomicAdd(a.active, 1);
+        if (ns != 2 && a.active) atomicAdd(a.active, 1);
+        if (ns != 2 && a.pass >= a.max_pass) atomicExch(a.fail, 1);   // not orthonormal within the cap
     }
 }
 

@@ -36,6 +36,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <atomic>
+
 #include "pr_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -530,20 +532,34 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
             long long gb = PROBE ? clock64() : 0;
             hw += gb - ga;
             const double2 *G = gth + (size_t)p * CL * 32 + vl;
-            double b0 = 0.0, b1 = 0.0, t0 = 0.0, t1 = 0.0;
+            // the two halves of the CTA list are summed separately and then
+            // added, for H = 1 and H = 2 alike: the result does not depend on
+            // the warp shape the batch size selects (bit-identical shards)
+            auto half = [&](int hh, double &Bh, double &Th) {
+                double b0 = 0.0, b1 = 0.0, t0 = 0.0, t1 = 0.0;
 #pragma unroll
-            for (int rr = 0; rr < CLH; ++rr) {
-                const int r = h * CLH + rr;
-                const double2 e = G[r * 32];
-                b0 = fma(ctad[CTAD_GB + 2 * r], e.x, b0);
-                b1 = fma(ctad[CTAD_GB + 2 * r + 1], e.y, b1);
-                t0 = fma(ctad[CTAD_GT + 2 * r], e.x, t0);
-                t1 = fma(ctad[CTAD_GT + 2 * r + 1], e.y, t1);
-            }
-            double Bx = b0 + b1, Tx = t0 + t1;
+                for (int rr = 0; rr < CL / 2; ++rr) {
+                    const int r = hh * (CL / 2) + rr;
+                    const double2 e = G[r * 32];
+                    b0 = fma(ctad[CTAD_GB + 2 * r], e.x, b0);
+                    b1 = fma(ctad[CTAD_GB + 2 * r + 1], e.y, b1);
+                    t0 = fma(ctad[CTAD_GT + 2 * r], e.x, t0);
+                    t1 = fma(ctad[CTAD_GT + 2 * r + 1], e.y, t1);
+                }
+                Bh = b0 + b1;
+                Th = t0 + t1;
+            };
+            double Bx, Tx;
             if constexpr (H == 2) {
+                half(h, Bx, Tx);
                 Bx += __shfl_xor_sync(0xffffffffu, Bx, 16);
                 Tx += __shfl_xor_sync(0xffffffffu, Tx, 16);
+            } else {
+                double B1, T1;
+                half(0, Bx, Tx);
+                half(1, B1, T1);
+                Bx += B1;
+                Tx += T1;
             }
             if (h == 0) coef[p * 32 + vl] = make_double2(Bx, Tx);
             __syncwarp();
@@ -661,16 +677,20 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
 {
     constexpr size_t smem = part_smem_t<CL, W, H, L, AFF>();
     static_assert(smem <= 227 * 1024, "partitioned stepper shared memory");
-    // function attributes are set once per process (one process drives one GPU)
-    static bool attr_done = false;
-    if (!attr_done) {
+    // function attributes are per device: set once for each device this
+    // process launches on (bit d of the mask)
+    static std::atomic<unsigned long long> attr_mask{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ULL << (dev & 63);
+    if (!(attr_mask.load(std::memory_order_acquire) & bit)) {
         cudaError_t e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, AFF>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess && CL > 8)
             e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, AFF>,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
-        attr_done = true;
+        attr_mask.fetch_or(bit, std::memory_order_release);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(groups * CL));

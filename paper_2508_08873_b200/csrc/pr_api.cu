@@ -172,12 +172,11 @@ void stepper_timed_end(cudaStream_t s, double dof_steps, double flops)
 
 int num_sms()
 {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
-            sms = 148;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+        cudaGetLastError();
+        sms = 148;
     }
     return sms;
 }
@@ -221,82 +220,72 @@ static void stage(const char *what, cudaStream_t s)
 }
 
 // -------------------------------------------------------------- QR driver
-// Iterated shifted CholeskyQR of nb blocks Q_b (rows x l), in place.
+// Iterated shifted CholeskyQR of nb blocks Q_b (rows x l), in place.  The
+// pass loop is controlled on the device: every pass up to the cap is enqueued
+// without a host check, a block that is done (state 2) makes every kernel of
+// the later passes return at once, the pass count lands in passes_dev, and a
+// block still active after the cap raises *fail (reported by pr_coarse_info).
+// So pr_build_coarse never waits for the device.  nchunk_total: the Gram
+// row-chunking depends on the global interval count only, so a shard computes
+// bit-identical bases.
+constexpr int QR_MAX_PASSES = 24;
+
 static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double *Rtot, int *fail,
-                        int *passes_out, cudaStream_t s)
+                        int *passes_dev, int nchunk, cudaStream_t s)
 {
     Scratch S(s);
     Lay L = lay(op, ld);
     const long rows = op.rows;
     const long xbs = (op.dim == 1) ? (long)l : (long)l * ld;
-    int nchunk = xty_chunks(rows, nb);
     long chunk_rows = (rows + nchunk - 1) / nchunk;
     double *part, *R;
-    int *state, *act, *active;
+    int *state, *act;
     PR_ALLOC(part, double, (size_t)nb * nchunk * l * l, S);
     PR_ALLOC(R, double, (size_t)nb * l * l, S);
     double *Rinv;
     PR_ALLOC(Rinv, double, (size_t)nb * l * l, S);
     PR_ALLOC(state, int, nb, S);
     PR_ALLOC(act, int, nb, S);
-    PR_ALLOC(active, int, 1, S);
-    // pinned landing slot for the device "active" counter (allocated once per thread)
-    static thread_local int *h_active = nullptr;
-    if (!h_active) PR_CUDA(cudaMallocHost(&h_active, sizeof(int)));
     PR_CUDA(cudaMemsetAsync(state, 0, nb * sizeof(int), s));
+    PR_CUDA(cudaMemsetAsync(passes_dev, 0, sizeof(int), s));
     if (Rtot) PR_CUDA(launch_eye(Rtot, nb, l, s));
-    // Passes are enqueued in groups before the host reads the counter: blocks
-    // that are done skip every kernel of later passes, so a speculative pass
-    // costs only its launches, while each host read costs a stream sync.
-    int pass = 0, done_at = 0;
-    const int group = 3;
-    for (;;) {
-        for (int g = 0; g < group; ++g) {
-            ++pass;
-            XtY x{state, Q, xbs, L.rs, L.vs, l, Q, xbs, L.rs, L.vs, l, rows, nb, nchunk, chunk_rows, part};
-            PR_CUDA(launch_xty(x, s));
-            stage("qr gram", s);
-            PR_CUDA(cudaMemsetAsync(active, 0, sizeof(int), s));
-            CholArgs c{part, nchunk, nb, l, rows, state, act, R, Rtot, active, fail};
-            c.Rinv = Rinv;
-            double *offI = nullptr;
-            if (debug_sync()) {
-                offI = S.get<double>(3 * nb);
-                if (offI) PR_CUDA(cudaMemsetAsync(offI, 0, 3 * nb * sizeof(double), s));
-                c.offI = offI;
-                c.shift_dbg = offI + nb;
-            }
-            PR_CUDA(launch_chol(c, s));
-            stage("qr chol", s);
-            if (offI) {
-                std::vector<double> h(3 * nb);
-                std::vector<int> hs(nb);
-                PR_CUDA(cudaMemcpy(h.data(), offI, 3 * nb * sizeof(double), cudaMemcpyDeviceToHost));
-                double smax = 0, amax = 0;
-                for (int i = 0; i < nb; ++i) { smax = std::max(smax, h[nb + 2 * i]); amax = std::max(amax, h[nb + 2 * i + 1]); }
-                fprintf(stderr, "[pr]   shift/||G||_F max %.3e, Cholesky retries max %.0f\n", smax, amax);
-                PR_CUDA(cudaMemcpy(hs.data(), state, nb * sizeof(int), cudaMemcpyDeviceToHost));
-                double mn = 1e300, mx = 0;
-                int cnt[3] = {0, 0, 0};
-                for (int i = 0; i < nb; ++i) { mn = std::min(mn, h[i]); mx = std::max(mx, h[i]); cnt[hs[i]]++; }
-                fprintf(stderr, "[pr] qr pass %d: ||G-I||_F min %.3e max %.3e; states after: shift %d plain1 %d done %d\n",
-                        pass, mn, mx, cnt[0], cnt[1], cnt[2]);
-            }
-            PR_CUDA(launch_trsm(Q, xbs, L.rs, L.vs, rows, l, nb, R, act, s));
-            PR_CUDA(launch_rinv_apply(Q, xbs, L.rs, L.vs, rows, l, nb, Rinv, act, s));
-            stage("qr apply", s);
+    for (int pass = 1; pass <= QR_MAX_PASSES; ++pass) {
+        XtY x{state, Q, xbs, L.rs, L.vs, l, Q, xbs, L.rs, L.vs, l, rows, nb, nchunk, chunk_rows, part};
+        PR_CUDA(launch_xty(x, s));
+        stage("qr gram", s);
+        CholArgs c{part, nchunk, nb, l, rows, state, act, R, Rtot, nullptr, fail};
+        c.Rinv = Rinv;
+        c.pass = pass;
+        c.max_pass = QR_MAX_PASSES;
+        c.passes = passes_dev;
+        double *offI = nullptr;
+        if (debug_sync()) {
+            offI = S.get<double>(3 * nb);
+            if (offI) PR_CUDA(cudaMemsetAsync(offI, 0, 3 * nb * sizeof(double), s));
+            c.offI = offI;
+            c.shift_dbg = offI + nb;
         }
-        PR_CUDA(cudaMemcpyAsync(h_active, active, sizeof(int), cudaMemcpyDeviceToHost, s));
-        PR_CUDA(cudaStreamSynchronize(s));
-        if (flags().qr_trace) fprintf(stderr, "[pr] qr after pass %d: active %d of %d\n", pass, *h_active, nb);
-        if (*h_active == 0) { done_at = pass; break; }
-        if (pass >= 24) {
-            set_error("CholeskyQR did not converge in 24 passes");
-            if (passes_out) *passes_out = pass;
-            return PR_ENOCONV;
+        PR_CUDA(launch_chol(c, s));
+        stage("qr chol", s);
+        if (offI) {
+            std::vector<double> h(3 * nb);
+            std::vector<int> hs(nb);
+            PR_CUDA(cudaMemcpy(h.data(), offI, 3 * nb * sizeof(double), cudaMemcpyDeviceToHost));
+            double smax = 0, amax = 0;
+            for (int i = 0; i < nb; ++i) { smax = std::max(smax, h[nb + 2 * i]); amax = std::max(amax, h[nb + 2 * i + 1]); }
+            fprintf(stderr, "[pr]   shift/||G||_F max %.3e, Cholesky retries max %.0f\n", smax, amax);
+            PR_CUDA(cudaMemcpy(hs.data(), state, nb * sizeof(int), cudaMemcpyDeviceToHost));
+            double mn = 1e300, mx = 0;
+            int cnt[3] = {0, 0, 0};
+            for (int i = 0; i < nb; ++i) { mn = std::min(mn, h[i]); mx = std::max(mx, h[i]); cnt[hs[i]]++; }
+            fprintf(stderr, "[pr] qr pass %d: ||G-I||_F min %.3e max %.3e; states after: shift %d plain1 %d done %d\n",
+                    pass, mn, mx, cnt[0], cnt[1], cnt[2]);
+            if (cnt[2] == nb) break;
         }
+        PR_CUDA(launch_trsm(Q, xbs, L.rs, L.vs, rows, l, nb, R, act, s));
+        PR_CUDA(launch_rinv_apply(Q, xbs, L.rs, L.vs, rows, l, nb, Rinv, act, s));
+        stage("qr apply", s);
     }
-    if (passes_out) *passes_out = done_at;
     return PR_OK;
 }
 
@@ -563,14 +552,75 @@ pr_status pr_gaussian_sketch(pr_op h, int first_interval, int n_intervals, int l
 }
 
 // ------------------------------------------------------------ build
+// pass counts of this chunk's two QRs -> running max in out[0..1]
+__global__ void k_imax2(const int *in, int *out)
+{
+    if (threadIdx.x < 2) out[threadIdx.x] = max(out[threadIdx.x], in[threadIdx.x]);
+}
+
+// [delta, eps] of the local intervals: max_q sigma_{q,1}, max_q sigma_{q,k+1}
+// (eq. bounds_delta_eps; eps from the computed sigma_{k+1},
+// P:1231-1232; 0 when p == 0)
+__global__ void k_delta_eps(const double *sigma, int nloc, int l, int k, int p, double *de)
+{
+    __shared__ double red[2][256];
+    double d = 0.0, e = 0.0;
+    for (int q = threadIdx.x; q < nloc; q += blockDim.x) {
+        d = fmax(d, sigma[(long)q * l]);
+        if (p > 0) e = fmax(e, sigma[(long)q * l + k]);
+    }
+    red[0][threadIdx.x] = d;
+    red[1][threadIdx.x] = e;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) {
+            red[0][threadIdx.x] = fmax(red[0][threadIdx.x], red[0][threadIdx.x + w]);
+            red[1][threadIdx.x] = fmax(red[1][threadIdx.x], red[1][threadIdx.x + w]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { de[0] = red[0][0]; de[1] = red[1][0]; }
+}
+
+// Scratch of one build chunk: Y, Z (and the 2D stepper's temporary) per interval.
+static size_t build_bytes_per_interval(const Op &op, int l)
+{
+    const size_t blk = (size_t)op.rows * l * sizeof(double);
+    return (op.dim == 1 ? 2 : 3) * blk + (size_t)3 * l * l * sizeof(double);
+}
+
+// Intervals per build chunk: all of them if their scratch fits the budget
+// (min(16 GiB, 40% of the free device memory)), else as many as fit (>= 1).
+// Results do not depend on the chunking (per-interval seeds, per-vector
+// stepper arithmetic, Gram chunking fixed by N_total).
+static int build_chunk(const Op &op, int l, int nl)
+{
+    size_t fr = 0, tot = 0;
+    size_t budget = (size_t)16 << 30;
+    if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min(budget, (size_t)(0.4 * (double)fr));
+    else cudaGetLastError();
+    const size_t per = build_bytes_per_interval(op, l);
+    long c = (long)(budget / std::max<size_t>(per, 1));
+    if (c < 1) c = 1;
+    if (c > nl) c = nl;
+    return (int)c;
+}
+
 pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local, int m, int k,
-                          int p, uint64_t seed, void *stream, pr_coarse *out)
+                          int p, uint64_t seed, pr_comm comm, void *stream, pr_coarse *out)
 {
     PR_REQUIRE(h && out, PR_EINVAL, "NULL op or out");
     const Op &op = h->op;
+    Comm *cm = comm_of(comm);
+    if (cm) {   // the canonical block partition of the intervals over the ranks
+        long f0, nl0;
+        shard_of(N_total, cm->rank, cm->world, f0, nl0);
+        first_interval = (int)f0;
+        n_local = (int)nl0;
+    }
     PR_REQUIRE(N_total >= 1 && n_local >= 1 && first_interval >= 0 &&
                    first_interval + n_local <= N_total && m >= 1 && k >= 1 && p >= 0,
-               PR_EINVAL, "bad interval range or rank");
+               PR_EINVAL, "bad interval range or rank (with a communicator: N >= world)");
     const int l = k + p;
     PR_REQUIRE(l <= 112 && l <= op.rows, PR_EDIM, "l = k + p must be <= 112 and <= rows");
     cudaStream_t s = (cudaStream_t)stream;
@@ -579,79 +629,92 @@ pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local,
     G->N_total = N_total; G->first = first_interval; G->nloc = n_local; G->m = m;
     G->k = k; G->p = p; G->l = l; G->rows = op.rows; G->dim = op.dim;
     G->stream = s;
+    G->comm = comm;
+    G->rank = cm ? cm->rank : 0;
+    G->world = cm ? cm->world : 1;
     const long rows = op.rows;
     const int nl = n_local;
     G->U = (double *)ws_alloc((size_t)nl * rows * k * sizeof(double), s);
     G->V = (double *)ws_alloc((size_t)nl * rows * k * sizeof(double), s);
     G->sigma = (double *)ws_alloc((size_t)nl * l * sizeof(double), s);
     G->C = (double *)ws_alloc((size_t)nl * k * k * sizeof(double), s);
-    G->fail = (int *)ws_alloc(2 * sizeof(int), s);
-    if (!G->U || !G->V || !G->sigma || !G->C || !G->fail) {
+    G->fail = (int *)ws_alloc(4 * sizeof(int), s);             // qr fail, svd fail, passes Y, passes Z
+    G->de = (double *)ws_alloc(2 * sizeof(double), s);
+    G->C_all = (G->world > 1) ? (double *)ws_alloc((size_t)N_total * k * k * sizeof(double), s) : G->C;
+    if (!G->U || !G->V || !G->sigma || !G->C || !G->fail || !G->de || !G->C_all) {
         pr_coarse_destroy(G);
         set_error("out of device memory");
         return PR_EOOM;
     }
     auto bail = [&](pr_status st) { pr_coarse_destroy(G); return st; };
-    cudaError_t e = cudaMemsetAsync(G->fail, 0, 2 * sizeof(int), s);
+    cudaError_t e = cudaMemsetAsync(G->fail, 0, 4 * sizeof(int), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(G->C, 0, (size_t)nl * k * k * sizeof(double), s);
     if (e != cudaSuccess) return bail(cuda_fail(e, "build init"));
+    const int nchunk = xty_chunks(rows, N_total);      // global: shard-independent arithmetic
+    const long cr = (rows + nchunk - 1) / nchunk;
     {
         Scratch S(s);
-        const long B = (long)nl * l;
-        const long ld = (op.dim == 1) ? ((B + 1) & ~1L) : rows;   // even ld: 16-B rows
-        double *Y = S.get<double>((size_t)rows * (op.dim == 1 ? ld : B));
-        double *Z = S.get<double>((size_t)rows * (op.dim == 1 ? ld : B));
-        double *Rtot = S.get<double>((size_t)nl * l * l);
-        double *Psi = S.get<double>((size_t)nl * l * l);
-        double *Phi = S.get<double>((size_t)nl * l * l);
-        if (!Y || !Z || !Rtot || !Psi || !Phi) { set_error("out of device memory"); return bail(PR_EOOM); }
-        pr_status st;
-        // step 1: Y = F' Omega (Omega generated inside the stepper)
-        st = propagate(op, PR_LINEAR, first_interval, m, (int)B, l, nullptr, nullptr, ld, Y, ld,
-                       nullptr, 0, 1, seed, s);
-        if (st != PR_OK) return bail(st);
-        stage("build step 1", s);
-        // step 2: W = orth(Y)
-        st = cholqr(op, Y, ld, nl, l, nullptr, G->fail, &G->qr_passes[0], s);
-        if (st != PR_OK) return bail(st);
-        stage("build step 2", s);
-        // step 3: Z = F'^* W
-        st = propagate(op, PR_ADJOINT, first_interval, m, (int)B, l, nullptr, Y, ld, Z, ld,
-                       nullptr, 0, 0, 0, s);
-        if (st != PR_OK) return bail(st);
-        stage("build step 3", s);
-        // Rounding-level regularisation of Z (reading R-QRF): the
-        // stepper damps its own rounding errors, so F'^* W has singular values
-        // far below u ||F'|| in the directions W does not resolve; lifting them
-        // to ~u with ||delta_c|| ~ 2^-52 (within the floating-point error of
-        // evaluating F'^* w_c, ||w_c|| = 1) saves the shifted CholeskyQR passes
-        // that would only amplify noise.  G changes by O(u sigma_1).
-        {
-            const double ndof = (op.dim == 1) ? (double)op.n : (double)op.n * op.n;
-            const double scale = ldexp(1.0, -52) / sqrt(ndof);
-            PR_CUDA(launch_sketch(op.dim, op.n, op.rows, first_interval, nl, l, seed, Z,
-                                  (op.dim == 1) ? ld : 1, (op.dim == 1) ? 1 : ld, s, scale, 1ULL));
+        const int nc = build_chunk(op, l, nl);
+        const long Bmax = (long)nc * l;
+        const long ld = (op.dim == 1) ? ((Bmax + 1) & ~1L) : rows;   // even ld: 16-B rows
+        double *Y = S.get<double>((size_t)rows * (op.dim == 1 ? ld : Bmax));
+        double *Z = S.get<double>((size_t)rows * (op.dim == 1 ? ld : Bmax));
+        double *Rtot = S.get<double>((size_t)nc * l * l);
+        double *Psi = S.get<double>((size_t)nc * l * l);
+        double *Phi = S.get<double>((size_t)nc * l * l);
+        int *pass_tmp = S.get<int>(2);
+        if (!Y || !Z || !Rtot || !Psi || !Phi || !pass_tmp) { set_error("out of device memory"); return bail(PR_EOOM); }
+        for (int c0 = 0; c0 < nl; c0 += nc) {
+            const int cn = std::min(nc, nl - c0);            // intervals of this chunk
+            const int q0 = first_interval + c0;
+            const long B = (long)cn * l;
+            pr_status st;
+            // step 1: Y = F' Omega (Omega generated from (seed, q, column))
+            st = propagate(op, PR_LINEAR, q0, m, (int)B, l, nullptr, nullptr, ld, Y, ld, nullptr, 0, 1, seed, s);
+            if (st != PR_OK) return bail(st);
+            stage("build step 1", s);
+            // step 2: W = orth(Y)
+            st = cholqr(op, Y, ld, cn, l, nullptr, G->fail, pass_tmp, nchunk, s);
+            if (st != PR_OK) return bail(st);
+            stage("build step 2", s);
+            // step 3: Z = F'^* W
+            st = propagate(op, PR_ADJOINT, q0, m, (int)B, l, nullptr, Y, ld, Z, ld, nullptr, 0, 0, 0, s);
+            if (st != PR_OK) return bail(st);
+            stage("build step 3", s);
+            // Rounding-level regularisation of Z (reading R-QRF): the
+            // stepper damps its own rounding errors, so F'^* W has singular values
+            // far below u ||F'|| in the directions W does not resolve; lifting them
+            // to ~u with ||delta_c|| ~ 2^-52 (within the floating-point error of
+            // evaluating F'^* w_c, ||w_c|| = 1) saves the shifted CholeskyQR passes
+            // that would only amplify noise.  G changes by O(u sigma_1).
+            {
+                const double ndof = (op.dim == 1) ? (double)op.n : (double)op.n * op.n;
+                const double scale = ldexp(1.0, -52) / sqrt(ndof);
+                PR_CUDA(launch_sketch(op.dim, op.n, op.rows, q0, cn, l, seed, Z, (op.dim == 1) ? ld : 1,
+                                      (op.dim == 1) ? 1 : ld, s, scale, 1ULL));
+            }
+            // step 4: V R_Z = Z
+            st = cholqr(op, Z, ld, cn, l, Rtot, G->fail, pass_tmp + 1, nchunk, s);
+            if (st != PR_OK) return bail(st);
+            stage("build step 4", s);
+            // pass counts: max over chunks
+            note_launch();
+            k_imax2<<<1, 32, 0, s>>>(pass_tmp, G->fail + 2);
+            // step 5: M = R_Z^T = Psi Sigma Phi^T
+            e = launch_jacobi(Rtot, cn, l, Psi, G->sigma + (long)c0 * l, Phi, G->fail + 1, s);
+            if (e != cudaSuccess) return bail(cuda_fail(e, "jacobi"));
+            stage("build step 5 (jacobi)", s);
+            // steps 5-6: psi = W Psi_k, phi = V Phi_k
+            Lay L = lay(op, ld);
+            const long xbs = (op.dim == 1) ? (long)l : (long)l * ld;
+            e = launch_lift(Y, xbs, L.rs, L.vs, rows, l, Psi, l, k, cn, G->U + (long)c0 * rows * k, s);
+            if (e == cudaSuccess) e = launch_lift(Z, xbs, L.rs, L.vs, rows, l, Phi, l, k, cn, G->V + (long)c0 * rows * k, s);
+            if (e != cudaSuccess) return bail(cuda_fail(e, "lift"));
+            stage("build lift", s);
         }
-        // step 4: V R_Z = Z
-        st = cholqr(op, Z, ld, nl, l, Rtot, G->fail, &G->qr_passes[1], s);
-        if (st != PR_OK) return bail(st);
-        stage("build step 4", s);
-        // step 5: M = R_Z^T = Psi Sigma Phi^T
-        e = launch_jacobi(Rtot, nl, l, Psi, G->sigma, Phi, G->fail + 1, s);
-        if (e != cudaSuccess) return bail(cuda_fail(e, "jacobi"));
-        stage("build step 5 (jacobi)", s);
-        // steps 5-6: psi = W Psi_k, phi = V Phi_k
-        Lay L = lay(op, ld);
-        const long xbs = (op.dim == 1) ? (long)l : (long)l * ld;
-        e = launch_lift(Y, xbs, L.rs, L.vs, rows, l, Psi, l, k, nl, G->U, s);
-        if (e == cudaSuccess) e = launch_lift(Z, xbs, L.rs, L.vs, rows, l, Phi, l, k, nl, G->V, s);
-        if (e != cudaSuccess) return bail(cuda_fail(e, "lift"));
-        stage("build lift", s);
-        // reduced sweep matrices C_q = Sigma_q V_q^T U_{q-1}, local q >= 1
+        // reduced sweep matrices C_q = Sigma_q V_q^T U_{q-1}, local q >= first + 1
         if (nl >= 2) {
             int nb = nl - 1;
-            int nchunk = xty_chunks(rows, nb);
-            long cr = (rows + nchunk - 1) / nchunk;
             double *part = S.get<double>((size_t)nb * nchunk * k * k);
             if (!part) { set_error("out of device memory"); return bail(PR_EOOM); }
             XtY x{nullptr, G->V + rows * k, rows * k, k, 1, k, G->U, rows * k, k, 1, k, rows, nb,
@@ -660,6 +723,37 @@ pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local,
             if (e == cudaSuccess)
                 e = launch_reduce_parts(part, nb, nchunk, k, k, G->sigma + l, l, G->C + (long)k * k, s);
             if (e != cudaSuccess) return bail(cuda_fail(e, "sweep matrices"));
+        }
+        note_launch();
+        k_delta_eps<<<1, 256, 0, s>>>(G->sigma, nl, l, k, p, G->de);
+        PR_CHECK_LAUNCH("k_delta_eps");
+        if (cm && cm->world > 1) {
+            // C_first needs the left neighbour's last U block (one boundary hop)
+            double *Uprev = S.get<double>((size_t)rows * k);
+            if (!Uprev) { set_error("out of device memory"); return bail(PR_EOOM); }
+            pr_status st = cm->shift_right(G->U + (long)(nl - 1) * rows * k, Uprev,
+                                          (size_t)rows * k * sizeof(double), s);
+            if (st != PR_OK) return bail(st);
+            if (cm->rank > 0) {
+                double *part = S.get<double>((size_t)nchunk * k * k);
+                if (!part) { set_error("out of device memory"); return bail(PR_EOOM); }
+                XtY x{nullptr, G->V, 0, k, 1, k, Uprev, 0, k, 1, k, rows, 1, nchunk, cr, part};
+                e = launch_xty(x, s);
+                if (e == cudaSuccess) e = launch_reduce_parts(part, 1, nchunk, k, k, G->sigma, 0, G->C, s);
+                if (e != cudaSuccess) return bail(cuda_fail(e, "sweep matrix C_first"));
+            }
+            // global delta, eps and every interval's sweep matrix (for the
+            // redundant k-dimensional sweep of pr_parareal)
+            st = cm->all_reduce_max(G->de, 2, s);
+            if (st != PR_OK) return bail(st);
+            std::vector<long> cnt(cm->world);
+            for (int r = 0; r < cm->world; ++r) {
+                long f0, n0;
+                shard_of(N_total, r, cm->world, f0, n0);
+                cnt[r] = n0 * k * k;
+            }
+            st = cm->all_gather_v(G->C, G->C_all, cnt.data(), sizeof(double), s);
+            if (st != PR_OK) return bail(st);
         }
     }
     *out = G;
@@ -670,26 +764,22 @@ pr_status pr_coarse_info(pr_coarse G, int *k, int *l, int *n_local, int *first_i
                          double *delta, double *eps, double *sigma_host, int *qr_passes)
 {
     PR_REQUIRE(G, PR_EINVAL, "NULL handle");
-    PR_CUDA(cudaDeviceSynchronize());
+    PR_CUDA(cudaStreamSynchronize(G->stream));
     if (k) *k = G->k;
     if (l) *l = G->l;
     if (n_local) *n_local = G->nloc;
     if (first_interval) *first_interval = G->first;
     if (m) *m = G->m;
-    if (qr_passes) { qr_passes[0] = G->qr_passes[0]; qr_passes[1] = G->qr_passes[1]; }
-    std::vector<double> sig((size_t)G->nloc * G->l);
-    PR_CUDA(cudaMemcpy(sig.data(), G->sigma, sig.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    int fl[2] = {0, 0};
+    if (sigma_host)
+        PR_CUDA(cudaMemcpy(sigma_host, G->sigma, (size_t)G->nloc * G->l * sizeof(double), cudaMemcpyDeviceToHost));
+    int fl[4] = {0, 0, 0, 0};
+    double de[2] = {0.0, 0.0};
     PR_CUDA(cudaMemcpy(fl, G->fail, sizeof fl, cudaMemcpyDeviceToHost));
-    if (sigma_host) memcpy(sigma_host, sig.data(), sig.size() * sizeof(double));
-    double dl = 0.0, ep = 0.0;
-    for (int q = 0; q < G->nloc; ++q) {
-        dl = std::max(dl, sig[(size_t)q * G->l]);
-        if (G->p > 0) ep = std::max(ep, sig[(size_t)q * G->l + G->k]);
-    }
-    if (delta) *delta = dl;
-    if (eps) *eps = (G->p > 0) ? ep : NAN;
-    if (fl[0]) { set_error("CholeskyQR broke down on the device"); return PR_ENOCONV; }
+    PR_CUDA(cudaMemcpy(de, G->de, sizeof de, cudaMemcpyDeviceToHost));
+    if (qr_passes) { qr_passes[0] = fl[2]; qr_passes[1] = fl[3]; }
+    if (delta) *delta = de[0];
+    if (eps) *eps = (G->p > 0) ? de[1] : NAN;
+    if (fl[0]) { set_error("CholeskyQR broke down or did not converge on the device"); return PR_ENOCONV; }
     if (fl[1]) { set_error("Jacobi SVD did not converge in 60 sweeps"); return PR_ENOCONV; }
     if (G->p == 0 && eps) { set_error("eps needs p >= 1"); return PR_EUNAVAIL; }
     return PR_OK;
@@ -715,6 +805,7 @@ pr_status pr_coarse_apply(pr_coarse G, int q_local, int nvec, const double *X, l
     long minld = (G->dim == 1) ? nvec : rows;
     PR_REQUIRE(ldx >= minld && ldy >= minld, PR_EDIM, "leading dimension too small");
     cudaStream_t s = (cudaStream_t)stream;
+    G->stream = s;
     Scratch S(s);
     Lay Lx = (G->dim == 1) ? Lay{ldx, 1} : Lay{1, ldx};
     Lay Ly = (G->dim == 1) ? Lay{ldy, 1} : Lay{1, ldy};
@@ -738,125 +829,207 @@ pr_status pr_coarse_destroy(pr_coarse G)
     if (!G) return PR_OK;
     cudaStream_t s = G->stream;   // ordered after the last call that used the handle
     ws_free(G->U, s); ws_free(G->V, s); ws_free(G->sigma, s); ws_free(G->C, s); ws_free(G->fail, s);
+    ws_free(G->de, s);
+    if (G->C_all != G->C) ws_free(G->C_all, s);
     delete G;
     return PR_OK;
 }
 
 // ---------------------------------------------------------------- Parareal
+// One schedule for one GPU and for an interval-sharded run (the handle's
+// communicator): rank r owns intervals q0 .. q0+nq-1 and the boundary blocks
+// 0..nq of every array (block i = boundary q0+i; block 0 is the halo = the
+// left neighbour's last block, u0 on rank 0).  Per iteration only the last
+// block of Fu and of u moves right, and the k x S reduced sweep
+// data of every interval is all-gathered so each rank runs the (cheap,
+// k-dimensional) sequential sweep over all N intervals itself (DESIGN.md
+// section 9).  With world = 1 every exchange is a no-op.
 pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_u0,
                       const pr_source *f, int K_iter, double *U_out, long ld_out, double *upd_host,
                       double *bnorm_host, double *hist, long hist_stride, void *stream)
 {
-    PR_REQUIRE(G && h && u0 && U_out, PR_EINVAL, "NULL argument");
+    PR_REQUIRE(G && h && U_out, PR_EINVAL, "NULL argument");
     const Op &op = h->op;
-    PR_REQUIRE(G->first == 0 && G->nloc == G->N_total, PR_EDIM,
-               "pr_parareal needs a coarse handle covering all intervals");
+    Comm *cm = comm_of(G->comm);
+    const int world = G->world, rank = G->rank;
+    PR_REQUIRE(world > 1 || (G->first == 0 && G->nloc == G->N_total), PR_EDIM,
+               "pr_parareal needs a coarse handle covering all intervals, or one built with a communicator");
+    PR_REQUIRE(rank > 0 || u0, PR_EINVAL, "u0 is NULL on rank 0");
     PR_REQUIRE(G->rows == op.rows && G->dim == op.dim, PR_EDIM, "coarse handle / operator mismatch");
     PR_REQUIRE(nsrc >= 1 && nsrc <= 128 && K_iter >= 0, PR_EINVAL, "nsrc must be 1..128, K_iter >= 0");
-    const int N = G->N_total, k = G->k, m = G->m, S = nsrc;
+    const int N = G->N_total, nq = G->nloc, q0 = G->first, k = G->k, m = G->m, S = nsrc;
     const long rows = op.rows;
-    const long nvec = (long)(N + 1) * S;
+    const long nvec = (long)(nq + 1) * S;             // local boundary blocks 0..nq
     long minld = (op.dim == 1) ? nvec : rows;
     PR_REQUIRE(ld_out >= minld, PR_EDIM, "ld_out too small");
-    PR_REQUIRE(ld_u0 >= (op.dim == 1 ? S : rows), PR_EDIM, "ld_u0 too small");
+    PR_REQUIRE(!u0 || ld_u0 >= (op.dim == 1 ? S : rows), PR_EDIM, "ld_u0 too small");
     {
-        pr_status st = check_source(op, f, 0, m, N);
+        pr_status st = check_source(op, f, q0, m, nq);
         if (st != PR_OK) return st;
         if (op.dim == 1 && f->kind == PR_SRC_SEP1D)
             PR_REQUIRE(f->nsrc == S, PR_EDIM, "source nsrc must equal nsrc");
     }
     cudaStream_t s = (cudaStream_t)stream;
+    G->stream = s;
     Scratch Sc(s);
     const long ld = ld_out;          // Fu and b share U_out's layout
     Lay L = lay(op, ld);
-    Lay L0 = lay(op, ld_u0);
     const size_t arr = (op.dim == 1) ? (size_t)rows * ld : (size_t)nvec * ld;
-    double *Fu, *bb, *qv, *ev, *part, *npart, *upd, *bn;
+    double *Fu, *bb, *qv, *dall, *ev, *part, *npart, *upd, *bn;
     PR_ALLOC(Fu, double, arr, Sc);
     PR_ALLOC(bb, double, arr, Sc);
-    const size_t red = (size_t)N * k * S;
-    PR_ALLOC(qv, double, red, Sc);
+    const size_t red_loc = (size_t)nq * k * S, red = (size_t)N * k * S;
+    PR_ALLOC(qv, double, red_loc, Sc);
+    dall = qv;
+    if (world > 1) PR_ALLOC(dall, double, red, Sc);
     PR_ALLOC(ev, double, red, Sc);
-    const int nchunk = xty_chunks(rows, N);
+    const int nchunk = xty_chunks(rows, N);            // global: shard-independent arithmetic
     const long cr = (rows + nchunk - 1) / nchunk;
-    PR_ALLOC(part, double, (size_t)N * nchunk * k * 2 * S, Sc);
+    PR_ALLOC(part, double, (size_t)nq * nchunk * k * 2 * S, Sc);
     PR_ALLOC(npart, double, (size_t)nvec * nchunk, Sc);
-    PR_ALLOC(upd, double, (size_t)(K_iter > 0 ? K_iter : 1) * nvec, Sc);
+    PR_ALLOC(upd, double, (size_t)(K_iter > 0 ? K_iter : 1) * nq * S, Sc);
     PR_ALLOC(bn, double, (size_t)nvec, Sc);
     const long blk = (op.dim == 1) ? (long)S : (long)S * ld;   // element offset of one block
-
-    // u^k_0 = u0 in the state and in block 0 of Fu (Fu_0 := u0)
-    PR_CUDA(launch_copy_vectors(u0, L0.rs, L0.vs, U_out, L.rs, L.vs, rows, S, s));
-    PR_CUDA(launch_copy_vectors(u0, L0.rs, L0.vs, Fu, L.rs, L.vs, rows, S, s));
-    if (op.dim == 2) {
-        // ghost entries of every block must be zero (the 2D stepper keeps them zero)
-        PR_CUDA(cudaMemsetAsync(bb, 0, (size_t)S * ld * sizeof(double), s));
+    double *hsend = nullptr, *hrecv = nullptr;                   // 1D halo staging (rows x S)
+    if (world > 1 && op.dim == 1) {
+        PR_ALLOC(hsend, double, (size_t)rows * S, Sc);
+        PR_ALLOC(hrecv, double, (size_t)rows * S, Sc);
     }
-    // offsets b_q = F_q 0 into blocks 1..N of bb
+    // block 0 of a := block nq of the left neighbour's a (rank 0 keeps its own)
+    auto halo = [&](double *a) -> pr_status {
+        if (world == 1) return PR_OK;
+        if (op.dim == 2)
+            return cm->shift_right(a + (long)nq * blk, a, (size_t)S * ld * sizeof(double), s);
+        PR_CUDA(launch_copy_vectors(a + (long)nq * blk, L.rs, L.vs, hsend, S, 1, rows, S, s));
+        pr_status st = cm->shift_right(hsend, hrecv, (size_t)rows * S * sizeof(double), s);
+        if (st != PR_OK) return st;
+        if (rank > 0) PR_CUDA(launch_copy_vectors(hrecv, S, 1, a, L.rs, L.vs, rows, S, s));
+        return PR_OK;
+    };
+    auto gather_red = [&]() -> pr_status {              // d of all intervals, in order
+        if (world == 1) return PR_OK;
+        std::vector<long> cnt(world);
+        for (int r = 0; r < world; ++r) {
+            long f0, n0;
+            shard_of(N, r, world, f0, n0);
+            cnt[r] = n0 * k * S;
+        }
+        return cm->all_gather_v(qv, dall, cnt.data(), sizeof(double), s);
+    };
+
+    // u^k_0 = u0 in the state and in block 0 of Fu (Fu_0 := u0) on rank 0
+    if (rank == 0) {
+        Lay L0 = lay(op, ld_u0);
+        PR_CUDA(launch_copy_vectors(u0, L0.rs, L0.vs, U_out, L.rs, L.vs, rows, S, s));
+        PR_CUDA(launch_copy_vectors(u0, L0.rs, L0.vs, Fu, L.rs, L.vs, rows, S, s));
+        PR_CUDA(launch_copy_vectors(u0, L0.rs, L0.vs, bb, L.rs, L.vs, rows, S, s));   // ||b_0|| := ||u0||
+    } else if (op.dim == 1) {
+        PR_CUDA(cudaMemset2DAsync(bb, ld * sizeof(double), 0, S * sizeof(double), rows, s));
+    }
+    if (op.dim == 2 && rank > 0) PR_CUDA(cudaMemsetAsync(bb, 0, (size_t)S * ld * sizeof(double), s));
+    // offsets b_q = F_q 0 into blocks 1..nq of bb
     {
-        pr_status st = propagate(op, PR_AFFINE, 0, m, N * S, S, f, nullptr, ld, bb + blk, ld,
+        pr_status st = propagate(op, PR_AFFINE, q0, m, nq * S, S, f, nullptr, ld, bb + blk, ld,
                                  nullptr, 0, 0, 0, s);
         if (st != PR_OK) return st;
     }
-    // ||b_j|| (b_0 := u0)
-    PR_CUDA(launch_copy_vectors(u0, L0.rs, L0.vs, bb, L.rs, L.vs, rows, S, s));
     PR_CUDA(launch_vecnorm_parts(bb, L.rs, L.vs, rows, (int)nvec, nchunk, cr, npart, s));
     PR_CUDA(launch_norm_finish(npart, (int)nvec, nchunk, bn, s));
-    // Fu blocks 1..N := b (initialisation uses G_q u = G'_q u + b_q)
-    PR_CUDA(launch_copy_vectors(bb + blk, L.rs, L.vs, Fu + blk, L.rs, L.vs, rows, N * S, s));
+    // Fu blocks 1..nq := b (initialisation uses G_q u = G'_q u + b_q)
+    PR_CUDA(launch_copy_vectors(bb + blk, L.rs, L.vs, Fu + blk, L.rs, L.vs, rows, nq * S, s));
+    pr_status st;
+    if ((st = halo(Fu)) != PR_OK) return st;
 
     const double *sig = G->sigma;
     // d_q = Sigma_q V_q^T (Fu[block q] - u[block q])   (one pass over V_q)
     auto project = [&](bool with_p) -> pr_status {
-        XtY x{nullptr, G->V, rows * k, k, 1, k, with_p ? U_out : Fu, blk, L.rs, L.vs, S, rows, N,
+        XtY x{nullptr, G->V, rows * k, k, 1, k, with_p ? U_out : Fu, blk, L.rs, L.vs, S, rows, nq,
               nchunk, cr, part};
         int pcols = 0;
         if (with_p) PR_CUDA(launch_xty_diff(x, Fu, S, pcols, s));
         else PR_CUDA(launch_xty(x, s));
-        PR_CUDA(launch_reduce_pq(part, N, nchunk, k, S, pcols, sig, G->l, qv, s));
-        return PR_OK;
+        PR_CUDA(launch_reduce_pq(part, nq, nchunk, k, S, pcols, sig, G->l, qv, s));
+        return gather_red();
     };
     auto expand = [&](bool norms) -> pr_status {
-        Expand ex{U_out + blk, L.rs, L.vs, Fu + blk, L.rs, L.vs, G->U, rows * k, ev, k, S, N, rows,
-                  nchunk, cr, norms ? npart + (size_t)S * nchunk : nullptr};
+        Expand ex{U_out + blk, L.rs, L.vs, Fu + blk, L.rs, L.vs, G->U, rows * k, ev + (size_t)q0 * k * S, k, S,
+                  nq, rows, nchunk, cr, norms ? npart : nullptr};
         PR_CUDA(launch_expand(ex, s));
         return PR_OK;
     };
-    pr_status st;
     // ---- initialisation: u^0_{q+1} = G_q u^0_q (p = 0)
     if ((st = project(false)) != PR_OK) return st;
-    PR_CUDA(launch_sweep(G->C, qv, N, k, S, ev, s));
+    PR_CUDA(launch_sweep(G->C_all, dall, N, k, S, ev, s));
     if ((st = expand(false)) != PR_OK) return st;
+    if ((st = halo(U_out)) != PR_OK) return st;
     stage("parareal init", s);
-    if (hist) {
-        PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, hist, L.rs, L.vs, rows, (int)nvec, s));
-    }
+    if (hist) PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, hist, L.rs, L.vs, rows, (int)nvec, s));
     // ---- iterations
     for (int it = 1; it <= K_iter; ++it) {
-        // fine solves of all intervals in one launch: Fu_{q+1} = F_q' u_q + b_q
-        st = propagate(op, PR_LINEAR, 0, m, N * S, S, nullptr, U_out, ld, Fu + blk, ld, bb + blk,
+        // fine solves of all local intervals in one launch: Fu_{q+1} = F_q' u_q + b_q
+        st = propagate(op, PR_LINEAR, q0, m, nq * S, S, nullptr, U_out, ld, Fu + blk, ld, bb + blk,
                        ld, 0, 0, s);
         if (st != PR_OK) return st;
+        if ((st = halo(Fu)) != PR_OK) return st;
         stage("parareal fine", s);
         if ((st = project(true)) != PR_OK) return st;
         stage("parareal project", s);
-        PR_CUDA(launch_sweep(G->C, qv, N, k, S, ev, s));
+        PR_CUDA(launch_sweep(G->C_all, dall, N, k, S, ev, s));
         stage("parareal sweep", s);
-        PR_CUDA(cudaMemsetAsync(npart, 0, (size_t)S * nchunk * sizeof(double), s));   // block 0
         if ((st = expand(true)) != PR_OK) return st;
+        PR_CUDA(launch_norm_finish(npart, nq * S, nchunk, upd + (size_t)(it - 1) * nq * S, s));
+        if ((st = halo(U_out)) != PR_OK) return st;
         stage("parareal expand", s);
-        PR_CUDA(launch_norm_finish(npart, (int)nvec, nchunk, upd + (size_t)(it - 1) * nvec, s));
-        if (hist) {
-            PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, hist + (size_t)it * hist_stride, L.rs,
-                                        L.vs, rows, (int)nvec, s));
-        }
+        if (hist)
+            PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, hist + (size_t)it * hist_stride, L.rs, L.vs, rows,
+                                        (int)nvec, s));
     }
-    if (upd_host && K_iter > 0)
-        PR_CUDA(cudaMemcpyAsync(upd_host, upd, (size_t)K_iter * nvec * sizeof(double),
-                                cudaMemcpyDeviceToHost, s));
-    if (bnorm_host)
-        PR_CUDA(cudaMemcpyAsync(bnorm_host, bn, (size_t)nvec * sizeof(double), cudaMemcpyDeviceToHost, s));
+    // ---- host outputs: update norms and ||b_j|| of ALL boundaries
+    std::vector<long> f0(world), n0(world);
+    for (int r = 0; r < world; ++r) shard_of(N, r, world, f0[r], n0[r]);
+    std::vector<double> hu, hb((size_t)(N + 1) * S);
+    if (upd_host && K_iter > 0) {
+        double *uall = upd;
+        if (world > 1) {
+            PR_ALLOC(uall, double, (size_t)K_iter * N * S, Sc);
+            std::vector<long> cnt(world);
+            for (int r = 0; r < world; ++r) cnt[r] = (long)K_iter * n0[r] * S;
+            if ((st = cm->all_gather_v(upd, uall, cnt.data(), sizeof(double), s)) != PR_OK) return st;
+        }
+        hu.resize((size_t)K_iter * N * S);
+        PR_CUDA(cudaMemcpyAsync(hu.data(), uall, hu.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    if (bnorm_host) {
+        double *ball = bn;
+        if (world > 1) {
+            PR_ALLOC(ball, double, (size_t)(N + 1) * S, Sc);
+            std::vector<long> cnt(world);
+            for (int r = 0; r < world; ++r) cnt[r] = (n0[r] + (r == 0 ? 1 : 0)) * S;
+            if ((st = cm->all_gather_v(rank == 0 ? bn : bn + S, ball, cnt.data(), sizeof(double), s)) != PR_OK)
+                return st;
+        }
+        PR_CUDA(cudaMemcpyAsync(hb.data(), ball, hb.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    int fl[2] = {0, 0};
+    PR_CUDA(cudaMemcpyAsync(fl, G->fail, sizeof fl, cudaMemcpyDeviceToHost, s));
     PR_CUDA(cudaStreamSynchronize(s));
+    if (upd_host && K_iter > 0) {
+        // gathered as [rank][it][i][s] -> upd_host[it][boundary][s], boundary 0 = 0
+        size_t off = 0;
+        for (int r = 0; r < world; ++r) {
+            for (int it = 0; it < K_iter; ++it)
+                for (long i = 0; i < n0[r]; ++i)
+                    for (int sI = 0; sI < S; ++sI)
+                        upd_host[((size_t)it * (N + 1) + f0[r] + i + 1) * S + sI] = hu[off++];
+        }
+        for (int it = 0; it < K_iter; ++it)
+            for (int sI = 0; sI < S; ++sI) upd_host[(size_t)it * (N + 1) * S + sI] = 0.0;
+    }
+    if (bnorm_host) memcpy(bnorm_host, hb.data(), hb.size() * sizeof(double));
+    if (fl[0] || fl[1]) {
+        set_error("the coarse handle's rSVD failed on the device (see pr_coarse_info); outputs undefined");
+        return PR_ENOCONV;
+    }
     return PR_OK;
 }
 
@@ -865,6 +1038,7 @@ pr_status pr_coarse_sweep_matrices(pr_coarse G, const double *U_prev, void *stre
 {
     PR_REQUIRE(G, PR_EINVAL, "NULL handle");
     cudaStream_t s = (cudaStream_t)stream;
+    G->stream = s;
     const long rows = G->rows;
     const int k = G->k;
     Scratch S(s);
@@ -872,7 +1046,7 @@ pr_status pr_coarse_sweep_matrices(pr_coarse G, const double *U_prev, void *stre
         PR_CUDA(cudaMemsetAsync(G->C, 0, (size_t)k * k * sizeof(double), s));
         return PR_OK;
     }
-    int nchunk = xty_chunks(rows, 1);
+    int nchunk = xty_chunks(rows, G->N_total);
     long cr = (rows + nchunk - 1) / nchunk;
     double *part;
     PR_ALLOC(part, double, (size_t)nchunk * k * k, S);
@@ -886,6 +1060,7 @@ pr_status pr_coarse_export(pr_coarse G, double *U, double *V, double *sigma, dou
 {
     PR_REQUIRE(G, PR_EINVAL, "NULL handle");
     cudaStream_t s = (cudaStream_t)stream;
+    G->stream = s;
     const size_t f = (size_t)G->nloc * G->rows * G->k * sizeof(double);
     if (U) PR_CUDA(cudaMemcpyAsync(U, G->U, f, cudaMemcpyDeviceToDevice, s));
     if (V) PR_CUDA(cudaMemcpyAsync(V, G->V, f, cudaMemcpyDeviceToDevice, s));
@@ -898,6 +1073,7 @@ pr_status pr_coarse_export_interval(pr_coarse G, int q_local, double *U_q, doubl
 {
     PR_REQUIRE(G && q_local >= 0 && q_local < G->nloc, PR_EINVAL, "bad handle or interval");
     cudaStream_t s = (cudaStream_t)stream;
+    G->stream = s;
     const size_t f = (size_t)G->rows * G->k;
     if (U_q) PR_CUDA(cudaMemcpyAsync(U_q, G->U + q_local * f, f * sizeof(double), cudaMemcpyDeviceToDevice, s));
     if (V_q) PR_CUDA(cudaMemcpyAsync(V_q, G->V + q_local * f, f * sizeof(double), cudaMemcpyDeviceToDevice, s));
@@ -913,10 +1089,11 @@ pr_status pr_coarse_project(pr_coarse G, int nsrc, const double *Y1, const doubl
     const int k = G->k, N = G->nloc, S = nsrc;
     PR_REQUIRE(ld >= (G->dim == 1 ? (long)N * S : rows), PR_EDIM, "ld too small");
     cudaStream_t s = (cudaStream_t)stream;
+    G->stream = s;
     Scratch Sc(s);
     const Lay L = (G->dim == 1) ? Lay{ld, 1} : Lay{1, ld};
     const long blk = (G->dim == 1) ? (long)S : (long)S * ld;
-    const int nchunk = xty_chunks(rows, N);
+    const int nchunk = xty_chunks(rows, G->N_total);
     const long cr = (rows + nchunk - 1) / nchunk;
     double *part;
     PR_ALLOC(part, double, (size_t)N * nchunk * k * 2 * S, Sc);
@@ -945,9 +1122,10 @@ pr_status pr_coarse_expand(pr_coarse G, int nsrc, const double *Fu, const double
     const int k = G->k, N = G->nloc, S = nsrc;
     PR_REQUIRE(ld >= (G->dim == 1 ? (long)N * S : rows), PR_EDIM, "ld too small");
     cudaStream_t s = (cudaStream_t)stream;
+    G->stream = s;
     Scratch Sc(s);
     const Lay L = (G->dim == 1) ? Lay{ld, 1} : Lay{1, ld};
-    const int nchunk = xty_chunks(rows, N);
+    const int nchunk = xty_chunks(rows, G->N_total);
     const long cr = (rows + nchunk - 1) / nchunk;
     double *npart = nullptr;
     if (upd) PR_ALLOC(npart, double, (size_t)N * S * nchunk, Sc);

@@ -177,6 +177,8 @@ struct CholArgs {
     double *offI = nullptr;           // optional per-batch ||G - I||_F of this pass (debug)
     double *shift_dbg = nullptr;      // optional per-batch final shift / ||G||_F and attempts (debug)
     double *Rinv = nullptr;           // per batch l x l: R^{-1} written for unshifted passes (act = 2)
+    int pass = 0, max_pass = 1 << 30; // this pass (1-based) and the cap: a batch still active after it fails
+    int *passes = nullptr;            // device: max pass index in which some batch was still active
 };
 cudaError_t launch_chol(const CholArgs &a, cudaStream_t s);
 cudaError_t launch_trsm(double *Q, long bs, long rs, long cs, long rows, int l, int nbatch,
@@ -228,6 +230,30 @@ cudaError_t launch_eye(double *R, int nbatch, int l, cudaStream_t s);
 cudaError_t launch_copy_vectors(const double *in, long irs, long ivs, double *out, long ors,
                                 long ovs, long rows, int nvec, cudaStream_t s);
 
+// ------------------------------------------------------------ communicator
+// (pr_comm.cu)  All operations are stream-ordered on s; see include/pr.h.
+struct Comm {
+    int rank = 0, world = 1;
+    virtual ~Comm() {}
+    // rank r sends `bytes` from send to rank r+1's recv (rank 0's recv untouched)
+    virtual pr_status shift_right(const void *send, void *recv, size_t bytes, cudaStream_t s) = 0;
+    // recv = concatenation of every rank's `bytes` of send, in rank order
+    virtual pr_status all_gather(const void *send, void *recv, size_t bytes, cudaStream_t s) = 0;
+    // elementwise max over ranks of count doubles, in place
+    virtual pr_status all_reduce_max(double *buf, int count, cudaStream_t s) = 0;
+    // concatenation of counts[r] elements (elem bytes each) of every rank r
+    pr_status all_gather_v(const void *send, void *recv, const long *counts, size_t elem, cudaStream_t s);
+};
+Comm *comm_of(pr_comm h);
+
+// contiguous block partition of total units over world ranks: (start, count) of rank
+inline void shard_of(long total, int rank, int world, long &start, long &count)
+{
+    const long base = total / world, rem = total % world;
+    start = rank * base + (rank < rem ? rank : rem);
+    count = base + (rank < rem ? 1 : 0);
+}
+
 // 2D separable stepper (k_sep2d.cu)
 struct Sep2dArgs {
     const Op *op;
@@ -258,4 +284,8 @@ struct pr_coarse_s {
     int *fail = nullptr;       // device flags [0]: qr, [1]: svd
     int qr_passes[2] = {0, 0};
     cudaStream_t stream = nullptr;   // stream of the last call that used the handle (destroy is ordered on it)
+    pr_comm comm = nullptr;          // the communicator the handle was built with (not owned)
+    int rank = 0, world = 1;
+    double *de = nullptr;            // device [delta, eps]: max over ALL ranks' intervals
+    double *C_all = nullptr;         // (N_total, k, k) sweep matrices of all intervals (== C at world 1)
 };

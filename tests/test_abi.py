@@ -53,6 +53,11 @@ def test_validation_before_launch(L):
     assert b"dt" in L.pr_last_error()
     assert L.pr_fine_propagate(None, 0, 0, 1, 1, 1, None, None, 0, None, 0, None, 0, None) == _lib.PR_EINVAL
     assert L.pr_bounds(0.5, 0.1, 0, 1, None, None, None, None, None) == _lib.PR_EINVAL
+    hs = (ctypes.c_void_p * 2)()
+    assert L.pr_comm_create_local(0, hs) == _lib.PR_EINVAL
+    assert L.pr_comm_info(None, None, None) == _lib.PR_EINVAL
+    assert L.pr_comm_create_nccl(2, 2, None, ctypes.byref(h)) == _lib.PR_EINVAL
+    assert L.pr_build_coarse(None, 4, 0, 4, 1, 1, 0, 0, None, None, ctypes.byref(h)) == _lib.PR_EINVAL
 
 
 def test_pr_bounds_matches_oracle_formulas(L):

@@ -51,7 +51,10 @@ def _stepper_path(pr_env, path):
                                         ("T4", 301, 16, 33), ("T4", 37, 7, 64), ("T1", 200, 12, 70),
                                         ("C1", 64, 5, 33), ("C2", 513, 7, 9), ("C4", 16384, 3, 17),
                                         ("C2", 4095, 256, 10), ("C2", 8192, 20, 3),
-                                        ("C4", 16383, 128, 6)])
+                                        ("C4", 16383, 128, 6),
+                                        # non-symmetric A: F'^* is a different map
+                                        ("T4N", 301, 16, 33), ("C4N", 4095, 64, 9),
+                                        ("C4N", 16383, 128, 6)])
 @pytest.mark.parametrize("mode", ["linear", "adjoint"])
 @pytest.mark.parametrize("path", ["fused", "part"])
 def test_fine_linear_adjoint(name, n, m, B, mode, path, pr_env):
@@ -132,7 +135,23 @@ def _check_interval(cfg, Gg, q, info, probes=6):
         assert np.linalg.norm(got[v] - ref[v]) <= TAU_1D * s1 * np.linalg.norm(X[v])
 
 
-@pytest.mark.parametrize("name", ["C1", "T1", "T1k1", "T4"])
+@pytest.mark.parametrize("name", ["C4N", "T4N"])
+def test_adjoint_differs_from_forward_nonsymmetric(name):
+    """On the convection-diffusion operator F'^* != F' (by ~beta h / kappa),
+    so the adjoint parity above would catch a forward/transpose mix-up."""
+    from paper_2508_08873_b200 import PR_ADJOINT, PR_LINEAR
+    cfg = get(name)
+    op_g = gpu_op(cfg)
+    X = np.random.default_rng(5).standard_normal((4, cfg.n))
+    a, b = empty_batch(cfg, 4), empty_batch(cfg, 4)
+    op_g.fine_propagate(PR_LINEAR, 0, cfg.m, to_gpu(cfg, X), a)
+    op_g.fine_propagate(PR_ADJOINT, 0, cfg.m, to_gpu(cfg, X), b)
+    fa, fb = from_gpu(cfg, a), from_gpu(cfg, b)
+    for v in range(4):
+        assert relnorm(fa[v], fb[v]) > 1e-6
+
+
+@pytest.mark.parametrize("name", ["C1", "T1", "T1k1", "T4", "T4N"])
 def test_build_all_intervals(name):
     from paper_2508_08873_b200 import Coarse
     cfg = get(name)
@@ -145,7 +164,7 @@ def test_build_all_intervals(name):
     assert info["eps"] == np.max(sig[:, cfg.k])
 
 
-@pytest.mark.parametrize("name,qs", [("C2", (0, 31, 63)), ("C4", (0, 255))])
+@pytest.mark.parametrize("name,qs", [("C2", (0, 31, 63)), ("C4", (0, 255)), ("C4N", (0, 255))])
 def test_build_full_size_sampled_intervals(name, qs):
     from paper_2508_08873_b200 import Coarse
     cfg = get(name)
@@ -187,7 +206,7 @@ def _run_parareal(cfg, K=None, keep_hist=True):
     return Gg, info, Uo, hist, upd, bn, u0
 
 
-@pytest.mark.parametrize("name", ["T1", "T4", "T1k1", "C1"])
+@pytest.mark.parametrize("name", ["T1", "T4", "T1k1", "C1", "T4N"])
 def test_parareal_all_iterates_match_oracle(name):
     cfg = get(name)
     Gg, info, Uo, hist, upd, bn, u0 = _run_parareal(cfg)

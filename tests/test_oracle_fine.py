@@ -255,3 +255,33 @@ def test_rowsum_pivots_are_condition_independent():
     rel_plain = np.max(np.abs(plain - ref)) / np.max(np.abs(ref))
     assert rel_acc < 50 * cfg.m * 1.1e-16
     assert rel_plain > 10 * rel_acc
+
+
+def test_convection_diffusion_operator_and_adjoint_dense():
+    """The test-only non-symmetric operator (T4N): the assembled A is the upwind
+    convection-diffusion stencil (independently re-evaluated here), its exact
+    row / column sums match, and the oracle's F' and F'^* equal the dense
+    (I + dt A)^{-m} and its transpose (adjoint = transposed steps in reverse
+    order), which differ by far more than rounding."""
+    from workloads.generators import BETA_CD
+    cfg = replace(get("T4N"), n=40, m=7)
+    op = make_op(cfg)
+    h = cfg.h
+    A = op.dense_A()
+    x = G.grid_1d(cfg.n)
+    kap = lambda y: 1.0 + 0.5 * np.sin(2.0 * np.pi * y)
+    for i in (0, 17, cfg.n - 1):
+        km, kp = kap(x[i] - h / 2), kap(x[i] + h / 2)
+        assert A[i, i] == pytest.approx((km + kp) / h ** 2 + BETA_CD / h + 0.5, rel=1e-14)
+        if i > 0:
+            assert A[i, i - 1] == pytest.approx(-km / h ** 2 - BETA_CD / h, rel=1e-14)
+        if i < cfg.n - 1:
+            assert A[i, i + 1] == pytest.approx(-kp / h ** 2, rel=1e-14)
+    rs, cs = G.operator_1d_sums(cfg)
+    np.testing.assert_allclose(A.sum(axis=1), rs, rtol=1e-9, atol=1e-9 * np.abs(A).max())
+    np.testing.assert_allclose(A.sum(axis=0), cs, rtol=1e-9, atol=1e-9 * np.abs(A).max())
+    F = np.linalg.matrix_power(np.linalg.inv(np.eye(cfg.n) + cfg.dt * A), cfg.m)
+    X = np.random.default_rng(9).standard_normal((3, cfg.n))
+    np.testing.assert_allclose(fine(op, 1, X, "linear"), X @ F.T, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(fine(op, 1, X, "adjoint"), X @ F, rtol=0, atol=1e-12)
+    assert np.linalg.norm(F - F.T) > 1e-4 * np.linalg.norm(F)

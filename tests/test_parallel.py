@@ -1,8 +1,10 @@
-"""Multi-process (gloo, CPU) tests of the interval-sharded Parareal orchestration
-(paper_2508_08873_b200/parallel.py): the halo/all-gather schedule must give
-bit-identical results for world sizes 1, 2 and 4, and agree with the oracle's
-direct Parareal.  The stages run on a test-only numpy backend with
-the same semantics as the CUDA library's distributed building blocks."""
+"""Multi-process (gloo, CPU) tests of the interval-sharded schedule: the
+executable model of libpr's sharded pr_parareal (tests/sched_model.py) must
+give bit-identical results for world sizes 1, 2, 3 (uneven shards) and 4, and
+agree with the oracle's direct Parareal.  The stages run on a
+test-only numpy backend with the semantics of the CUDA library's stages.  Also
+the communicator bootstrap of paper_2508_08873_b200/parallel.py (NCCL unique
+id made on rank 0 and broadcast) with a host-only stand-in for the library."""
 import os
 import socket
 
@@ -13,7 +15,8 @@ import torch
 from oracle.fine import fine, make_op
 from oracle.parareal import parareal as oracle_parareal
 from oracle.rsvd import rsvd_interval
-from paper_2508_08873_b200.parallel import Blocks, Comm, parareal_sharded, shard
+from paper_2508_08873_b200.parallel import nccl_comm, shard
+from sched_model import Blocks, TorchComm, parareal_sharded
 from workloads import generators as G
 from workloads.configs import get
 
@@ -102,7 +105,7 @@ def _run(rank, world, outdir, port):
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
         torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
-    comm = Comm()
+    comm = TorchComm()
     q0, nq = shard(cfg.N, comm.rank, comm.world)
     be = NumpyBackend(cfg, truncs, q0, nq)
     blocks = Blocks(1, cfg.n, cfg.nsrc, "cpu")
@@ -138,7 +141,7 @@ def _gather(outdir, world, cfg):
 def runs(tmp_path_factory):
     out = str(tmp_path_factory.mktemp("par"))
     _run(0, 1, out, 0)
-    for world in (2, 4):
+    for world in (2, 3, 4):
         torch.multiprocessing.spawn(_run, args=(world, out, _free_port()), nprocs=world, join=True)
     return out
 
@@ -146,7 +149,7 @@ def runs(tmp_path_factory):
 def test_sharded_parareal_is_world_size_invariant(runs):
     cfg = get(CFG)
     u1, upd1 = _gather(runs, 1, cfg)
-    for world in (2, 4):
+    for world in (2, 3, 4):
         uw, updw = _gather(runs, world, cfg)
         np.testing.assert_array_equal(uw, u1)
         np.testing.assert_array_equal(updw, upd1)
@@ -170,3 +173,35 @@ def test_shard_partition():
             assert sum(c for _, c in spans) == total
             for (s0, c0), (s1, _) in zip(spans, spans[1:]):
                 assert s0 + c0 == s1
+
+
+class _FakeComm:
+    """Host-only stand-in for paper_2508_08873_b200.Comm (no NCCL, no GPU)."""
+    made = []
+
+    @staticmethod
+    def nccl_unique_id():
+        return bytes(range(128))
+
+    @classmethod
+    def nccl(cls, rank, world, uid):
+        return (rank, world, uid)
+
+
+def _boot(rank, world, outdir, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.distributed.init_process_group("gloo", rank=rank, world_size=world)
+    r, w, uid = nccl_comm(api=_FakeComm)
+    np.save(os.path.join(outdir, f"boot_{rank}.npy"), np.frombuffer(uid, dtype=np.uint8))
+    assert (r, w) == (rank, world)
+    torch.distributed.destroy_process_group()
+
+
+def test_nccl_bootstrap_broadcasts_rank0_id(tmp_path):
+    """Every rank joins with rank 0's unique id (the other ranks never make one)."""
+    world = 3
+    torch.multiprocessing.spawn(_boot, args=(world, str(tmp_path), _free_port()), nprocs=world, join=True)
+    for r in range(world):
+        got = np.load(os.path.join(str(tmp_path), f"boot_{r}.npy"))
+        np.testing.assert_array_equal(got, np.arange(128, dtype=np.uint8))

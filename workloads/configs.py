@@ -89,7 +89,11 @@ T1 = replace(C1, name="T1", n=200, N=8, m=12, k=3, p=2, K=6)
 T1_K1 = replace(C1, name="T1k1", n=157, N=6, m=10, k=1, p=1, K=6)
 T4 = replace(C4, name="T4", n=301, N=8, m=16, k=4, p=4, K=6, nsrc=5)
 T2D = replace(C3, name="T2D", n=63, N=6, m=10, k=6, p=3, K=5)
-VARIANTS = {c.name: c for c in (T1, T1_K1, T4, T2D)}
+# non-symmetric (convection-diffusion) operators: A != A^T, so F'^* is a true
+# transposed solve (rSVD step 3) -- small and at C4's grid
+T4N = replace(C4, name="T4N", problem="convection_diffusion", n=301, N=8, m=16, k=4, p=4, K=6, nsrc=5)
+C4N = replace(C4, name="C4N", problem="convection_diffusion")
+VARIANTS = {c.name: c for c in (T1, T1_K1, T4, T2D, T4N, C4N)}
 
 
 def get(name: str) -> Config:

@@ -20,6 +20,8 @@ import numpy as np
 
 from .configs import Config
 
+BETA_CD = 20.0      # advection speed of the test-only convection_diffusion operator
+
 
 # --------------------------------------------------------------------------- grid
 def grid_1d(n: int) -> np.ndarray:
@@ -41,6 +43,11 @@ def operator_1d(cfg: Config):
     heat (C1, C2):            A = tridiag(-1, 2, -1) / h^2                (Z2)
     reaction_diffusion (C4):  A u = -(kappa u_x)_x + 0.5 u, kappa at the
                               midpoints x_{i+-1/2}, conservative form    (Z2)
+    convection_diffusion (test-only T4N / C4N, non-symmetric):
+                              C4's operator plus beta u_x, beta = 20, upwind
+                              (u_i - u_{i-1}) / h -- an M-matrix with A != A^T,
+                              so F' is not normal and F'^* != F' (the regime
+                              of Exp 2)
     """
     n, h = cfg.n, cfg.h
     if cfg.problem == "heat":
@@ -54,6 +61,13 @@ def operator_1d(cfg: Config):
         km, kp = kap[:-1], kap[1:]          # kappa_{i-1/2}, kappa_{i+1/2}
         diag = (km + kp) / (h * h) + 0.5
         sub = -km / (h * h)
+        sup = -kp / (h * h)
+    elif cfg.problem == "convection_diffusion":
+        xf = (np.arange(n + 1, dtype=np.float64) + 0.5) * h
+        kap = 1.0 + 0.5 * np.sin(2.0 * np.pi * xf)
+        km, kp = kap[:-1], kap[1:]
+        diag = (km + kp) / (h * h) + BETA_CD / h + 0.5
+        sub = -km / (h * h) - BETA_CD / h
         sup = -kp / (h * h)
     else:
         raise ValueError(cfg.problem)
@@ -81,6 +95,19 @@ def operator_1d_sums(cfg: Config):
         rs = np.full(n, 0.5)
         rs[0] += kap[0] / (h * h)
         rs[-1] += kap[-1] / (h * h)
+    elif cfg.problem == "convection_diffusion":
+        # interior rows and columns sum to the reaction coefficient 0.5 (the
+        # advection stencil -beta/h, +beta/h cancels in both directions); the
+        # boundary rows / columns keep the eliminated Dirichlet couplings
+        xf = (np.arange(n + 1, dtype=np.float64) + 0.5) * h
+        kap = 1.0 + 0.5 * np.sin(2.0 * np.pi * xf)
+        rs = np.full(n, 0.5)
+        rs[0] += kap[0] / (h * h) + BETA_CD / h
+        rs[-1] += kap[-1] / (h * h)
+        cs = np.full(n, 0.5)
+        cs[0] += kap[0] / (h * h)
+        cs[-1] += kap[-1] / (h * h) + BETA_CD / h
+        return rs, cs
     else:
         raise ValueError(cfg.problem)
     return rs, rs.copy()
