@@ -173,25 +173,26 @@ class Workload:
         return self.U
 
 
-def _fp64_alu_peak(dev):
-    """FP64 vector (DFMA) ceiling from unit counts and the clock: SMs x 4 sub-
-    partitions x 16 DFMA lanes/clk (measured: 2.1 cycles per DFMA warp-
-    instruction per sub-partition) x 2 flops x max SM clock (MEASURED_PEAKS.json)."""
-    import torch
-    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+def _fp64_peaks(dev):
+    """Measured FP64 ceilings of this pool's B200 (profiles/fp64_peaks.json,
+    written by tools/fp64_peaks.py: DFMA and DMMA microkernels and cuBLAS
+    DGEMM 8192^3); MEASURED_PEAKS.json carries no FP64 figure.  Falls back to
+    a live DGEMM measurement and the unit-count DFMA figure, saying so."""
     try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            mhz = float(json.load(f)["sm_max_mhz"])
-        src = "derived: SMs x 64 DFMA/clk x 2 flops x sm_max_mhz (MEASURED_PEAKS.json)"
+        with open(os.path.join(ROOT, "profiles", "fp64_peaks.json")) as f:
+            d = json.load(f)
+        return {"dfma": float(d["dfma_tflops"]), "dgemm": float(d["dgemm_tflops"]),
+                "dmma": float(d.get("dmma_m8n8k4_tflops", 0.0)),
+                "source": "measured (profiles/fp64_peaks.json, tools/fp64_peaks.py)"}
     except Exception:
-        mhz = 1965.0
-        src = "derived: SMs x 64 DFMA/clk x 2 flops x 1965 MHz (fallback clock)"
-    return sms * 64 * 2 * mhz * 1e6 / 1e12, src
+        import torch
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        return {"dfma": sms * 64 * 2 * 1965e6 / 1e12, "dgemm": _fp64_peak(dev), "dmma": 0.0,
+                "source": "fallback: DFMA from unit counts x 1965 MHz, DGEMM measured live"}
 
 
 def _fp64_peak(dev):
-    """Measured FP64 ceiling on this GPU: cuBLAS DGEMM 8192^3 (best of 5, CUDA
-    events).  MEASURED_PEAKS.json carries no FP64 figure."""
+    """cuBLAS DGEMM 8192^3 measured live (best of 5, CUDA events)."""
     import torch
     n = 8192
     a = torch.randn((n, n), dtype=torch.float64, device=dev)
@@ -248,6 +249,49 @@ def oracle_sample(cfg):
     return float(dof), dt
 
 
+def _host_info():
+    """CPU model (lscpu) and the number of host threads the oracle may use."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.lower().startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "threads_used": _cores()}
+
+
+def oracle_one_thread(cfg):
+    """Per-core rate of the oracle: the rSVD forward solves of one interval
+    (l vectors x m steps, the oracle's fine solver as it stands) with one
+    thread, in a subprocess with OMP / BLAS pinned to 1 thread."""
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    try:
+        out = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-1t", "--config", cfg.name],
+                             capture_output=True, text=True, timeout=300, env=env).stdout
+        return json.loads(out.strip().splitlines()[-1])
+    except Exception as e:
+        return {"error": str(e)[:200]}
+
+
+def _oracle_1t_main(cfg):
+    from oracle import _clib
+    from oracle.fine import fine, make_op
+    _clib.build()
+    op = make_op(cfg)
+    nv = min(cfg.l, 16) if cfg.dim == 2 else cfg.l
+    shape = (nv, cfg.n) if cfg.dim == 1 else (nv, cfg.n, cfg.n)
+    X = np.random.default_rng(0).standard_normal(shape)
+    t0 = time.perf_counter()
+    fine(op, 1, X, "linear")
+    sec = time.perf_counter() - t0
+    dof = float(nv * cfg.n_dof * cfg.m)
+    print(json.dumps({"value": dof / sec, "unit": "DOF-steps/s", "threads": 1,
+                      "sample": f"{nv} fine solves (F' of interval 1, {cfg.m} steps): {dof:.3g} DOF-steps in {sec:.2f} s"}))
+
+
 def _cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -265,10 +309,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sub", action="store_true", help="skip the C3 (2D) sub-record")
+    ap.add_argument("--oracle-1t", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
 
     from workloads.configs import get
     cfg = get(args.config)
+    if args.oracle_1t:
+        _oracle_1t_main(cfg)
+        return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -300,7 +349,7 @@ def main():
                 "data": "synthetic (seeded generators, workloads/)", "config": config,
                 "impl": "reference",
                 "cpu_baseline": {"value": value, "unit": "DOF-steps/s", "cores": _cores(),
-                                 "kind": "oracle", "sample": sample},
+                                 "kind": "oracle", "sample": sample, "host": _host_info()},
                 "e2e": {"value": value, "unit": "DOF-steps/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -323,54 +372,116 @@ def main():
         torch.cuda.synchronize()
 
     wl = Workload(cfg, rank, world, dev)
-    for _ in range(args.warmup):
-        wl.step()
-    barrier()
-
-    # ---------------------------------------------------- timed device run
+    peaks = _fp64_peaks(dev)
     sampler = ClockSampler(local_rank)
     sampler.start()
+    rec = _timed(wl, args.steps, args.warmup, barrier, world, dev, peaks)
+    clocks = sampler.stop()
+    value, ms_per_step, dof_total = rec["value"], rec["ms_per_step"], rec["dof_steps_per_step"]
+    roofline = rec.pop("roofline")
+
+    # ------------------------------------------------------------- e2e run
+    e2e = None
+    if not args.no_e2e:
+        e2e = _e2e(wl, args.steps, barrier, world)
+
+    # ------------------------------------------- 2D sub-record (C3, 1 GPU)
+    sub = None
+    if world == 1 and cfg.name != "C3" and not args.no_sub:
+        from workloads.configs import get as _get
+        c3 = _get("C3")
+        del wl
+        torch.cuda.empty_cache()
+        wl3 = Workload(c3, rank, world, dev)
+        sub = {"workload": "C3", "note": "the 2D (FP64 tensor-core) path: BASELINE.json configs[2], "
+                                         "same step definition, timed after the headline workload"}
+        sub.update(_timed(wl3, args.steps, args.warmup, barrier, world, dev, peaks))
+        del wl3
+
+    # --------------------------------------------------------- CPU baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import _clib
+        _clib.build()
+        dof, sec = oracle_sample(cfg)
+        cpu = {"value": dof / sec, "unit": "DOF-steps/s", "cores": _cores(), "kind": "oracle",
+               "sample": f"rSVD of interval 1 + {cfg.K + 1} fine solves of interval 1 x "
+                         f"{cfg.nsrc} sources ({dof:.3g} DOF-steps, {sec:.1f} s)",
+               "host": _host_info(), "one_thread": oracle_one_thread(cfg)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "DOF-steps/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (seeded generators, workloads/)",
+                "config": config,
+                "build_ms": rec["build_ms"], "parareal_ms": rec["parareal_ms"],
+                "dof_steps_per_step": dof_total, "phases": rec["phases"],
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": rec["gpu_launches"], "clocks": clocks,
+                "fp64_peaks": peaks}
+        if sub is not None:
+            line["sub"] = sub
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def _timed(wl, steps, warmup, barrier, world, dev, peaks):
+    """W untimed steps, then K steps bracketed by barrier + synchronize, max
+    over ranks; device time per step, per-phase fine-solve rates (SURVEY §8(d)
+    "Definitions") and the roofline of the dominant fine-stepper kernel."""
+    import torch
+    from paper_2508_08873_b200 import counters, profile
+    from paper_2508_08873_b200.api import phase_counters
+    cfg = wl.cfg
+    for _ in range(warmup):
+        wl.step()
+    barrier()
     counters(reset=True)
     profile(True)
     barrier()
     ev = [_event()]
     mid = []
-    for _ in range(args.steps):
+    for _ in range(steps):
         wl.step(events=mid)
         ev.append(_event())
     barrier()
     profile(False)
-    clocks = sampler.stop()
     total_ms = ev[0].elapsed_time(ev[-1])
-    build_ms = [ev[i].elapsed_time(mid[i]) for i in range(args.steps)]
-    par_ms = [mid[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
+    build_ms = [ev[i].elapsed_time(mid[i]) for i in range(steps)]
+    par_ms = [mid[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    ph = phase_counters(reset=False)
     ctr = counters(reset=True)
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         import torch.distributed as dist
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
-    dof_total = wl.dof_steps() * world if world == 1 else _sum_dof(wl, world)
-    value = dof_total / (ms_per_step / 1e3)
-
-    # ------------------------------------------- roofline of the fine stepper
+    ms_per_step = total_ms / steps
+    dof_total = wl.dof_steps() if world == 1 else _sum_dof(wl, world)
+    phases = {}
+    for name in ("build", "offsets", "iteration"):
+        p = ph[name]
+        if p["launches"]:
+            phases[name] = {"launches_per_step": p["launches"] / steps, "ms_per_step": p["ms"] / steps,
+                            "dof_steps_per_s": p["dof_steps"] / (p["ms"] / 1e3) if p["ms"] > 0 else None}
     st_ms = ctr["stepper_ms"] / max(ctr["stepper_launches"], 1)
     st_dof = ctr["stepper_dof_steps"] / max(ctr["stepper_launches"], 1)
     st_fl = ctr["stepper_flops"] / max(ctr["stepper_launches"], 1)
     if cfg.dim == 1 and st_fl > 0:
-        # K1P (partitioned stepper): the state stays on chip for all m steps, so
-        # HBM carries only the input and output (16 B per DOF per launch); the
-        # bound is the FP64 pipe, 5 algorithmic flops per DOF-step
-        peak, src = _fp64_alu_peak(dev)
+        # K1P: the state stays on chip for all m steps, so HBM carries only the
+        # input and output (16 B per DOF per launch); the bound is the FP64
+        # pipe: 5 algorithmic flops per DOF-step (+2R with an R-term source)
         achieved = st_fl / (st_ms / 1e3) / 1e12 if st_ms > 0 else None
         roofline = {"kernel": "k_part_step (K1P, cluster-partitioned implicit Euler, state in registers)",
-                    "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": (achieved / peak) if achieved else None,
+                    "bound": "alu", "achieved": achieved, "peak": peaks["dfma"], "unit": "TFLOP/s",
+                    "frac": (achieved / peaks["dfma"]) if achieved else None,
                     "traffic": _ncu_traffic(cfg.name),
                     "algorithmic_flops_per_launch": st_fl,
                     "algorithmic_bytes_per_launch": 16.0 * st_dof / cfg.m,
-                    "peak_source": src}
+                    "peak_source": "FP64 FMA pipe, " + peaks["source"]}
     elif cfg.dim == 1:
         peak, peak_kind = _peaks()
         achieved = 16.0 * st_dof / (st_ms / 1e3) / 1e9 if st_ms > 0 else None
@@ -381,48 +492,21 @@ def main():
                     "algorithmic_bytes_per_launch": 16.0 * st_dof,
                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
     else:
-        peak = _fp64_peak(dev)
         achieved = st_fl / (st_ms / 1e3) / 1e12 if st_ms > 0 else None
         roofline = {"kernel": "k_gemm_st (K2, FP64 DMMA sine-transform passes + fused Euler steps)",
-                    "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": (achieved / peak) if achieved else None,
+                    "bound": "tensor", "achieved": achieved, "peak": peaks["dgemm"], "unit": "TFLOP/s",
+                    "frac": (achieved / peaks["dgemm"]) if achieved else None,
                     "traffic": _ncu_traffic(cfg.name),
                     "algorithmic_flops_per_launch": st_fl,
-                    "peak_source": "measured live: cuBLAS DGEMM 8192^3 (fp64 has no entry in "
-                                   "MEASURED_PEAKS.json)"}
+                    "peak_source": "cuBLAS DGEMM 8192^3, " + peaks["source"],
+                    "dmma_pipe_peak": peaks.get("dmma")}
     roofline.update({"launches_timed": ctr["stepper_launches"],
                      "ms_per_launch": st_ms,
                      "share_of_step": ctr["stepper_ms"] / total_ms if total_ms > 0 else None})
-
-    # ------------------------------------------------------------- e2e run
-    e2e = None
-    if not args.no_e2e:
-        e2e = _e2e(wl, args.steps, barrier, world)
-
-    # --------------------------------------------------------- CPU baseline
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        from oracle import _clib
-        _clib.build()
-        dof, sec = oracle_sample(cfg)
-        cpu = {"value": dof / sec, "unit": "DOF-steps/s", "cores": _cores(), "kind": "oracle",
-               "sample": f"rSVD of interval 1 + {cfg.K + 1} fine solves of interval 1 x "
-                         f"{cfg.nsrc} sources ({dof:.3g} DOF-steps, {sec:.1f} s)"}
-
-    if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "DOF-steps/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic (seeded generators, workloads/)",
-                "config": config,
-                "build_ms": statistics.median(build_ms), "parareal_ms": statistics.median(par_ms),
-                "dof_steps_per_step": dof_total,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": ctr["kernel_launches"], "clocks": clocks}
-        print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
-        dist.destroy_process_group()
+    return {"value": dof_total / (ms_per_step / 1e3), "ms_per_step": ms_per_step,
+            "build_ms": statistics.median(build_ms), "parareal_ms": statistics.median(par_ms),
+            "dof_steps_per_step": dof_total, "phases": phases, "roofline": roofline,
+            "gpu_launches": ctr["kernel_launches"]}
 
 
 def _sum_dof(wl, world):

@@ -82,6 +82,13 @@ pr_status pr_profile(int enable);
 pr_status pr_counters(int reset, long *kernel_launches, long *stepper_launches, double *stepper_ms,
                       double *stepper_dof_steps, double *stepper_flops);
 
+/* The same timed fine-propagation launches split by the phase that issued
+ * them (SURVEY §8(d) "Definitions": build fwd+adj, offsets b_n, Parareal
+ * iterations): arrays of PR_NPHASES entries (host, nullable), indexed by
+ * PR_PHASE_*.  reset != 0 clears the timed launches afterwards. */
+enum { PR_PHASE_DIRECT = 0, PR_PHASE_BUILD = 1, PR_PHASE_OFFSETS = 2, PR_PHASE_ITERATION = 3, PR_NPHASES = 4 };
+pr_status pr_phase_counters(int reset, long *launches, double *ms, double *dof_steps);
+
 typedef struct pr_op_s *pr_op;
 typedef struct pr_coarse_s *pr_coarse;
 typedef struct pr_comm_s *pr_comm;

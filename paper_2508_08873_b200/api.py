@@ -304,6 +304,18 @@ def counters(reset: bool = False) -> dict:
                 stepper_dof_steps=dof.value, stepper_flops=fl.value)
 
 
+PHASES = ("direct", "build", "offsets", "iteration")
+
+
+def phase_counters(reset: bool = False) -> dict:
+    """Timed fine-propagation launches per phase (pr_phase_counters)."""
+    n = (ctypes.c_long * 4)()
+    ms = (ctypes.c_double * 4)()
+    dof = (ctypes.c_double * 4)()
+    check(L.lib().pr_phase_counters(1 if reset else 0, n, ms, dof), "pr_phase_counters")
+    return {name: dict(launches=n[i], ms=ms[i], dof_steps=dof[i]) for i, name in enumerate(PHASES)}
+
+
 def reduced_sweep(C, d, N: int, k: int, nsrc: int, e, stream=None):
     check(L.lib().pr_reduced_sweep(_ptr(C), _ptr(d), int(N), int(k), int(nsrc), _ptr(e),
                                    _stream(stream)), "pr_reduced_sweep")

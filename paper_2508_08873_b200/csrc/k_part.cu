@@ -788,8 +788,12 @@ cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose,
         }
     }
     // algorithmic FP64 flops per DOF-step: Thomas with precomputed factors,
-    // y = w r - ga y' (3) and x = y - cp x' (2)  (bench.py roofline)
-    if (prof) stepper_timed_end(s, (double)sa.n * (double)sa.B * (double)sa.m, 5.0 * (double)sa.n * (double)sa.B * (double)sa.m);
+    // y = w r - ga y' (3) and x = y - cp x' (2), plus 2R for an R-term source
+    // (bench.py roofline)
+    if (prof) {
+        const double dof = (double)sa.n * (double)sa.B * (double)sa.m;
+        stepper_timed_end(s, dof, (5.0 + 2.0 * a.R) * dof);
+    }
     if (want_prof && e == cudaSuccess) {
         unsigned long long h[1024 * 4];
         cudaMemcpyAsync(h, dprof, sizeof(h), cudaMemcpyDeviceToHost, s);

@@ -143,10 +143,19 @@ static std::atomic<int> g_prof{0};
 struct TimedLaunch {
     cudaEvent_t a, b;
     double dof_steps, flops;
+    int phase;
 };
 static std::mutex g_prof_mu;
 static std::vector<TimedLaunch> g_timed;
 static thread_local cudaEvent_t g_pending_begin = nullptr;
+static thread_local int g_phase = PR_PHASE_DIRECT;
+
+// phase of the fine-propagation launches issued by this thread (pr_phase_counters)
+struct PhaseScope {
+    int saved;
+    explicit PhaseScope(int p) : saved(g_phase) { g_phase = p; }
+    ~PhaseScope() { g_phase = saved; }
+};
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 bool profiling() { return g_prof.load(std::memory_order_relaxed) != 0; }
@@ -166,7 +175,7 @@ void stepper_timed_end(cudaStream_t s, double dof_steps, double flops)
     if (cudaEventCreate(&e) != cudaSuccess) return;
     cudaEventRecord(e, s);
     std::lock_guard<std::mutex> lk(g_prof_mu);
-    g_timed.push_back({g_pending_begin, e, dof_steps, flops});
+    g_timed.push_back({g_pending_begin, e, dof_steps, flops, g_phase});
     g_pending_begin = nullptr;
 }
 
@@ -390,6 +399,33 @@ pr_status pr_counters(int reset, long *kernel_launches, long *stepper_launches, 
     if (stepper_dof_steps) *stepper_dof_steps = dof;
     if (reset) {
         for (auto &t : g_timed) { cudaEventDestroy(t.a); cudaEventDestroy(t.b); }
+        g_timed.clear();
+        g_launches.store(0);
+    }
+    return PR_OK;
+}
+
+pr_status pr_phase_counters(int reset, long *launches, double *ms, double *dof_steps)
+{
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    long n[PR_NPHASES] = {0};
+    double t[PR_NPHASES] = {0.0}, d[PR_NPHASES] = {0.0};
+    for (auto &x : g_timed) {
+        float f = 0.f;
+        cudaEventSynchronize(x.b);
+        if (cudaEventElapsedTime(&f, x.a, x.b) == cudaSuccess && x.phase >= 0 && x.phase < PR_NPHASES) {
+            n[x.phase] += 1;
+            t[x.phase] += f;
+            d[x.phase] += x.dof_steps;
+        }
+    }
+    for (int i = 0; i < PR_NPHASES; ++i) {
+        if (launches) launches[i] = n[i];
+        if (ms) ms[i] = t[i];
+        if (dof_steps) dof_steps[i] = d[i];
+    }
+    if (reset) {
+        for (auto &x : g_timed) { cudaEventDestroy(x.a); cudaEventDestroy(x.b); }
         g_timed.clear();
         g_launches.store(0);
     }
@@ -652,6 +688,7 @@ pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local,
     if (e != cudaSuccess) return bail(cuda_fail(e, "build init"));
     const int nchunk = xty_chunks(rows, N_total);      // global: shard-independent arithmetic
     const long cr = (rows + nchunk - 1) / nchunk;
+    PhaseScope phase(PR_PHASE_BUILD);
     {
         Scratch S(s);
         const int nc = build_chunk(op, l, nl);
@@ -929,6 +966,7 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
     if (op.dim == 2 && rank > 0) PR_CUDA(cudaMemsetAsync(bb, 0, (size_t)S * ld * sizeof(double), s));
     // offsets b_q = F_q 0 into blocks 1..nq of bb
     {
+        PhaseScope phase(PR_PHASE_OFFSETS);
         pr_status st = propagate(op, PR_AFFINE, q0, m, nq * S, S, f, nullptr, ld, bb + blk, ld,
                                  nullptr, 0, 0, 0, s);
         if (st != PR_OK) return st;
@@ -967,6 +1005,7 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
     // ---- iterations
     for (int it = 1; it <= K_iter; ++it) {
         // fine solves of all local intervals in one launch: Fu_{q+1} = F_q' u_q + b_q
+        PhaseScope phase(PR_PHASE_ITERATION);
         st = propagate(op, PR_LINEAR, q0, m, nq * S, S, nullptr, U_out, ld, Fu + blk, ld, bb + blk,
                        ld, 0, 0, s);
         if (st != PR_OK) return st;
