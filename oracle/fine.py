@@ -127,7 +127,7 @@ def fine_2d(op: Op2D, interval: int, X: np.ndarray, mode: str = "linear", src=No
         return fine_2d(op, interval, X[None], mode, src)[0]
     nvec, n = X.shape[0], op.n
     S = op.S
-    V = np.ascontiguousarray(np.einsum("ij,bjk->bik", S, X))      # x-transform
+    V = np.ascontiguousarray(np.matmul(S, X))                     # x-transform: S along the x index
     shift = np.tile(op.dt * op.lam, nvec)
     for j in range(1, op.m + 1):
         if mode == "affine" and src is not None:
@@ -136,7 +136,7 @@ def fine_2d(op: Op2D, interval: int, X: np.ndarray, mode: str = "linear", src=No
             Sg = S @ gx[:, g - 1, :].T                                 # (n, nb)
             V += op.dt * (Sg @ gy[:, g - 1, :])[None]                  # S f_g
         thomas_batch(*op.Ty, V.reshape(nvec * n, n), shift, rowsum=op.Ty_rs)
-    return np.einsum("ij,bjk->bik", S, V)
+    return np.matmul(S, V)
 
 
 class Op2DBanded:

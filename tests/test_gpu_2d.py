@@ -130,6 +130,7 @@ def _parareal_2d(cfg, hist_on=True):
     Uo = empty_batch(cfg, cfg.N + 1)
     hist = torch.zeros((cfg.K + 1,) + tuple(Uo.shape), dtype=torch.float64, device="cuda") if hist_on else None
     upd, bn = parareal(Gg, opg, to_gpu(cfg, u0), gpu_source(cfg), cfg.K, Uo, nsrc=1, hist=hist)
+    _parareal_2d.last_info = Gg.info()
     return Uo, hist, upd, bn, u0
 
 
@@ -205,3 +206,48 @@ def test_lifted_factors_orthonormal_2d():
         assert float((V.T @ V - I).abs().max()) < 1e-13
         P = cfg.n + 1
         assert float(U.view(P, P, cfg.k)[0].abs().max()) == 0.0      # ghosts stay zero
+
+
+def _parareal_vs_oracle_iterates(cfg, kmax, tau):
+    """Every iterate u^k_n, k <= kmax, and the update norms of the GPU's
+    Parareal (reduced sweep) against the oracle's direct form on
+    the oracle's own per-interval rSVDs (parallel worker pool)."""
+    from oracle_pool import rsvd_intervals
+    Uo, hist, upd, bn, u0 = _parareal_2d(cfg)
+    info = _parareal_2d.last_info
+    truncs = rsvd_intervals(cfg)
+    sig = np.stack([t.sigma for t in truncs])
+    assert np.max(np.abs(info["sigma"] - sig)) <= tau * sig.max()
+    op_o = make_op(cfg)
+    res = oracle_parareal(op_o, truncs, u0, cfg.N, kmax, G.source_2d(cfg))
+    scale = np.max(np.linalg.norm(res.U.reshape(kmax + 1, cfg.N + 1, -1), axis=-1))
+    errs = []
+    for k in range(kmax + 1):
+        got = from_gpu(cfg, hist[k]).reshape(cfg.N + 1, -1)
+        err = np.max(np.linalg.norm(got - res.U[k][:, 0].reshape(cfg.N + 1, -1), axis=-1))
+        errs.append(err / scale)
+        assert err <= tau * scale, (k, err / scale)
+    assert np.max(np.abs(upd[:kmax, :, 0] - res.upd[1:kmax + 1, :, 0])) <= tau * scale
+    return errs, res
+
+
+@pytest.mark.timeout(1200)
+def test_parareal_c3_iterates_k0_to_3_match_oracle():
+    """C3 is the configuration whose Parareal really iterates (SURVEY A.5:
+    relative error 4e-4 at k = 0 to ~1e-10 at k = 2): iterates 0..3 of the
+    full-size run against the oracle's direct form."""
+    from dataclasses import replace as _r
+    cfg = _r(C3, K=3)
+    errs, res = _parareal_vs_oracle_iterates(cfg, 3, TAU_2D)
+    # the iteration really moves: the k = 0 iterate is far from the converged one
+    scale = np.max(np.abs(res.U))
+    assert np.max(np.abs(res.U[0] - res.U[3])) > 1e-6 * scale
+
+
+@pytest.mark.timeout(1800)
+def test_parareal_c5_geometry_matches_oracle():
+    """C5's 511^2 grid, k = 96, p = 16 on 16 intervals: build and all Parareal
+    iterates against the oracle (BASELINE.json configs[4] geometry)."""
+    from workloads.configs import get as _get
+    cfg = _get("C5G")
+    _parareal_vs_oracle_iterates(cfg, cfg.K, TAU_2D)
