@@ -230,9 +230,23 @@ pr_status pr_gaussian_sketch(pr_op op, int first_interval, int n_intervals, int 
  * Asynchronous (no host synchronisation: the CholeskyQR pass loop is
  * controlled on the device, at most 24 passes); errors detected on the device
  * (no convergence) are reported by pr_coarse_info and pr_parareal.
+ * opts (nullable = the paper's basic algorithm, both fields 0):
+ *   power_iterations q (0..16): W = span{(F' F'^*)^q F' omega_i},
+ *     evaluated as q rounds of orthonormalise / F'^* / orthonormalise / F'
+ *     (same span; 2q more batched fine solves per interval);
+ *   independent_adjoint (0/1): step 3 applies F'^* to an independent Gaussian
+ *     set Psi (Philox counter word 3 = 2) instead of w_1..w_l, so the forward
+ *     and adjoint solves are independent; G' then comes from the
+ *     two-sided sketch F' ~ W C V^T, C = (Psi^T W)^{-1} R_Z^T (Z = F'^* Psi =
+ *     V R_Z), whose SVD replaces step 5's M.  Less accurate (the paper says so).
  * Errors: EINVAL, EDIM (l > 112 or l > rows), EOOM, ENCCL. */
+typedef struct {
+    int power_iterations;
+    int independent_adjoint;
+} pr_rsvd_opts;
 pr_status pr_build_coarse(pr_op op, int N_total, int first_interval, int n_local, int m,
-                          int k, int p, uint64_t seed, pr_comm comm, void *stream, pr_coarse *out);
+                          int k, int p, uint64_t seed, const pr_rsvd_opts *opts, pr_comm comm,
+                          void *stream, pr_coarse *out);
 
 /* Synchronizes with the stream of the handle's last call.  k, l, n_local,
  * first_interval, m; delta = max_q sigma_{q,1} and eps = max_q sigma_{q,k+1}

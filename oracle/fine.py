@@ -167,6 +167,15 @@ def fine_2d_banded(op: Op2DBanded, interval: int, X: np.ndarray, mode: str = "li
     return V.reshape(nvec, n, n)
 
 
+class DenseOp:
+    """A linear F' given by its matrix (tests only: operators with a prescribed
+    SVD for the rSVD pins).  mode 'linear' applies F, 'adjoint' F^T."""
+
+    def __init__(self, F: np.ndarray):
+        self.F = np.asarray(F, dtype=np.float64)
+        self.n = self.F.shape[0]
+
+
 # ---------------------------------------------------------------- dispatch
 def make_op(cfg):
     from workloads import generators as G
@@ -178,6 +187,9 @@ def make_op(cfg):
 
 
 def fine(op, interval, X, mode="linear", src=None, src_index=None):
+    if isinstance(op, DenseOp):
+        X = np.asarray(X, dtype=np.float64)
+        return X @ (op.F if mode == "adjoint" else op.F.T)
     if isinstance(op, Op1D):
         return fine_1d(op, interval, X, mode, src, src_index)
     return fine_2d(op, interval, X, mode, src)

@@ -6,7 +6,8 @@ large to pass in (C5: 1.5e10 values), so the CUDA path and this oracle each
 implement the same counter-based generator (reading R-RNG):
 
   Philox4x64-10 (Salmon et al., SC'11), key = (seed, 0),
-  counter = (i // 4, c, q, 0)   for row i, column c (0..l-1), interval q (0-based);
+  counter = (i // 4, c, q, s)   for row i, column c (0..l-1), interval q (0-based),
+                                stream s (0: Omega; 2: the independent adjoint sketch);
   the four 64-bit outputs x0..x3 give rows 4*(i//4) + 0..3 by Box-Muller:
       u1 = ((x0 >> 11) + 1) * 2^-53  in (0, 1],   u2 = (x1 >> 11) * 2^-53,
       z0 = sqrt(-2 ln u1) cos(2 pi u2),  z1 = sqrt(-2 ln u1) sin(2 pi u2),
@@ -69,12 +70,14 @@ def _box_muller(xa, xb):
     return r * np.cos(th), r * np.sin(th)
 
 
-def gaussian_sketch(seed: int, interval: int, nrows: int, ncols: int) -> np.ndarray:
-    """Omega_q (nrows x ncols), i.i.d. N(0,1), for 0-based interval q."""
+def gaussian_sketch(seed: int, interval: int, nrows: int, ncols: int, stream: int = 0) -> np.ndarray:
+    """Omega_q (nrows x ncols), i.i.d. N(0,1), for 0-based interval q.  The
+    fourth counter word selects an independent stream (0: the sketch Omega of
+    step 1; 2: the independent adjoint sketch Psi)."""
     nb = (nrows + 3) // 4
     blk = np.arange(nb, dtype=np.uint64)[:, None]
     col = np.arange(ncols, dtype=np.uint64)[None, :]
-    x0, x1, x2, x3 = philox4x64_10(blk, col, np.uint64(interval), np.uint64(0), seed, 0)
+    x0, x1, x2, x3 = philox4x64_10(blk, col, np.uint64(interval), np.uint64(stream), seed, 0)
     z0, z1 = _box_muller(x0, x1)
     z2, z3 = _box_muller(x2, x3)
     out = np.stack([z0, z1, z2, z3], axis=1).reshape(nb * 4, ncols)

@@ -24,7 +24,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .fine import Op1D, fine
+from .fine import DenseOp, Op1D, fine
 from .linalg import householder_qr, jacobi_svd
 from .rng import gaussian_sketch
 
@@ -44,7 +44,7 @@ class Truncated:
 
 def _as_vectors(op, cols: np.ndarray) -> np.ndarray:
     """(n_dof, l) column block -> fine-solver batch layout."""
-    if isinstance(op, Op1D):
+    if isinstance(op, (Op1D, DenseOp)):
         return np.ascontiguousarray(cols.T)
     n = op.n
     return np.ascontiguousarray(cols.T.reshape(-1, n, n))
@@ -54,23 +54,43 @@ def _as_columns(op, vecs: np.ndarray) -> np.ndarray:
     return np.ascontiguousarray(vecs.reshape(vecs.shape[0], -1).T)
 
 
-def rsvd_interval(op, interval: int, k: int, p: int, seed: int) -> Truncated:
-    """Steps 1-6 for the 1-based interval n = `interval`."""
+def rsvd_interval(op, interval: int, k: int, p: int, seed: int, power_iterations: int = 0,
+                  independent_adjoint: bool = False) -> Truncated:
+    """Steps 1-6 for the 1-based interval n = `interval`.
+
+    power_iterations q: W = span{(F' F'^*)^q F' omega_i}, evaluated
+    with an orthonormalisation (Householder) between the applications -- the
+    same span in exact arithmetic (reading R-POW).
+    independent_adjoint: step 3 applies F'^* to an independent
+    Gaussian set Psi (stream 2) instead of the w_i; with Z = F'^* Psi and
+    V = orth(Z), F' is approximated by W C V^T where C solves the two-sided
+    sketch equation Psi^T W C = Psi^T F' V = Z^T V (Martinsson & Tropp's
+    reconstruction, reading R-IND), and C replaces M of step 5."""
     l = k + p
-    n_dof = op.n if isinstance(op, Op1D) else op.n * op.n
+    n_dof = op.n if isinstance(op, Op1D) else (op.F.shape[0] if isinstance(op, DenseOp) else op.n * op.n)
     # step 1
     Omega = gaussian_sketch(seed, interval - 1, n_dof, l)
     Y = _as_columns(op, fine(op, interval, _as_vectors(op, Omega), "linear"))
+    for _ in range(power_iterations):
+        Qy, _ = householder_qr(Y)
+        Qz, _ = householder_qr(_as_columns(op, fine(op, interval, _as_vectors(op, Qy), "adjoint")))
+        Y = _as_columns(op, fine(op, interval, _as_vectors(op, Qz), "linear"))
     # step 2
     W, _ = householder_qr(Y)
-    # step 3
-    Z = _as_columns(op, fine(op, interval, _as_vectors(op, W), "adjoint"))
-    # step 4
-    Vb, _ = householder_qr(Z)
-    # step 5: M_ij = (F'^* w_i, v_j)
-    M = Z.T @ Vb
-    Psi, sig, Phi = jacobi_svd(M)
-    U = W @ Psi[:, :k]
+    if not independent_adjoint:
+        # step 3
+        Z = _as_columns(op, fine(op, interval, _as_vectors(op, W), "adjoint"))
+        # step 4
+        Vb, _ = householder_qr(Z)
+        # step 5: M_ij = (F'^* w_i, v_j)
+        M = Z.T @ Vb
+    else:
+        Psi = gaussian_sketch(seed, interval - 1, n_dof, l, stream=2)
+        Z = _as_columns(op, fine(op, interval, _as_vectors(op, Psi), "adjoint"))
+        Vb, _ = householder_qr(Z)
+        M = np.linalg.solve(Psi.T @ W, Z.T @ Vb)
+    Psi_, sig, Phi = jacobi_svd(M)
+    U = W @ Psi_[:, :k]
     V = Vb @ Phi[:, :k]
     # step 6
     return Truncated(U=U, sigma=sig, V=V, k=k)
@@ -85,7 +105,7 @@ def exact_truncated(Fdense: np.ndarray, k: int) -> Truncated:
 
 def dense_transfer(op, interval: int = 1, mode: str = "linear") -> np.ndarray:
     """Matrix of F_n' by applying it to every unit vector (tiny grids only)."""
-    n_dof = op.n if isinstance(op, Op1D) else op.n * op.n
+    n_dof = op.n if isinstance(op, Op1D) else (op.F.shape[0] if isinstance(op, DenseOp) else op.n * op.n)
     E = np.eye(n_dof)
     return _as_columns(op, fine(op, interval, _as_vectors(op, E), mode))
 

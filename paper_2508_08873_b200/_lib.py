@@ -43,6 +43,10 @@ class Source(ctypes.Structure):
                 ("gx", ctypes.c_void_p), ("gy", ctypes.c_void_p)]
 
 
+class RsvdOpts(ctypes.Structure):
+    _fields_ = [("power_iterations", ctypes.c_int), ("independent_adjoint", ctypes.c_int)]
+
+
 _lib = None
 
 
@@ -68,7 +72,7 @@ def lib():
             "pr_op_info": ([vp, ctypes.POINTER(lg), ip, ip], I),
             "pr_fine_propagate": ([vp, I, I, I, I, I, ctypes.POINTER(Source), vp, lg, vp, lg, vp, lg, vp], I),
             "pr_gaussian_sketch": ([vp, I, I, I, U64, vp, lg, vp], I),
-            "pr_build_coarse": ([vp, I, I, I, I, I, I, U64, vp, vp, ctypes.POINTER(vp)], I),
+            "pr_build_coarse": ([vp, I, I, I, I, I, I, U64, ctypes.POINTER(RsvdOpts), vp, vp, ctypes.POINTER(vp)], I),
             "pr_coarse_info": ([vp, ip, ip, ip, ip, ip, dp, dp, dp, ip], I),
             "pr_coarse_factors": ([vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)], I),
             "pr_coarse_apply": ([vp, I, I, vp, lg, vp, lg, vp], I),

@@ -188,12 +188,15 @@ class Coarse:
     @classmethod
     def build(cls, op: Operator, N_total: int, m: int, k: int, p: int, seed: int,
               first_interval: int = 0, n_local: int = None, comm: "Comm" = None,
-              stream=None) -> "Coarse":
+              stream=None, power_iterations: int = 0, independent_adjoint: bool = False) -> "Coarse":
         if n_local is None:
             n_local = N_total - first_interval
         h = ctypes.c_void_p()
+        opts = None
+        if power_iterations or independent_adjoint:
+            opts = ctypes.byref(L.RsvdOpts(int(power_iterations), 1 if independent_adjoint else 0))
         check(L.lib().pr_build_coarse(op._h, int(N_total), int(first_interval), int(n_local),
-                                      int(m), int(k), int(p), ctypes.c_uint64(int(seed)),
+                                      int(m), int(k), int(p), ctypes.c_uint64(int(seed)), opts,
                                       comm._h if comm is not None else None,
                                       _stream(stream), ctypes.byref(h)), "pr_build_coarse")
         return cls(h, comm, int(N_total))

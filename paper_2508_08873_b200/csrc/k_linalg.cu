@@ -2165,3 +2165,106 @@ cudaError_t launch_eye(double *R, int nbatch, int l, cudaStream_t s)
 }
 
 }  // namespace pr
+
+namespace pr {
+
+// ----------------------------------------------- small pivoted LU solve
+// One CTA per batch: A X = R^T (l x l, row-major in global memory), written as
+// X^T.  A in shared memory is eliminated column by column with partial
+// pivoting (row swaps applied to the right-hand side too), then the l
+// right-hand sides are back-substituted one per thread.
+constexpr int LU_THREADS = 256;
+
+__global__ void __launch_bounds__(LU_THREADS) k_lu_solve_rt(const double *Ag, const double *Rg, int l, double *XT,
+                                                            int *fail)
+{
+    extern __shared__ __align__(16) double sm[];
+    double *A = sm;                  // l x l
+    double *Bm = sm + (size_t)l * l; // l x l right-hand sides, Bm[i*l + c]
+    __shared__ int piv;
+    __shared__ double pv[LU_THREADS];
+    __shared__ int pi[LU_THREADS];
+    const int b = blockIdx.x;
+    const long per = (long)l * l;
+    for (int e = threadIdx.x; e < l * l; e += LU_THREADS) {
+        A[e] = Ag[b * per + e];
+        const int i = e / l, c = e % l;
+        Bm[e] = Rg[b * per + (long)c * l + i];        // R^T
+    }
+    __syncthreads();
+    for (int j = 0; j < l; ++j) {
+        // pivot: max |A[i][j]|, i >= j (fixed-order tree reduction)
+        double best = -1.0;
+        int bi = j;
+        for (int i = j + threadIdx.x; i < l; i += LU_THREADS) {
+            const double v = fabs(A[i * l + j]);
+            if (v > best) { best = v; bi = i; }
+        }
+        pv[threadIdx.x] = best;
+        pi[threadIdx.x] = bi;
+        __syncthreads();
+        for (int w = LU_THREADS / 2; w > 0; w >>= 1) {
+            if (threadIdx.x < w) {
+                const double o = pv[threadIdx.x + w];
+                const int oi = pi[threadIdx.x + w];
+                if (o > pv[threadIdx.x] || (o == pv[threadIdx.x] && oi < pi[threadIdx.x])) {
+                    pv[threadIdx.x] = o;
+                    pi[threadIdx.x] = oi;
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            piv = pi[0];
+            if (!(pv[0] > 0.0) || !isfinite(pv[0])) atomicExch(fail, 1);
+        }
+        __syncthreads();
+        const int r = piv;
+        if (r != j) {
+            for (int c = threadIdx.x; c < l; c += LU_THREADS) {
+                double t = A[j * l + c]; A[j * l + c] = A[r * l + c]; A[r * l + c] = t;
+                t = Bm[j * l + c]; Bm[j * l + c] = Bm[r * l + c]; Bm[r * l + c] = t;
+            }
+        }
+        __syncthreads();
+        const double d = A[j * l + j];
+        const double inv = (d != 0.0) ? 1.0 / d : 0.0;
+        // eliminate rows below j (multipliers stored in A's column j)
+        for (int i = j + 1 + threadIdx.x; i < l; i += LU_THREADS) A[i * l + j] *= inv;
+        __syncthreads();
+        const int rem = l - j - 1;
+        for (int e = threadIdx.x; e < rem * l; e += LU_THREADS) {
+            const int i = j + 1 + e / l, c = e % l;
+            const double mlt = A[i * l + j];
+            if (c > j) A[i * l + c] -= mlt * A[j * l + c];
+            Bm[i * l + c] -= mlt * Bm[j * l + c];
+        }
+        __syncthreads();
+    }
+    // back substitution, one right-hand side per thread: U x = y
+    for (int c = threadIdx.x; c < l; c += LU_THREADS) {
+        for (int i = l - 1; i >= 0; --i) {
+            double t = Bm[i * l + c];
+            for (int k2 = i + 1; k2 < l; ++k2) t -= A[i * l + k2] * Bm[k2 * l + c];
+            Bm[i * l + c] = t / A[i * l + i];
+        }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < l * l; e += LU_THREADS) {
+        const int i = e / l, c = e % l;
+        XT[b * per + (long)c * l + i] = Bm[e];        // X^T
+    }
+}
+
+cudaError_t launch_lu_solve_rt(const double *A, const double *R, int nbatch, int l, double *XT, int *fail,
+                               cudaStream_t s)
+{
+    const size_t smem = (size_t)2 * l * l * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(k_lu_solve_rt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    note_launch();
+    k_lu_solve_rt<<<nbatch, LU_THREADS, smem, s>>>(A, R, l, XT, fail);
+    return cudaGetLastError();
+}
+
+}  // namespace pr

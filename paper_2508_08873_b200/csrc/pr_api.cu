@@ -302,14 +302,14 @@ static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double 
 static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi,
                            const pr_source *f, const double *in, long ld_in, double *out,
                            long ld_out, const double *off, long ld_off, int sketch,
-                           unsigned long long seed, cudaStream_t s)
+                           unsigned long long seed, cudaStream_t s, unsigned long long ctr3 = 0ULL)
 {
     if (B == 0) return PR_OK;
     if (op.dim == 2) {
         Sep2dArgs a{&op, mode, q0, m, B, vpi, f, in, ld_in, out, ld_out, off, ld_off};
         if (sketch) {
             PR_CUDA(cudaMemset2DAsync(out, ld_out * sizeof(double), 0, op.rows * sizeof(double), B, s));
-            PR_CUDA(launch_sketch(2, op.n, op.rows, q0, B / vpi, vpi, seed, out, 1, ld_out, s));
+            PR_CUDA(launch_sketch(2, op.n, op.rows, q0, B / vpi, vpi, seed, out, 1, ld_out, s, 0.0, ctr3));
             a.in = out;
             a.ld_in = ld_out;
         }
@@ -320,7 +320,7 @@ static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi
         // Omega materialised by the fully parallel generator, then stepped in place
         // (a thread-serial Philox inside the stepper's first pass costs more than
         // the extra write + read)
-        PR_CUDA(launch_sketch(1, op.n, op.rows, q0, B / vpi, vpi, seed, out, ld_out, 1, s));
+        PR_CUDA(launch_sketch(1, op.n, op.rows, q0, B / vpi, vpi, seed, out, ld_out, 1, s, 0.0, ctr3));
         in = out;
         ld_in = ld_out;
         sketch = 0;
@@ -643,9 +643,14 @@ static int build_chunk(const Op &op, int l, int nl)
 }
 
 pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local, int m, int k,
-                          int p, uint64_t seed, pr_comm comm, void *stream, pr_coarse *out)
+                          int p, uint64_t seed, const pr_rsvd_opts *opts, pr_comm comm, void *stream,
+                          pr_coarse *out)
 {
     PR_REQUIRE(h && out, PR_EINVAL, "NULL op or out");
+    const int qpow = opts ? opts->power_iterations : 0;
+    const int indep = opts ? opts->independent_adjoint : 0;
+    PR_REQUIRE(qpow >= 0 && qpow <= 16 && (indep == 0 || indep == 1), PR_EINVAL,
+               "power_iterations must be 0..16 and independent_adjoint 0 or 1");
     const Op &op = h->op;
     Comm *cm = comm_of(comm);
     if (cm) {   // the canonical block partition of the intervals over the ranks
@@ -710,12 +715,29 @@ pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local,
             st = propagate(op, PR_LINEAR, q0, m, (int)B, l, nullptr, nullptr, ld, Y, ld, nullptr, 0, 1, seed, s);
             if (st != PR_OK) return bail(st);
             stage("build step 1", s);
+            // power iterations: W = span{(F' F'^*)^q F' omega}, with
+            // re-orthonormalisation between the applications (same span, stable)
+            for (int it = 0; it < qpow; ++it) {
+                st = cholqr(op, Y, ld, cn, l, nullptr, G->fail, pass_tmp, nchunk, s);
+                if (st == PR_OK)
+                    st = propagate(op, PR_ADJOINT, q0, m, (int)B, l, nullptr, Y, ld, Z, ld, nullptr, 0, 0, 0, s);
+                if (st == PR_OK) st = cholqr(op, Z, ld, cn, l, nullptr, G->fail, pass_tmp, nchunk, s);
+                if (st == PR_OK)
+                    st = propagate(op, PR_LINEAR, q0, m, (int)B, l, nullptr, Z, ld, Y, ld, nullptr, 0, 0, 0, s);
+                if (st != PR_OK) return bail(st);
+            }
             // step 2: W = orth(Y)
             st = cholqr(op, Y, ld, cn, l, nullptr, G->fail, pass_tmp, nchunk, s);
             if (st != PR_OK) return bail(st);
             stage("build step 2", s);
-            // step 3: Z = F'^* W
-            st = propagate(op, PR_ADJOINT, q0, m, (int)B, l, nullptr, Y, ld, Z, ld, nullptr, 0, 0, 0, s);
+            // step 3: Z = F'^* W -- or, with independent_adjoint,
+            // Z = F'^* Psi on an independent Gaussian set (Philox stream 2),
+            // which needs no result of steps 1-2
+            if (indep)
+                st = propagate(op, PR_ADJOINT, q0, m, (int)B, l, nullptr, nullptr, ld, Z, ld, nullptr, 0, 1, seed, s,
+                               2ULL);
+            else
+                st = propagate(op, PR_ADJOINT, q0, m, (int)B, l, nullptr, Y, ld, Z, ld, nullptr, 0, 0, 0, s);
             if (st != PR_OK) return bail(st);
             stage("build step 3", s);
             // Rounding-level regularisation of Z (reading R-QRF): the
@@ -725,8 +747,9 @@ pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local,
             // evaluating F'^* w_c, ||w_c|| = 1) saves the shifted CholeskyQR passes
             // that would only amplify noise.  G changes by O(u sigma_1).
             {
+                // columns of W have norm 1; those of Psi ~ sqrt(ndof)
                 const double ndof = (op.dim == 1) ? (double)op.n : (double)op.n * op.n;
-                const double scale = ldexp(1.0, -52) / sqrt(ndof);
+                const double scale = indep ? ldexp(1.0, -52) : ldexp(1.0, -52) / sqrt(ndof);
                 PR_CUDA(launch_sketch(op.dim, op.n, op.rows, q0, cn, l, seed, Z, (op.dim == 1) ? ld : 1,
                                       (op.dim == 1) ? 1 : ld, s, scale, 1ULL));
             }
@@ -737,8 +760,30 @@ pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local,
             // pass counts: max over chunks
             note_launch();
             k_imax2<<<1, 32, 0, s>>>(pass_tmp, G->fail + 2);
-            // step 5: M = R_Z^T = Psi Sigma Phi^T
-            e = launch_jacobi(Rtot, cn, l, Psi, G->sigma + (long)c0 * l, Phi, G->fail + 1, s);
+            // step 5: M = R_Z^T = Psi Sigma Phi^T  (M_ij = (F'^* w_i, v_j))
+            const double *Mt = Rtot;            // k_jacobi takes M^T (row-major)
+            if (indep) {
+                // single-view two-sided sketch: F' ~ W C V^T with Psi^T W C = Z^T V
+                // = R_Z^T, i.e. C = (Psi^T W)^{-1} R_Z^T; M := C (Martinsson & Tropp's
+                // reconstruction from the independent adjoint sketch)
+                double *Psi_b = S.get<double>((size_t)rows * (op.dim == 1 ? ld : Bmax));
+                double *A = S.get<double>((size_t)cn * l * l);
+                double *part = S.get<double>((size_t)cn * nchunk * l * l);
+                double *Ct = S.get<double>((size_t)cn * l * l);
+                if (!Psi_b || !A || !part || !Ct) { set_error("out of device memory"); return bail(PR_EOOM); }
+                Lay L = lay(op, ld);
+                const long xbs = (op.dim == 1) ? (long)l : (long)l * ld;
+                if (op.dim == 2)
+                    PR_CUDA(cudaMemset2DAsync(Psi_b, ld * sizeof(double), 0, rows * sizeof(double), B, s));
+                PR_CUDA(launch_sketch(op.dim, op.n, op.rows, q0, cn, l, seed, Psi_b, L.rs, L.vs, s, 0.0, 2ULL));
+                XtY x{nullptr, Psi_b, xbs, L.rs, L.vs, l, Y, xbs, L.rs, L.vs, l, rows, cn, nchunk, cr, part};
+                PR_CUDA(launch_xty(x, s));
+                PR_CUDA(launch_reduce_parts(part, cn, nchunk, l, l, nullptr, 0, A, s));
+                // Ct = C^T from A C = R_Z^T (pivoted LU, one CTA per interval)
+                PR_CUDA(launch_lu_solve_rt(A, Rtot, cn, l, Ct, G->fail + 1, s));
+                Mt = Ct;
+            }
+            e = launch_jacobi(Mt, cn, l, Psi, G->sigma + (long)c0 * l, Phi, G->fail + 1, s);
             if (e != cudaSuccess) return bail(cuda_fail(e, "jacobi"));
             stage("build step 5 (jacobi)", s);
             // steps 5-6: psi = W Psi_k, phi = V Phi_k

@@ -189,6 +189,11 @@ cudaError_t launch_rinv_apply(double *Q, long bs, long rs, long cs, long rows, i
 
 cudaError_t launch_jacobi(const double *Rtot, int nbatch, int l, double *Psi, double *sigma,
                           double *Phi, int *fail, cudaStream_t s);
+// per batch b: X_b^T with A_b X_b = R_b^T (A, R, out: l x l row-major; R upper),
+// Gaussian elimination with partial pivoting in shared memory; *fail on a
+// zero pivot
+cudaError_t launch_lu_solve_rt(const double *A, const double *R, int nbatch, int l, double *XT, int *fail,
+                               cudaStream_t s);
 
 // out_b[row, r] = sum_j X_b[row, j] * C_b[j, r]  (j < l, r < k); out is (nbatch, rows, k)
 cudaError_t launch_lift(const double *X, long xbs, long xrs, long xcs, long rows, int l,

@@ -57,7 +57,7 @@ def test_validation_before_launch(L):
     assert L.pr_comm_create_local(0, hs) == _lib.PR_EINVAL
     assert L.pr_comm_info(None, None, None) == _lib.PR_EINVAL
     assert L.pr_comm_create_nccl(2, 2, None, ctypes.byref(h)) == _lib.PR_EINVAL
-    assert L.pr_build_coarse(None, 4, 0, 4, 1, 1, 0, 0, None, None, ctypes.byref(h)) == _lib.PR_EINVAL
+    assert L.pr_build_coarse(None, 4, 0, 4, 1, 1, 0, 0, None, None, None, ctypes.byref(h)) == _lib.PR_EINVAL
 
 
 def test_pr_bounds_matches_oracle_formulas(L):

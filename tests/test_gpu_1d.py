@@ -269,3 +269,27 @@ def test_lifted_factors_orthonormal_and_deterministic(name):
         assert float((U.T @ U - I).abs().max()) < 1e-13
         assert float((V.T @ V - I).abs().max()) < 1e-13
         assert torch.equal(U, U2) and torch.equal(V, V2)
+
+
+@pytest.mark.parametrize("q,indep", [(1, False), (0, True), (2, True)])
+@pytest.mark.parametrize("name", ["C1", "T4", "T4N"])
+def test_build_rsvd_variants_match_oracle(name, q, indep):
+    """Power iterations and the independent adjoint sketch
+    (P:335-337): every interval's sigma and G_q' against the oracle's variant."""
+    from paper_2508_08873_b200 import Coarse
+    cfg = get(name)
+    Gg = Coarse.build(gpu_op(cfg), cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega, power_iterations=q,
+                      independent_adjoint=indep)
+    info = Gg.info()
+    op_o = make_op(cfg)
+    for qi in range(cfg.N):
+        tr = rsvd_interval(op_o, qi + 1, cfg.k, cfg.p, cfg.seed_omega, power_iterations=q,
+                           independent_adjoint=indep)
+        s1 = tr.sigma[0]
+        assert np.max(np.abs(info["sigma"][qi] - tr.sigma)) <= TAU_1D * s1, qi
+        X = np.random.default_rng(qi).standard_normal((4, cfg.n))
+        Y = empty_batch(cfg, 4)
+        Gg.apply(qi, to_gpu(cfg, X), Y, 1)
+        got, ref = from_gpu(cfg, Y), tr.apply_linear(X)
+        for v in range(4):
+            assert np.linalg.norm(got[v] - ref[v]) <= TAU_1D * s1 * np.linalg.norm(X[v]), (qi, v)

@@ -251,3 +251,42 @@ def test_parareal_c5_geometry_matches_oracle():
     from workloads.configs import get as _get
     cfg = _get("C5G")
     _parareal_vs_oracle_iterates(cfg, cfg.K, TAU_2D)
+
+
+@pytest.mark.parametrize("q,indep", [(1, False), (0, True)])
+def test_build_2d_rsvd_variants_match_oracle(q, indep):
+    from paper_2508_08873_b200 import Coarse
+    cfg = get("T2D")
+    Gg = Coarse.build(gpu_op(cfg), cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega, power_iterations=q,
+                      independent_adjoint=indep)
+    info = Gg.info()
+    op_o = make_op(cfg)
+    for qi in (0, cfg.N - 1):
+        tr = rsvd_interval(op_o, qi + 1, cfg.k, cfg.p, cfg.seed_omega, power_iterations=q,
+                           independent_adjoint=indep)
+        s1 = tr.sigma[0]
+        assert np.max(np.abs(info["sigma"][qi] - tr.sigma)) <= TAU_2D * s1
+        X = np.random.default_rng(qi).standard_normal((2, cfg.n, cfg.n))
+        Y = empty_batch(cfg, 2)
+        Gg.apply(qi, to_gpu(cfg, X), Y, 2)
+        got = from_gpu(cfg, Y).reshape(2, -1)
+        ref = tr.apply_linear(X.reshape(2, -1))
+        for v in range(2):
+            assert np.linalg.norm(got[v] - ref[v]) <= TAU_2D * s1 * np.linalg.norm(X[v])
+
+
+@pytest.mark.timeout(1800)
+def test_c5_power_iteration_build_matches_oracle():
+    """C5's slowly decaying spectrum is where q >= 1 matters:
+    the GPU build with q = 1 on two C5-geometry intervals against the oracle."""
+    from paper_2508_08873_b200 import Coarse
+    from workloads.configs import get as _get
+    cfg = _get("C5G")
+    first, nloc = 6, 2
+    Gg = Coarse.build(gpu_op(cfg), cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega, first_interval=first,
+                      n_local=nloc, power_iterations=1)
+    info = Gg.info()
+    op_o = make_op(cfg)
+    for ql in range(nloc):
+        tr = rsvd_interval(op_o, first + ql + 1, cfg.k, cfg.p, cfg.seed_omega, power_iterations=1)
+        assert np.max(np.abs(info["sigma"][ql] - tr.sigma)) <= TAU_2D * tr.sigma[0]
