@@ -214,8 +214,16 @@ __global__ void k_part_iface(int CL, int K, const double *ends, double *ctad, in
             rs[r] = E[e] + (w == 0 ? E[2 + e] : 0.0) + (w == K - 1 ? E[4 + e] : 0.0);
         }
         ok = band_factor(M, A, rs, F) && ok;
-        for (int r = 0; r < M; ++r)
-            for (int d = 0; d < 5; ++d) D[r * 5 + d] = F[r][d];
+        // stored for the stepper's interface warp with the back substitution
+        // pre-scaled: {l2, l1, 1/u, u1/u, u2/u}, so its dependent chain is one
+        // FMA per row in both directions
+        for (int r = 0; r < M; ++r) {
+            D[r * 5 + 0] = F[r][0];
+            D[r * 5 + 1] = F[r][1];
+            D[r * 5 + 2] = F[r][2];
+            D[r * 5 + 3] = F[r][3] * F[r][2];
+            D[r * 5 + 4] = F[r][4] * F[r][2];
+        }
         for (int col = 0; col < M; ++col) {          // rows 0 and M-1 of M_C^{-1}
             for (int r = 0; r < M; ++r) x[r] = (r == col) ? 1.0 : 0.0;
             band_solve(M, F, x);
@@ -286,7 +294,8 @@ constexpr int PART_RSM = 8;            // shared-memory stride of the source row
 // (double2) | chunk end values [2][K][32] (double2) | (B_{C-1}, T_{C+1}) [2][32]
 // (double2) | interface data | per chunk: {w, -ga, V2, W2} [L] | -cp [L] | {V, W} [L] |
 // source rows [L][8] (AFF) | cluster addresses [2][CL] (u32) | local solution [2][2K][32]
-template <int CL, int W, int H, int L, bool AFF>
+// (vector slots: 32 = the largest group, VPG <= 32)
+template <int CL, int W, int H, int L, int VPT, bool AFF>
 constexpr size_t part_smem_t()
 {
     constexpr int K = W * H;
@@ -328,44 +337,122 @@ __device__ __forceinline__ void mbar_arrive(unsigned bar)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
 }
 
-// Warps 0..W-1 each own H chunks (H = 2: the two half-warps hold different chunks
-// of the same 16 vectors), with the chunk state in registers, and only sweep;
-// warp W is the interface warp: it turns the chunks' raw end values into
-// super-chunk values (banded solve with the local factors), exchanges them
-// across the cluster, and hands each chunk its (b_{c-1}, t_{c+1}) -- all while
-// the compute warps run the next sweep.  Local hand-offs use mbarriers: ebar[p]
-// (W compute warps arrive: raw ends of a step of parity p written), cbar[p]
-// (interface warp arrives: interface values of a step of parity p written);
-// gbar[p] counts the cluster gather bytes.
-template <int CL, int W, int H, int L, bool AFF>
-__global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
+// The interface warp's banded solve, streamed through shared memory: rows are
+// processed in blocks of 8 whose operands are loaded (restrict: no aliasing
+// with the stores) before the block's dependent chain runs, so each row
+// costs one dependent FMA per direction.  g: raw ends of the K chunks
+// (double2, stride 32), F: band factors (5 per row), z: the lane's column
+// (stride 32).
+template <int K>
+__device__ __forceinline__ void band_forward(const double2 *__restrict__ g, const double *__restrict__ F,
+                                             double *__restrict__ z, double &T0, double &T1, double &B0,
+                                             double &B1)
 {
-    // clock64 probes (PR_PART_PROF) exist only in builds with -DPR_PART_PROBES
-#ifdef PR_PART_PROBES
-    const bool PROBE = a.prof != nullptr;
-#else
-    constexpr bool PROBE = false;
-#endif
-    constexpr int VPW = 32 / H;          // vectors per warp
+    constexpr int BK = (K < 4) ? K : 4;   // chunks (2 BK rows) per block
+    T0 = T1 = B0 = B1 = 0.0;
+    double y1 = 0.0, y2 = 0.0;
+#pragma unroll
+    for (int u0 = 0; u0 < K; u0 += BK) {
+        double2 gv[BK];
+        double f0[2 * BK], f1[2 * BK];
+#pragma unroll
+        for (int b = 0; b < BK; ++b) {
+            gv[b] = g[(u0 + b) * 32];
+            f0[2 * b] = F[(2 * (u0 + b)) * 5 + 0];
+            f1[2 * b] = F[(2 * (u0 + b)) * 5 + 1];
+            f0[2 * b + 1] = F[(2 * (u0 + b) + 1) * 5 + 0];
+            f1[2 * b + 1] = F[(2 * (u0 + b) + 1) * 5 + 1];
+        }
+        double out[2 * BK];
+#pragma unroll
+        for (int b = 0; b < BK; ++b) {
+            const int i = 2 * (u0 + b);
+            T0 = fma(F[CTAD_R0 + i], gv[b].x, T0);
+            T1 = fma(F[CTAD_R0 + i + 1], gv[b].y, T1);
+            B0 = fma(F[CTAD_RM + i], gv[b].x, B0);
+            B1 = fma(F[CTAD_RM + i + 1], gv[b].y, B1);
+            double y = gv[b].x;
+            if (i >= 2) y = fma(-f0[2 * b], y2, y);
+            if (i >= 1) y = fma(-f1[2 * b], y1, y);
+            double yb = gv[b].y;
+            if (i >= 1) yb = fma(-f0[2 * b + 1], y1, yb);
+            yb = fma(-f1[2 * b + 1], y, yb);
+            out[2 * b] = y;
+            out[2 * b + 1] = yb;
+            y2 = y;
+            y1 = yb;
+        }
+#pragma unroll
+        for (int r = 0; r < 2 * BK; ++r) z[(size_t)(2 * u0 + r) * 32] = out[r];
+    }
+}
+
+template <int M>
+__device__ __forceinline__ void band_backward(const double *__restrict__ F, double *__restrict__ z)
+{
+    constexpr int BR = (M < 8) ? M : 8;   // rows per block
+    double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+    for (int i0 = M - BR; i0 >= 0; i0 -= BR) {
+        double zv[BR], inv[BR], u1[BR], u2[BR];
+#pragma unroll
+        for (int r = 0; r < BR; ++r) {
+            const int i = i0 + r;
+            zv[r] = z[(size_t)i * 32];
+            inv[r] = F[i * 5 + 2];
+            u1[r] = F[i * 5 + 3];
+            u2[r] = F[i * 5 + 4];
+        }
+#pragma unroll
+        for (int r = BR - 1; r >= 0; --r) {
+            const int i = i0 + r;
+            double t = zv[r] * inv[r];
+            if (i + 2 < M) t = fma(-u2[r], t2, t);
+            if (i + 1 < M) t = fma(-u1[r], t1, t);
+            zv[r] = t;
+            t2 = t1;
+            t1 = t;
+        }
+#pragma unroll
+        for (int r = 0; r < BR; ++r) z[(size_t)(i0 + r) * 32] = zv[r];
+    }
+}
+
+// Warps 0..W-1 each own H chunks (the warp's lanes split into H groups of
+// LPC = 32/H lanes, one chunk each) and only sweep; each lane carries VPT
+// vectors of its chunk, so a group of VPG = LPC * VPT vectors runs on a
+// cluster and every shared-memory coefficient load (a warp broadcast) feeds
+// VPT independent recurrences.  Warps W and W+1 are the interface warps: W
+// turns the chunks' raw end values into super-chunk values (two rows of the
+// local inverse, sent first, then the banded local solve), W+1 gathers every
+// CTA's values and forms each chunk's (b_{c-1}, t_{c+1}) -- all while the
+// compute warps run the next sweep.  Local
+// hand-offs use mbarriers: ebar[p] (W compute warps arrive: raw ends of a step
+// of parity p written), cbar[p] (interface warp arrives: interface values of a
+// step of parity p written); gbar[p] counts the cluster gather bytes.
+template <int CL, int W, int H, int L, int VPT, bool AFF>
+__global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
+{
+    constexpr int LPC = 32 / H;          // lanes per chunk
+    constexpr int VPG = LPC * VPT;       // vectors per cluster group
+    static_assert(VPG == 16 || VPG == 32, "the interface warp splits 32 lanes over VPG vectors");
+    constexpr int HI = 32 / VPG;         // interface-warp lanes per vector
     constexpr int K = W * H;             // chunks per CTA
     constexpr int M = 2 * K;             // local interface unknowns
     constexpr int RSM = AFF ? PART_RSM : 0;
     extern __shared__ __align__(16) double sm[];
-    const long long tk0 = PROBE ? clock64() : 0;
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.block_rank();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int vl = lane % VPW, h = lane / VPW;
-    const long v = (long)(blockIdx.x / CL) * VPW + vl;   // vector
-    const bool valid = v < a.B;
+    const long gbase = (long)(blockIdx.x / CL) * VPG;                // first vector of the group
     unsigned long long *bar = reinterpret_cast<unsigned long long *>(sm);   // gbar[2] ebar[2] cbar[2]
     double2 *gth = reinterpret_cast<double2 *>(sm + 6);              // [2][CL][32]
     double2 *rawE = gth + 2 * CL * 32;                               // [2][K][32]
     double2 *coef = rawE + 2 * K * 32;                               // [2][32]: (B_{C-1}, T_{C+1})
     double *ctad = reinterpret_cast<double *>(coef + 2 * 32);
     double *regions = ctad + PART_CTAD;
-    // chunk regions are padded by 4 doubles so the two chunks read by the
-    // half-warps of one warp (H = 2) fall in different shared-memory banks
+    // chunk regions are padded by 4 doubles so that the chunks the lane groups
+    // of one warp read fall in different shared-memory banks
     constexpr int RSTR = L * (7 + RSM) + 4;
     unsigned *rmap = reinterpret_cast<unsigned *>(regions + (size_t)K * RSTR);  // [2][CL]
     auto cd_of = [&](int u) { return reinterpret_cast<double4 *>(regions + (size_t)u * RSTR); };
@@ -382,16 +469,19 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(gbar + 8) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(ebar), "r"(W) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(ebar + 8), "r"(W) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(cbar) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(cbar + 8) : "memory");
+        // interface values of a step are complete when both the publish warp
+        // (local solution z) and the gather warp ((B_{C-1}, T_{C+1})) arrived
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" :: "r"(cbar) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" :: "r"(cbar + 8) : "memory");
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // ctad / rmap are written by all warps and read below (sA1..sB2, neighbours)
-    // by warps that may run ahead: make the copies visible before any use
+    // ctad / rmap are written by all warps and read below (neighbours) by
+    // warps that may run ahead: make the copies visible before any use
     __syncthreads();
 
     if (w < W) {
         // ------------------------------------------------ compute warp: chunk c
+        const int h = lane / LPC, li = lane % LPC;
         const int u = w * H + h;                     // chunk within the CTA
         const int c = C * K + u;
         const int s0 = c * L;
@@ -412,135 +502,153 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
                     spu[r] = (grow < a.n && r < a.RS) ? a.spaceT[(size_t)grow * a.RS + r] : 0.0;
             }
         }
+        __syncwarp();
         const double4 *cd = cd_of(u);
         const double *cu = reinterpret_cast<const double *>(cd) + 4 * L;
         const double2 *vw = reinterpret_cast<const double2 *>(cu + L);
         const double *sp = cu + 3 * L;
-        double S[L];
+        long vv[VPT];
+        bool valid[VPT];
 #pragma unroll
-        for (int i = 0; i < L; ++i)
-            S[i] = (a.in && valid && s0 + i < a.n) ? a.in[(long)(s0 + i) * a.ld_in + v] : 0.0;
-        // (b_{c-1}, t_{c+1}) of a step from the CTA's (B_{C-1}, T_{C+1}) and local solution
+        for (int t = 0; t < VPT; ++t) {
+            vv[t] = gbase + li + t * LPC;
+            valid[t] = vv[t] < a.B;
+        }
+        double S[VPT][L];
+#pragma unroll
+        for (int t = 0; t < VPT; ++t)
+#pragma unroll
+            for (int i = 0; i < L; ++i)
+                S[t][i] = (a.in && valid[t] && s0 + i < a.n) ? a.in[(long)(s0 + i) * a.ld_in + vv[t]] : 0.0;
+        // (b_{c-1}, t_{c+1}) of a step from the CTA's (B_{C-1}, T_{C+1}), this
+        // chunk's super-spike entries and the local solution z
         const double *zsb = reinterpret_cast<const double *>(rmap + 2 * CL);
-        // this chunk's super-spike entries, held in registers for the hand-off
-        const double sA1 = (u == 0) ? 0.0 : ctad[CTAD_A + 2 * u - 1], sB1 = (u == 0) ? 0.0 : ctad[CTAD_B + 2 * u - 1];
-        const double sA2 = (u == K - 1) ? 0.0 : ctad[CTAD_A + 2 * u + 2];
-        const double sB2 = (u == K - 1) ? 0.0 : ctad[CTAD_B + 2 * u + 2];
-        auto neighbours = [&](int pp, double &b, double &t) {
-            const double2 bt = coef[pp * 32 + vl];
-            const double *zz = zsb + (size_t)pp * M * 32 + vl;
-            b = (u == 0) ? bt.x : fma(sA1, bt.x, fma(sB1, bt.y, zz[(2 * u - 1) * 32]));
-            t = (u == K - 1) ? bt.y : fma(sA2, bt.x, fma(sB2, bt.y, zz[(2 * u + 2) * 32]));
+        auto neighbours = [&](int pp, int vs, double &b, double &t) {
+            const double2 bt = coef[pp * 32 + vs];
+            const double *zz = zsb + (size_t)pp * M * 32 + vs;
+            b = (u == 0) ? bt.x
+                         : fma(ctad[CTAD_A + 2 * u - 1], bt.x, fma(ctad[CTAD_B + 2 * u - 1], bt.y, zz[(2 * u - 1) * 32]));
+            t = (u == K - 1) ? bt.y
+                             : fma(ctad[CTAD_A + 2 * u + 2], bt.x, fma(ctad[CTAD_B + 2 * u + 2], bt.y, zz[(2 * u + 2) * 32]));
         };
         cluster.sync();
-        const long long tk1 = PROBE ? clock64() : 0;
-        const int q = valid ? a.q0 + (int)(v / a.vpi) : a.q0;
-        const int src = (AFF && valid) ? (int)(v % a.nsrc) : 0;
-        double ca = 0.0, cc = 0.0;     // (b_{c-1}, t_{c+1}) of step j-1: coefficients of V2, W2
+        int q[VPT], src[VPT];
+#pragma unroll
+        for (int t = 0; t < VPT; ++t) {
+            q[t] = valid[t] ? a.q0 + (int)(vv[t] / a.vpi) : a.q0;
+            src[t] = (AFF && valid[t]) ? (int)(vv[t] % a.nsrc) : 0;
+        }
+        double ca[VPT], cc[VPT];     // (b_{c-1}, t_{c+1}) of step j-1: coefficients of V2, W2
+#pragma unroll
+        for (int t = 0; t < VPT; ++t) ca[t] = cc[t] = 0.0;
         for (int j = 1; j <= a.m; ++j) {
-            long long t0 = PROBE ? clock64() : 0;
-            double alpha[AFF ? PART_RSM : 1];
+            double alpha[VPT][AFF ? PART_RSM : 1];
             if constexpr (AFF) {
 #pragma unroll
-                for (int r = 0; r < PART_RSM; ++r) {
-                    double al = 0.0;
-                    if (r < a.R && valid)
-                        al = a.dt * a.amp[(long)src * a.R + r] * a.time[(long)r * a.nsteps + (long)q * a.m + j - 1];
-                    alpha[r] = al;
-                }
+                for (int t = 0; t < VPT; ++t)
+#pragma unroll
+                    for (int r = 0; r < PART_RSM; ++r) {
+                        double al = 0.0;
+                        if (r < a.R && valid[t])
+                            al = a.dt * a.amp[(long)src[t] * a.R + r] *
+                                 a.time[(long)r * a.nsteps + (long)q[t] * a.m + j - 1];
+                        alpha[t][r] = al;
+                    }
             }
             // S_j = T_c^{-1}(S_{j-1} + ca V2 + cc W2 + dt f_j); down: y_i = w_i x_i - ga_i y_{i-1}
-            double yp = 0.0;
+            double yp[VPT];
+#pragma unroll
+            for (int t = 0; t < VPT; ++t) yp[t] = 0.0;
 #pragma unroll
             for (int i = 0; i < L; ++i) {
                 const double4 q4 = cd[i];
-                double x = fma(q4.z, ca, fma(q4.w, cc, S[i]));
-                if constexpr (AFF) {
 #pragma unroll
-                    for (int r = 0; r < PART_RSM; ++r) x = fma(alpha[r], sp[i * RSM + r], x);
+                for (int t = 0; t < VPT; ++t) {
+                    double x = fma(q4.z, ca[t], fma(q4.w, cc[t], S[t][i]));
+                    if constexpr (AFF) {
+#pragma unroll
+                        for (int r = 0; r < PART_RSM; ++r) x = fma(alpha[t][r], sp[i * RSM + r], x);
+                    }
+                    yp[t] = fma(q4.y, yp[t], q4.x * x);
+                    S[t][i] = yp[t];
                 }
-                yp = fma(q4.y, yp, q4.x * x);
-                S[i] = yp;
             }
             // up: S_i = y_i - cp_i S_{i+1}
-            double gn = 0.0;
+            double gn[VPT];
+#pragma unroll
+            for (int t = 0; t < VPT; ++t) gn[t] = 0.0;
 #pragma unroll
             for (int i = L - 1; i >= 0; --i) {
-                gn = fma(cu[i], gn, S[i]);
-                S[i] = gn;
+                const double cui = cu[i];
+#pragma unroll
+                for (int t = 0; t < VPT; ++t) {
+                    gn[t] = fma(cui, gn[t], S[t][i]);
+                    S[t][i] = gn[t];
+                }
             }
-            long long t1 = PROBE ? clock64() : 0;
             const int p = j & 1;
             if (j >= 2) {              // interface values of step j-1 (formed during this sweep)
                 const int pp = (j - 1) & 1;
                 mbar_wait(cbar + 8 * pp, ((j - 2) >> 1) & 1);
-                neighbours(pp, ca, cc);
+#pragma unroll
+                for (int t = 0; t < VPT; ++t) neighbours(pp, li + t * LPC, ca[t], cc[t]);
             }
             {                          // chunk ends of g_j = S_j + ca V2 + cc W2
                 const double4 q0 = cd[0], q1 = cd[L - 1];
-                rawE[(p * K + u) * 32 + vl] = make_double2(fma(q0.z, ca, fma(q0.w, cc, S[0])),
-                                                           fma(q1.z, ca, fma(q1.w, cc, S[L - 1])));
+#pragma unroll
+                for (int t = 0; t < VPT; ++t)
+                    rawE[(p * K + u) * 32 + li + t * LPC] =
+                        make_double2(fma(q0.z, ca[t], fma(q0.w, cc[t], S[t][0])),
+                                     fma(q1.z, ca[t], fma(q1.w, cc[t], S[t][L - 1])));
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(ebar + 8 * p);
-            if (PROBE && vl == 0) {
-                long long t2 = clock64();
-                unsigned long long *pr = a.prof + (size_t)c * 4;
-                atomicAdd(pr + 0, (unsigned long long)(t1 - t0));
-                atomicAdd(pr + 1, (unsigned long long)(t2 - t1));
-            }
         }
-        const long long tl = PROBE ? clock64() : 0;
         const int pm = a.m & 1;
         mbar_wait(cbar + 8 * pm, ((a.m - 1) >> 1) & 1);
-        double2 e;                                               // (b_m, t_m) of the neighbours
-        neighbours(pm, e.x, e.y);
-        if (valid) {
 #pragma unroll
-            for (int i = 0; i < L; ++i) {
-                if (s0 + i < a.n) {
-                    const double4 q4 = cd[i];
-                    const double2 VW = vw[i];
-                    double x = fma(q4.z, ca, fma(q4.w, cc, S[i]));
-                    x = fma(VW.x, e.x, fma(VW.y, e.y, x));
-                    if (a.off) x += a.off[(long)(s0 + i) * a.ld_off + v];
-                    a.out[(long)(s0 + i) * a.ld_out + v] = x;
+        for (int t = 0; t < VPT; ++t) {
+            double ex, ey;                                       // (b_m, t_m) of the neighbours
+            neighbours(pm, li + t * LPC, ex, ey);
+            if (valid[t]) {
+#pragma unroll
+                for (int i = 0; i < L; ++i) {
+                    if (s0 + i < a.n) {
+                        const double4 q4 = cd[i];
+                        const double2 VW = vw[i];
+                        double x = fma(q4.z, ca[t], fma(q4.w, cc[t], S[t][i]));
+                        x = fma(VW.x, ex, fma(VW.y, ey, x));
+                        if (a.off) x += a.off[(long)(s0 + i) * a.ld_off + vv[t]];
+                        a.out[(long)(s0 + i) * a.ld_out + vv[t]] = x;
+                    }
                 }
             }
         }
-        if (PROBE && threadIdx.x == 0) {
-            const long long tk2 = clock64();
-            atomicAdd(a.prof + (size_t)(512 + C) * 4 + 0, (unsigned long long)(tk1 - tk0));
-            atomicAdd(a.prof + (size_t)(512 + C) * 4 + 1, (unsigned long long)(tk2 - tl));
-        }
     } else {
         // ------------------------------------------------ interface warp
-        // lane = (half h, vector vl); with H = 2 the two half-warps split the
-        // cluster sends and the gather dot products
+        // lane = (part hi, vector vl); with HI = 2 the two half-warps split the
+        // cluster sends and the gather dot products of the same 16 vectors
+        const int hi = lane / VPG, vl = lane % VPG;
         cluster.sync();
         double *zs = reinterpret_cast<double *>(rmap + 2 * CL);          // [2][M][32]
-        constexpr int CLH = CL / H;                                      // CTAs per half-warp
+        constexpr int CLH = CL / HI;                                     // CTAs per lane part
         // step j's values from every super-chunk -> (B_{C-1}, T_{C+1}) of step j
-        unsigned long long hx1 = 0, hx2 = 0, hw = 0, hg = 0;
         auto gather = [&](int j) {
             const int p = j & 1;
             if (lane == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                             :: "r"(gbar + 8 * p), "r"((unsigned)(CL * VPW * sizeof(double2))) : "memory");
-            long long ga = PROBE ? clock64() : 0;
+                             :: "r"(gbar + 8 * p), "r"((unsigned)(CL * VPG * sizeof(double2))) : "memory");
             mbar_wait(gbar + 8 * p, ((j - 1) >> 1) & 1);
-            long long gb = PROBE ? clock64() : 0;
-            hw += gb - ga;
-            const double2 *G = gth + (size_t)p * CL * 32 + vl;
+            const double2 *Gt = gth + (size_t)p * CL * 32 + vl;
             // the two halves of the CTA list are summed separately and then
-            // added, for H = 1 and H = 2 alike: the result does not depend on
-            // the warp shape the batch size selects (bit-identical shards)
+            // added, for HI = 1 and HI = 2 alike: the result does not depend on
+            // the lane split the group size selects (bit-identical shards)
             auto half = [&](int hh, double &Bh, double &Th) {
                 double b0 = 0.0, b1 = 0.0, t0 = 0.0, t1 = 0.0;
 #pragma unroll
                 for (int rr = 0; rr < CL / 2; ++rr) {
                     const int r = hh * (CL / 2) + rr;
-                    const double2 e = G[r * 32];
+                    const double2 e = Gt[r * 32];
                     b0 = fma(ctad[CTAD_GB + 2 * r], e.x, b0);
                     b1 = fma(ctad[CTAD_GB + 2 * r + 1], e.y, b1);
                     t0 = fma(ctad[CTAD_GT + 2 * r], e.x, t0);
@@ -550,8 +658,8 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
                 Th = t0 + t1;
             };
             double Bx, Tx;
-            if constexpr (H == 2) {
-                half(h, Bx, Tx);
+            if constexpr (HI == 2) {
+                half(hi, Bx, Tx);
                 Bx += __shfl_xor_sync(0xffffffffu, Bx, 16);
                 Tx += __shfl_xor_sync(0xffffffffu, Tx, 16);
             } else {
@@ -561,84 +669,46 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
                 Bx += B1;
                 Tx += T1;
             }
-            if (h == 0) coef[p * 32 + vl] = make_double2(Bx, Tx);
+            if (hi == 0) coef[p * 32 + vl] = make_double2(Bx, Tx);
             __syncwarp();
             if (lane == 0) mbar_arrive(cbar + 8 * p);
-            if (PROBE) hg += clock64() - gb;
         };
-        // chunk end values of step j -> local solve z = M_C^{-1} g_C -> (T_C, B_C) to every CTA
+        // chunk end values of step j -> local solve z = M_C^{-1} g_C -> (T_C, B_C)
+        // to every CTA.  The band solve streams through shared memory with the
+        // two recurrence carries in registers (one dependent FMA per row in
+        // each direction; loads of g and of the forward values are off the
+        // chain), so M = 2K up to 64 needs no register array.  Each lane works
+        // in its own slot (vl + VPG * hi) and the hi = 0 lanes hold the result.
         auto publish = [&](int j) {
             const int p = j & 1;
             mbar_wait(ebar + 8 * p, ((j - 1) >> 1) & 1);
-            long long pa = PROBE ? clock64() : 0;
-            double z[M];
-#pragma unroll
-            for (int uu = 0; uu < K; ++uu) {
-                const double2 r = rawE[(p * K + uu) * 32 + vl];
-                z[2 * uu] = r.x;
-                z[2 * uu + 1] = r.y;
-            }
-            // (T_C, B_C) from the two stored rows of M_C^{-1} (independent FMAs),
-            // sent first; the full local solution follows with the band factors
-            // while the cluster exchange is in flight
-            double T0 = 0.0, T1 = 0.0, B0 = 0.0, B1 = 0.0;
-#pragma unroll
-            for (int i = 0; i < M; i += 2) {
-                T0 = fma(ctad[CTAD_R0 + i], z[i], T0);
-                T1 = fma(ctad[CTAD_R0 + i + 1], z[i + 1], T1);
-                B0 = fma(ctad[CTAD_RM + i], z[i], B0);
-                B1 = fma(ctad[CTAD_RM + i + 1], z[i + 1], B1);
-            }
+            const double2 *rE = rawE + (size_t)p * K * 32 + vl;
+            double *zl = zs + (size_t)p * M * 32 + vl + VPG * hi;
+            // forward elimination y = L^{-1} g (stored), and (T_C, B_C) from the
+            // two stored rows of M_C^{-1} applied to g (independent FMAs)
+            double T0, T1, B0, B1;
+            band_forward<K>(rE, ctad, zl, T0, T1, B0, B1);
             const double Tv = T0 + T1, Bv = B0 + B1;
             const unsigned off = (unsigned)(((p * CL + C) * 32 + vl) * sizeof(double2));
 #pragma unroll
             for (int rr = 0; rr < CLH; ++rr) {
-                const int r = h * CLH + rr;
+                const int r = hi * CLH + rr;
                 st_async_v2(rmap[r] + off, Tv, Bv, rmap[CL + r] + 8 * p);
             }
-            long long pb = PROBE ? clock64() : 0;
-            hx1 += pb - pa;
-            // band factors, row i: l2, l1, 1/u, u1, u2
-#pragma unroll
-            for (int i = 0; i < M; ++i) {
-                if (i >= 2) z[i] = fma(-ctad[i * 5 + 0], z[i - 2], z[i]);
-                if (i >= 1) z[i] = fma(-ctad[i * 5 + 1], z[i - 1], z[i]);
-            }
-#pragma unroll
-            for (int i = M - 1; i >= 0; --i) {
-                if (i + 1 < M) z[i] = fma(-ctad[i * 5 + 3], z[i + 1], z[i]);
-                if (i + 2 < M) z[i] = fma(-ctad[i * 5 + 4], z[i + 2], z[i]);
-                z[i] *= ctad[i * 5 + 2];
-            }
-            if (h == 0) {
-#pragma unroll
-                for (int i = 0; i < M; ++i) zs[((size_t)p * M + i) * 32 + vl] = z[i];
-            }
+            // back substitution with the pre-scaled factors {.., 1/u, u1/u, u2/u}
+            band_backward<M>(ctad, zl);
             __syncwarp();
-            if (PROBE) hx2 += clock64() - pb;
         };
-        unsigned long long tw = 0, tp = 0, tg = 0;
-        for (int j = 1; j <= a.m; ++j) {
-            long long t0 = PROBE ? clock64() : 0;
-            if (j >= 2) gather(j - 1);
-            long long t1 = PROBE ? clock64() : 0;
-            publish(j);
-            long long t2 = PROBE ? clock64() : 0;
-            tg += t1 - t0;
-            tp += t2 - t1;
+        // two warps: warp W publishes step j (its local solve overlaps the
+        // cluster exchange), warp W+1 gathers step j; each arrives on cbar
+        if (w == W) {
+            for (int j = 1; j <= a.m; ++j) {
+                publish(j);
+                if (lane == 0) mbar_arrive(cbar + 8 * (j & 1));
+            }
+        } else {
+            for (int j = 1; j <= a.m; ++j) gather(j);
         }
-        gather(a.m);
-        if (PROBE && lane == 0) {
-            unsigned long long *pr = a.prof + (size_t)(C * K) * 4;
-            atomicAdd(pr + 2, tg);
-            atomicAdd(pr + 3, tp);
-            unsigned long long *px = a.prof + (size_t)(600 + C) * 4;
-            atomicAdd(px + 0, hx1);
-            atomicAdd(px + 1, hx2);
-            atomicAdd(px + 2, hw);
-            atomicAdd(px + 3, hg);
-        }
-        (void)tw;
     }
     cluster.sync();                // no CTA leaves while cluster peers may still target it
 }
@@ -646,11 +716,14 @@ __global__ void __launch_bounds__(32 * (W + 1), 1) k_part_step(PartArgs a)
 // ---------------------------------------------------------------- driver
 bool part_config(int n, int &P, int &L, int &CL, int &K)
 {
-    // chunks of L = 32 rows (one warp per chunk, up to 16 CTAs) up to n = 512,
-    // else 64 rows in 16 CTAs of K = 1..16 chunks: P (a power of two) chunks
-    // cover P*L >= n rows, the rest identity padding.
-    if (n < 64 || n > PART_CLMAX * PART_KMAX * 64) return false;
-    L = (n <= 512) ? 32 : 64;
+    // chunks of L = 32 rows up to n = 512 (one warp per chunk, up to 16 CTAs),
+    // else 64 rows in 16 CTAs of K = 1..16 chunks.  PR_PART_VPT2=1 selects for
+    // n > 8192 32-row chunks with two vectors per lane instead (K = 32 chunks
+    // per CTA: half the coefficient loads per DOF-step, but a 64-unknown local
+    // interface solve per step, measured slower on C4).  P (a power of two)
+    // chunks cover P*L >= n rows, the rest identity padding.
+    if (n < 64 || n > PART_CLMAX * 32 * 32) return false;
+    L = (n <= 512 || (n > 8192 && flags().part_vpt2)) ? 32 : 64;
     const int need = (n + L - 1) / L;
     P = 2;
     while (P < need) P *= 2;
@@ -672,10 +745,10 @@ cudaError_t launch_part_setup(int n, int P, int L, int CL, int K, const double *
     return cudaGetLastError();
 }
 
-template <int CL, int W, int H, int L, bool AFF>
+template <int CL, int W, int H, int L, int VPT, bool AFF>
 static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
 {
-    constexpr size_t smem = part_smem_t<CL, W, H, L, AFF>();
+    constexpr size_t smem = part_smem_t<CL, W, H, L, VPT, AFF>();
     static_assert(smem <= 227 * 1024, "partitioned stepper shared memory");
     // function attributes are per device: set once for each device this
     // process launches on (bit d of the mask)
@@ -684,17 +757,17 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     cudaGetDevice(&dev);
     const unsigned long long bit = 1ULL << (dev & 63);
     if (!(attr_mask.load(std::memory_order_acquire) & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, AFF>,
+        cudaError_t e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, VPT, AFF>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess && CL > 8)
-            e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, AFF>,
+            e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, VPT, AFF>,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         attr_mask.fetch_or(bit, std::memory_order_release);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(groups * CL));
-    cfg.blockDim = dim3(32 * (W + 1));
+    cfg.blockDim = dim3(32 * (W + 2));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -706,20 +779,22 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     cfg.numAttrs = 1;
     if (flags().part_prof) {
         int nc = -1;
-        cudaError_t eo = cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, AFF>, &cfg);
+        cudaError_t eo = cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, VPT, AFF>, &cfg);
         fprintf(stderr, "part: max active clusters %d (%s), smem %zu B, groups %ld\n", nc,
                 eo == cudaSuccess ? "ok" : cudaGetErrorString(eo), smem, groups);
         (void)cudaGetLastError();
     }
     note_launch();
-    return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, AFF>, a);
+    return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF>, a);
 }
 
-template <int CL, int W, int H, int L>
+template <int CL, int W, int H, int L, int VPT = 1>
 static cudaError_t part_launch_aff(const PartArgs &a, long B, cudaStream_t s)
 {
-    const long groups = (B + 32 / H - 1) / (32 / H);
-    return a.R > 0 ? part_launch<CL, W, H, L, true>(a, groups, s) : part_launch<CL, W, H, L, false>(a, groups, s);
+    constexpr long VPG = (32 / H) * VPT;
+    const long groups = (B + VPG - 1) / VPG;
+    return a.R > 0 ? part_launch<CL, W, H, L, VPT, true>(a, groups, s)
+                   : part_launch<CL, W, H, L, VPT, false>(a, groups, s);
 }
 
 bool part_preferred(const Op &op, long B, int m)
@@ -744,7 +819,7 @@ cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose,
     a.spaceT = sa.spaceT; a.time = sa.time; a.amp = sa.amp;
     a.nsteps = sa.nsteps; a.nsrc = sa.nsrc; a.q0 = sa.q0; a.vpi = sa.vpi; a.dt = sa.dt;
     if (sa.B == 0) return cudaSuccess;
-    const int P = op.part_P, K = op.part_K;
+    const int K = op.part_K;
     // two chunks per warp (16 vectors per warp) when that spreads a small batch
     // over more SMs, or when K chunks would need more than 8 compute warps
     int H = 1;
@@ -755,23 +830,20 @@ cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose,
             if ((f == 1 && K <= 8) || f == 2) H = f;
         }
     }
-    static unsigned long long *dprof = nullptr;
-    const bool want_prof = flags().part_prof;
-    if (want_prof) {
-        if (!dprof) cudaMalloc(&dprof, 1024 * 4 * sizeof(unsigned long long));
-        cudaMemsetAsync(dprof, 0, 1024 * 4 * sizeof(unsigned long long), s);
-        a.prof = dprof;
-    }
     const bool prof = profiling();
     if (prof) stepper_timed_begin(s);
     cudaError_t e = cudaErrorInvalidValue;
-    if (op.part_L == 32) {
+    if (op.part_L == 32 && K == 1) {
         switch (op.part_CL) {
         case 2: e = part_launch_aff<2, 1, 1, 32>(a, sa.B, s); break;
         case 4: e = part_launch_aff<4, 1, 1, 32>(a, sa.B, s); break;
         case 8: e = part_launch_aff<8, 1, 1, 32>(a, sa.B, s); break;
         case 16: e = part_launch_aff<16, 1, 1, 32>(a, sa.B, s); break;
         }
+    } else if (op.part_L == 32) {
+        // n > 8192: 32-row chunks, 4 chunks per warp (8 lanes each), two
+        // vectors per lane: groups of 16 vectors
+        if (op.part_CL == 16 && K == 32) e = part_launch_aff<16, 8, 4, 32, 2>(a, sa.B, s);
     } else if (op.part_CL == 16 && H == 1) {
         switch (K) {
         case 1: e = part_launch_aff<16, 1, 1, 64>(a, sa.B, s); break;
@@ -793,23 +865,6 @@ cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose,
     if (prof) {
         const double dof = (double)sa.n * (double)sa.B * (double)sa.m;
         stepper_timed_end(s, dof, (5.0 + 2.0 * a.R) * dof);
-    }
-    if (want_prof && e == cudaSuccess) {
-        unsigned long long h[1024 * 4];
-        cudaMemcpyAsync(h, dprof, sizeof(h), cudaMemcpyDeviceToHost, s);
-        cudaStreamSynchronize(s);
-        const long groups = (sa.B + 32 / H - 1) / (32 / H);
-        const double norm = (double)groups * sa.m;
-        fprintf(stderr, "part P=%d L=%d CL=%d K=%d H=%d m=%d groups=%ld  cycles/step [sweep hand-off | helper: gather(incl. wait) publish(incl. wait)]:\n", P,
-                op.part_L, op.part_CL, K, H, sa.m, groups);
-        fprintf(stderr, "  CTA 0 per group: prologue %.0f epilogue %.0f cycles\n", (double)h[512 * 4] / groups,
-                (double)h[512 * 4 + 1] / groups);
-        fprintf(stderr, "  interface warp of CTA 0 per step: to-send %.0f band-solve %.0f gather-wait %.0f gather %.0f\n",
-                (double)h[600 * 4] / norm, (double)h[600 * 4 + 1] / norm, (double)h[600 * 4 + 2] / norm,
-                (double)h[600 * 4 + 3] / norm);
-        for (int c = 0; c < P; c += (P > 16 ? P / 16 : 1))
-            fprintf(stderr, "  chunk %3d: %8.0f %8.0f | %8.0f %8.0f\n", c + (P > 16 ? 1 : 0), h[(c + (P > 16 ? 1 : 0)) * 4] / norm,
-                    h[(c + (P > 16 ? 1 : 0)) * 4 + 1] / norm, h[c * 4 + 2] / norm, h[c * 4 + 3] / norm);
     }
     return e;
 }

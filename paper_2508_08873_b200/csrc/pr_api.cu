@@ -122,6 +122,7 @@ static void read_flags()
     f.part_prof = on("PR_PART_PROF");
     f.qr_trace = on("PR_QR_TRACE");
     f.debug_sync = on("PR_DEBUG_SYNC");
+    f.part_vpt2 = on("PR_PART_VPT2");
     f.part_h = num("PR_PART_H");
     f.stepper_pd = num("PR_STEPPER_PD");
     f.stepper_vpt = num("PR_STEPPER_VPT");

@@ -50,6 +50,7 @@ void ws_free(void *p, cudaStream_t s);
 struct Flags {
     bool no_part = false, no_xty_rm = false, no_trsm_dmma = false, no_rinv_cm = false,
          no_expand_mma = false, part_prof = false, qr_trace = false, debug_sync = false;
+    bool part_vpt2 = false;
     int part_h = 0, stepper_pd = 0, stepper_vpt = 0;
 };
 const Flags &flags();
@@ -121,7 +122,7 @@ cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s);
 
 // partitioned stepper (k_part.cu): configuration for n (false: not supported),
 // setup (ends: P x 8 scratch), selection and launch
-constexpr int PART_KMAX = 16;                  // chunks per CTA
+constexpr int PART_KMAX = 32;                  // chunks per CTA
 constexpr int PART_CLMAX = 16;                 // CTAs per cluster
 constexpr int PART_CTAD = 5 * 2 * PART_KMAX + 8 * PART_KMAX + 4 * PART_CLMAX;
 // P = CL * K chunks of L rows (K chunks per CTA)
