@@ -149,10 +149,18 @@ class Workload:
             self.comm = nccl_comm()
 
     def dof_steps(self) -> float:
-        """Fine-solve DOF-steps this rank performs per step."""
+        """Fine-solve DOF-steps this rank performs per step: the rSVD build
+        (2 l solves per interval), the offsets b_n (one solve per interval and
+        source term when there are more sources than terms -- libpr combines
+        them by linearity, reading R-SRC -- else one per source) and
+        K iterations of one solve per interval and source."""
         c = self.cfg
         build = self.nq * 2 * c.l * c.n_dof * c.m
-        par = (c.K + 1) * self.nq * self.ns * c.n_dof * c.m
+        nb = self.ns
+        if c.dim == 1:
+            R = self.host["time"].shape[0]
+            nb = min(self.ns, R)
+        par = (c.K * self.ns + nb) * self.nq * c.n_dof * c.m
         return float(build + par)
 
     def step(self, events=None, op=None, src=None, u0=None):

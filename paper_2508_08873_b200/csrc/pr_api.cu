@@ -123,6 +123,7 @@ static void read_flags()
     f.qr_trace = on("PR_QR_TRACE");
     f.debug_sync = on("PR_DEBUG_SYNC");
     f.part_vpt2 = on("PR_PART_VPT2");
+    f.no_src_basis = on("PR_NO_SRC_BASIS");
     f.part_h = num("PR_PART_H");
     f.stepper_pd = num("PR_STEPPER_PD");
     f.stepper_vpt = num("PR_STEPPER_VPT");
@@ -918,6 +919,33 @@ pr_status pr_coarse_destroy(pr_coarse G)
     return PR_OK;
 }
 
+// ---------------------------------------------------- offsets by source basis
+// b_{q,s} = F_q(0) for source s = sum_r amp[s, r] b^{(r)}_q, where b^{(r)}_q is
+// F_q(0) for the single separable term time[r, .] * space[r, .] (F_q(0) is
+// linear in the source; reading R-SRC).  S sources of R <= 8 terms
+// then cost N*R offset fine solves instead of N*S.
+__global__ void k_eye(double *E, int R)
+{
+    const int t = threadIdx.x;
+    if (t < R * R) E[t] = (t / R == t % R) ? 1.0 : 0.0;
+}
+
+// out[i*ld + q*S + s] = sum_r amp[s*R + r] * basis[i*ldb + q*R + r]
+__global__ void k_combine_offsets(const double *basis, long ldb, int R, const double *amp, int S, int nq,
+                                  long rows, double *out, long ld)
+{
+    const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long per = (long)nq * S;
+    if (idx >= per * rows) return;
+    const long i = idx / per, c = idx % per;
+    const int q = (int)(c / S), sI = (int)(c % S);
+    const double *bv = basis + i * ldb + (long)q * R;
+    const double *av = amp + (long)sI * R;
+    double acc = 0.0;
+    for (int r = 0; r < R; ++r) acc = fma(av[r], bv[r], acc);
+    out[i * ld + c] = acc;
+}
+
 // ---------------------------------------------------------------- Parareal
 // One schedule for one GPU and for an interval-sharded run (the handle's
 // communicator): rank r owns intervals q0 .. q0+nq-1 and the boundary blocks
@@ -1013,9 +1041,30 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
     // offsets b_q = F_q 0 into blocks 1..nq of bb
     {
         PhaseScope phase(PR_PHASE_OFFSETS);
-        pr_status st = propagate(op, PR_AFFINE, q0, m, nq * S, S, f, nullptr, ld, bb + blk, ld,
-                                 nullptr, 0, 0, 0, s);
-        if (st != PR_OK) return st;
+        pr_status st;
+        if (op.dim == 1 && f->kind == PR_SRC_SEP1D && f->nterms < S && !flags().no_src_basis) {
+            const int R = f->nterms;
+            const long ldb = ((long)nq * R + 1) & ~1L;
+            double *eye, *basis;
+            PR_ALLOC(eye, double, (size_t)R * R, Sc);
+            PR_ALLOC(basis, double, (size_t)rows * ldb, Sc);
+            note_launch();
+            k_eye<<<1, 64, 0, s>>>(eye, R);
+            PR_CHECK_LAUNCH("k_eye");
+            pr_source fb = *f;
+            fb.nsrc = R;
+            fb.amp = eye;
+            st = propagate(op, PR_AFFINE, q0, m, nq * R, R, &fb, nullptr, ldb, basis, ldb, nullptr, 0, 0, 0, s);
+            if (st != PR_OK) return st;
+            const long tot = rows * nq * S;
+            note_launch();
+            k_combine_offsets<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(basis, ldb, R, f->amp, S, nq, rows,
+                                                                            bb + blk, ld);
+            PR_CHECK_LAUNCH("k_combine_offsets");
+        } else {
+            st = propagate(op, PR_AFFINE, q0, m, nq * S, S, f, nullptr, ld, bb + blk, ld, nullptr, 0, 0, 0, s);
+            if (st != PR_OK) return st;
+        }
     }
     PR_CUDA(launch_vecnorm_parts(bb, L.rs, L.vs, rows, (int)nvec, nchunk, cr, npart, s));
     PR_CUDA(launch_norm_finish(npart, (int)nvec, nchunk, bn, s));

@@ -41,7 +41,7 @@ pr_status cuda_fail(cudaError_t e, const char *where);
 void *ws_alloc(size_t bytes, cudaStream_t s);
 void ws_free(void *p, cudaStream_t s);
 
-// Diagnostic switches from the environment (PR_NO_PART, PR_NO_XTY_RM,
+// Diagnostic switches from the environment (PR_NO_PART, PR_NO_SRC_BASIS, PR_NO_XTY_RM,
 // PR_NO_TRSM_DMMA, PR_NO_RINV_CM, PR_NO_EXPAND_MMA select the alternate
 // kernels that tests/test_gpu_alt_paths.py exercises; PR_PART_H, PR_STEPPER_PD,
 // PR_STEPPER_VPT force a launch shape; PR_PART_PROF, PR_QR_TRACE,
@@ -50,7 +50,7 @@ void ws_free(void *p, cudaStream_t s);
 struct Flags {
     bool no_part = false, no_xty_rm = false, no_trsm_dmma = false, no_rinv_cm = false,
          no_expand_mma = false, part_prof = false, qr_trace = false, debug_sync = false;
-    bool part_vpt2 = false;
+    bool part_vpt2 = false, no_src_basis = false;
     int part_h = 0, stepper_pd = 0, stepper_vpt = 0;
 };
 const Flags &flags();

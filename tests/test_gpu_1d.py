@@ -206,7 +206,7 @@ def _run_parareal(cfg, K=None, keep_hist=True):
     return Gg, info, Uo, hist, upd, bn, u0
 
 
-@pytest.mark.parametrize("name", ["T1", "T4", "T1k1", "C1", "T4N"])
+@pytest.mark.parametrize("name", ["T1", "T4", "T1k1", "C1", "T4N", "T4S"])
 def test_parareal_all_iterates_match_oracle(name):
     cfg = get(name)
     Gg, info, Uo, hist, upd, bn, u0 = _run_parareal(cfg)

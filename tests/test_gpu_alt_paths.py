@@ -3,6 +3,8 @@
 kernel of the default path by its simpler fallback:
 
   PR_NO_PART        fused LU/UL streaming stepper (K1) instead of K1P
+  PR_NO_SRC_BASIS   offsets b_n with the full source per source instead of the
+                    source-basis combination
   PR_NO_XTY_RM      CUDA-core cross products instead of the row-major DMMA Gram
   PR_NO_TRSM_DMMA   row-wise substitution instead of the blocked DMMA TRSM
   PR_NO_RINV_CM     generic R^{-1} apply instead of the column-major DMMA one (2D)
@@ -67,13 +69,43 @@ def _run(name):
     assert np.max(np.abs(got - res.U[cfg.K])) <= tau * scale
 
 
-SWITCHES = ["PR_NO_PART", "PR_NO_XTY_RM", "PR_NO_TRSM_DMMA", "PR_NO_RINV_CM", "PR_NO_EXPAND_MMA"]
+SWITCHES = ["PR_NO_PART", "PR_NO_SRC_BASIS", "PR_NO_XTY_RM", "PR_NO_TRSM_DMMA", "PR_NO_RINV_CM",
+            "PR_NO_EXPAND_MMA", "PR_PART_VPT2"]
 
 
 @pytest.mark.parametrize("switch", SWITCHES)
 @pytest.mark.parametrize("name", ["T4", "T2D"])
 def test_alternate_kernel_matches_oracle(name, switch, pr_env):
-    if switch == "PR_NO_PART" and name == "T2D":
-        pytest.skip("PR_NO_PART concerns the 1D stepper only")
+    if switch in ("PR_NO_PART", "PR_NO_SRC_BASIS", "PR_PART_VPT2") and name == "T2D":
+        pytest.skip(f"{switch} concerns the 1D path only")
     pr_env(**{switch: "1"})
     _run(name)
+
+
+@pytest.mark.parametrize("mode", ["linear", "adjoint", "affine"])
+def test_two_vectors_per_lane_layout_at_c4_size(mode, pr_env):
+    """PR_PART_VPT2: K1P with 32-row chunks and two vectors per lane (n > 8192)
+    against the oracle's Thomas steps at C4's full grid (non-symmetric C4N)."""
+    from gpu_util import relnorm
+    from oracle.fine import fine
+    from paper_2508_08873_b200 import PR_ADJOINT, PR_AFFINE, PR_LINEAR
+    pr_env(PR_PART_VPT2="1")
+    cfg = get("C4N")
+    op_o, op_g = make_op(cfg), gpu_op(cfg)
+    S = 4
+    X = np.random.default_rng(3).standard_normal((2 * S, cfg.n))
+    out = empty_batch(cfg, 2 * S)
+    if mode == "affine":
+        from dataclasses import replace
+        cfg_s = replace(cfg, nsrc=S)
+        op_g.fine_propagate(PR_AFFINE, 5, cfg.m, to_gpu(cfg, X), out, vecs_per_interval=S,
+                            source=gpu_source(cfg_s))
+        src = G.source_1d(cfg_s)
+        ref = np.concatenate([fine(op_o, 6 + j, X[j * S:(j + 1) * S], "affine", src, np.arange(S))
+                              for j in range(2)])
+    else:
+        op_g.fine_propagate(PR_LINEAR if mode == "linear" else PR_ADJOINT, 5, cfg.m, to_gpu(cfg, X), out)
+        ref = fine(op_o, 6, X, mode)
+    got = from_gpu(cfg, out)
+    for v in range(2 * S):
+        assert relnorm(got[v], ref[v]) <= TAU_1D

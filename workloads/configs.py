@@ -93,7 +93,9 @@ T2D = replace(C3, name="T2D", n=63, N=6, m=10, k=6, p=3, K=5)
 # transposed solve (rSVD step 3) -- small and at C4's grid
 T4N = replace(C4, name="T4N", problem="convection_diffusion", n=301, N=8, m=16, k=4, p=4, K=6, nsrc=5)
 C4N = replace(C4, name="C4N", problem="convection_diffusion")
-VARIANTS = {c.name: c for c in (T1, T1_K1, T4, T2D, T4N, C4N)}
+# more sources (12) than source terms (8): the offsets go through the source basis
+T4S = replace(T4, name="T4S", nsrc=12)
+VARIANTS = {c.name: c for c in (T1, T1_K1, T4, T2D, T4N, C4N, T4S)}
 
 
 def get(name: str) -> Config:
