@@ -44,6 +44,18 @@ namespace cg = cooperative_groups;
 
 namespace pr {
 
+// dev aid: clock64 phase probes, compiled only with -DPR_PART_PROBES (they cost
+// registers); PR_PART_PROF=1 then prints per-step phase cycles per CTA
+#ifdef PR_PART_PROBES
+#define PROBE_T(v) const long long v = clock64()
+#define PROBE_ADD(slot, v) (pacc[slot] += (unsigned long long)(v))
+#else
+#define PROBE_T(v)
+#define PROBE_ADD(slot, v)
+#endif
+constexpr int PART_NPROBE = 16;
+constexpr unsigned PART_IDLE_NS = 64;   // default interface-warp poll back-off
+
 // per-CTA interface data (PART_CTAD doubles): band factors of the local
 // interface matrix M_C (2K rows x 5) | alpha (2K) | beta (2K) | rows of the
 // global inverse for B_{C-1} (2CL) and T_{C+1} (2CL) | rows 0 and 2K-1 of
@@ -54,15 +66,37 @@ constexpr int CTAD_GB = CTAD_B + 2 * PART_KMAX;
 constexpr int CTAD_GT = CTAD_GB + 2 * PART_CLMAX;
 constexpr int CTAD_R0 = CTAD_GT + 2 * PART_CLMAX;     // row 0 of M_C^{-1} (T_C)
 constexpr int CTAD_RM = CTAD_R0 + 2 * PART_KMAX;      // row 2K-1 of M_C^{-1} (B_C)
+// split band solve (two halves of K rows each, R-PART): responses of the
+// forward elimination of rows K..2K-1 to the carried values (y_{K-2}, y_{K-1})
+// and of the back substitution of rows 0..K-1 to (x_K, x_{K+1})
+constexpr int CTAD_FP = CTAD_RM + 2 * PART_KMAX;
+constexpr int CTAD_FQ = CTAD_FP + PART_KMAX;
+constexpr int CTAD_BR = CTAD_FQ + PART_KMAX;
+constexpr int CTAD_BT = CTAD_BR + PART_KMAX;
 
 // ------------------------------------------------------------------ setup
-// One thread per chunk c (rows s0..s0+L-1): local LU of T_c in row-sum form and
-// the local solves V, W (spikes), V2 = T_c^{-1} V, W2 = T_c^{-1} W and rho = T_c^{-1} s.
-// rowc row i: {w_i, -ga_i, -cp_i, V_i, W_i, V2_i, W2_i, 0};
-// ends[c] = {rho_top, rho_bot, V_top, V_bot, W_top, W_bot, 0, 0}.
+// One thread per chunk c (rows s0..s0+L-1): local LU of T_c in row-sum form
+// (pivots p_k, reading R-ACC), the local solves V, W (spikes),
+// V2 = T_c^{-1} V, W2 = T_c^{-1} W and rho = T_c^{-1} s, and the chunk-local
+// similarity scaling of the stepper (reading R-SCALE).
+//
+// Scaled form.  With x = D x~, D = diag(d_k), d_0 = 1, d_{k+1} = d_k p_k / (-c_k),
+// the local solve T_c x = r becomes two one-coefficient recurrences
+//   down  z~_k = r~_k + nl_k z~_{k-1},   nl_k = -(a_k / p_{k-1}) d_{k-1} / d_k
+//   up    x~_k = w_k z~_k + x~_{k+1},    w_k  = 1 / p_k
+// (the super-diagonal of the scaled U is -p_k, so its multiplier is exactly 1):
+// 2 FMAs and 2 coefficients per row instead of 3 and 3.  Every term is
+// non-negative for an M-matrix and non-negative data, as in the row-sum form.
+// A chunk with a zero coupling c_k inside real rows (k < L-1, row < n-1) or a
+// scale outside [2^-900, 2^900] cannot be scaled: *noscale is set and the
+// operator uses the streaming stepper instead.  (c_k = 0 at row n-1 and on
+// identity padding rows is harmless: the state there is exactly 0.)
+//
+// rowc row i (PART_ROWC): {w_i, nl_i, V2_i/d_i, W2_i/d_i, V_i, W_i, d_i, 1/d_i};
+// ends[c] (PART_ENDS) = {rho, V, W at (top, bottom) of the chunk, 0, 0} (physical).
 __global__ void k_part_setup(int n, int P, int L, const double *subA, const double *supA,
                              const double *rsA, const double *diagA, double dt, int transpose,
-                             double *rowc, double *ends, int *bad)
+                             double *rowc, double *ends, int *bad, int *noscale)
 {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= P) return;
@@ -82,50 +116,70 @@ __global__ void k_part_setup(int n, int P, int L, const double *subA, const doub
     };
     // local LU: T_c drops a_{s0} and c_{e0-1}; its row sums are s_i minus the
     // dropped (non-positive) entries
+    double w[64], ga[64], cp[64], d[64];            // L <= 64
     double r = 0.0, den = 1.0;
-    for (int i = s0; i < e0; ++i) {
-        const double ai = (i == s0) ? 0.0 : a_of(i);
-        const double ci = (i == e0 - 1) ? 0.0 : c_of(i);
+    bool scal = true;
+    for (int k = 0; k < L; ++k) {
+        const int i = s0 + k;
+        const double ai = (k == 0) ? 0.0 : a_of(i);
+        const double ci = (k == L - 1) ? 0.0 : c_of(i);
         double sl = s_of(i);
-        if (i == s0) sl -= a_of(i);
-        if (i == e0 - 1) sl -= c_of(i);
-        r = (i == s0) ? sl : sl - ai * (r / den);
+        if (k == 0) sl -= a_of(i);
+        if (k == L - 1) sl -= c_of(i);
+        r = (k == 0) ? sl : sl - ai * (r / den);
         den = r - ci;
         if (!(den > 0.0) || !isfinite(den)) atomicExch(bad, 1);
-        const double w = 1.0 / den;
-        double *R = rowc + (size_t)i * 8;
-        R[0] = w;
-        R[1] = -(w * ai);
-        R[2] = -(w * ci);
-        R[7] = 0.0;
+        w[k] = 1.0 / den;
+        ga[k] = w[k] * ai;
+        cp[k] = w[k] * ci;
+        if (k == 0) d[0] = 1.0;
+        if (k + 1 < L) {
+            if (ci != 0.0) {
+                d[k + 1] = d[k] * (den / -ci);
+            } else {
+                d[k + 1] = d[k];
+                if (i < n - 1) scal = false;
+            }
+            const double ad = fabs(d[k + 1]);
+            if (!(ad < 0x1p900 && ad > 0x1p-900)) scal = false;
+        }
     }
-    // T_c x = rhs: forward y_i = w_i rhs_i - ga_i y_{i-1}, back x_i = y_i - cp_i x_{i+1}
-    double y[64];                                   // L <= 64
-    double *E = ends + (size_t)c * 8;
-    for (int which = 0; which < 5; ++which) {       // 0: V, 1: W, 2: rho, 3: V2, 4: W2
+    if (!scal) atomicExch(noscale, 1);
+    for (int k = 0; k < L; ++k) {
+        double *R = rowc + (size_t)(s0 + k) * PART_ROWC;
+        R[0] = w[k];
+        R[1] = (k == 0) ? 0.0 : -(a_of(s0 + k) * w[k - 1]) * (d[k - 1] / d[k]);
+        R[6] = d[k];
+        R[7] = 1.0 / d[k];
+    }
+    // T_c x = rhs: forward y_k = w_k rhs_k - ga_k y_{k-1}, back x_k = y_k - cp_k x_{k+1}
+    double y[64];
+    double *E = ends + (size_t)c * PART_ENDS;
+    for (int which = 0; which < 5; ++which) {       // 0 V, 1 W, 2 rho, 3 V2, 4 W2
         double yp = 0.0;
-        for (int i = s0; i < e0; ++i) {
-            const double *R = rowc + (size_t)i * 8;
+        for (int k = 0; k < L; ++k) {
+            const double *R = rowc + (size_t)(s0 + k) * PART_ROWC;
             double rhs = 0.0;
-            if (which == 0 && i == s0) rhs = -a_of(s0);
-            if (which == 1 && i == e0 - 1) rhs = -c_of(e0 - 1);
-            if (which == 2) rhs = s_of(i);
-            if (which == 3) rhs = R[3];
-            if (which == 4) rhs = R[4];
-            yp = fma(R[1], yp, R[0] * rhs);
-            y[i - s0] = yp;
+            if (which == 0 && k == 0) rhs = -a_of(s0);
+            if (which == 1 && k == L - 1) rhs = -c_of(e0 - 1);
+            if (which == 2) rhs = s_of(s0 + k);
+            if (which == 3) rhs = R[4];
+            if (which == 4) rhs = R[5];
+            yp = fma(-ga[k], yp, w[k] * rhs);
+            y[k] = yp;
         }
         double xn = 0.0;
-        for (int i = e0 - 1; i >= s0; --i) {
-            double *R = rowc + (size_t)i * 8;
-            const double x = fma(R[2], xn, y[i - s0]);
-            if (which == 0) R[3] = x;
-            if (which == 1) R[4] = x;
-            if (which == 3) R[5] = x;
-            if (which == 4) R[6] = x;
+        for (int k = L - 1; k >= 0; --k) {
+            double *R = rowc + (size_t)(s0 + k) * PART_ROWC;
+            const double x = fma(-cp[k], xn, y[k]);
+            if (which == 0) R[4] = x;
+            if (which == 1) R[5] = x;
+            if (which == 3) R[2] = x / d[k];
+            if (which == 4) R[3] = x / d[k];
             if (which < 3) {
-                if (i == s0) E[which == 0 ? 2 : which == 1 ? 4 : 0] = x;
-                if (i == e0 - 1) E[which == 0 ? 3 : which == 1 ? 5 : 1] = x;
+                const int top = which == 0 ? 2 : which == 1 ? 4 : 0;
+                if (k == 0) E[top] = x;
+                if (k == L - 1) E[top + 1] = x;
             }
             xn = x;
         }
@@ -206,7 +260,7 @@ __global__ void k_part_iface(int CL, int K, const double *ends, double *ctad, in
         for (int i = 0; i < PART_CTAD; ++i) D[i] = 0.0;
         for (int r = 0; r < M; ++r) {
             const int w = r / 2, e = r % 2;
-            const double *E = ends + (size_t)(C * K + w) * 8;
+            const double *E = ends + (size_t)(C * K + w) * PART_ENDS;
             for (int d = 0; d < 5; ++d) A[r][d] = 0.0;
             A[r][2] = 1.0;
             if (w > 0) A[r][(2 * w - 1) - r + 2] = -E[2 + e];
@@ -224,13 +278,33 @@ __global__ void k_part_iface(int CL, int K, const double *ends, double *ctad, in
             D[r * 5 + 3] = F[r][3] * F[r][2];
             D[r * 5 + 4] = F[r][4] * F[r][2];
         }
+        if (K >= 2) {                                // split-solve responses (K rows per half)
+            for (int e = 0; e < 2; ++e) {                // forward: carried (y_{K-2}, y_{K-1}) = unit
+                double ym2 = e == 0 ? 1.0 : 0.0, ym1 = e == 0 ? 0.0 : 1.0;
+                for (int r = K; r < M; ++r) {
+                    const double y = -F[r][0] * ym2 - F[r][1] * ym1;
+                    D[(e == 0 ? CTAD_FP : CTAD_FQ) + r - K] = y;
+                    ym2 = ym1;
+                    ym1 = y;
+                }
+            }
+            for (int e = 0; e < 2; ++e) {                // backward: carried (x_K, x_{K+1}) = unit
+                double xp1 = e == 0 ? 1.0 : 0.0, xp2 = e == 0 ? 0.0 : 1.0;
+                for (int r = K - 1; r >= 0; --r) {
+                    const double x = -(F[r][3] * F[r][2]) * xp1 - (F[r][4] * F[r][2]) * xp2;
+                    D[(e == 0 ? CTAD_BR : CTAD_BT) + r] = x;
+                    xp2 = xp1;
+                    xp1 = x;
+                }
+            }
+        }
         for (int col = 0; col < M; ++col) {          // rows 0 and M-1 of M_C^{-1}
             for (int r = 0; r < M; ++r) x[r] = (r == col) ? 1.0 : 0.0;
             band_solve(M, F, x);
             D[CTAD_R0 + col] = x[0];
             D[CTAD_RM + col] = x[M - 1];
         }
-        const double *E0 = ends + (size_t)(C * K) * 8, *E1 = ends + (size_t)(C * K + K - 1) * 8;
+        const double *E0 = ends + (size_t)(C * K) * PART_ENDS, *E1 = ends + (size_t)(C * K + K - 1) * PART_ENDS;
         for (int r = 0; r < M; ++r) x[r] = 0.0;
         x[0] = E0[2];
         x[1] = E0[3];
@@ -243,7 +317,7 @@ __global__ void k_part_iface(int CL, int K, const double *ends, double *ctad, in
         band_solve(M, F, x);
         for (int r = 0; r < M; ++r) D[CTAD_B + r] = x[r];
         const double bT = x[0], bB = x[M - 1];
-        for (int r = 0; r < M; ++r) x[r] = ends[(size_t)(C * K + r / 2) * 8 + r % 2];
+        for (int r = 0; r < M; ++r) x[r] = ends[(size_t)(C * K + r / 2) * PART_ENDS + r % 2];
         band_solve(M, F, x);
         // global rows 2C (T_C) and 2C+1 (B_C)
         for (int e = 0; e < 2; ++e) {
@@ -286,6 +360,8 @@ struct PartArgs {
     int nsteps, nsrc, q0, vpi;
     double dt;
     unsigned long long *prof;          // dev aid (PR_PART_PROF): per-phase clock sums, or null
+    unsigned idle_ns;                  // interface-warp poll back-off
+    int noiface;                       // dev aid (PR_PART_NOIFACE): sweeps only, wrong results
 };
 
 constexpr int PART_RSM = 8;            // shared-memory stride of the source rows
@@ -300,7 +376,7 @@ constexpr size_t part_smem_t()
 {
     constexpr int K = W * H;
     return (6 + (size_t)4 * CL * 32 + (size_t)4 * K * 32 + 4 * 32 + PART_CTAD +
-            (size_t)K * (L * (7 + (AFF ? PART_RSM : 0)) + 4) + CL + (size_t)4 * K * 32) * sizeof(double);
+            (size_t)K * (L * (4 + (AFF ? PART_RSM : 0)) + 4) + CL + (size_t)4 * K * 32 + 4 * 32) * sizeof(double);
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void *p)
@@ -329,6 +405,22 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity)
                      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                      "selp.u32 %0, 1, 0, p;\n\t}"
                      : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+    }
+}
+
+// the interface warps' waits span most of a sweep: back off between polls so
+// the spinning warp does not take issue slots from the compute warps of its
+// SM sub-partition
+__device__ __forceinline__ void mbar_wait_idle(unsigned bar, unsigned parity, unsigned ns)
+{
+    unsigned done = 0;
+    for (;;) {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(bar), "r"(parity) : "memory");
+        if (done) break;
+        if (ns) __nanosleep(ns);
     }
 }
 
@@ -418,18 +510,140 @@ __device__ __forceinline__ void band_backward(const double *__restrict__ F, doub
     }
 }
 
+// Split band solve (K >= 2): the 2K rows of the local interface system in two
+// halves of K rows.  Each half is eliminated from a zero carried state; the
+// second half's forward values and the first half's back-substituted values
+// are then corrected with the precomputed responses to the carried pair
+// (CTAD_FP/FQ, CTAD_BR/BT), an exact rewriting (R-PART).  One lane per half
+// (HI = 2: the two half-warps) or one lane doing both (HI = 1) performs the
+// same operations in the same order, so the result does not depend on the
+// group size.  Half hf: forward over its rows from zero state, with the partial
+// dot products of rows 0 / 2K-1 of M_C^{-1} (T_C, B_C).
+template <int K>
+__device__ __forceinline__ void half_forward(int hf, const double2 *__restrict__ g, const double *__restrict__ F,
+                                             double *__restrict__ z, double &T, double &B, double &y2o,
+                                             double &y1o)
+{
+    constexpr int NC = K / 2;                 // chunks per half
+    constexpr int BK = (NC < 4) ? NC : 4;     // chunks per block
+    const int c0 = hf * NC;
+    double T0 = 0.0, T1 = 0.0, B0 = 0.0, B1 = 0.0, y1 = 0.0, y2 = 0.0;
+#pragma unroll
+    for (int u0 = 0; u0 < NC; u0 += BK) {
+        double2 gv[BK];
+        double f0[2 * BK], f1[2 * BK];
+#pragma unroll
+        for (int b = 0; b < BK; ++b) {
+            const int i = 2 * (c0 + u0 + b);
+            gv[b] = g[(c0 + u0 + b) * 32];
+            f0[2 * b] = F[i * 5 + 0];
+            f1[2 * b] = F[i * 5 + 1];
+            f0[2 * b + 1] = F[(i + 1) * 5 + 0];
+            f1[2 * b + 1] = F[(i + 1) * 5 + 1];
+        }
+        double out[2 * BK];
+#pragma unroll
+        for (int b = 0; b < BK; ++b) {
+            const int i = 2 * (c0 + u0 + b);
+            T0 = fma(F[CTAD_R0 + i], gv[b].x, T0);
+            T1 = fma(F[CTAD_R0 + i + 1], gv[b].y, T1);
+            B0 = fma(F[CTAD_RM + i], gv[b].x, B0);
+            B1 = fma(F[CTAD_RM + i + 1], gv[b].y, B1);
+            const int r = 2 * (u0 + b);       // row within the half
+            double y = gv[b].x;
+            if (r >= 2) y = fma(-f0[2 * b], y2, y);
+            if (r >= 1) y = fma(-f1[2 * b], y1, y);
+            double yb = gv[b].y;
+            if (r >= 1) yb = fma(-f0[2 * b + 1], y1, yb);
+            yb = fma(-f1[2 * b + 1], y, yb);
+            out[2 * b] = y;
+            out[2 * b + 1] = yb;
+            y2 = y;
+            y1 = yb;
+        }
+#pragma unroll
+        for (int r = 0; r < 2 * BK; ++r) z[(size_t)(2 * (c0 + u0) + r) * 32] = out[r];
+    }
+    T = T0 + T1;
+    B = B0 + B1;
+    y2o = y2;
+    y1o = y1;
+}
+
+// back substitution over half hf from a zero carried state; returns the first
+// two values of the half.  fix: the half's forward values first get the
+// carried-pair correction y_i += y_{K-2} FP_i + y_{K-1} FQ_i (second half)
+template <int K>
+__device__ __forceinline__ void half_backward(int hf, const double *__restrict__ F, double *__restrict__ z,
+                                              double &x0o, double &x1o, bool fix, double ym2, double ym1)
+{
+    constexpr int BR = (K < 8) ? K : 8;       // rows per block
+    const int r0 = hf * K;
+    if (!fix) ym2 = ym1 = 0.0;
+    double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+    for (int i0 = K - BR; i0 >= 0; i0 -= BR) {
+        double zv[BR], inv[BR], u1[BR], u2[BR];
+#pragma unroll
+        for (int r = 0; r < BR; ++r) {
+            const int i = r0 + i0 + r;
+            zv[r] = fma(F[CTAD_FP + i0 + r], ym2, fma(F[CTAD_FQ + i0 + r], ym1, z[(size_t)i * 32]));
+            inv[r] = F[i * 5 + 2];
+            u1[r] = F[i * 5 + 3];
+            u2[r] = F[i * 5 + 4];
+        }
+#pragma unroll
+        for (int r = BR - 1; r >= 0; --r) {
+            const int il = i0 + r;            // row within the half
+            double t = zv[r] * inv[r];
+            if (il + 2 < K) t = fma(-u2[r], t2, t);
+            if (il + 1 < K) t = fma(-u1[r], t1, t);
+            zv[r] = t;
+            t2 = t1;
+            t1 = t;
+        }
+#pragma unroll
+        for (int r = 0; r < BR; ++r) z[(size_t)(r0 + i0 + r) * 32] = zv[r];
+    }
+    x0o = t1;
+    x1o = t2;
+}
+
+// Interface super-values of a half (hf) of the local rows: the partial dot
+// products of rows 0 / 2K-1 of M_C^{-1} with the raw ends (T_C, B_C), with
+// four independent accumulators; sent before the band solve runs.
+template <int K>
+__device__ __forceinline__ void half_dots(int hf, const double2 *__restrict__ g, const double *__restrict__ F,
+                                          double &T, double &B)
+{
+    constexpr int NC = K / 2;
+    double T0 = 0.0, T1 = 0.0, B0 = 0.0, B1 = 0.0;
+#pragma unroll
+    for (int b = 0; b < NC; ++b) {
+        const int cu = hf * NC + b, i = 2 * cu;
+        const double2 gv = g[cu * 32];
+        T0 = fma(F[CTAD_R0 + i], gv.x, T0);
+        T1 = fma(F[CTAD_R0 + i + 1], gv.y, T1);
+        B0 = fma(F[CTAD_RM + i], gv.x, B0);
+        B1 = fma(F[CTAD_RM + i + 1], gv.y, B1);
+    }
+    T = T0 + T1;
+    B = B0 + B1;
+}
+
 // Warps 0..W-1 each own H chunks (the warp's lanes split into H groups of
 // LPC = 32/H lanes, one chunk each) and only sweep; each lane carries VPT
 // vectors of its chunk, so a group of VPG = LPC * VPT vectors runs on a
-// cluster and every shared-memory coefficient load (a warp broadcast) feeds
-// VPT independent recurrences.  Warps W and W+1 are the interface warps: W
-// turns the chunks' raw end values into super-chunk values (two rows of the
-// local inverse, sent first, then the banded local solve), W+1 gathers every
-// CTA's values and forms each chunk's (b_{c-1}, t_{c+1}) -- all while the
-// compute warps run the next sweep.  Local
-// hand-offs use mbarriers: ebar[p] (W compute warps arrive: raw ends of a step
-// of parity p written), cbar[p] (interface warp arrives: interface values of a
-// step of parity p written); gbar[p] counts the cluster gather bytes.
+// cluster and every shared-memory coefficient load feeds VPT independent
+// recurrences.  Warps W (publish) and W+1 (gather) are the interface warps:
+// the publish warp turns the chunks' raw end values into the super-chunk values
+// (T_C, B_C) (two rows of the local inverse), sends them to every CTA of the
+// cluster and then runs the banded local solve; the gather warp forms
+// (B_{C-1}, T_{C+1}) from every CTA's values -- all while the compute warps
+// run the next sweep (one-step lag, see the setup comment and R-PART).
+// Hand-offs use mbarriers: ebar[p] (W compute warps arrive: raw ends of a
+// step of parity p written), cbar[p] (publish + gather arrive: interface
+// values of a step of parity p written); gbar[p] counts the gather bytes.
 template <int CL, int W, int H, int L, int VPT, bool AFF>
 __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
 {
@@ -439,6 +653,7 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
     constexpr int HI = 32 / VPG;         // interface-warp lanes per vector
     constexpr int K = W * H;             // chunks per CTA
     constexpr int M = 2 * K;             // local interface unknowns
+    constexpr bool SPLIT = K >= 16;      // split band solve (two halves)
     constexpr int RSM = AFF ? PART_RSM : 0;
     extern __shared__ __align__(16) double sm[];
     cg::cluster_group cluster = cg::this_cluster();
@@ -453,9 +668,12 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
     double *regions = ctad + PART_CTAD;
     // chunk regions are padded by 4 doubles so that the chunks the lane groups
     // of one warp read fall in different shared-memory banks
-    constexpr int RSTR = L * (7 + RSM) + 4;
+    constexpr int RSTR = L * (4 + RSM) + 4;
     unsigned *rmap = reinterpret_cast<unsigned *>(regions + (size_t)K * RSTR);  // [2][CL]
-    auto cd_of = [&](int u) { return reinterpret_cast<double4 *>(regions + (size_t)u * RSTR); };
+    double *zs = reinterpret_cast<double *>(rmap + 2 * CL);                     // [2][M][32]
+    double2 *zfx = reinterpret_cast<double2 *>(zs + 2 * M * 32);                // [2][32]
+    // chunk region: {V2~, W2~} [L] (double2) | nl [L] | w [L] | scaled source rows [L][RSM]
+    auto cd_of = [&](int u) { return reinterpret_cast<double2 *>(regions + (size_t)u * RSTR); };
     const unsigned bar0 = smem_u32(bar), gth0 = smem_u32(gth);
     const unsigned gbar = bar0, ebar = bar0 + 16, cbar = bar0 + 32;
 
@@ -465,14 +683,13 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
         rmap[CL + threadIdx.x] = cluster_map(bar0, threadIdx.x);
     }
     if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(gbar) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(gbar + 8) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(ebar), "r"(W) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(ebar + 8), "r"(W) : "memory");
-        // interface values of a step are complete when both the publish warp
-        // (local solution z) and the gather warp ((B_{C-1}, T_{C+1})) arrived
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" :: "r"(cbar) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" :: "r"(cbar + 8) : "memory");
+        for (int q = 0; q < 2; ++q) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(gbar + 8 * q) : "memory");
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(ebar + 8 * q), "r"(W) : "memory");
+            // interface values of a step are complete when both the publish warp
+            // (local solution z) and the gather warp ((B_{C-1}, T_{C+1})) arrived
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" :: "r"(cbar + 8 * q) : "memory");
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // ctad / rmap are written by all warps and read below (neighbours) by
@@ -488,25 +705,28 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
 #pragma unroll 4
         for (int i = lane; i < H * L; i += 32) {     // this warp's H chunk regions
             const int uu = w * H + i / L, row = i % L;
-            const double2 *R = reinterpret_cast<const double2 *>(a.rowc + ((size_t)(C * K + uu) * L + row) * 8);
-            const double2 r01 = R[0], r23 = R[1], r45 = R[2], r67 = R[3];
-            double4 *cdu = cd_of(uu);
-            cdu[row] = make_double4(r01.x, r01.y, r45.y, r67.x);
-            reinterpret_cast<double *>(cdu)[4 * L + row] = r23.x;
-            reinterpret_cast<double2 *>(reinterpret_cast<double *>(cdu) + 5 * L)[row] = make_double2(r23.y, r45.x);
+            const double2 *R =
+                reinterpret_cast<const double2 *>(a.rowc + ((size_t)(C * K + uu) * L + row) * PART_ROWC);
+            const double2 r01 = R[0], r23 = R[1], r67 = R[3];
+            double2 *cdu = cd_of(uu);
+            cdu[row] = r23;                                              // {V2~, W2~}
+            reinterpret_cast<double *>(cdu)[2 * L + row] = r01.y;        // nl
+            reinterpret_cast<double *>(cdu)[3 * L + row] = r01.x;        // w
             if constexpr (AFF) {
                 const int grow = (C * K + uu) * L + row;
-                double *spu = reinterpret_cast<double *>(cdu) + 7 * L + row * RSM;
+                double *spu = reinterpret_cast<double *>(cdu) + 4 * L + row * RSM;
 #pragma unroll
                 for (int r = 0; r < RSM; ++r)
-                    spu[r] = (grow < a.n && r < a.RS) ? a.spaceT[(size_t)grow * a.RS + r] : 0.0;
+                    spu[r] = (grow < a.n && r < a.RS) ? a.spaceT[(size_t)grow * a.RS + r] * r67.y : 0.0;
             }
         }
         __syncwarp();
-        const double4 *cd = cd_of(u);
-        const double *cu = reinterpret_cast<const double *>(cd) + 4 * L;
-        const double2 *vw = reinterpret_cast<const double2 *>(cu + L);
-        const double *sp = cu + 3 * L;
+        const double2 *cd = cd_of(u);
+        const double *nl = reinterpret_cast<const double *>(cd) + 2 * L;
+        const double *wv = nl + L;
+        const double *sp = wv + L;
+        const double *rowc_u = a.rowc + (size_t)c * L * PART_ROWC;     // this chunk's rows (global)
+        const double dbot = rowc_u[(L - 1) * PART_ROWC + 6];            // d_{L-1} (d_0 = 1)
         long vv[VPT];
         bool valid[VPT];
 #pragma unroll
@@ -514,22 +734,52 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
             vv[t] = gbase + li + t * LPC;
             valid[t] = vv[t] < a.B;
         }
+        // the state in the chunk's scaled coordinates x~ = x / d.  Loads are
+        // issued unconditionally from clamped addresses (no per-row branch, so
+        // all rows are in flight together) and masked afterwards.
         double S[VPT][L];
+        {
+            long vc[VPT];
 #pragma unroll
-        for (int t = 0; t < VPT; ++t)
+            for (int t = 0; t < VPT; ++t) vc[t] = valid[t] ? vv[t] : 0;
+            if (a.in) {
 #pragma unroll
-            for (int i = 0; i < L; ++i)
-                S[t][i] = (a.in && valid[t] && s0 + i < a.n) ? a.in[(long)(s0 + i) * a.ld_in + vv[t]] : 0.0;
+                for (int i = 0; i < L; ++i) {
+                    const int row = (s0 + i < a.n) ? s0 + i : a.n - 1;
+                    const double dinv = (s0 + i < a.n) ? rowc_u[i * PART_ROWC + 7] : 0.0;
+#pragma unroll
+                    for (int t = 0; t < VPT; ++t) {
+                        const double v = __ldg(a.in + (long)row * a.ld_in + vc[t]);
+                        S[t][i] = valid[t] ? v * dinv : 0.0;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < L; ++i)
+#pragma unroll
+                    for (int t = 0; t < VPT; ++t) S[t][i] = 0.0;
+            }
+        }
         // (b_{c-1}, t_{c+1}) of a step from the CTA's (B_{C-1}, T_{C+1}), this
-        // chunk's super-spike entries and the local solution z
-        const double *zsb = reinterpret_cast<const double *>(rmap + 2 * CL);
+        // chunk's super-spike entries and the local solution z.  Split solve:
+        // the first half's z still lacks x_K BR + x_{K+1} BT, applied here.
+        const double *zsb = zs;
         auto neighbours = [&](int pp, int vs, double &b, double &t) {
             const double2 bt = coef[pp * 32 + vs];
             const double *zz = zsb + (size_t)pp * M * 32 + vs;
-            b = (u == 0) ? bt.x
-                         : fma(ctad[CTAD_A + 2 * u - 1], bt.x, fma(ctad[CTAD_B + 2 * u - 1], bt.y, zz[(2 * u - 1) * 32]));
+            auto zval = [&](int pos) {
+                double v = zz[pos * 32];
+                if constexpr (SPLIT) {
+                    if (pos < K) {
+                        const double2 fx = zfx[pp * 32 + vs];
+                        v = fma(ctad[CTAD_BR + pos], fx.x, fma(ctad[CTAD_BT + pos], fx.y, v));
+                    }
+                }
+                return v;
+            };
+            b = (u == 0) ? bt.x : fma(ctad[CTAD_A + 2 * u - 1], bt.x, fma(ctad[CTAD_B + 2 * u - 1], bt.y, zval(2 * u - 1)));
             t = (u == K - 1) ? bt.y
-                             : fma(ctad[CTAD_A + 2 * u + 2], bt.x, fma(ctad[CTAD_B + 2 * u + 2], bt.y, zz[(2 * u + 2) * 32]));
+                             : fma(ctad[CTAD_A + 2 * u + 2], bt.x, fma(ctad[CTAD_B + 2 * u + 2], bt.y, zval(2 * u + 2)));
         };
         cluster.sync();
         int q[VPT], src[VPT];
@@ -538,10 +788,15 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
             q[t] = valid[t] ? a.q0 + (int)(vv[t] / a.vpi) : a.q0;
             src[t] = (AFF && valid[t]) ? (int)(vv[t] % a.nsrc) : 0;
         }
-        double ca[VPT], cc[VPT];     // (b_{c-1}, t_{c+1}) of step j-1: coefficients of V2, W2
+        double ca[VPT], cc[VPT];     // (b_{c-1}, t_{c+1}) of step j-1: coefficients of V2~, W2~
 #pragma unroll
         for (int t = 0; t < VPT; ++t) ca[t] = cc[t] = 0.0;
+#ifdef PR_PART_PROBES
+        unsigned long long pacc[PART_NPROBE] = {};
+        PROBE_T(tl0);
+#endif
         for (int j = 1; j <= a.m; ++j) {
+            PROBE_T(t0);
             double alpha[VPT][AFF ? PART_RSM : 1];
             if constexpr (AFF) {
 #pragma unroll
@@ -555,82 +810,104 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
                         alpha[t][r] = al;
                     }
             }
-            // S_j = T_c^{-1}(S_{j-1} + ca V2 + cc W2 + dt f_j); down: y_i = w_i x_i - ga_i y_{i-1}
-            double yp[VPT];
-#pragma unroll
-            for (int t = 0; t < VPT; ++t) yp[t] = 0.0;
+            // S_j = T_c^{-1}(S_{j-1} + ca V2 + cc W2 + dt f_j) in scaled form:
+            // down z_i = x_i + nl_i z_{i-1}, up S_i = w_i z_i + S_{i+1}
+            double zp[VPT];
 #pragma unroll
             for (int i = 0; i < L; ++i) {
-                const double4 q4 = cd[i];
+                const double2 q2 = cd[i];
+                const double nli = nl[i];
 #pragma unroll
                 for (int t = 0; t < VPT; ++t) {
-                    double x = fma(q4.z, ca[t], fma(q4.w, cc[t], S[t][i]));
+                    double x = fma(q2.x, ca[t], fma(q2.y, cc[t], S[t][i]));
                     if constexpr (AFF) {
 #pragma unroll
                         for (int r = 0; r < PART_RSM; ++r) x = fma(alpha[t][r], sp[i * RSM + r], x);
                     }
-                    yp[t] = fma(q4.y, yp[t], q4.x * x);
-                    S[t][i] = yp[t];
+                    zp[t] = (i == 0) ? x : fma(nli, zp[t], x);
+                    S[t][i] = zp[t];
                 }
             }
-            // up: S_i = y_i - cp_i S_{i+1}
+            PROBE_T(t1);
+            PROBE_ADD(0, t1 - t0);
             double gn[VPT];
 #pragma unroll
-            for (int t = 0; t < VPT; ++t) gn[t] = 0.0;
-#pragma unroll
             for (int i = L - 1; i >= 0; --i) {
-                const double cui = cu[i];
+                const double wi = wv[i];
 #pragma unroll
                 for (int t = 0; t < VPT; ++t) {
-                    gn[t] = fma(cui, gn[t], S[t][i]);
+                    gn[t] = (i == L - 1) ? wi * S[t][i] : fma(wi, S[t][i], gn[t]);
                     S[t][i] = gn[t];
                 }
             }
             const int p = j & 1;
-            if (j >= 2) {              // interface values of step j-1 (formed during this sweep)
+            PROBE_T(t2);
+            PROBE_ADD(1, t2 - t1);
+            if (j >= 2 && !a.noiface) {   // interface values of step j-1 (formed during this sweep)
                 const int pp = (j - 1) & 1;
                 mbar_wait(cbar + 8 * pp, ((j - 2) >> 1) & 1);
 #pragma unroll
                 for (int t = 0; t < VPT; ++t) neighbours(pp, li + t * LPC, ca[t], cc[t]);
             }
-            {                          // chunk ends of g_j = S_j + ca V2 + cc W2
-                const double4 q0 = cd[0], q1 = cd[L - 1];
+            PROBE_T(t3);
+            PROBE_ADD(2, t3 - t2);
+            {                          // physical chunk ends of g_j = S_j + ca V2 + cc W2
+                const double2 q0 = cd[0], q1 = cd[L - 1];
 #pragma unroll
                 for (int t = 0; t < VPT; ++t)
                     rawE[(p * K + u) * 32 + li + t * LPC] =
-                        make_double2(fma(q0.z, ca[t], fma(q0.w, cc[t], S[t][0])),
-                                     fma(q1.z, ca[t], fma(q1.w, cc[t], S[t][L - 1])));
+                        make_double2(fma(q0.x, ca[t], fma(q0.y, cc[t], S[t][0])),
+                                     dbot * fma(q1.x, ca[t], fma(q1.y, cc[t], S[t][L - 1])));
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(ebar + 8 * p);
+            if (lane == 0 && !a.noiface) mbar_arrive(ebar + 8 * p);
+            PROBE_T(t4);
+            PROBE_ADD(3, t4 - t3);
         }
+#ifdef PR_PART_PROBES
+        PROBE_T(tl1);
+        PROBE_ADD(11, tl1 - tl0);
+        if (lane == 0 && w == 0 && a.prof)
+            for (int k = 0; k < 4; ++k) atomicAdd(a.prof + k, pacc[k]);
+        if (lane == 0 && w == 0 && a.prof) atomicAdd(a.prof + 11, pacc[11]);
+        if (lane == 0 && w == 0 && a.prof) atomicAdd(a.prof + 10, (unsigned long long)a.m);
+#endif
+        // x_m = S_m + ca V2 + cc W2 + b_m V + t_m W, branch-free per row (the
+        // row data loads are uniform over the chunk's lanes), masked stores
         const int pm = a.m & 1;
-        mbar_wait(cbar + 8 * pm, ((a.m - 1) >> 1) & 1);
+        double ex[VPT], ey[VPT];                     // (b_m, t_m) of the neighbours
 #pragma unroll
-        for (int t = 0; t < VPT; ++t) {
-            double ex, ey;                                       // (b_m, t_m) of the neighbours
-            neighbours(pm, li + t * LPC, ex, ey);
-            if (valid[t]) {
+        for (int t = 0; t < VPT; ++t) ex[t] = ey[t] = 0.0;
+        if (!a.noiface) {
+            mbar_wait(cbar + 8 * pm, ((a.m - 1) >> 1) & 1);
 #pragma unroll
-                for (int i = 0; i < L; ++i) {
-                    if (s0 + i < a.n) {
-                        const double4 q4 = cd[i];
-                        const double2 VW = vw[i];
-                        double x = fma(q4.z, ca[t], fma(q4.w, cc[t], S[t][i]));
-                        x = fma(VW.x, ex, fma(VW.y, ey, x));
-                        if (a.off) x += a.off[(long)(s0 + i) * a.ld_off + vv[t]];
-                        a.out[(long)(s0 + i) * a.ld_out + vv[t]] = x;
-                    }
+            for (int t = 0; t < VPT; ++t) neighbours(pm, li + t * LPC, ex[t], ey[t]);
+        }
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+            const double2 q2 = cd[i];
+            const double2 *R = reinterpret_cast<const double2 *>(rowc_u + i * PART_ROWC);
+            const double2 VW = __ldg(R + 2), dd = __ldg(R + 3);
+            const bool rok = s0 + i < a.n;
+#pragma unroll
+            for (int t = 0; t < VPT; ++t) {
+                double x = fma(q2.x, ca[t], fma(q2.y, cc[t], S[t][i]));
+                x = fma(VW.x, ex[t], fma(VW.y, ey[t], dd.x * x));
+                if (rok && valid[t]) {
+                    if (a.off) x += a.off[(long)(s0 + i) * a.ld_off + vv[t]];
+                    a.out[(long)(s0 + i) * a.ld_out + vv[t]] = x;
                 }
             }
         }
     } else {
-        // ------------------------------------------------ interface warp
+        // ------------------------------------------------ interface warps
         // lane = (part hi, vector vl); with HI = 2 the two half-warps split the
-        // cluster sends and the gather dot products of the same 16 vectors
+        // cluster sends, the solve halves and the gather dot products
         const int hi = lane / VPG, vl = lane % VPG;
+#ifdef PR_PART_PROBES
+        unsigned long long pacc[PART_NPROBE] = {};
+#endif
         cluster.sync();
-        double *zs = reinterpret_cast<double *>(rmap + 2 * CL);          // [2][M][32]
         constexpr int CLH = CL / HI;                                     // CTAs per lane part
         // step j's values from every super-chunk -> (B_{C-1}, T_{C+1}) of step j
         auto gather = [&](int j) {
@@ -638,7 +915,10 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
             if (lane == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                              :: "r"(gbar + 8 * p), "r"((unsigned)(CL * VPG * sizeof(double2))) : "memory");
-            mbar_wait(gbar + 8 * p, ((j - 1) >> 1) & 1);
+            PROBE_T(g0);
+            mbar_wait_idle(gbar + 8 * p, ((j - 1) >> 1) & 1, a.idle_ns);
+            PROBE_T(g1);
+            PROBE_ADD(8, g1 - g0);
             const double2 *Gt = gth + (size_t)p * CL * 32 + vl;
             // the two halves of the CTA list are summed separately and then
             // added, for HI = 1 and HI = 2 alike: the result does not depend on
@@ -672,36 +952,92 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
             if (hi == 0) coef[p * 32 + vl] = make_double2(Bx, Tx);
             __syncwarp();
             if (lane == 0) mbar_arrive(cbar + 8 * p);
+            PROBE_T(g2);
+            PROBE_ADD(9, g2 - g1);
         };
-        // chunk end values of step j -> local solve z = M_C^{-1} g_C -> (T_C, B_C)
-        // to every CTA.  The band solve streams through shared memory with the
-        // two recurrence carries in registers (one dependent FMA per row in
-        // each direction; loads of g and of the forward values are off the
-        // chain), so M = 2K up to 64 needs no register array.  Each lane works
-        // in its own slot (vl + VPG * hi) and the hi = 0 lanes hold the result.
+        // chunk end values of step j -> (T_C, B_C) to every CTA, then the local
+        // solve z = M_C^{-1} g_C (off the exchange's critical path)
         auto publish = [&](int j) {
             const int p = j & 1;
-            mbar_wait(ebar + 8 * p, ((j - 1) >> 1) & 1);
+            PROBE_T(p0);
+            mbar_wait_idle(ebar + 8 * p, ((j - 1) >> 1) & 1, a.idle_ns);
+            PROBE_T(p1);
+            PROBE_ADD(4, p1 - p0);
             const double2 *rE = rawE + (size_t)p * K * 32 + vl;
-            double *zl = zs + (size_t)p * M * 32 + vl + VPG * hi;
-            // forward elimination y = L^{-1} g (stored), and (T_C, B_C) from the
-            // two stored rows of M_C^{-1} applied to g (independent FMAs)
-            double T0, T1, B0, B1;
-            band_forward<K>(rE, ctad, zl, T0, T1, B0, B1);
-            const double Tv = T0 + T1, Bv = B0 + B1;
             const unsigned off = (unsigned)(((p * CL + C) * 32 + vl) * sizeof(double2));
+            if constexpr (SPLIT) {
+                // (T, B) partial sums of half 0 and half 1, added in that order
+                double T0h, T1h, B0h, B1h;
+                if constexpr (HI == 2) {
+                    double Tm, Bm;
+                    half_dots<K>(hi, rE, ctad, Tm, Bm);
+                    const double To = __shfl_xor_sync(0xffffffffu, Tm, 16);
+                    const double Bo = __shfl_xor_sync(0xffffffffu, Bm, 16);
+                    T0h = hi ? To : Tm;
+                    T1h = hi ? Tm : To;
+                    B0h = hi ? Bo : Bm;
+                    B1h = hi ? Bm : Bo;
+                } else {
+                    half_dots<K>(0, rE, ctad, T0h, B0h);
+                    half_dots<K>(1, rE, ctad, T1h, B1h);
+                }
+                const double Tv = T0h + T1h, Bv = B0h + B1h;
 #pragma unroll
-            for (int rr = 0; rr < CLH; ++rr) {
-                const int r = hi * CLH + rr;
-                st_async_v2(rmap[r] + off, Tv, Bv, rmap[CL + r] + 8 * p);
+                for (int rr = 0; rr < CLH; ++rr) {
+                    const int r = hi * CLH + rr;
+                    st_async_v2(rmap[r] + off, Tv, Bv, rmap[CL + r] + 8 * p);
+                }
+                PROBE_T(p2);
+                PROBE_ADD(5, p2 - p1);
+                // split solve: all lanes write the common result slot vl
+                double *zc = zs + (size_t)p * M * 32 + vl;
+                double y2c, y1c;                      // half 0's carried pair
+                double Tx, Bx;                        // (unused: the dots above)
+                if constexpr (HI == 2) {
+                    double y2m, y1m;
+                    half_forward<K>(hi, rE, ctad, zc, Tx, Bx, y2m, y1m);
+                    y2c = __shfl_xor_sync(0xffffffffu, y2m, 16);
+                    y1c = __shfl_xor_sync(0xffffffffu, y1m, 16);
+                } else {
+                    double y2x, y1x;
+                    half_forward<K>(0, rE, ctad, zc, Tx, Bx, y2c, y1c);
+                    half_forward<K>(1, rE, ctad, zc, Tx, Bx, y2x, y1x);
+                }
+                PROBE_T(p3);
+                PROBE_ADD(6, p3 - p2);
+                double2 *zfix = zfx + p * 32 + vl;
+                if constexpr (HI == 2) {
+                    double x0m, x1m;
+                    half_backward<K>(hi, ctad, zc, x0m, x1m, hi == 1, y2c, y1c);
+                    if (hi == 1) *zfix = make_double2(x0m, x1m);
+                } else {
+                    double xk, xk1, x0x, x1x;
+                    half_backward<K>(1, ctad, zc, xk, xk1, true, y2c, y1c);
+                    half_backward<K>(0, ctad, zc, x0x, x1x, false, 0.0, 0.0);
+                    *zfix = make_double2(xk, xk1);
+                }
+                __syncwarp();
+                PROBE_T(p4);
+                PROBE_ADD(7, p4 - p3);
+            } else {
+                double *zl = zs + (size_t)p * M * 32 + vl + VPG * hi;
+                // forward elimination y = L^{-1} g (stored), and (T_C, B_C) from the
+                // two stored rows of M_C^{-1} applied to g (independent FMAs)
+                double T0, T1, B0, B1;
+                band_forward<K>(rE, ctad, zl, T0, T1, B0, B1);
+                const double Tv = T0 + T1, Bv = B0 + B1;
+#pragma unroll
+                for (int rr = 0; rr < CLH; ++rr) {
+                    const int r = hi * CLH + rr;
+                    st_async_v2(rmap[r] + off, Tv, Bv, rmap[CL + r] + 8 * p);
+                }
+                // back substitution with the pre-scaled factors {.., 1/u, u1/u, u2/u}
+                band_backward<M>(ctad, zl);
+                __syncwarp();
             }
-            // back substitution with the pre-scaled factors {.., 1/u, u1/u, u2/u}
-            band_backward<M>(ctad, zl);
-            __syncwarp();
         };
-        // two warps: warp W publishes step j (its local solve overlaps the
-        // cluster exchange), warp W+1 gathers step j; each arrives on cbar
-        if (w == W) {
+        if (a.noiface) {
+        } else if (w == W) {
             for (int j = 1; j <= a.m; ++j) {
                 publish(j);
                 if (lane == 0) mbar_arrive(cbar + 8 * (j & 1));
@@ -709,6 +1045,11 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
         } else {
             for (int j = 1; j <= a.m; ++j) gather(j);
         }
+#ifdef PR_PART_PROBES
+        if (lane == 0 && a.prof)
+            for (int k = 4; k < 10; ++k)
+                if (pacc[k]) atomicAdd(a.prof + k, pacc[k]);
+#endif
     }
     cluster.sync();                // no CTA leaves while cluster peers may still target it
 }
@@ -734,10 +1075,11 @@ bool part_config(int n, int &P, int &L, int &CL, int &K)
 
 cudaError_t launch_part_setup(int n, int P, int L, int CL, int K, const double *subA, const double *supA,
                               const double *rsA, const double *diagA, double dt, int transpose, double *rowc,
-                              double *ctad, double *ends, int *bad, cudaStream_t s)
+                              double *ctad, double *ends, int *bad, int *noscale, cudaStream_t s)
 {
     note_launch();
-    k_part_setup<<<(P + 63) / 64, 64, 0, s>>>(n, P, L, subA, supA, rsA, diagA, dt, transpose, rowc, ends, bad);
+    k_part_setup<<<(P + 63) / 64, 64, 0, s>>>(n, P, L, subA, supA, rsA, diagA, dt, transpose, rowc, ends, bad,
+                                              noscale);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     note_launch();
@@ -785,6 +1127,25 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
         (void)cudaGetLastError();
     }
     note_launch();
+#ifdef PR_PART_PROBES
+    if (flags().part_prof) {
+        PartArgs b = a;
+        cudaMalloc(&b.prof, PART_NPROBE * sizeof(unsigned long long));
+        cudaMemsetAsync(b.prof, 0, PART_NPROBE * sizeof(unsigned long long), s);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF>, b);
+        unsigned long long h[PART_NPROBE];
+        cudaMemcpyAsync(h, b.prof, sizeof(h), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        cudaFree(b.prof);
+        const double st = h[10] ? (double)h[10] : 1.0;   // steps x CTAs (compute warp 0)
+        fprintf(stderr,
+                "part probes (cycles per CTA-step): down %.0f up %.0f wait-iface %.0f ends %.0f | "
+                "publish: wait %.0f dots+send %.0f fwd %.0f bwd %.0f | gather: wait %.0f dot %.0f | loop/step %.0f\n",
+                h[0] / st, h[1] / st, h[2] / st, h[3] / st, h[4] / st, h[5] / st, h[6] / st, h[7] / st,
+                h[8] / st, h[9] / st, h[11] / st);
+        return e;
+    }
+#endif
     return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF>, a);
 }
 
@@ -818,6 +1179,8 @@ cudaError_t launch_stepper_part(const Op &op, const StepArgs &sa, int transpose,
     a.RS = sa.R > 0 ? stepper_rs(sa.R) : 0;
     a.spaceT = sa.spaceT; a.time = sa.time; a.amp = sa.amp;
     a.nsteps = sa.nsteps; a.nsrc = sa.nsrc; a.q0 = sa.q0; a.vpi = sa.vpi; a.dt = sa.dt;
+    a.idle_ns = flags().part_idle_ns >= 0 ? (unsigned)flags().part_idle_ns : PART_IDLE_NS;
+    a.noiface = flags().part_noiface;
     if (sa.B == 0) return cudaSuccess;
     const int K = op.part_K;
     // two chunks per warp (16 vectors per warp) when that spreads a small batch

@@ -127,6 +127,8 @@ static void read_flags()
     f.part_h = num("PR_PART_H");
     f.stepper_pd = num("PR_STEPPER_PD");
     f.stepper_vpt = num("PR_STEPPER_VPT");
+    if (getenv("PR_PART_IDLE_NS")) f.part_idle_ns = num("PR_PART_IDLE_NS");
+    f.part_noiface = on("PR_PART_NOIFACE");
     g_flags = f;
 }
 
@@ -461,7 +463,7 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
         return st;
     };
     cudaError_t e = cudaMalloc(&d_in, 5 * nb);
-    if (e == cudaSuccess) e = cudaMalloc(&d_bad, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&d_bad, 2 * sizeof(int));   // {bad pivot, not scalable}
     if (e == cudaSuccess) e = cudaMalloc(&op.dn_fw, n * sizeof(Coef));
     if (e == cudaSuccess) e = cudaMalloc(&op.up_fw, n * sizeof(Coef));
     if (e == cudaSuccess) e = cudaMalloc(&op.dn_tr, n * sizeof(Coef));
@@ -473,7 +475,7 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
     if (e == cudaSuccess) e = cudaMemcpy(dsup, sup, nb, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && rowsum) e = cudaMemcpy(drs, rowsum, nb, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && colsum) e = cudaMemcpy(dcs, colsum, nb, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemset(d_bad, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(d_bad, 0, 2 * sizeof(int));
     if (e == cudaSuccess)
         e = launch_factor_1d(n, dsub, dsup, rowsum ? drs : nullptr, ddiag, dt, 0, op.dn_fw, op.up_fw, d_bad, 0);
     if (e == cudaSuccess)
@@ -483,24 +485,32 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
     double *d_ends = nullptr;
     if (e == cudaSuccess && part_config(n, pP, pL, pCL, pK)) {
         op.part_P = pP; op.part_L = pL; op.part_CL = pCL; op.part_K = pK;
-        const size_t rb = (size_t)pP * pL * 8 * sizeof(double), cb = (size_t)pCL * PART_CTAD * sizeof(double);
+        const size_t rb = (size_t)pP * pL * PART_ROWC * sizeof(double), cb = (size_t)pCL * PART_CTAD * sizeof(double);
         e = cudaMalloc(&op.part_rowc_fw, rb);
         if (e == cudaSuccess) e = cudaMalloc(&op.part_rowc_tr, rb);
         if (e == cudaSuccess) e = cudaMalloc(&op.part_ctad_fw, cb);
         if (e == cudaSuccess) e = cudaMalloc(&op.part_ctad_tr, cb);
-        if (e == cudaSuccess) e = cudaMalloc(&d_ends, (size_t)8 * pP * sizeof(double));
+        if (e == cudaSuccess) e = cudaMalloc(&d_ends, (size_t)PART_ENDS * pP * sizeof(double));
         if (e == cudaSuccess)
             e = launch_part_setup(n, pP, pL, pCL, pK, dsub, dsup, rowsum ? drs : nullptr, ddiag, dt, 0,
-                                  op.part_rowc_fw, op.part_ctad_fw, d_ends, d_bad, 0);
+                                  op.part_rowc_fw, op.part_ctad_fw, d_ends, d_bad, d_bad + 1, 0);
         if (e == cudaSuccess)
             e = launch_part_setup(n, pP, pL, pCL, pK, dsub, dsup, colsum ? dcs : nullptr, ddiag, dt, 1,
-                                  op.part_rowc_tr, op.part_ctad_tr, d_ends, d_bad, 0);
+                                  op.part_rowc_tr, op.part_ctad_tr, d_ends, d_bad, d_bad + 1, 0);
     }
-    int bad = 0;
-    if (e == cudaSuccess) e = cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost);
+    int bad[2] = {0, 0};
+    if (e == cudaSuccess) e = cudaMemcpy(bad, d_bad, 2 * sizeof(int), cudaMemcpyDeviceToHost);
     cudaFree(d_ends);
+    if (e == cudaSuccess && bad[1] && op.part_P) {
+        // the chunk-local scaling of the partitioned stepper does not exist for
+        // this operator (decoupled rows or extreme coupling ratios, k_part.cu):
+        // every fine solve uses the streaming stepper K1
+        cudaFree(op.part_rowc_fw); cudaFree(op.part_ctad_fw); cudaFree(op.part_rowc_tr); cudaFree(op.part_ctad_tr);
+        op.part_rowc_fw = op.part_ctad_fw = op.part_rowc_tr = op.part_ctad_tr = nullptr;
+        op.part_P = op.part_L = op.part_CL = op.part_K = 0;
+    }
     if (e != cudaSuccess) return fail(cuda_fail(e, "pr_op_create_tridiag factor"));
-    if (bad) {
+    if (bad[0]) {
         set_error("non-positive or non-finite pivot in the factorisation of I + dt A");
         return fail(PR_ESINGULAR);
     }

@@ -52,6 +52,8 @@ struct Flags {
          no_expand_mma = false, part_prof = false, qr_trace = false, debug_sync = false;
     bool part_vpt2 = false, no_src_basis = false;
     int part_h = 0, stepper_pd = 0, stepper_vpt = 0;
+    int part_idle_ns = -1;
+    bool part_noiface = false; // PR_PART_NOIFACE: K1P sweeps without the interface (timing aid; wrong results)     // PR_PART_IDLE_NS: interface-warp poll back-off (dev aid; -1 = default)
 };
 const Flags &flags();
 
@@ -81,7 +83,8 @@ struct Op {
     Coef *dn_fw = nullptr, *up_fw = nullptr, *dn_tr = nullptr, *up_tr = nullptr;
     // 1D partitioned stepper (k_part.cu, small batches): P = CL * W chunks of
     // L rows (rows >= n: identity padding).  rowc: (P*L) x 8 per-row
-    // {w, -ga, -cp, V, W, V2, W2, 0}; ctad: CL x PART_CTAD per-CTA interface data.
+    // {w, nl, V2/d, W2/d, V, W, d, 1/d} (scaled form, k_part.cu); ctad: CL x PART_CTAD
+    // per-CTA interface data.
     int part_P = 0, part_L = 0, part_CL = 0, part_K = 0;
     double *part_rowc_fw = nullptr, *part_ctad_fw = nullptr;
     double *part_rowc_tr = nullptr, *part_ctad_tr = nullptr;
@@ -124,12 +127,14 @@ cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s);
 // setup (ends: P x 8 scratch), selection and launch
 constexpr int PART_KMAX = 32;                  // chunks per CTA
 constexpr int PART_CLMAX = 16;                 // CTAs per cluster
-constexpr int PART_CTAD = 5 * 2 * PART_KMAX + 8 * PART_KMAX + 4 * PART_CLMAX;
+constexpr int PART_CTAD = 5 * 2 * PART_KMAX + 12 * PART_KMAX + 4 * PART_CLMAX;
+constexpr int PART_ROWC = 8;                   // doubles per row of the K1P row data
+constexpr int PART_ENDS = 8;                   // doubles per chunk of the K1P end data
 // P = CL * K chunks of L rows (K chunks per CTA)
 bool part_config(int n, int &P, int &L, int &CL, int &K);
 cudaError_t launch_part_setup(int n, int P, int L, int CL, int K, const double *subA, const double *supA,
                               const double *rsA, const double *diagA, double dt, int transpose, double *rowc,
-                              double *ctad, double *ends, int *bad, cudaStream_t s);
+                              double *ctad, double *ends, int *bad, int *noscale, cudaStream_t s);
 bool part_preferred(const Op &op, long B, int m);
 cudaError_t launch_stepper_part(const Op &op, const StepArgs &a, int transpose, cudaStream_t s);
 // scale == 0: out = Omega; else out += scale * (independent N(0,1) field, counter word 3 = ctr3)
