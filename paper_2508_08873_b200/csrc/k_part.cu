@@ -517,17 +517,15 @@ __device__ __forceinline__ void band_backward(const double *__restrict__ F, doub
 // (CTAD_FP/FQ, CTAD_BR/BT), an exact rewriting (R-PART).  One lane per half
 // (HI = 2: the two half-warps) or one lane doing both (HI = 1) performs the
 // same operations in the same order, so the result does not depend on the
-// group size.  Half hf: forward over its rows from zero state, with the partial
-// dot products of rows 0 / 2K-1 of M_C^{-1} (T_C, B_C).
+// group size.  Half hf: forward elimination over its rows from zero state.
 template <int K>
 __device__ __forceinline__ void half_forward(int hf, const double2 *__restrict__ g, const double *__restrict__ F,
-                                             double *__restrict__ z, double &T, double &B, double &y2o,
-                                             double &y1o)
+                                             double *__restrict__ z, double &y2o, double &y1o)
 {
     constexpr int NC = K / 2;                 // chunks per half
     constexpr int BK = (NC < 4) ? NC : 4;     // chunks per block
     const int c0 = hf * NC;
-    double T0 = 0.0, T1 = 0.0, B0 = 0.0, B1 = 0.0, y1 = 0.0, y2 = 0.0;
+    double y1 = 0.0, y2 = 0.0;
 #pragma unroll
     for (int u0 = 0; u0 < NC; u0 += BK) {
         double2 gv[BK];
@@ -544,11 +542,6 @@ __device__ __forceinline__ void half_forward(int hf, const double2 *__restrict__
         double out[2 * BK];
 #pragma unroll
         for (int b = 0; b < BK; ++b) {
-            const int i = 2 * (c0 + u0 + b);
-            T0 = fma(F[CTAD_R0 + i], gv[b].x, T0);
-            T1 = fma(F[CTAD_R0 + i + 1], gv[b].y, T1);
-            B0 = fma(F[CTAD_RM + i], gv[b].x, B0);
-            B1 = fma(F[CTAD_RM + i + 1], gv[b].y, B1);
             const int r = 2 * (u0 + b);       // row within the half
             double y = gv[b].x;
             if (r >= 2) y = fma(-f0[2 * b], y2, y);
@@ -564,8 +557,6 @@ __device__ __forceinline__ void half_forward(int hf, const double2 *__restrict__
 #pragma unroll
         for (int r = 0; r < 2 * BK; ++r) z[(size_t)(2 * (c0 + u0) + r) * 32] = out[r];
     }
-    T = T0 + T1;
-    B = B0 + B1;
     y2o = y2;
     y1o = y1;
 }
@@ -992,16 +983,15 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
                 // split solve: all lanes write the common result slot vl
                 double *zc = zs + (size_t)p * M * 32 + vl;
                 double y2c, y1c;                      // half 0's carried pair
-                double Tx, Bx;                        // (unused: the dots above)
                 if constexpr (HI == 2) {
                     double y2m, y1m;
-                    half_forward<K>(hi, rE, ctad, zc, Tx, Bx, y2m, y1m);
+                    half_forward<K>(hi, rE, ctad, zc, y2m, y1m);
                     y2c = __shfl_xor_sync(0xffffffffu, y2m, 16);
                     y1c = __shfl_xor_sync(0xffffffffu, y1m, 16);
                 } else {
                     double y2x, y1x;
-                    half_forward<K>(0, rE, ctad, zc, Tx, Bx, y2c, y1c);
-                    half_forward<K>(1, rE, ctad, zc, Tx, Bx, y2x, y1x);
+                    half_forward<K>(0, rE, ctad, zc, y2c, y1c);
+                    half_forward<K>(1, rE, ctad, zc, y2x, y1x);
                 }
                 PROBE_T(p3);
                 PROBE_ADD(6, p3 - p2);
