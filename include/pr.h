@@ -139,6 +139,31 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
                                const double *rowsum, const double *colsum, double dt,
                                pr_op *out);
 
+/* Time-dependent 1D pencil: step g = 1..nsteps
+ * (global, g = q*m + j) solves
+ *     (M + dt A(t_g)) u_g = M u_{g-1} + dt l(t_g)
+ * with its own tridiagonal left-hand side L_g = M + dt A(t_g): lsub / ldiag /
+ * lsup are host arrays of nsteps x n (row-major by step; lsub[g*n] and
+ * lsup[g*n + n-1] ignored).  Exp 2's conductivity kappa(x, t) =
+ * 1 + 0.9 sin(7 pi t + 2 pi x) with Neumann boundary rows (eq.
+ * ex2) gives L_g that differ per step, so the interval operators F_q' are not
+ * normal; a non-symmetric A (advection) is allowed too.  lrowsum
+ * (host, nsteps x n, may be NULL): exact row sums of L_g, for the R-ACC pivots
+ * (requires L_g to be an M-matrix).  msub / mdiag / msup (host, length n,
+ * all NULL for M = I): the mass matrix of linear finite elements.
+ * l(t) enters through the PR_AFFINE source (the caller passes the assembled
+ * load vectors as `space`).  The adjoint PR_ADJOINT is the Euclidean
+ * transpose of the product, steps in reverse order:
+ *     F_q'^T = (M^T L_{q,1}^{-T}) ... (M^T L_{q,m}^{-T})      (reading R-ADJ).
+ * Fine propagation over intervals q with (q+1)*m > nsteps fails with EDIM.
+ * All steps are factored once, on the device (k_pencil.cu).  Synchronizing.
+ * Errors: EINVAL (n < 2, nsteps < 1, dt <= 0, NULL step arrays, partial M),
+ * ESINGULAR (zero / non-finite pivot, or non-positive in row-sum form), EOOM,
+ * ECUDA. */
+pr_status pr_op_create_pencil(int n, int nsteps, const double *lsub, const double *ldiag,
+                              const double *lsup, const double *lrowsum, const double *msub,
+                              const double *mdiag, const double *msup, double dt, pr_op *out);
+
 /* 2D operator: 5-point Laplacian on the unit square with homogeneous
  * Dirichlet conditions, n x n interior points, A = T (x) I + I (x) T,
  * T = tridiag(-1, 2, -1)/h^2.  Solved in the sine eigenbasis of T (DESIGN.md

@@ -176,9 +176,92 @@ class DenseOp:
         self.n = self.F.shape[0]
 
 
+# ------------------------------------------------- time-dependent pencils
+class OpPencil:
+    """Time-dependent 1D pencil (Exp 2): step
+    g (global, 1-based) solves (M + dt A(t_g)) u_g = M u_{g-1} + dt l(t_g)
+    with its own tridiagonal L_g = M + dt A(t_g).  L: (sub, diag, sup) arrays
+    of shape (nsteps, n); rowsum: exact row sums of L_g (nsteps, n) or None;
+    M: (sub, diag, sup) of length n, or None for M = I."""
+
+    def __init__(self, L, dt: float, m: int, rowsum=None, M=None):
+        self.L = tuple(np.asarray(a, float) for a in L)
+        self.nsteps, self.n = self.L[1].shape
+        self.dt, self.m = float(dt), int(m)
+        self.rowsum = None if rowsum is None else np.asarray(rowsum, float)
+        self.M = None if M is None else tuple(np.asarray(a, float) for a in M)
+
+
+def _tridiag_apply(T, X, transpose=False):
+    """rows of X times the tridiagonal T = (sub, diag, sup) (or its transpose)."""
+    sub, diag, sup = T
+    Y = X * diag
+    if not transpose:
+        Y[:, 1:] += X[:, :-1] * sub[1:]          # T[i, i-1] x_{i-1}
+        Y[:, :-1] += X[:, 1:] * sup[:-1]         # T[i, i+1] x_{i+1}
+    else:
+        Y[:, 1:] += X[:, :-1] * sup[:-1]         # T^T[i, i-1] = T[i-1, i]
+        Y[:, :-1] += X[:, 1:] * sub[1:]          # T^T[i, i+1] = T[i+1, i]
+    return Y
+
+
+def fine_pencil(op: OpPencil, interval: int, X: np.ndarray, mode: str = "linear", src=None,
+                src_index=None) -> np.ndarray:
+    """F_n (affine), F_n' (linear) or F_n'^T (adjoint, Euclidean transpose of the
+    product: the transposed steps in reverse order, each followed by M^T)."""
+    X = np.array(X, dtype=np.float64, order="C", copy=True)
+    if X.ndim == 1:
+        return fine_pencil(op, interval, X[None, :], mode, src, src_index)[0]
+    nvec = X.shape[0]
+    g0 = (interval - 1) * op.m
+    assert g0 + op.m <= op.nsteps, "interval beyond the operator's steps"
+    if mode == "adjoint":
+        for j in range(op.m, 0, -1):
+            g = g0 + j
+            a, d, c = (arr[g - 1] for arr in op.L)
+            aT = np.zeros_like(a)
+            cT = np.zeros_like(c)
+            aT[1:] = c[:-1]                      # L^T[i, i-1] = L[i-1, i]
+            cT[:-1] = a[1:]                      # L^T[i, i+1] = L[i+1, i]
+            thomas_batch(aT, d, cT, X)
+            if op.M is not None:
+                X = np.ascontiguousarray(_tridiag_apply(op.M, X, transpose=True))
+        return X
+    for j in range(1, op.m + 1):
+        g = g0 + j
+        if op.M is not None:
+            X = np.ascontiguousarray(_tridiag_apply(op.M, X))
+        if mode == "affine" and src is not None:
+            space, time, amp = src
+            idx = np.zeros(nvec, dtype=int) if src_index is None else np.asarray(src_index)
+            coef = amp[idx] * time[:, g - 1][None, :]
+            X += op.dt * (coef @ space)
+        a, d, c = (arr[g - 1] for arr in op.L)
+        thomas_batch(a, d, c, X, rowsum=None if op.rowsum is None else op.rowsum[g - 1])
+    return X
+
+
+def dense_step_product(op: OpPencil, interval: int) -> np.ndarray:
+    """F_n' as the dense product of its steps, (L_g^{-1} M) for g in the interval
+    (brute force for tiny n; a pin for fine_pencil)."""
+    n = op.n
+    F = np.eye(n)
+    Md = np.eye(n) if op.M is None else (np.diag(op.M[1]) + np.diag(op.M[0][1:], -1) + np.diag(op.M[2][:-1], 1))
+    for j in range(1, op.m + 1):
+        g = (interval - 1) * op.m + j
+        a, d, c = (arr[g - 1] for arr in op.L)
+        Lg = np.diag(d) + np.diag(a[1:], -1) + np.diag(c[:-1], 1)
+        F = np.linalg.solve(Lg, Md @ F)
+    return F
+
+
 # ---------------------------------------------------------------- dispatch
 def make_op(cfg):
     from workloads import generators as G
+    if cfg.problem.startswith("exp2"):
+        from workloads import exp2
+        L, rs, M = exp2.step_matrices(cfg.problem, cfg.n, cfg.T, cfg.N * cfg.m)
+        return OpPencil(L, cfg.dt, cfg.m, rowsum=rs, M=M)
     if cfg.dim == 1:
         rs, cs = G.operator_1d_sums(cfg)
         return Op1D(*G.operator_1d(cfg), cfg.dt, cfg.m, rowsum=rs, colsum=cs)
@@ -192,6 +275,8 @@ def fine(op, interval, X, mode="linear", src=None, src_index=None):
         return X @ (op.F if mode == "adjoint" else op.F.T)
     if isinstance(op, Op1D):
         return fine_1d(op, interval, X, mode, src, src_index)
+    if isinstance(op, OpPencil):
+        return fine_pencil(op, interval, X, mode, src, src_index)
     return fine_2d(op, interval, X, mode, src)
 
 

@@ -24,7 +24,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .fine import DenseOp, Op1D, fine
+from .fine import DenseOp, Op1D, OpPencil, fine
 from .linalg import householder_qr, jacobi_svd
 from .rng import gaussian_sketch
 
@@ -44,7 +44,7 @@ class Truncated:
 
 def _as_vectors(op, cols: np.ndarray) -> np.ndarray:
     """(n_dof, l) column block -> fine-solver batch layout."""
-    if isinstance(op, (Op1D, DenseOp)):
+    if isinstance(op, (Op1D, OpPencil, DenseOp)):
         return np.ascontiguousarray(cols.T)
     n = op.n
     return np.ascontiguousarray(cols.T.reshape(-1, n, n))
@@ -67,7 +67,7 @@ def rsvd_interval(op, interval: int, k: int, p: int, seed: int, power_iterations
     sketch equation Psi^T W C = Psi^T F' V = Z^T V (Martinsson & Tropp's
     reconstruction, reading R-IND), and C replaces M of step 5."""
     l = k + p
-    n_dof = op.n if isinstance(op, Op1D) else (op.F.shape[0] if isinstance(op, DenseOp) else op.n * op.n)
+    n_dof = op.n if isinstance(op, (Op1D, OpPencil)) else (op.F.shape[0] if isinstance(op, DenseOp) else op.n * op.n)
     # step 1
     Omega = gaussian_sketch(seed, interval - 1, n_dof, l)
     Y = _as_columns(op, fine(op, interval, _as_vectors(op, Omega), "linear"))
@@ -105,7 +105,7 @@ def exact_truncated(Fdense: np.ndarray, k: int) -> Truncated:
 
 def dense_transfer(op, interval: int = 1, mode: str = "linear") -> np.ndarray:
     """Matrix of F_n' by applying it to every unit vector (tiny grids only)."""
-    n_dof = op.n if isinstance(op, Op1D) else (op.F.shape[0] if isinstance(op, DenseOp) else op.n * op.n)
+    n_dof = op.n if isinstance(op, (Op1D, OpPencil)) else (op.F.shape[0] if isinstance(op, DenseOp) else op.n * op.n)
     E = np.eye(n_dof)
     return _as_columns(op, fine(op, interval, _as_vectors(op, E), mode))
 

@@ -19,7 +19,7 @@ PR_LINEAR, PR_ADJOINT, PR_AFFINE = 0, 1, 2
 PR_SRC_NONE, PR_SRC_SEP1D, PR_SRC_BUMP2D = 0, 1, 2
 
 # every symbol include/pr.h declares
-EXPORTS = ["pr_last_error", "pr_version", "pr_reload_env", "pr_profile", "pr_counters", "pr_phase_counters", "pr_op_create_tridiag", "pr_op_create_sep2d",
+EXPORTS = ["pr_last_error", "pr_version", "pr_reload_env", "pr_profile", "pr_counters", "pr_phase_counters", "pr_op_create_tridiag", "pr_op_create_pencil", "pr_op_create_sep2d",
            "pr_op_destroy", "pr_op_info", "pr_fine_propagate", "pr_gaussian_sketch",
            "pr_build_coarse", "pr_coarse_info", "pr_coarse_factors", "pr_coarse_apply",
            "pr_coarse_destroy", "pr_parareal", "pr_bounds", "pr_coarse_sweep_matrices",
@@ -67,6 +67,7 @@ def lib():
             "pr_counters": ([I, ctypes.POINTER(lg), ctypes.POINTER(lg), dp, dp, dp], I),
             "pr_phase_counters": ([I, ctypes.POINTER(lg), dp, dp], I),
             "pr_op_create_tridiag": ([I, dp, dp, dp, dp, dp, D, ctypes.POINTER(vp)], I),
+            "pr_op_create_pencil": ([I, I, dp, dp, dp, dp, dp, dp, dp, D, ctypes.POINTER(vp)], I),
             "pr_op_create_sep2d": ([I, D, ctypes.POINTER(vp)], I),
             "pr_op_destroy": ([vp], I),
             "pr_op_info": ([vp, ctypes.POINTER(lg), ip, ip], I),

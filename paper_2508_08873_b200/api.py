@@ -65,6 +65,21 @@ class Operator:
         return cls(h)
 
     @classmethod
+    def pencil(cls, lsub, ldiag, lsup, dt: float, lrowsum=None, mass=None) -> "Operator":
+        """Time-dependent pencil: (nsteps, n) arrays of the step matrices
+        M + dt A(t_g); mass = (msub, mdiag, msup) or None (M = I)."""
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (lsub, ldiag, lsup)]
+        nsteps, n = arrs[1].shape
+        rs = None if lrowsum is None else np.ascontiguousarray(lrowsum, dtype=np.float64)
+        ms = [None] * 3 if mass is None else [np.ascontiguousarray(a, dtype=np.float64) for a in mass]
+        h = ctypes.c_void_p()
+        check(L.lib().pr_op_create_pencil(int(n), int(nsteps), *[_hptr(a) for a in arrs],
+                                          _hptr(rs) if rs is not None else None,
+                                          *[_hptr(a) if a is not None else None for a in ms],
+                                          float(dt), ctypes.byref(h)), "pr_op_create_pencil")
+        return cls(h)
+
+    @classmethod
     def sep2d(cls, n: int, dt: float) -> "Operator":
         h = ctypes.c_void_p()
         check(L.lib().pr_op_create_sep2d(int(n), float(dt), ctypes.byref(h)), "pr_op_create_sep2d")

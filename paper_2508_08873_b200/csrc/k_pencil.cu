@@ -1,0 +1,197 @@
+// k_pencil.cu -- K1T: batched 1D backward-Euler stepper for TIME-DEPENDENT
+// pencils (eq. ex2), with an optional
+// mass matrix (row 2; linear finite elements):
+//
+//     (M + dt A(t_g)) u_g = M u_{g-1} + dt l(t_g),      g = q*m + j,
+//
+// every step with its own tridiagonal left-hand side L_g = M + dt A(t_g)
+// (Exp 2: kappa(x, t) = 1 + 0.9 sin(7 pi t + 2 pi x), Neumann rows), so the
+// interval operators F_q' differ and are not normal.  The adjoint
+// is the true transpose of the product, steps in REVERSE order (R-ADJ):
+//     F_q'^T = (M^T L_{q,1}^{-T}) ... (M^T L_{q,m}^{-T}).
+//
+// Factorisation (k_pencil_factor, once per operator, one thread per step):
+// L_g = L' U' with L' lower bidiagonal {sub a_i, diag p_i}, U' unit upper
+// {super c'_i = c_i / p_i}; pivots from the exact row sums when given (reading
+// R-ACC), else p_i = b_i - a_i c_{i-1} / p_{i-1}.  Per row and step:
+//     {w_i = 1/p_i, ga_i = w_i a_i, cp_i = w_i c_i, gt_i = w_i a_{i+1}}
+//   forward  L_g x = r:   y_i = w_i r_i - ga_i y_{i-1};  x_i = y_i - cp_i x_{i+1}
+//   adjoint  L_g^T z = r: v_i = r_i - cp_{i-1} v_{i-1};  z_i = w_i v_i - gt_i z_{i+1}
+//
+// Stepper (k_pencil_step): one thread per vector of the interleaved (n x ld)
+// batch (a warp's 32 vectors of one row are one 256-byte segment), two
+// streaming passes per step over the state in the output buffer; the mass
+// matrix product M x (or M^T z) is formed on the fly in the down pass from a
+// three-row register window; the per-row factors of a step are warp-uniform
+// loads (L1 broadcast).  HBM-bound: 32 B per DOF-step (+ 0 for M, formed from
+// the window) -- no pass fusion here because consecutive steps have different
+// factors (the time-independent K1/K1P paths fuse).
+#include "pr_internal.cuh"
+
+namespace pr {
+
+__global__ void k_pencil_factor(int n, int nsteps, const double *__restrict__ lsub,
+                                const double *__restrict__ ldiag, const double *__restrict__ lsup,
+                                const double *__restrict__ lrs, Coef *fac, int *bad)
+{
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= nsteps) return;
+    const double *a = lsub + (size_t)g * n, *b = ldiag + (size_t)g * n, *c = lsup + (size_t)g * n;
+    const double *s = lrs ? lrs + (size_t)g * n : nullptr;
+    Coef *F = fac + (size_t)g * n;
+    double p = 1.0, r = 0.0;
+    bool ok = true;
+    for (int i = 0; i < n; ++i) {
+        const double ai = (i > 0) ? a[i] : 0.0;
+        const double ci = (i < n - 1) ? c[i] : 0.0;
+        double piv;
+        if (s) {
+            r = (i == 0) ? s[0] : s[i] - ai * (r / p);
+            piv = r - ci;
+            if (!(piv > 0.0)) ok = false;
+        } else {
+            piv = (i == 0) ? b[0] : b[i] - ai * (c[i - 1] / p);
+        }
+        if (!(piv != 0.0) || !isfinite(piv)) ok = false;
+        p = piv;
+        const double w = 1.0 / piv;
+        const double an = (i + 1 < n) ? a[i + 1] : 0.0;
+        F[i] = Coef{w, w * ai, w * ci, w * an};
+    }
+    if (!ok) atomicExch(bad, 1);
+}
+
+struct PencilArgs {
+    int n, m;
+    long B;
+    const Coef *fac;                   // nsteps x n
+    const double *msub, *mdiag, *msup; // null: M = I
+    const double *in; long ld_in;      // null -> zero input
+    double *out; long ld_out;
+    const double *off; long ld_off;
+    int q0, vpi;
+    int R;                             // source terms (0: none)
+    const double *spaceT; int rs;      // n x rs
+    const double *time;                // R x nsteps
+    const double *amp;                 // nsrc x R
+    int nsteps, nsrc;
+    double dt;
+};
+
+template <int MODE>                    // 0 linear, 1 affine, 2 adjoint
+__global__ void __launch_bounds__(128) k_pencil_step(PencilArgs a)
+{
+    const long v = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= a.B) return;
+    const int n = a.n;
+    const int q = a.q0 + (int)(v / a.vpi);
+    double *X = a.out + v;
+    const long ldx = a.ld_out;
+    const bool hasM = a.mdiag != nullptr;
+    double al[8];
+    for (int s = 0; s < a.m; ++s) {
+        const int j = (MODE == 2) ? a.m - s : s + 1;       // 1-based step within the interval
+        const long g = (long)q * a.m + j;                   // 1-based global step
+        const Coef *F = a.fac + (g - 1) * n;
+        // input of this step's down pass: the previous state (or U_in)
+        const double *Src = (s == 0) ? (a.in ? a.in + v : nullptr) : X;
+        const long lds = (s == 0) ? a.ld_in : ldx;
+        if (MODE == 1) {
+            for (int r = 0; r < 8; ++r) al[r] = 0.0;
+            const int src = (int)(v % a.nsrc);
+            for (int r = 0; r < a.R && r < 8; ++r)
+                al[r] = a.dt * a.amp[(long)src * a.R + r] * a.time[(long)r * a.nsteps + g - 1];
+        }
+        auto ld_src = [&](int i) -> double { return Src ? Src[(long)i * lds] : 0.0; };
+        // down pass (rows ascending); window xm / x0 / xp of the input
+        double xm = 0.0, x0 = ld_src(0), y = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double xp = (i + 1 < n) ? ld_src(i + 1) : 0.0;
+            double r;
+            if (MODE == 2) {
+                // r = M^T z_prev after the first adjoint step, the input before it
+                if (hasM && s > 0)
+                    r = fma(a.mdiag[i], x0, (i > 0 ? a.msup[i - 1] * xm : 0.0) + (i + 1 < n ? a.msub[i + 1] * xp : 0.0));
+                else
+                    r = x0;
+                const double cpm = (i > 0) ? F[i - 1].c : 0.0;
+                y = fma(-cpm, y, r);                              // v_i = r_i - cp_{i-1} v_{i-1}
+            } else {
+                r = hasM ? fma(a.mdiag[i], x0, (i > 0 ? a.msub[i] * xm : 0.0) + (i + 1 < n ? a.msup[i] * xp : 0.0))
+                         : x0;
+                if (MODE == 1) {
+                    double f = 0.0;
+                    for (int k = 0; k < a.R && k < 8; ++k) f = fma(al[k], a.spaceT[(long)i * a.rs + k], f);
+                    r += f;
+                }
+                const Coef c = F[i];
+                y = fma(-c.b, y, c.a * r);                        // y_i = w_i r_i - ga_i y_{i-1}
+            }
+            X[(long)i * ldx] = y;
+            xm = x0;
+            x0 = xp;
+        }
+        // up pass (rows descending)
+        double xn = 0.0;
+        for (int i = n - 1; i >= 0; --i) {
+            const Coef c = F[i];
+            const double yi = X[(long)i * ldx];
+            xn = (MODE == 2) ? fma(-c.d, xn, c.a * yi)             // z_i = w_i v_i - gt_i z_{i+1}
+                             : fma(-c.c, xn, yi);                 // x_i = y_i - cp_i x_{i+1}
+            X[(long)i * ldx] = xn;
+        }
+    }
+    if (a.m == 0) {                    // F' = identity
+        for (int i = 0; i < n; ++i) X[(long)i * ldx] = a.in ? a.in[v + (long)i * a.ld_in] : 0.0;
+    }
+    if (MODE == 2 && hasM && a.m > 0) {   // the last factor M^T of the adjoint
+        double zm = 0.0, z0 = X[0];
+        for (int i = 0; i < n; ++i) {
+            const double zp = (i + 1 < n) ? X[(long)(i + 1) * ldx] : 0.0;
+            X[(long)i * ldx] = fma(a.mdiag[i], z0, (i > 0 ? a.msup[i - 1] * zm : 0.0) + (i + 1 < n ? a.msub[i + 1] * zp : 0.0));
+            zm = z0;
+            z0 = zp;
+        }
+    }
+    if (a.off)
+        for (int i = 0; i < n; ++i) X[(long)i * ldx] += a.off[v + (long)i * a.ld_off];
+}
+
+cudaError_t launch_pencil_factor(int n, int nsteps, const double *lsub, const double *ldiag,
+                                 const double *lsup, const double *lrs, Coef *fac, int *bad,
+                                 cudaStream_t s)
+{
+    note_launch();
+    k_pencil_factor<<<(nsteps + 63) / 64, 64, 0, s>>>(n, nsteps, lsub, ldiag, lsup, lrs, fac, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stepper_pencil(const Op &op, int mode, const StepArgs &sa, cudaStream_t s)
+{
+    if (sa.B == 0) return cudaSuccess;
+    PencilArgs a{};
+    a.n = sa.n; a.m = sa.m; a.B = sa.B;
+    a.fac = op.pen_fac;
+    a.msub = op.pen_m; a.mdiag = op.pen_m ? op.pen_m + op.n : nullptr; a.msup = op.pen_m ? op.pen_m + 2 * op.n : nullptr;
+    a.in = sa.in; a.ld_in = sa.ld_in; a.out = sa.out; a.ld_out = sa.ld_out;
+    a.off = sa.off; a.ld_off = sa.ld_off;
+    a.q0 = sa.q0; a.vpi = sa.vpi;
+    a.R = sa.R; a.spaceT = sa.spaceT; a.rs = sa.R > 0 ? stepper_rs(sa.R) : 0;
+    a.time = sa.time; a.amp = sa.amp; a.nsteps = sa.nsteps; a.nsrc = sa.nsrc > 0 ? sa.nsrc : 1;
+    a.dt = sa.dt;
+    const int threads = 128;
+    const unsigned blocks = (unsigned)((sa.B + threads - 1) / threads);
+    const bool prof = profiling();
+    if (prof) stepper_timed_begin(s);
+    note_launch();
+    if (mode == PR_ADJOINT) k_pencil_step<2><<<blocks, threads, 0, s>>>(a);
+    else if (sa.R > 0) k_pencil_step<1><<<blocks, threads, 0, s>>>(a);
+    else k_pencil_step<0><<<blocks, threads, 0, s>>>(a);
+    if (prof) {
+        const double dof = (double)sa.n * (double)sa.B * (double)sa.m;
+        stepper_timed_end(s, dof, (5.0 + (op.pen_m ? 5.0 : 0.0) + 2.0 * sa.R) * dof);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace pr

@@ -356,8 +356,15 @@ static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi
         a.nsteps = f->nsteps;
         a.nsrc = f->nsrc;
     }
-    if (part_preferred(op, B, m)) PR_CUDA(launch_stepper_part(op, a, mode == PR_ADJOINT, s));
-    else PR_CUDA(launch_stepper_1d(a, s));
+    if (op.pencil) {
+        PR_REQUIRE((long)(q0 + (B + vpi - 1) / vpi) * m <= op.pen_nsteps, PR_EDIM,
+                   "intervals beyond the time-dependent operator's step count");
+        PR_CUDA(launch_stepper_pencil(op, mode, a, s));
+    } else if (part_preferred(op, B, m)) {
+        PR_CUDA(launch_stepper_part(op, a, mode == PR_ADJOINT, s));
+    } else {
+        PR_CUDA(launch_stepper_1d(a, s));
+    }
     return PR_OK;
 }
 
@@ -520,6 +527,66 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
     return PR_OK;
 }
 
+pr_status pr_op_create_pencil(int n, int nsteps, const double *lsub, const double *ldiag,
+                              const double *lsup, const double *lrowsum, const double *msub,
+                              const double *mdiag, const double *msup, double dt, pr_op *out)
+{
+    PR_REQUIRE(out, PR_EINVAL, "out is NULL");
+    PR_REQUIRE(n >= 2 && nsteps >= 1 && lsub && ldiag && lsup, PR_EINVAL,
+               "n < 2, nsteps < 1 or NULL step matrices");
+    PR_REQUIRE(dt > 0.0 && isfinite(dt), PR_EINVAL, "dt must be positive");
+    PR_REQUIRE((msub == nullptr) == (mdiag == nullptr) && (mdiag == nullptr) == (msup == nullptr),
+               PR_EINVAL, "give all three mass-matrix arrays or none");
+    *out = nullptr;
+    pr_op h = new pr_op_s();
+    Op &op = h->op;
+    op.dim = 1;
+    op.n = n;
+    op.rows = n;
+    op.dt = dt;
+    op.pencil = 1;
+    op.pen_nsteps = nsteps;
+    const size_t sn = (size_t)nsteps * n;
+    double *d_in = nullptr;
+    int *d_bad = nullptr;
+    auto fail = [&](pr_status st) {
+        cudaFree(d_in);
+        cudaFree(d_bad);
+        cudaFree(op.pen_fac);
+        cudaFree(op.pen_m);
+        delete h;
+        return st;
+    };
+    cudaError_t e = cudaMalloc(&d_in, (lrowsum ? 4 : 3) * sn * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&d_bad, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&op.pen_fac, sn * sizeof(Coef));
+    if (e == cudaSuccess && mdiag) e = cudaMalloc(&op.pen_m, 3 * (size_t)n * sizeof(double));
+    if (e != cudaSuccess) return fail(cuda_fail(e, "pr_op_create_pencil alloc"));
+    double *da = d_in, *db = d_in + sn, *dc = d_in + 2 * sn, *drs = lrowsum ? d_in + 3 * sn : nullptr;
+    e = cudaMemcpy(da, lsub, sn * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(db, ldiag, sn * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dc, lsup, sn * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && drs) e = cudaMemcpy(drs, lrowsum, sn * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && mdiag) {
+        e = cudaMemcpy(op.pen_m, msub, n * sizeof(double), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(op.pen_m + n, mdiag, n * sizeof(double), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(op.pen_m + 2 * n, msup, n * sizeof(double), cudaMemcpyHostToDevice);
+    }
+    if (e == cudaSuccess) e = cudaMemset(d_bad, 0, sizeof(int));
+    if (e == cudaSuccess) e = launch_pencil_factor(n, nsteps, da, db, dc, drs, op.pen_fac, d_bad, 0);
+    int bad = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return fail(cuda_fail(e, "pr_op_create_pencil factor"));
+    if (bad) {
+        set_error("zero, negative (row-sum form) or non-finite pivot in a step matrix M + dt A(t_g)");
+        return fail(PR_ESINGULAR);
+    }
+    cudaFree(d_in);
+    cudaFree(d_bad);
+    *out = h;
+    return PR_OK;
+}
+
 pr_status pr_op_destroy(pr_op h)
 {
     if (!h) return PR_OK;
@@ -527,6 +594,7 @@ pr_status pr_op_destroy(pr_op h)
     cudaFree(op.dn_fw); cudaFree(op.up_fw); cudaFree(op.dn_tr); cudaFree(op.up_tr);
     cudaFree(op.part_rowc_fw); cudaFree(op.part_ctad_fw); cudaFree(op.part_rowc_tr); cudaFree(op.part_ctad_tr);
     cudaFree(op.S); cudaFree(op.lam);
+    cudaFree(op.pen_fac); cudaFree(op.pen_m);
     delete h;
     return PR_OK;
 }

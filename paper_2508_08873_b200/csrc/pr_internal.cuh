@@ -88,6 +88,12 @@ struct Op {
     int part_P = 0, part_L = 0, part_CL = 0, part_K = 0;
     double *part_rowc_fw = nullptr, *part_ctad_fw = nullptr;
     double *part_rowc_tr = nullptr, *part_ctad_tr = nullptr;
+    // time-dependent pencil (k_pencil.cu, pr_op_create_pencil): per-step factors
+    // of L_g = M + dt A(t_g) (pen_nsteps x n Coef {w, ga, cp, gt}) and the mass
+    // matrix M (3n: sub | diag | sup) or null (M = I)
+    int pencil = 0, pen_nsteps = 0;
+    Coef *pen_fac = nullptr;
+    double *pen_m = nullptr;
     // 2D: P = n+1; S (P x P) sine matrix with zero row/col 0; lam[P] eigenvalues of T.
     int P = 0;
     double *S = nullptr;
@@ -122,6 +128,11 @@ cudaError_t launch_factor_1d(int n, const double *subA, const double *supA, cons
                              const double *diagA, double dt, int transpose, Coef *DN, Coef *UP,
                              int *bad, cudaStream_t s);
 cudaError_t launch_stepper_1d(const StepArgs &a, cudaStream_t s);
+// time-dependent pencil stepper (k_pencil.cu)
+cudaError_t launch_pencil_factor(int n, int nsteps, const double *lsub, const double *ldiag,
+                                 const double *lsup, const double *lrs, Coef *fac, int *bad,
+                                 cudaStream_t s);
+cudaError_t launch_stepper_pencil(const Op &op, int mode, const StepArgs &sa, cudaStream_t s);
 
 // partitioned stepper (k_part.cu): configuration for n (false: not supported),
 // setup (ends: P x 8 scratch), selection and launch

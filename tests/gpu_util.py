@@ -21,6 +21,10 @@ def cuda_available() -> bool:
 
 def gpu_op(cfg):
     from paper_2508_08873_b200 import Operator
+    if cfg.problem.startswith("exp2"):             # time-dependent pencil (workloads/exp2.py)
+        from workloads import exp2
+        L, rs, M = exp2.step_matrices(cfg.problem, cfg.n, cfg.T, cfg.N * cfg.m)
+        return Operator.pencil(*L, cfg.dt, lrowsum=rs, mass=M)
     if cfg.dim == 1:
         rs, cs = G.operator_1d_sums(cfg)
         return Operator.tridiag(*G.operator_1d(cfg), cfg.dt, rowsum=rs, colsum=cs)

@@ -107,3 +107,15 @@ def get(name: str) -> Config:
 # dt = 1/(512*64)): the full-size 2D Parareal the oracle can follow on one GPU
 C5G = replace(C5, name="C5G", N=16, T=C5.T * 16 / 512)
 VARIANTS[C5G.name] = C5G
+
+# the paper's Experiment 2 (eq. ex2):
+# time-dependent conductivity, Neumann conditions, linear finite elements with
+# 100 elements (n = 101 nodes), 100 time steps on [0, 1] in N = 10 intervals,
+# rank R = 5 with p = 1 oversampling vector; problem data in
+# workloads/exp2.py.  E2FD: the finite-difference (M = I, non-symmetric A)
+# version; E2L: the same problem at GPU scale (4096 nodes, 64 x 64 steps).
+E2 = Config("E2", 1, 101, 1.0, 10, 10, 5, 1, 8, "exp2_fem", "exp2", "exp2", seed=BASE_SEED + 5)
+E2FD = replace(E2, name="E2FD", problem="exp2_fd")
+E2L = replace(E2, name="E2L", n=4096, N=64, m=64, k=16, p=4)
+for _c in (E2, E2FD, E2L):
+    VARIANTS[_c.name] = _c

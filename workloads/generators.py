@@ -134,6 +134,9 @@ def laplacian_1d_for_2d_sums(cfg: Config):
 # ------------------------------------------------------------------------ u0
 def initial_value(cfg: Config) -> np.ndarray:
     """u0 on the interior grid: shape (n,) in 1D, (n, n) [x-index, y-index] in 2D."""
+    if cfg.u0 == "exp2":                           # 10 chi_[0.6, 0.8] (workloads/exp2.py)
+        from . import exp2
+        return exp2.initial_value(cfg.n)
     rng = np.random.default_rng(cfg.seed_u0)
     if cfg.dim == 1:
         x = grid_1d(cfg.n)
@@ -161,6 +164,9 @@ def initial_value(cfg: Config) -> np.ndarray:
 # ---------------------------------------------------------------------- source
 def source_1d(cfg: Config):
     """Separable sampled source: (space[R, n], time[R, N*m], amp[nsrc, R])."""
+    if cfg.source == "exp2":                       # Exp 2 (workloads/exp2.py)
+        from . import exp2
+        return exp2.source(cfg.problem, cfg.n, cfg.T, cfg.N * cfg.m, cfg.nsrc)
     x = grid_1d(cfg.n)
     t = step_times(cfg)
     if cfg.source == "c1":                         # f = sin(pi x) cos(2 pi t)
