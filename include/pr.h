@@ -330,6 +330,60 @@ pr_status pr_parareal(pr_coarse G, pr_op op, int nsrc, const double *u0, long ld
                       double *upd_host, double *bnorm_host, double *hist, long hist_stride,
                       void *stream);
 
+/* pr_parareal with the a posteriori stopping rule: iterate until the bound of
+ * eq. apost_bound,
+ *     max_{n, s} eps * sum_{m=1}^{n-1} delta^{n-m-1} ||u^k_m - u^{k-1}_m||,
+ * with delta, eps of the coarse handle (eq. bounds_delta_eps, eps from the
+ * computed sigma_{k+1}), is <= tol, or K_max iterations; *k_done
+ * receives the number of iterations run (the arrays are filled for those).
+ * One device-to-host read of the update norms per iteration.  Errors: as
+ * pr_parareal, plus EINVAL (tol <= 0, k_done NULL) and EUNAVAIL (p == 0). */
+pr_status pr_parareal_tol(pr_coarse G, pr_op op, int nsrc, const double *u0, long ld_u0,
+                          const pr_source *f, int K_max, double tol, double *U_out, long ld_out,
+                          double *upd_host, double *bnorm_host, double *hist, long hist_stride,
+                          int *k_done, void *stream);
+
+/* --------------------------------------------------------------- reporting
+ * (SURVEY 8(f) row 3.)  Arrays of boundary blocks as in pr_parareal: block j
+ * (nsrc vectors, op layout) belongs to t_j, j = 0..N. */
+
+/* The sequential fine solution u_0 = u0, u_{q+1} = F_{q+1} u_q, q < N
+ * (P:136-139): N dependent batched launches.  U_out: (N+1)*nsrc vectors. */
+pr_status pr_sequential(pr_op op, int nsrc, const double *u0, long ld_u0, const pr_source *f, int N,
+                        int m, double *U_out, long ld_out, void *stream);
+
+/* The l2-in-space, max-in-time error of a Parareal iterate (the
+ * numerator of eq. def_efficiency): u^k(t) on [t_{q-1}, t_q) is the fine
+ * trajectory F_q started from u^k_{q-1} (and t = T the end of interval N's;
+ * reading R-TRAJ), compared with the fine trajectory from u_{q-1}.  Evaluated
+ * exactly as the LINEAR propagation of e_{q-1} = u^k_{q-1} - u_{q-1} (the
+ * source cancels, eq. F_n_affine), m one-step launches with a norm after each.
+ * U, Uref: (N+1)*nsrc vectors (same ld).  err_host (nsrc): max over t;
+ * ivl_host (nullable, N*nsrc): the max over interval q+1 at [q*nsrc + s].
+ * Synchronizing.  Errors: EINVAL, EDIM. */
+pr_status pr_trajectory_error(pr_op op, int nsrc, int N, int m, const double *U, long ldU,
+                              const double *Uref, long ldR, double *err_host, double *ivl_host,
+                              void *stream);
+
+/* Efficiency of the a posteriori estimator, eq. def_efficiency:
+ *   eta^k = traj_err[k] / max_{1 <= n < N} eps sum_{m=1}^{n-1} delta^{n-m-1} upd_k[m]
+ * for k = 1..K (host arrays, one source: upd as pr_parareal's K x (N+1),
+ * traj_err K+1 values for k = 0..K, eta K values).  Host only. */
+pr_status pr_efficiency(double delta, double eps, int N, int K, const double *upd,
+                        const double *traj_err, double *eta);
+
+/* Classical Parareal (eq. def_Parareal) with a coarse PROPAGATOR instead of
+ * the spectral G (the baselines of P:157-158 and P:209-215, the dashed lines
+ * of the paper's figures): G_{q+1} v = one backward-Euler step of `coarse`
+ * (time step Delta T: its step q+1, source fc sampled at t_{q+1}), or G = 0
+ * when coarse == NULL (u^0_q = 0 for q >= 1).  F_{q+1} = m steps of
+ * op with source f.  The coarse sweep is sequential (N launches per
+ * iteration).  upd_host (nullable, host, K x (N+1) x nsrc); hist as
+ * pr_parareal.  Synchronizing.  Errors: EINVAL, EDIM. */
+pr_status pr_parareal_classical(pr_op coarse, const pr_source *fc, pr_op op, int nsrc, const double *u0,
+                                long ld_u0, const pr_source *f, int N, int m, int K_iter, double *U_out,
+                                long ld_out, double *upd_host, double *hist, long hist_stride, void *stream);
+
 /* ------------------------------------------------- distributed building blocks
  * Stages of pr_parareal on the intervals a handle owns (first .. first+n_local-1),
  * for an interval-sharded Parareal over several GPUs.  Arrays

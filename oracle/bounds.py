@@ -63,3 +63,11 @@ def a_priori_eps_inf_time(delta, eps, N, k, e0):
     if N - k < 1:
         return 0.0
     return (eps / (1.0 - delta)) ** k * max(e0[n] for n in range(1, N - k + 1))
+
+
+def efficiency(delta, eps, upd_k, traj_err_k, N):
+    """eq. def_efficiency, as printed (the max over 1 <= n < N,
+    reading Z21):
+        eta^k = max_t ||u^k(t) - u(t)|| / max_{1<=n<N} eps sum_{m=1}^{n-1} delta^{n-m-1} ||u^k_m - u^{k-1}_m||."""
+    den = max(a_posteriori(delta, eps, upd_k, n) for n in range(1, N))
+    return traj_err_k / den

@@ -280,6 +280,32 @@ def fine(op, interval, X, mode="linear", src=None, src_index=None):
     return fine_2d(op, interval, X, mode, src)
 
 
+def fine_trajectory(op, interval, X, src=None, src_index=None):
+    """[x_0, x_1, ..., x_m]: the affine fine trajectory of interval `interval`
+    from X, one step at a time (Op1D / OpPencil)."""
+    X = np.array(X, dtype=np.float64)
+    out = [X.copy()]
+    if isinstance(op, Op1D):
+        one = Op1D.__new__(Op1D)
+        one.__dict__.update(op.__dict__)
+        one.m = 1
+        for j in range(1, op.m + 1):
+            g = (interval - 1) * op.m + j        # global step of step j
+            X = fine_1d(one, g, X, "affine", src, src_index) if src is not None else fine_1d(one, g, X, "linear")
+            out.append(X.copy())
+        return out
+    if isinstance(op, OpPencil):
+        one = OpPencil.__new__(OpPencil)
+        one.__dict__.update(op.__dict__)
+        one.m = 1
+        for j in range(1, op.m + 1):
+            g = (interval - 1) * op.m + j
+            X = fine_pencil(one, g, X, "affine" if src is not None else "linear", src, src_index)
+            out.append(X.copy())
+        return out
+    raise TypeError("fine_trajectory: 1D operators only")
+
+
 def sequential_reference(op, u0, N: int, src=None, src_index=None):
     """u_{n+1} = F_{n+1} u_n, 0 <= n < N (P:136-139).  u0: (nvec, ...) batch."""
     out = [np.array(u0, dtype=np.float64)]

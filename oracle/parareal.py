@@ -55,3 +55,40 @@ def parareal(op, truncs, u0: np.ndarray, N: int, K: int, src, src_index=None) ->
         d = (U[k + 1] - U[k]).reshape((N + 1) * shp[0], -1)
         upd[k + 1] = np.linalg.norm(d, axis=1).reshape(N + 1, shp[0])
     return PararealResult(U=U, b=b, upd=upd)
+
+
+def parareal_classical(op, Gfun, u0: np.ndarray, N: int, K: int, src, src_index=None) -> PararealResult:
+    """eq. def_Parareal with an arbitrary coarse solver Gfun(n, x) = G_n x
+    (affine; e.g. one coarse backward-Euler step, or 0)."""
+    u0 = np.asarray(u0, dtype=np.float64)
+    shp = u0.shape
+    U = np.zeros((K + 1, N + 1) + shp)
+    upd = np.zeros((K + 1, N + 1, shp[0]))
+    U[0, 0] = u0
+    for n in range(N):
+        U[0, n + 1] = Gfun(n + 1, U[0, n])
+    for k in range(K):
+        Fu = [fine(op, n + 1, U[k, n], "affine", src, src_index) for n in range(N)]
+        Gold = [Gfun(n + 1, U[k, n]) for n in range(N)]
+        U[k + 1, 0] = u0
+        for n in range(N):
+            U[k + 1, n + 1] = Gfun(n + 1, U[k + 1, n]) + Fu[n] - Gold[n]
+        d = (U[k + 1] - U[k]).reshape((N + 1) * shp[0], -1)
+        upd[k + 1] = np.linalg.norm(d, axis=1).reshape(N + 1, shp[0])
+    return PararealResult(U=U, b=np.zeros((N + 1,) + shp), upd=upd)
+
+
+def trajectory_error(op, Uk: np.ndarray, Uref: np.ndarray, N: int, src, src_index=None):
+    """max over t in [0, T] of ||u^k(t) - u(t)||: inside
+    [t_{n-1}, t_n) both are the fine trajectories (one step at a time, with the
+    source) started from u^k_{n-1} and u_{n-1}; t = T is the end of interval
+    N's (reading R-TRAJ).  Uk, Uref: (N+1, nvec, n).  Returns (nvec,)."""
+    from .fine import fine_trajectory
+    best = np.zeros(Uk.shape[1])
+    for n in range(1, N + 1):
+        a = fine_trajectory(op, n, Uk[n - 1], src, src_index)
+        b = fine_trajectory(op, n, Uref[n - 1], src, src_index)
+        last = len(a) if n == N else len(a) - 1
+        for j in range(last):
+            best = np.maximum(best, np.linalg.norm((a[j] - b[j]).reshape(a[j].shape[0], -1), axis=1))
+    return best

@@ -5,7 +5,8 @@ include/pr.h); this package is its ctypes binding.  There is no CPU
 fallback: the first call raises OSError if libpr.so has not been built
 (`python -c "import __graft_entry__ as g; g.build()"`).
 """
-from .api import Coarse, Comm, Operator, SourceTerm, bounds, counters, parareal, profile  # noqa: F401
+from .api import (Coarse, Comm, Operator, SourceTerm, bounds, counters, efficiency, parareal,  # noqa: F401
+                  parareal_classical, parareal_tol, profile, sequential, trajectory_error)
 from ._lib import PR_ADJOINT, PR_AFFINE, PR_LINEAR, PrError, lib  # noqa: F401
 
 

@@ -22,7 +22,8 @@ PR_SRC_NONE, PR_SRC_SEP1D, PR_SRC_BUMP2D = 0, 1, 2
 EXPORTS = ["pr_last_error", "pr_version", "pr_reload_env", "pr_profile", "pr_counters", "pr_phase_counters", "pr_op_create_tridiag", "pr_op_create_pencil", "pr_op_create_sep2d",
            "pr_op_destroy", "pr_op_info", "pr_fine_propagate", "pr_gaussian_sketch",
            "pr_build_coarse", "pr_coarse_info", "pr_coarse_factors", "pr_coarse_apply",
-           "pr_coarse_destroy", "pr_parareal", "pr_bounds", "pr_coarse_sweep_matrices",
+           "pr_coarse_destroy", "pr_parareal", "pr_parareal_tol", "pr_bounds", "pr_sequential",
+           "pr_trajectory_error", "pr_efficiency", "pr_parareal_classical", "pr_coarse_sweep_matrices",
            "pr_coarse_export", "pr_coarse_export_interval", "pr_coarse_project", "pr_reduced_sweep", "pr_coarse_expand",
            "pr_comm_nccl_unique_id", "pr_comm_create_nccl", "pr_comm_create_local", "pr_comm_info",
            "pr_comm_destroy"]
@@ -79,7 +80,13 @@ def lib():
             "pr_coarse_apply": ([vp, I, I, vp, lg, vp, lg, vp], I),
             "pr_coarse_destroy": ([vp], I),
             "pr_parareal": ([vp, vp, I, vp, lg, ctypes.POINTER(Source), I, vp, lg, dp, dp, vp, lg, vp], I),
+            "pr_parareal_tol": ([vp, vp, I, vp, lg, ctypes.POINTER(Source), I, D, vp, lg, dp, dp, vp, lg, ip, vp], I),
             "pr_bounds": ([D, D, I, I, dp, dp, dp, dp, dp], I),
+            "pr_sequential": ([vp, I, vp, lg, ctypes.POINTER(Source), I, I, vp, lg, vp], I),
+            "pr_trajectory_error": ([vp, I, I, I, vp, lg, vp, lg, dp, dp, vp], I),
+            "pr_efficiency": ([D, D, I, I, dp, dp, dp], I),
+            "pr_parareal_classical": ([vp, ctypes.POINTER(Source), vp, I, vp, lg, ctypes.POINTER(Source), I, I, I,
+                                       vp, lg, dp, vp, lg, vp], I),
             "pr_coarse_sweep_matrices": ([vp, vp, vp], I),
             "pr_coarse_export": ([vp, vp, vp, vp, vp, vp], I),
             "pr_coarse_export_interval": ([vp, I, vp, vp, vp], I),

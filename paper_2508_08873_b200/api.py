@@ -291,6 +291,67 @@ def parareal(G: Coarse, op: Operator, u0, source: SourceTerm, K: int, U_out, nsr
     return upd, bn
 
 
+def parareal_tol(G: Coarse, op: Operator, u0, source: SourceTerm, K_max: int, tol: float, U_out,
+                 nsrc: int = 1, hist=None, stream=None):
+    """pr_parareal_tol: a posteriori stopping.  Returns (k_done, upd[k_done,
+    N+1, nsrc], bnorm[N+1, nsrc])."""
+    Np1 = G.N_total + 1
+    upd = np.zeros((max(K_max, 1), Np1, nsrc))
+    bn = np.zeros((Np1, nsrc))
+    kd = ctypes.c_int()
+    hs = int(hist.stride(0)) if hist is not None else 0
+    check(L.lib().pr_parareal_tol(G._h, op._h, int(nsrc), _ptr(u0), _ld(u0, op.dim),
+                                  ctypes.byref(source.struct), int(K_max), float(tol), _ptr(U_out),
+                                  _ld(U_out, op.dim), _hptr(upd), _hptr(bn),
+                                  _ptr(hist) if hist is not None else None, hs, ctypes.byref(kd),
+                                  _stream(stream)), "pr_parareal_tol")
+    return kd.value, upd[:kd.value], bn
+
+
+def sequential(op: Operator, u0, source: SourceTerm, N: int, m: int, U_out, nsrc: int = 1, stream=None):
+    """pr_sequential: u_0 = u0, u_{q+1} = F_{q+1} u_q into U_out ((N+1)*nsrc vectors)."""
+    check(L.lib().pr_sequential(op._h, int(nsrc), _ptr(u0), _ld(u0, op.dim), ctypes.byref(source.struct),
+                                int(N), int(m), _ptr(U_out), _ld(U_out, op.dim), _stream(stream)),
+          "pr_sequential")
+    return U_out
+
+
+def trajectory_error(op: Operator, U, Uref, N: int, m: int, nsrc: int = 1, stream=None):
+    """pr_trajectory_error: (err[nsrc], per_interval[N, nsrc]) host arrays."""
+    err = np.zeros(nsrc)
+    ivl = np.zeros((N, nsrc))
+    check(L.lib().pr_trajectory_error(op._h, int(nsrc), int(N), int(m), _ptr(U), _ld(U, op.dim),
+                                      _ptr(Uref), _ld(Uref, op.dim), _hptr(err), _hptr(ivl),
+                                      _stream(stream)), "pr_trajectory_error")
+    return err, ivl
+
+
+def efficiency(delta: float, eps: float, upd: np.ndarray, traj_err: np.ndarray):
+    """pr_efficiency (eq. def_efficiency): upd (K, N+1), traj_err (K+1,) -> eta (K,)."""
+    upd = np.ascontiguousarray(upd, dtype=np.float64)
+    te = np.ascontiguousarray(traj_err, dtype=np.float64)
+    K, Np1 = upd.shape
+    eta = np.zeros(K)
+    check(L.lib().pr_efficiency(float(delta), float(eps), Np1 - 1, K, _hptr(upd), _hptr(te), _hptr(eta)),
+          "pr_efficiency")
+    return eta
+
+
+def parareal_classical(coarse, coarse_source, op: Operator, u0, source: SourceTerm, N: int, m: int, K: int,
+                       U_out, nsrc: int = 1, hist=None, stream=None):
+    """pr_parareal_classical: coarse = Operator (one backward-Euler step per
+    interval, source coarse_source) or None (G = 0).  Returns upd[K, N+1, nsrc]."""
+    upd = np.zeros((max(K, 1), N + 1, nsrc))
+    hs = int(hist.stride(0)) if hist is not None else 0
+    check(L.lib().pr_parareal_classical(coarse._h if coarse is not None else None,
+                                        ctypes.byref(coarse_source.struct) if coarse_source is not None else None,
+                                        op._h, int(nsrc), _ptr(u0), _ld(u0, op.dim), ctypes.byref(source.struct),
+                                        int(N), int(m), int(K), _ptr(U_out), _ld(U_out, op.dim),
+                                        _hptr(upd), _ptr(hist) if hist is not None else None, hs,
+                                        _stream(stream)), "pr_parareal_classical")
+    return upd[:K]
+
+
 def bounds(delta: float, eps: float, bnorm: np.ndarray, upd: np.ndarray):
     """bnorm: (N+1,), upd: (K, N+1) -> dict of a priori / a posteriori bounds."""
     bnorm = np.ascontiguousarray(bnorm, dtype=np.float64)

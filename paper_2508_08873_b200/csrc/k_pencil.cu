@@ -70,6 +70,7 @@ struct PencilArgs {
     double *out; long ld_out;
     const double *off; long ld_off;
     int q0, vpi;
+    int step0, mstride;                // global step of step j: q*mstride + step0 + j
     int R;                             // source terms (0: none)
     const double *spaceT; int rs;      // n x rs
     const double *time;                // R x nsteps
@@ -91,7 +92,7 @@ __global__ void __launch_bounds__(128) k_pencil_step(PencilArgs a)
     double al[8];
     for (int s = 0; s < a.m; ++s) {
         const int j = (MODE == 2) ? a.m - s : s + 1;       // 1-based step within the interval
-        const long g = (long)q * a.m + j;                   // 1-based global step
+        const long g = (long)q * a.mstride + a.step0 + j;   // 1-based global step
         const Coef *F = a.fac + (g - 1) * n;
         // input of this step's down pass: the previous state (or U_in)
         const double *Src = (s == 0) ? (a.in ? a.in + v : nullptr) : X;
@@ -176,6 +177,7 @@ cudaError_t launch_stepper_pencil(const Op &op, int mode, const StepArgs &sa, cu
     a.in = sa.in; a.ld_in = sa.ld_in; a.out = sa.out; a.ld_out = sa.ld_out;
     a.off = sa.off; a.ld_off = sa.ld_off;
     a.q0 = sa.q0; a.vpi = sa.vpi;
+    a.step0 = sa.step0; a.mstride = sa.mstride > 0 ? sa.mstride : sa.m;
     a.R = sa.R; a.spaceT = sa.spaceT; a.rs = sa.R > 0 ? stepper_rs(sa.R) : 0;
     a.time = sa.time; a.amp = sa.amp; a.nsteps = sa.nsteps; a.nsrc = sa.nsrc > 0 ? sa.nsrc : 1;
     a.dt = sa.dt;

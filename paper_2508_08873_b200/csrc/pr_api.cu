@@ -306,7 +306,8 @@ static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double 
 static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi,
                            const pr_source *f, const double *in, long ld_in, double *out,
                            long ld_out, const double *off, long ld_off, int sketch,
-                           unsigned long long seed, cudaStream_t s, unsigned long long ctr3 = 0ULL)
+                           unsigned long long seed, cudaStream_t s, unsigned long long ctr3 = 0ULL,
+                           int step0 = 0, int mstride = 0)
 {
     if (B == 0) return PR_OK;
     if (op.dim == 2) {
@@ -342,6 +343,8 @@ static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi
     a.seed = seed;
     a.q0 = q0;
     a.vpi = vpi;
+    a.step0 = step0;
+    a.mstride = mstride;
     a.R = 0;
     a.dt = op.dt;
     if (mode == PR_AFFINE && f && f->kind == PR_SRC_SEP1D && f->nterms > 0) {
@@ -357,7 +360,8 @@ static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi
         a.nsrc = f->nsrc;
     }
     if (op.pencil) {
-        PR_REQUIRE((long)(q0 + (B + vpi - 1) / vpi) * m <= op.pen_nsteps, PR_EDIM,
+        const long ms = mstride > 0 ? mstride : m;
+        PR_REQUIRE((long)(q0 + (B + vpi - 1) / vpi - 1) * ms + step0 + m <= op.pen_nsteps, PR_EDIM,
                    "intervals beyond the time-dependent operator's step count");
         PR_CUDA(launch_stepper_pencil(op, mode, a, s));
     } else if (part_preferred(op, B, m)) {
@@ -1033,9 +1037,10 @@ __global__ void k_combine_offsets(const double *basis, long ldb, int R, const do
 // data of every interval is all-gathered so each rank runs the (cheap,
 // k-dimensional) sequential sweep over all N intervals itself (DESIGN.md
 // section 9).  With world = 1 every exchange is a no-op.
-pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_u0,
-                      const pr_source *f, int K_iter, double *U_out, long ld_out, double *upd_host,
-                      double *bnorm_host, double *hist, long hist_stride, void *stream)
+static pr_status parareal_core(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_u0,
+                               const pr_source *f, int K_iter, double *U_out, long ld_out, double *upd_host,
+                               double *bnorm_host, double *hist, long hist_stride, void *stream, double tol,
+                               int *k_done)
 {
     PR_REQUIRE(G && h && U_out, PR_EINVAL, "NULL argument");
     const Op &op = h->op;
@@ -1175,7 +1180,16 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
     if ((st = halo(U_out)) != PR_OK) return st;
     stage("parareal init", s);
     if (hist) PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, hist, L.rs, L.vs, rows, (int)nvec, s));
-    // ---- iterations
+    // ---- iterations (tol > 0: stop at the first k whose a posteriori bound
+    // max_n eps sum_{m<n} delta^{n-m-1} ||u^k_m - u^{k-1}_m|| (eq. apost_bound) <= tol)
+    double de[2] = {0.0, 0.0};
+    if (tol > 0.0) {
+        PR_CUDA(cudaMemcpyAsync(de, G->de, sizeof de, cudaMemcpyDeviceToHost, s));
+        PR_CUDA(cudaStreamSynchronize(s));
+    }
+    std::vector<long> sf0(world), sn0(world);
+    for (int r = 0; r < world; ++r) shard_of(N, r, world, sf0[r], sn0[r]);
+    int K_run = K_iter;
     for (int it = 1; it <= K_iter; ++it) {
         // fine solves of all local intervals in one launch: Fu_{q+1} = F_q' u_q + b_q
         PhaseScope phase(PR_PHASE_ITERATION);
@@ -1195,7 +1209,34 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
         if (hist)
             PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, hist + (size_t)it * hist_stride, L.rs, L.vs, rows,
                                         (int)nvec, s));
+        if (tol > 0.0) {
+            double *ua = upd + (size_t)(it - 1) * nq * S;
+            if (world > 1) {
+                double *uall;
+                PR_ALLOC(uall, double, (size_t)N * S, Sc);
+                std::vector<long> cnt(world);
+                for (int r = 0; r < world; ++r) cnt[r] = sn0[r] * S;
+                if ((st = cm->all_gather_v(ua, uall, cnt.data(), sizeof(double), s)) != PR_OK) return st;
+                ua = uall;
+            }
+            std::vector<double> hu1((size_t)N * S);      // boundary j = 1..N at index j-1
+            PR_CUDA(cudaMemcpyAsync(hu1.data(), ua, hu1.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+            PR_CUDA(cudaStreamSynchronize(s));
+            double bound = 0.0;
+            for (int sI = 0; sI < S; ++sI)
+                for (int n = 1; n <= N; ++n) {
+                    double acc = 0.0;
+                    for (int mm = 1; mm <= n - 1; ++mm) acc += pow(de[0], n - mm - 1) * hu1[(size_t)(mm - 1) * S + sI];
+                    bound = std::max(bound, de[1] * acc);
+                }
+            if (bound <= tol) {
+                K_run = it;
+                break;
+            }
+        }
     }
+    if (k_done) *k_done = K_run;
+    K_iter = K_run;
     // ---- host outputs: update norms and ||b_j|| of ALL boundaries
     std::vector<long> f0(world), n0(world);
     for (int r = 0; r < world; ++r) shard_of(N, r, world, f0[r], n0[r]);
@@ -1243,6 +1284,25 @@ pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_
         return PR_ENOCONV;
     }
     return PR_OK;
+}
+
+pr_status pr_parareal(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_u0,
+                      const pr_source *f, int K_iter, double *U_out, long ld_out, double *upd_host,
+                      double *bnorm_host, double *hist, long hist_stride, void *stream)
+{
+    return parareal_core(G, h, nsrc, u0, ld_u0, f, K_iter, U_out, ld_out, upd_host, bnorm_host, hist,
+                         hist_stride, stream, 0.0, nullptr);
+}
+
+pr_status pr_parareal_tol(pr_coarse G, pr_op h, int nsrc, const double *u0, long ld_u0,
+                          const pr_source *f, int K_max, double tol, double *U_out, long ld_out,
+                          double *upd_host, double *bnorm_host, double *hist, long hist_stride,
+                          int *k_done, void *stream)
+{
+    PR_REQUIRE(tol > 0.0 && k_done, PR_EINVAL, "pr_parareal_tol needs tol > 0 and k_done");
+    PR_REQUIRE(G && G->p > 0, PR_EUNAVAIL, "the a posteriori bound needs eps (p >= 1)");
+    return parareal_core(G, h, nsrc, u0, ld_u0, f, K_max, U_out, ld_out, upd_host, bnorm_host, hist,
+                         hist_stride, stream, tol, k_done);
 }
 
 // ------------------------------------------------------ distributed stages
@@ -1397,6 +1457,209 @@ pr_status pr_bounds(double delta, double eps, int N, int K, const double *bnorm,
             apost_sup[k - 1] = (delta < 1.0) ? eps / (1.0 - delta) * mx : NAN;   // eq. apost_bound_sup
         }
     }
+    return PR_OK;
+}
+
+// ============================================================ reporting
+// (the sequential fine reference, the max-over-time error
+// of the paper's figures, the estimator efficiency eta^k, and the classical
+// Parareal baselines G = 0 and G = one coarse backward-Euler step.)
+
+// out = x - y (op-layout vector blocks)
+__global__ void k_vdiff(const double *x, const double *y, long rs, long vs, long rows, int nvec, double *out)
+{
+    const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= rows * nvec) return;
+    const long v = idx % nvec, i = idx / nvec;
+    const long o = i * rs + v * vs;
+    out[o] = x[o] - y[o];
+}
+
+// mx[c] = max(mx[c], nrm[c]) for c < cnt (c >= lo only)
+__global__ void k_runmax(double *mx, const double *nrm, int lo, int cnt)
+{
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < cnt && c >= lo) mx[c] = fmax(mx[c], nrm[c]);
+}
+
+pr_status pr_sequential(pr_op h, int nsrc, const double *u0, long ld_u0, const pr_source *f, int N, int m,
+                        double *U_out, long ld_out, void *stream)
+{
+    PR_REQUIRE(h && u0 && U_out, PR_EINVAL, "NULL argument");
+    const Op &op = h->op;
+    PR_REQUIRE(nsrc >= 1 && N >= 1 && m >= 0, PR_EINVAL, "bad sizes");
+    const long rows = op.rows;
+    const long nvec = (long)(N + 1) * nsrc;
+    PR_REQUIRE(ld_out >= ((op.dim == 1) ? nvec : rows), PR_EDIM, "ld_out too small");
+    PR_REQUIRE(ld_u0 >= ((op.dim == 1) ? nsrc : rows), PR_EDIM, "ld_u0 too small");
+    {
+        pr_status st = check_source(op, f, 0, m, N);
+        if (st != PR_OK) return st;
+        if (op.dim == 1 && f->kind == PR_SRC_SEP1D)
+            PR_REQUIRE(f->nsrc == nsrc, PR_EDIM, "source nsrc must equal nsrc");
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    Lay L = lay(op, ld_out), L0 = lay(op, ld_u0);
+    const long blk = (op.dim == 1) ? (long)nsrc : (long)nsrc * ld_out;
+    PR_CUDA(launch_copy_vectors(u0, L0.rs, L0.vs, U_out, L.rs, L.vs, rows, nsrc, s));
+    for (int q = 0; q < N; ++q) {       // u_{q+1} = F_{q+1} u_q
+        pr_status st = propagate(op, PR_AFFINE, q, m, nsrc, nsrc, f, U_out + q * blk, ld_out,
+                                 U_out + (q + 1) * blk, ld_out, nullptr, 0, 0, 0, s);
+        if (st != PR_OK) return st;
+    }
+    return PR_OK;
+}
+
+pr_status pr_trajectory_error(pr_op h, int nsrc, int N, int m, const double *U, long ldU,
+                              const double *Uref, long ldR, double *err_host, double *ivl_host,
+                              void *stream)
+{
+    PR_REQUIRE(h && U && Uref && err_host, PR_EINVAL, "NULL argument");
+    const Op &op = h->op;
+    PR_REQUIRE(nsrc >= 1 && N >= 1 && m >= 1, PR_EINVAL, "bad sizes");
+    PR_REQUIRE(ldU == ldR, PR_EDIM, "U and Uref must share the leading dimension");
+    const long rows = op.rows;
+    const int B = N * nsrc;              // error vectors at the starts of intervals 1..N
+    PR_REQUIRE(ldU >= ((op.dim == 1) ? (long)(N + 1) * nsrc : rows), PR_EDIM, "ld too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    Scratch Sc(s);
+    const long ld = ldU;
+    Lay L = lay(op, ld);
+    const size_t arr = (op.dim == 1) ? (size_t)rows * ld : (size_t)B * ld;
+    double *E, *mx, *nrm, *npart;
+    PR_ALLOC(E, double, arr, Sc);
+    PR_ALLOC(mx, double, (size_t)B, Sc);
+    PR_ALLOC(nrm, double, (size_t)B, Sc);
+    const int nchunk = xty_chunks(rows, N);
+    const long cr = (rows + nchunk - 1) / nchunk;
+    PR_ALLOC(npart, double, (size_t)B * nchunk, Sc);
+    // e_{q-1} = u^k_{q-1} - u_{q-1}: the source cancels, so the trajectory error
+    // inside interval q is the LINEAR propagation of e_{q-1} (eq. F_n_affine)
+    note_launch();
+    k_vdiff<<<(unsigned)((rows * B + 255) / 256), 256, 0, s>>>(U, Uref, L.rs, L.vs, rows, B, E);
+    PR_CHECK_LAUNCH("k_vdiff");
+    PR_CUDA(launch_vecnorm_parts(E, L.rs, L.vs, rows, B, nchunk, cr, npart, s));
+    PR_CUDA(launch_norm_finish(npart, B, nchunk, mx, s));
+    for (int j = 1; j <= m; ++j) {
+        pr_status st = propagate(op, PR_LINEAR, 0, 1, B, nsrc, nullptr, E, ld, E, ld, nullptr, 0, 0, 0, s,
+                                 0ULL, j - 1, m);
+        if (st != PR_OK) return st;
+        PR_CUDA(launch_vecnorm_parts(E, L.rs, L.vs, rows, B, nchunk, cr, npart, s));
+        PR_CUDA(launch_norm_finish(npart, B, nchunk, nrm, s));
+        // t in [t_{q-1}, t_q) for every interval; t = T (j = m) for the last one (R-TRAJ)
+        const int lo = (j < m) ? 0 : (N - 1) * nsrc;
+        note_launch();
+        k_runmax<<<(B + 127) / 128, 128, 0, s>>>(mx, nrm, lo, B);
+        PR_CHECK_LAUNCH("k_runmax");
+    }
+    std::vector<double> hm(B);
+    PR_CUDA(cudaMemcpyAsync(hm.data(), mx, B * sizeof(double), cudaMemcpyDeviceToHost, s));
+    PR_CUDA(cudaStreamSynchronize(s));
+    for (int sI = 0; sI < nsrc; ++sI) {
+        double e = 0.0;
+        for (int q = 0; q < N; ++q) e = std::max(e, hm[(size_t)q * nsrc + sI]);
+        err_host[sI] = e;
+    }
+    if (ivl_host) memcpy(ivl_host, hm.data(), B * sizeof(double));
+    return PR_OK;
+}
+
+pr_status pr_efficiency(double delta, double eps, int N, int K, const double *upd, const double *traj_err,
+                        double *eta)
+{
+    PR_REQUIRE(N >= 2 && K >= 1 && upd && traj_err && eta, PR_EINVAL, "bad arguments");
+    const int W = N + 1;
+    for (int k = 1; k <= K; ++k) {
+        const double *u = upd + (size_t)(k - 1) * W;
+        double den = 0.0;              // eq. def_efficiency: max over 1 <= n < N (as printed, Z21)
+        for (int n = 1; n < N; ++n) {
+            double acc = 0.0;
+            for (int mm = 1; mm <= n - 1; ++mm) acc += pow(delta, n - mm - 1) * u[mm];
+            den = std::max(den, eps * acc);
+        }
+        eta[k - 1] = traj_err[k] / den;
+    }
+    return PR_OK;
+}
+
+pr_status pr_parareal_classical(pr_op coarse, const pr_source *fc, pr_op h, int nsrc, const double *u0,
+                                long ld_u0, const pr_source *f, int N, int m, int K_iter, double *U_out,
+                                long ld_out, double *upd_host, double *hist, long hist_stride, void *stream)
+{
+    PR_REQUIRE(h && u0 && U_out, PR_EINVAL, "NULL argument");
+    const Op &op = h->op;
+    PR_REQUIRE(nsrc >= 1 && N >= 1 && m >= 0 && K_iter >= 0, PR_EINVAL, "bad sizes");
+    const long rows = op.rows;
+    const int S = nsrc;
+    const long nvec = (long)(N + 1) * S;
+    PR_REQUIRE(ld_out >= ((op.dim == 1) ? nvec : rows), PR_EDIM, "ld_out too small");
+    PR_REQUIRE(ld_u0 >= ((op.dim == 1) ? S : rows), PR_EDIM, "ld_u0 too small");
+    if (coarse) {
+        PR_REQUIRE(coarse->op.rows == rows && coarse->op.dim == op.dim, PR_EDIM, "coarse / fine operator mismatch");
+        pr_status st = check_source(coarse->op, fc, 0, 1, N);
+        if (st != PR_OK) return st;
+    }
+    {
+        pr_status st = check_source(op, f, 0, m, N);
+        if (st != PR_OK) return st;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    Scratch Sc(s);
+    const long ld = ld_out;
+    Lay L = lay(op, ld), L0 = lay(op, ld_u0);
+    const size_t arr = (op.dim == 1) ? (size_t)rows * ld : (size_t)nvec * ld;
+    const long blk = (op.dim == 1) ? (long)S : (long)S * ld;
+    double *Fu, *Gu, *Uold, *npart, *upd;
+    PR_ALLOC(Fu, double, arr, Sc);
+    PR_ALLOC(Gu, double, arr, Sc);
+    PR_ALLOC(Uold, double, arr, Sc);
+    const int nchunk = xty_chunks(rows, N);
+    const long cr = (rows + nchunk - 1) / nchunk;
+    PR_ALLOC(npart, double, (size_t)nvec * nchunk, Sc);
+    PR_ALLOC(upd, double, (size_t)(K_iter > 0 ? K_iter : 1) * nvec, Sc);
+    pr_status st;
+    // G_{q+1} x (+ off): one backward-Euler step of the coarse operator over
+    // interval q+1 (its step q+1, time step Delta T), or 0
+    auto Gstep = [&](int q, int nb, const double *in, double *out, const double *off) -> pr_status {
+        if (coarse)
+            return propagate(coarse->op, PR_AFFINE, q, 1, nb * S, S, fc, in, ld, out, ld, off, ld, 0, 0, s);
+        if (off) PR_CUDA(launch_copy_vectors(off, L.rs, L.vs, out, L.rs, L.vs, rows, nb * S, s));
+        else if (op.dim == 1) PR_CUDA(cudaMemset2DAsync(out, ld * sizeof(double), 0, nb * S * sizeof(double), rows, s));
+        else PR_CUDA(cudaMemsetAsync(out, 0, (size_t)nb * S * ld * sizeof(double), s));
+        return PR_OK;
+    };
+    // initialisation u^0_0 = u0, u^0_{q+1} = G_{q+1} u^0_q
+    PR_CUDA(launch_copy_vectors(u0, L0.rs, L0.vs, U_out, L.rs, L.vs, rows, S, s));
+    for (int q = 0; q < N; ++q)
+        if ((st = Gstep(q, 1, U_out + q * blk, U_out + (q + 1) * blk, nullptr)) != PR_OK) return st;
+    if (hist) PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, hist, L.rs, L.vs, rows, (int)nvec, s));
+    for (int it = 1; it <= K_iter; ++it) {
+        PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, Uold, L.rs, L.vs, rows, (int)nvec, s));
+        // F_{q+1} u^k_q and G_{q+1} u^k_q for all q (parallel)
+        if ((st = propagate(op, PR_AFFINE, 0, m, N * S, S, f, Uold, ld, Fu + blk, ld, nullptr, 0, 0, 0, s)) != PR_OK)
+            return st;
+        if ((st = Gstep(0, N, Uold, Gu + blk, nullptr)) != PR_OK) return st;
+        // c_{q+1} = F u^k_q - G u^k_q into Fu
+        note_launch();
+        k_vdiff<<<(unsigned)((rows * N * S + 255) / 256), 256, 0, s>>>(Fu + blk, Gu + blk, L.rs, L.vs, rows,
+                                                                         N * S, Fu + blk);
+        PR_CHECK_LAUNCH("k_vdiff");
+        // sequential sweep u^{k+1}_{q+1} = G_{q+1} u^{k+1}_q + c_{q+1} (eq. def_Parareal)
+        for (int q = 0; q < N; ++q)
+            if ((st = Gstep(q, 1, U_out + q * blk, U_out + (q + 1) * blk, Fu + (q + 1) * blk)) != PR_OK) return st;
+        // update norms ||u^{k+1}_j - u^k_j||, all boundaries
+        note_launch();
+        k_vdiff<<<(unsigned)((rows * nvec + 255) / 256), 256, 0, s>>>(U_out, Uold, L.rs, L.vs, rows, (int)nvec, Gu);
+        PR_CHECK_LAUNCH("k_vdiff");
+        PR_CUDA(launch_vecnorm_parts(Gu, L.rs, L.vs, rows, (int)nvec, nchunk, cr, npart, s));
+        PR_CUDA(launch_norm_finish(npart, (int)nvec, nchunk, upd + (size_t)(it - 1) * nvec, s));
+        if (hist)
+            PR_CUDA(launch_copy_vectors(U_out, L.rs, L.vs, hist + (size_t)it * hist_stride, L.rs, L.vs, rows,
+                                        (int)nvec, s));
+    }
+    if (upd_host && K_iter > 0)
+        PR_CUDA(cudaMemcpyAsync(upd_host, upd, (size_t)K_iter * nvec * sizeof(double), cudaMemcpyDeviceToHost, s));
+    PR_CUDA(cudaStreamSynchronize(s));
     return PR_OK;
 }
 

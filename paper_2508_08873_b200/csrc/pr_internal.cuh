@@ -114,6 +114,10 @@ struct StepArgs {
     unsigned long long seed;
     int q0;                            // first interval
     int vpi;                           // vectors per interval
+    // step numbering (time-dependent pencils only): step j (1-based) of this
+    // launch is global step q*mstride + step0 + j (mstride 0: = m)
+    int step0;
+    int mstride;
     // source (PR_SRC_SEP1D) -- R == 0: none
     int R;
     const double *spaceT;              // (n x stepper_rs(R)) row-major, zero-padded transpose
