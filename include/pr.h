@@ -164,6 +164,25 @@ pr_status pr_op_create_pencil(int n, int nsteps, const double *lsub, const doubl
                               const double *lsup, const double *lrowsum, const double *msub,
                               const double *mdiag, const double *msup, double dt, pr_op *out);
 
+/* Weighted view of a pencil with a mass matrix: the
+ * operator in the coordinates u^ = C u of the inner product (u, v)_M = u^T M v,
+ * M = C^T C (Cholesky, C upper bidiagonal).  Its fine solver is
+ * F^ = C F C^{-1}; the Euclidean SVD of F^' IS the generalized SVD of F'
+ * with respect to (.,.)_M of eq. svd (sigma equal, psi = C^{-1} psi^,
+ * phi = C^{-1} phi^), and F^'^T = C^{-T} F'^T C^T is F'^* = M^{-1} F'^T M in
+ * these coordinates (reading R-WIP).  So pr_build_coarse / pr_parareal /
+ * pr_bounds on the view run the paper's method in the M inner product
+ * (Exp 1's L^2 choice): states, coarse factors and update norms are
+ * in u^ coordinates (||u^|| = ||u||_M); map with pr_op_weight_apply.  The view
+ * shares the base's device arrays: destroy it before the base.  Errors: EINVAL
+ * (not a pencil with M), ESINGULAR (M not SPD), ECUDA. */
+pr_status pr_op_create_weighted(pr_op base, pr_op *out);
+enum { PR_TO_WEIGHTED = 0, PR_FROM_WEIGHTED = 1 };
+/* Y = C X (PR_TO_WEIGHTED) or C^{-1} X (PR_FROM_WEIGHTED) for B vectors (1D
+ * layout; X == Y allowed).  Asynchronous.  Errors: EINVAL, EDIM. */
+pr_status pr_op_weight_apply(pr_op view, int direction, int B, const double *X, long ldx, double *Y, long ldy,
+                             void *stream);
+
 /* 2D operator: 5-point Laplacian on the unit square with homogeneous
  * Dirichlet conditions, n x n interior points, A = T (x) I + I (x) T,
  * T = tridiag(-1, 2, -1)/h^2.  Solved in the sine eigenbasis of T (DESIGN.md

@@ -5,6 +5,9 @@
   oracle uses Householder reflections (Golub & Van Loan, Alg. 5.2.1), which is
   unconditionally stable on the numerically rank-deficient snapshot blocks
   (SURVEY §0 finding 6).  No column dropping: l stays fixed (reading Z7).
+* weighted_gram_schmidt: the same basis in the inner product (u, v)_M =
+  u^T M v of V: classical Gram-Schmidt with one full
+  reorthogonalisation pass (CGS2), every inner product and norm in M.
 * jacobi_svd: SVD of the small matrix M of step 5 by the
   one-sided (Hestenes) Jacobi method, cyclic-by-rows ordering, no LAPACK.
   Singular values sorted descending; each right singular vector's
@@ -41,6 +44,23 @@ def householder_qr(Y: np.ndarray):
             continue
         Q[j:, :] -= 2.0 * np.outer(v, v @ Q[j:, :])
     return Q, R
+
+
+def weighted_gram_schmidt(Y: np.ndarray, Mx):
+    """W (n x l) with W^T M W = I and span W = span Y; Mx(X) applies the SPD
+    inner-product matrix to the columns of X."""
+    Y = np.array(Y, dtype=np.float64, copy=True)
+    n, l = Y.shape
+    W = np.zeros((n, l))
+    for j in range(l):
+        v = Y[:, j].copy()
+        for _ in range(2):                      # CGS2
+            if j > 0:
+                r = W[:, :j].T @ Mx(v[:, None])[:, 0]
+                v -= W[:, :j] @ r
+        nrm = np.sqrt(float(v @ Mx(v[:, None])[:, 0]))
+        W[:, j] = v / nrm if nrm > 0 else 0.0
+    return W
 
 
 def jacobi_svd(M: np.ndarray, tol: float = None, max_sweeps: int = 60):

@@ -25,7 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .fine import DenseOp, Op1D, OpPencil, fine
-from .linalg import householder_qr, jacobi_svd
+from .linalg import householder_qr, jacobi_svd, weighted_gram_schmidt
 from .rng import gaussian_sketch
 
 
@@ -55,7 +55,7 @@ def _as_columns(op, vecs: np.ndarray) -> np.ndarray:
 
 
 def rsvd_interval(op, interval: int, k: int, p: int, seed: int, power_iterations: int = 0,
-                  independent_adjoint: bool = False) -> Truncated:
+                  independent_adjoint: bool = False, inner=None) -> Truncated:
     """Steps 1-6 for the 1-based interval n = `interval`.
 
     power_iterations q: W = span{(F' F'^*)^q F' omega_i}, evaluated
@@ -68,6 +68,9 @@ def rsvd_interval(op, interval: int, k: int, p: int, seed: int, power_iterations
     reconstruction, reading R-IND), and C replaces M of step 5."""
     l = k + p
     n_dof = op.n if isinstance(op, (Op1D, OpPencil)) else (op.F.shape[0] if isinstance(op, DenseOp) else op.n * op.n)
+    if inner is not None:
+        assert power_iterations == 0 and not independent_adjoint
+        return _rsvd_weighted(op, interval, k, l, seed, inner, n_dof)
     # step 1
     Omega = gaussian_sketch(seed, interval - 1, n_dof, l)
     Y = _as_columns(op, fine(op, interval, _as_vectors(op, Omega), "linear"))
@@ -94,6 +97,34 @@ def rsvd_interval(op, interval: int, k: int, p: int, seed: int, power_iterations
     V = Vb @ Phi[:, :k]
     # step 6
     return Truncated(U=U, sigma=sig, V=V, k=k)
+
+
+def _rsvd_weighted(op, interval, k, l, seed, inner, n_dof) -> Truncated:
+    """Steps 1-6 with (.,.)_V = (.,.)_M, M = inner (tridiagonal (sub, diag, sup);
+    the generalized SVD of eq. svd).  The V-adjoint is
+    F'^* = M^{-1} F'^T M ((F'^* w, v)_M = (w, F' v)_M).  The basis of the
+    Gram-Schmidt steps 2 and 4 is M-orthonormal; M_ij = (F'^* w_i, v_j)_M.
+    The returned V holds M phi_r, so that apply_linear(x) = sum psi sigma (phi, x)_M.
+    Test vectors: standard Gaussian in V, i.e. with E[(omega, v)_M^2] = ||v||_M^2:
+    omega = C^{-1} xi, xi ~ N(0, I) (the seeded Philox draws), M = C^T C
+    (reading R-WIP; the Cholesky factor is a library routine here).  The same
+    seed then gives the same test vectors as the GPU's weighted view."""
+    from .fine import _tridiag_apply
+    ms, md, mp = (np.asarray(a, float) for a in inner)
+    Mx = lambda X: _tridiag_apply((ms, md, mp), X.T).T          # columns
+    Mfull = np.diag(md) + np.diag(ms[1:], -1) + np.diag(mp[:-1], 1)
+    Cup = np.linalg.cholesky(Mfull).T                           # M = C^T C (library routine)
+    Omega = np.linalg.solve(Cup, gaussian_sketch(seed, interval - 1, n_dof, l))
+    Y = _as_columns(op, fine(op, interval, _as_vectors(op, Omega), "linear"))
+    W = weighted_gram_schmidt(Y, Mx)
+    FtMW = _as_columns(op, fine(op, interval, _as_vectors(op, Mx(W)), "adjoint"))   # F'^T M W
+    Z = np.linalg.solve(Mfull, FtMW)                             # F'^* W
+    Vb = weighted_gram_schmidt(Z, Mx)
+    Mm = Z.T @ Mx(Vb)                                            # (F'^* w_i, v_j)_M
+    Psi_, sig, Phi = jacobi_svd(Mm)
+    U = W @ Psi_[:, :k]
+    V = Vb @ Phi[:, :k]
+    return Truncated(U=U, sigma=sig, V=Mx(V), k=k)
 
 
 def exact_truncated(Fdense: np.ndarray, k: int) -> Truncated:

@@ -17,9 +17,11 @@ STATUS_NAMES = ["PR_OK", "PR_EINVAL", "PR_EDIM", "PR_ESINGULAR", "PR_ENOCONV", "
                 "PR_EOOM", "PR_ECUDA", "PR_ENCCL"]
 PR_LINEAR, PR_ADJOINT, PR_AFFINE = 0, 1, 2
 PR_SRC_NONE, PR_SRC_SEP1D, PR_SRC_BUMP2D = 0, 1, 2
+PR_TO_WEIGHTED, PR_FROM_WEIGHTED = 0, 1
 
 # every symbol include/pr.h declares
-EXPORTS = ["pr_last_error", "pr_version", "pr_reload_env", "pr_profile", "pr_counters", "pr_phase_counters", "pr_op_create_tridiag", "pr_op_create_pencil", "pr_op_create_sep2d",
+EXPORTS = ["pr_last_error", "pr_version", "pr_reload_env", "pr_profile", "pr_counters", "pr_phase_counters", "pr_op_create_tridiag", "pr_op_create_pencil", "pr_op_create_weighted",
+           "pr_op_weight_apply", "pr_op_create_sep2d",
            "pr_op_destroy", "pr_op_info", "pr_fine_propagate", "pr_gaussian_sketch",
            "pr_build_coarse", "pr_coarse_info", "pr_coarse_factors", "pr_coarse_apply",
            "pr_coarse_destroy", "pr_parareal", "pr_parareal_tol", "pr_bounds", "pr_sequential",
@@ -69,6 +71,8 @@ def lib():
             "pr_phase_counters": ([I, ctypes.POINTER(lg), dp, dp], I),
             "pr_op_create_tridiag": ([I, dp, dp, dp, dp, dp, D, ctypes.POINTER(vp)], I),
             "pr_op_create_pencil": ([I, I, dp, dp, dp, dp, dp, dp, dp, D, ctypes.POINTER(vp)], I),
+            "pr_op_create_weighted": ([vp, ctypes.POINTER(vp)], I),
+            "pr_op_weight_apply": ([vp, I, I, vp, lg, vp, lg, vp], I),
             "pr_op_create_sep2d": ([I, D, ctypes.POINTER(vp)], I),
             "pr_op_destroy": ([vp], I),
             "pr_op_info": ([vp, ctypes.POINTER(lg), ip, ip], I),

@@ -79,6 +79,25 @@ class Operator:
                                           float(dt), ctypes.byref(h)), "pr_op_create_pencil")
         return cls(h)
 
+    def weighted(self) -> "Operator":
+        """The view in the mass-matrix inner product (pr_op_create_weighted);
+        keeps this operator alive."""
+        h = ctypes.c_void_p()
+        check(L.lib().pr_op_create_weighted(self._h, ctypes.byref(h)), "pr_op_create_weighted")
+        v = Operator(h)
+        v._base = self
+        return v
+
+    def to_weighted(self, X, Y, stream=None):
+        check(L.lib().pr_op_weight_apply(self._h, L.PR_TO_WEIGHTED, int(X.shape[1]), _ptr(X), _ld(X, 1), _ptr(Y),
+                                         _ld(Y, 1), _stream(stream)), "pr_op_weight_apply")
+        return Y
+
+    def from_weighted(self, X, Y, stream=None):
+        check(L.lib().pr_op_weight_apply(self._h, L.PR_FROM_WEIGHTED, int(X.shape[1]), _ptr(X), _ld(X, 1),
+                                         _ptr(Y), _ld(Y, 1), _stream(stream)), "pr_op_weight_apply")
+        return Y
+
     @classmethod
     def sep2d(cls, n: int, dt: float) -> "Operator":
         h = ctypes.c_void_p()

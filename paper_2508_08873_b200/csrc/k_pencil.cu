@@ -158,6 +158,63 @@ __global__ void __launch_bounds__(128) k_pencil_step(PencilArgs a)
         for (int i = 0; i < n; ++i) X[(long)i * ldx] += a.off[v + (long)i * a.ld_off];
 }
 
+// The Cholesky factor of the mass matrix (weighted views, R-WIP): one thread per
+// vector, rows in the order the recurrence needs (in place safe).
+template <int MODE>
+__global__ void k_bidiag(int n, const double *__restrict__ cd, const double *__restrict__ ce, long B,
+                         const double *in, long irs, long ivs, double *out, long ors, long ovs)
+{
+    const long v = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= B) return;
+    const double *x = in ? in + v * ivs : nullptr;
+    double *y = out + v * ovs;
+    auto X = [&](int i) -> double { return x ? x[(long)i * irs] : 0.0; };
+    if (MODE == BIDIAG_C) {              // y_i = c_ii x_i + c_{i,i+1} x_{i+1}   (ascending)
+        double xi = X(0);
+        for (int i = 0; i < n; ++i) {
+            const double xn = (i + 1 < n) ? X(i + 1) : 0.0;
+            y[(long)i * ors] = fma(cd[i], xi, (i + 1 < n) ? ce[i] * xn : 0.0);
+            xi = xn;
+        }
+    } else if (MODE == BIDIAG_CT) {      // y_i = c_ii x_i + c_{i-1,i} x_{i-1}   (descending)
+        double xi = X(n - 1);
+        for (int i = n - 1; i >= 0; --i) {
+            const double xp = (i > 0) ? X(i - 1) : 0.0;
+            y[(long)i * ors] = fma(cd[i], xi, (i > 0) ? ce[i - 1] * xp : 0.0);
+            xi = xp;
+        }
+    } else if (MODE == BIDIAG_CINV) {    // C y = x: back substitution
+        double yn = 0.0;
+        for (int i = n - 1; i >= 0; --i) {
+            const double r = (i + 1 < n) ? fma(-ce[i], yn, X(i)) : X(i);
+            yn = r / cd[i];
+            y[(long)i * ors] = yn;
+        }
+    } else {                             // C^T y = x: forward substitution
+        double yp = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double r = (i > 0) ? fma(-ce[i - 1], yp, X(i)) : X(i);
+            yp = r / cd[i];
+            y[(long)i * ors] = yp;
+        }
+    }
+}
+
+cudaError_t launch_bidiag(int mode, int n, const double *cdiag, const double *csup, long B, const double *in,
+                          long irs, long ivs, double *out, long ors, long ovs, cudaStream_t s)
+{
+    if (B == 0) return cudaSuccess;
+    note_launch();
+    const unsigned blocks = (unsigned)((B + 127) / 128);
+    switch (mode) {
+    case BIDIAG_C: k_bidiag<BIDIAG_C><<<blocks, 128, 0, s>>>(n, cdiag, csup, B, in, irs, ivs, out, ors, ovs); break;
+    case BIDIAG_CT: k_bidiag<BIDIAG_CT><<<blocks, 128, 0, s>>>(n, cdiag, csup, B, in, irs, ivs, out, ors, ovs); break;
+    case BIDIAG_CINV: k_bidiag<BIDIAG_CINV><<<blocks, 128, 0, s>>>(n, cdiag, csup, B, in, irs, ivs, out, ors, ovs); break;
+    default: k_bidiag<BIDIAG_CTINV><<<blocks, 128, 0, s>>>(n, cdiag, csup, B, in, irs, ivs, out, ors, ovs); break;
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pencil_factor(int n, int nsteps, const double *lsub, const double *ldiag,
                                  const double *lsup, const double *lrs, Coef *fac, int *bad,
                                  cudaStream_t s)

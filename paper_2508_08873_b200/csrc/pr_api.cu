@@ -302,6 +302,15 @@ static pr_status cholqr(const Op &op, double *Q, long ld, int nb, int l, double 
     return PR_OK;
 }
 
+// out += off for B vectors of a 1D batch (row strides ld_off / ld_out)
+__global__ void k_vadd(const double *off, long ld_off, long rows, long B, double *out, long ld_out)
+{
+    const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= rows * B) return;
+    const long i = idx / B, v = idx % B;
+    out[i * ld_out + v] += off[i * ld_off + v];
+}
+
 // One fine-propagation launch (1D or 2D), shared by the ABI and the drivers.
 static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi,
                            const pr_source *f, const double *in, long ld_in, double *out,
@@ -310,6 +319,31 @@ static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi
                            int step0 = 0, int mstride = 0)
 {
     if (B == 0) return PR_OK;
+    if (op.weighted) {
+        // F^ = C F C^{-1} (LINEAR / AFFINE: the source term maps with C too) and
+        // its Euclidean adjoint C^{-T} F'^T C^T, in place in `out` (R-WIP)
+        Op base = op;
+        base.weighted = 0;
+        const double *cd = op.wC, *ce = op.wC + op.n;
+        if (sketch) {
+            PR_CUDA(launch_sketch(1, op.n, op.rows, q0, B / vpi, vpi, seed, out, ld_out, 1, s, 0.0, ctr3));
+            in = out;
+            ld_in = ld_out;
+        }
+        PR_CUDA(launch_bidiag(mode == PR_ADJOINT ? BIDIAG_CT : BIDIAG_CINV, op.n, cd, ce, B, in, ld_in, 1, out,
+                              ld_out, 1, s));
+        pr_status st = propagate(base, mode, q0, m, B, vpi, f, out, ld_out, out, ld_out, nullptr, 0, 0, 0, s, 0ULL,
+                                 step0, mstride);
+        if (st != PR_OK) return st;
+        PR_CUDA(launch_bidiag(mode == PR_ADJOINT ? BIDIAG_CTINV : BIDIAG_C, op.n, cd, ce, B, out, ld_out, 1, out,
+                              ld_out, 1, s));
+        if (off) {
+            note_launch();
+            k_vadd<<<(unsigned)((op.rows * (long)B + 255) / 256), 256, 0, s>>>(off, ld_off, op.rows, B, out, ld_out);
+            PR_CHECK_LAUNCH("k_vadd");
+        }
+        return PR_OK;
+    }
     if (op.dim == 2) {
         Sep2dArgs a{&op, mode, q0, m, B, vpi, f, in, ld_in, out, ld_out, off, ld_off};
         if (sketch) {
@@ -595,11 +629,64 @@ pr_status pr_op_destroy(pr_op h)
 {
     if (!h) return PR_OK;
     Op &op = h->op;
+    if (h->view) {
+        cudaFree(op.wC);
+        delete h;
+        return PR_OK;
+    }
     cudaFree(op.dn_fw); cudaFree(op.up_fw); cudaFree(op.dn_tr); cudaFree(op.up_tr);
     cudaFree(op.part_rowc_fw); cudaFree(op.part_ctad_fw); cudaFree(op.part_rowc_tr); cudaFree(op.part_ctad_tr);
     cudaFree(op.S); cudaFree(op.lam);
     cudaFree(op.pen_fac); cudaFree(op.pen_m);
     delete h;
+    return PR_OK;
+}
+
+pr_status pr_op_create_weighted(pr_op base, pr_op *out)
+{
+    PR_REQUIRE(base && out, PR_EINVAL, "NULL argument");
+    const Op &b = base->op;
+    PR_REQUIRE(b.pencil && b.pen_m && !b.weighted, PR_EINVAL,
+               "a weighted view needs a pencil operator with a mass matrix");
+    const int n = b.n;
+    std::vector<double> m(3 * (size_t)n), c(2 * (size_t)n);
+    PR_CUDA(cudaMemcpy(m.data(), b.pen_m, m.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    const double *ms = m.data(), *md = m.data() + n, *mp = m.data() + 2 * n;
+    // M = C^T C, C upper bidiagonal (Cholesky of the SPD tridiagonal mass matrix)
+    for (int i = 0; i < n; ++i) {
+        const double e = (i > 0) ? c[n + i - 1] : 0.0;
+        const double d2 = md[i] - e * e;
+        PR_REQUIRE(d2 > 0.0 && isfinite(d2), PR_ESINGULAR, "mass matrix not positive definite");
+        c[i] = sqrt(d2);
+        c[n + i] = (i + 1 < n) ? mp[i] / c[i] : 0.0;
+        (void)ms;
+    }
+    pr_op h = new pr_op_s();
+    h->op = b;                   // shares the base's factor arrays
+    h->view = true;
+    h->op.weighted = 1;
+    h->op.wC = nullptr;
+    cudaError_t e = cudaMalloc(&h->op.wC, c.size() * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(h->op.wC, c.data(), c.size() * sizeof(double), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(h->op.wC);
+        delete h;
+        return cuda_fail(e, "pr_op_create_weighted");
+    }
+    *out = h;
+    return PR_OK;
+}
+
+pr_status pr_op_weight_apply(pr_op view, int direction, int B, const double *X, long ldx, double *Y, long ldy,
+                             void *stream)
+{
+    PR_REQUIRE(view && Y && (X || B == 0), PR_EINVAL, "NULL argument");
+    const Op &op = view->op;
+    PR_REQUIRE(op.weighted, PR_EINVAL, "not a weighted view");
+    PR_REQUIRE(direction == PR_TO_WEIGHTED || direction == PR_FROM_WEIGHTED, PR_EINVAL, "bad direction");
+    PR_REQUIRE(B >= 0 && ldx >= B && ldy >= B, PR_EDIM, "leading dimension too small");
+    PR_CUDA(launch_bidiag(direction == PR_TO_WEIGHTED ? BIDIAG_C : BIDIAG_CINV, op.n, op.wC, op.wC + op.n, B, X,
+                          ldx, 1, Y, ldy, 1, (cudaStream_t)stream));
     return PR_OK;
 }
 

@@ -94,6 +94,11 @@ struct Op {
     int pencil = 0, pen_nsteps = 0;
     Coef *pen_fac = nullptr;
     double *pen_m = nullptr;
+    // weighted view (pr_op_create_weighted): propagation in the coordinates
+    // u^ = C u of the mass-matrix inner product, M = C^T C (C upper bidiagonal:
+    // wC = diag (n) | super (n)); shares every other array with its base op
+    int weighted = 0;
+    double *wC = nullptr;
     // 2D: P = n+1; S (P x P) sine matrix with zero row/col 0; lam[P] eigenvalues of T.
     int P = 0;
     double *S = nullptr;
@@ -137,6 +142,12 @@ cudaError_t launch_pencil_factor(int n, int nsteps, const double *lsub, const do
                                  const double *lsup, const double *lrs, Coef *fac, int *bad,
                                  cudaStream_t s);
 cudaError_t launch_stepper_pencil(const Op &op, int mode, const StepArgs &sa, cudaStream_t s);
+// y = C x, C^T x, C^{-1} x, C^{-T} x for B vectors (op layout, row stride rs,
+// vector stride vs; in == out allowed; in == null: zero input); C upper
+// bidiagonal {diag, super} (k_pencil.cu)
+enum { BIDIAG_C = 0, BIDIAG_CT = 1, BIDIAG_CINV = 2, BIDIAG_CTINV = 3 };
+cudaError_t launch_bidiag(int mode, int n, const double *cdiag, const double *csup, long B, const double *in,
+                          long irs, long ivs, double *out, long ors, long ovs, cudaStream_t s);
 
 // partitioned stepper (k_part.cu): configuration for n (false: not supported),
 // setup (ends: P x 8 scratch), selection and launch
@@ -297,6 +308,7 @@ pr_status run_sep2d(const Sep2dArgs &a, cudaStream_t s);
 // ------------------------------------------------------------- handles
 struct pr_op_s {
     pr::Op op;
+    bool view = false;     // a weighted view: owns only op.wC
 };
 
 struct pr_coarse_s {

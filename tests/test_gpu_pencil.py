@@ -111,3 +111,51 @@ def test_pencil_parareal_iterates_match_oracle(name):
         ref = res.U[K][:, 0]
         scale = np.max(np.linalg.norm(ref, axis=1))
         assert np.max(np.linalg.norm(got - ref, axis=1)) <= TAU_1D * scale, K
+
+
+# ------------------------------------------- mass-matrix inner product (row 2)
+def test_weighted_view_build_and_parareal_match_oracle():
+    """pr_build_coarse / pr_parareal on the weighted view = the paper's method
+    in the M inner product (generalized SVD): sigma and G_q' (in
+    physical coordinates, G' x = C^{-1} G^' C x) against the oracle's weighted
+    rSVD, and the Parareal iterates mapped back with C^{-1}."""
+    import torch
+    from paper_2508_08873_b200 import Coarse, parareal
+    cfg = get("E2")
+    base = gpu_op(cfg)
+    view = base.weighted()
+    Gg = Coarse.build(view, cfg.N, cfg.m, cfg.k, cfg.p, cfg.seed_omega)
+    info = Gg.info()
+    op_o = make_op(cfg)
+    truncs = []
+    for q in range(cfg.N):
+        tr = rsvd_interval(op_o, q + 1, cfg.k, cfg.p, cfg.seed_omega, inner=op_o.M)
+        truncs.append(tr)
+        s1 = tr.sigma[0]
+        assert np.max(np.abs(info["sigma"][q] - tr.sigma)) <= TAU_1D * s1, q
+        X = np.random.default_rng(q).standard_normal((4, cfg.n))
+        Xh = empty_batch(cfg, 4)
+        view.to_weighted(to_gpu(cfg, X), Xh)
+        Yh = empty_batch(cfg, 4)
+        Gg.apply(q, Xh, Yh, 1)
+        Y = empty_batch(cfg, 4)
+        view.from_weighted(Yh, Y)
+        got, ref = from_gpu(cfg, Y), tr.apply_linear(X)
+        # the normwise bound holds in the M norm; in Euclidean norms it picks up
+        # cond(C) = sqrt(cond(M)) <= sqrt(3) (P1 mass matrix): factor 2
+        for v in range(4):
+            assert np.linalg.norm(got[v] - ref[v]) <= 2 * TAU_1D * s1 * np.linalg.norm(X[v]), (q, v)
+    u0 = G.initial_value(cfg)[None, :]
+    u0g = torch.tensor(np.ascontiguousarray(u0.T), dtype=torch.float64, device="cuda")
+    u0h = torch.zeros_like(u0g)
+    view.to_weighted(u0g, u0h)
+    for K in (0, 2):
+        Uh = torch.zeros((cfg.n, cfg.N + 1), dtype=torch.float64, device="cuda")
+        parareal(Gg, view, u0h, gpu_source(cfg), K, Uh, nsrc=1)
+        U = torch.zeros_like(Uh)
+        view.from_weighted(Uh, U)
+        res = oracle_parareal(op_o, truncs, u0, cfg.N, K, G.source_1d(cfg))
+        got = U.cpu().numpy().T
+        ref = res.U[K][:, 0]
+        scale = np.max(np.linalg.norm(ref, axis=1))
+        assert np.max(np.linalg.norm(got - ref, axis=1)) <= TAU_1D * scale, K
