@@ -311,3 +311,33 @@ def test_build_rsvd_variants_match_oracle(name, q, indep):
         got, ref = from_gpu(cfg, Y), tr.apply_linear(X)
         for v in range(4):
             assert np.linalg.norm(got[v] - ref[v]) <= TAU_1D * s1 * np.linalg.norm(X[v]), (qi, v)
+
+
+# ---------------------------------------------------- race detector by repetition
+@pytest.mark.parametrize("name,B,env", [("C2", 64, None), ("C2", 2560, None), ("C4", 1024, None),
+                                        ("C4", 1024, "PR_PART_VPT2"), ("T4", 40, None)])
+def test_part_stepper_bitwise_repeatable(name, B, env, monkeypatch):
+    """compute-sanitizer is not available on the GPU pool; a race in K1P's
+    shared-memory / DSMEM / mbarrier hand-offs would show up as run-to-run
+    differences.  20 identical launches (LINEAR and ADJOINT) must agree bit for
+    bit (H = 1 and H = 2 chunk layouts, the two-vectors-per-lane layout)."""
+    import torch
+    from paper_2508_08873_b200 import PR_ADJOINT, PR_LINEAR, lib
+    if env:
+        monkeypatch.setenv(env, "1")
+    lib().pr_reload_env()
+    try:
+        cfg = get(name)
+        op = gpu_op(cfg)
+        X = torch.randn(cfg.n, B, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(7))
+        for mode in (PR_LINEAR, PR_ADJOINT):
+            Y0 = torch.empty_like(X)
+            op.fine_propagate(mode, 0, cfg.m, X, Y0)
+            for _ in range(20):
+                Y = torch.empty_like(X)
+                op.fine_propagate(mode, 0, cfg.m, X, Y)
+                assert torch.equal(Y, Y0)
+    finally:
+        if env:
+            monkeypatch.delenv(env)
+        lib().pr_reload_env()
