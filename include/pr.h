@@ -292,6 +292,25 @@ pr_status pr_build_coarse(pr_op op, int N_total, int first_interval, int n_local
                           int k, int p, uint64_t seed, const pr_rsvd_opts *opts, pr_comm comm,
                           void *stream, pr_coarse *out);
 
+/* A posteriori estimate of the coarse error ||F_q' - G_q'|| for every local
+ * interval (the failure-probability estimator behind an adaptive choice of p,
+ * P:305-310; Halko, Martinsson & Tropp, Lemma 4.1):
+ *   est_q = 10 sqrt(2/pi) max_{i<=r} ||(F_q' - G_q') omega_i||,
+ * omega_i fresh N(0,1) probes (Philox counter word 3 = 3); est_q >= the true
+ * norm with probability >= 1 - 10^{-r}.  r batched fine solves per interval.
+ * est_host: host, n_local.  Synchronizing.  Errors: EINVAL, EDIM, EOOM. */
+pr_status pr_coarse_estimate(pr_coarse G, pr_op op, int r, uint64_t seed, double *est_host, void *stream);
+
+/* Adaptive oversampling: build with p = p0, estimate the coarse
+ * error (pr_coarse_estimate, r probes), and rebuild with p doubled until the
+ * largest estimate over ALL intervals (all ranks) is <= tol or p reaches
+ * p_max; *p_used is the p of the returned handle.  Errors: as pr_build_coarse,
+ * plus EINVAL (p0 < 1, p_max < p0, tol <= 0, r < 1). */
+pr_status pr_build_coarse_adaptive(pr_op op, int N_total, int first_interval, int n_local, int m, int k,
+                                   int p0, int p_max, double tol, int r, uint64_t seed,
+                                   const pr_rsvd_opts *opts, pr_comm comm, void *stream, pr_coarse *out,
+                                   int *p_used);
+
 /* Synchronizes with the stream of the handle's last call.  k, l, n_local,
  * first_interval, m; delta = max_q sigma_{q,1} and eps = max_q sigma_{q,k+1}
  * over ALL intervals (all ranks when built with a communicator; eq.

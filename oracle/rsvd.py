@@ -147,3 +147,14 @@ def delta_eps(truncs) -> tuple:
     delta = max(t.sigma[0] for t in truncs)
     eps = max(t.sigma[t.k] if t.k < len(t.sigma) else 0.0 for t in truncs)
     return delta, eps
+
+
+def coarse_error_estimate(op, trunc: Truncated, interval: int, r: int, seed: int) -> float:
+    """The failure-probability estimator of an adaptive p (Halko,
+    Martinsson & Tropp 2011, Lemma 4.1): 10 sqrt(2/pi) max_{i<=r} ||(F' - G') omega_i||,
+    omega_i i.i.d. N(0,1) (Philox counter word 3 = 3)."""
+    n_dof = op.n if isinstance(op, (Op1D, OpPencil)) else (op.F.shape[0] if isinstance(op, DenseOp) else op.n * op.n)
+    Om = gaussian_sketch(seed, interval - 1, n_dof, r, stream=3)
+    FO = _as_columns(op, fine(op, interval, _as_vectors(op, Om), "linear"))
+    GO = trunc.apply_linear(Om.T).T
+    return 10.0 * np.sqrt(2.0 / np.pi) * float(np.max(np.linalg.norm(FO - GO, axis=0)))

@@ -23,7 +23,7 @@ PR_TO_WEIGHTED, PR_FROM_WEIGHTED = 0, 1
 EXPORTS = ["pr_last_error", "pr_version", "pr_reload_env", "pr_profile", "pr_counters", "pr_phase_counters", "pr_op_create_tridiag", "pr_op_create_pencil", "pr_op_create_weighted",
            "pr_op_weight_apply", "pr_op_create_sep2d",
            "pr_op_destroy", "pr_op_info", "pr_fine_propagate", "pr_gaussian_sketch",
-           "pr_build_coarse", "pr_coarse_info", "pr_coarse_factors", "pr_coarse_apply",
+           "pr_build_coarse", "pr_coarse_estimate", "pr_build_coarse_adaptive", "pr_coarse_info", "pr_coarse_factors", "pr_coarse_apply",
            "pr_coarse_destroy", "pr_parareal", "pr_parareal_tol", "pr_bounds", "pr_sequential",
            "pr_trajectory_error", "pr_efficiency", "pr_parareal_classical", "pr_coarse_sweep_matrices",
            "pr_coarse_export", "pr_coarse_export_interval", "pr_coarse_project", "pr_reduced_sweep", "pr_coarse_expand",
@@ -79,6 +79,9 @@ def lib():
             "pr_fine_propagate": ([vp, I, I, I, I, I, ctypes.POINTER(Source), vp, lg, vp, lg, vp, lg, vp], I),
             "pr_gaussian_sketch": ([vp, I, I, I, U64, vp, lg, vp], I),
             "pr_build_coarse": ([vp, I, I, I, I, I, I, U64, ctypes.POINTER(RsvdOpts), vp, vp, ctypes.POINTER(vp)], I),
+            "pr_coarse_estimate": ([vp, vp, I, U64, dp, vp], I),
+            "pr_build_coarse_adaptive": ([vp, I, I, I, I, I, I, I, D, I, U64, ctypes.POINTER(RsvdOpts), vp, vp,
+                                          ctypes.POINTER(vp), ip], I),
             "pr_coarse_info": ([vp, ip, ip, ip, ip, ip, dp, dp, dp, ip], I),
             "pr_coarse_factors": ([vp, ctypes.POINTER(vp), ctypes.POINTER(vp), ctypes.POINTER(vp)], I),
             "pr_coarse_apply": ([vp, I, I, vp, lg, vp, lg, vp], I),

@@ -235,6 +235,29 @@ class Coarse:
                                       _stream(stream), ctypes.byref(h)), "pr_build_coarse")
         return cls(h, comm, int(N_total))
 
+    @classmethod
+    def build_adaptive(cls, op: Operator, N_total: int, m: int, k: int, p0: int, p_max: int, tol: float,
+                       seed: int, r: int = 10, first_interval: int = 0, n_local: int = None,
+                       comm: "Comm" = None, stream=None):
+        """pr_build_coarse_adaptive: returns (Coarse, p_used)."""
+        if n_local is None:
+            n_local = N_total - first_interval
+        h = ctypes.c_void_p()
+        pu = ctypes.c_int()
+        check(L.lib().pr_build_coarse_adaptive(op._h, int(N_total), int(first_interval), int(n_local), int(m),
+                                               int(k), int(p0), int(p_max), float(tol), int(r),
+                                               ctypes.c_uint64(int(seed)), None,
+                                               comm._h if comm is not None else None, _stream(stream),
+                                               ctypes.byref(h), ctypes.byref(pu)), "pr_build_coarse_adaptive")
+        return cls(h, comm, int(N_total)), pu.value
+
+    def estimate(self, op: Operator, r: int = 10, seed: int = 0, stream=None) -> np.ndarray:
+        """pr_coarse_estimate: per-interval estimate of ||F_q' - G_q'||."""
+        est = np.zeros(self.info(raise_on_error=False)["n_local"])
+        check(L.lib().pr_coarse_estimate(self._h, op._h, int(r), ctypes.c_uint64(int(seed)), _hptr(est),
+                                         _stream(stream)), "pr_coarse_estimate")
+        return est
+
     def info(self, raise_on_error: bool = True) -> dict:
         k, l, nl, first, m = (ctypes.c_int() for _ in range(5))
         delta, eps = ctypes.c_double(), ctypes.c_double()

@@ -311,6 +311,23 @@ __global__ void k_vadd(const double *off, long ld_off, long rows, long B, double
     out[i * ld_out + v] += off[i * ld_off + v];
 }
 
+// out = x - y (op-layout vector blocks)
+__global__ void k_vdiff(const double *x, const double *y, long rs, long vs, long rows, int nvec, double *out)
+{
+    const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= rows * nvec) return;
+    const long v = idx % nvec, i = idx / nvec;
+    const long o = i * rs + v * vs;
+    out[o] = x[o] - y[o];
+}
+
+// mx[c] = max(mx[c], nrm[c]) for c < cnt (c >= lo only)
+__global__ void k_runmax(double *mx, const double *nrm, int lo, int cnt)
+{
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < cnt && c >= lo) mx[c] = fmax(mx[c], nrm[c]);
+}
+
 // One fine-propagation launch (1D or 2D), shared by the ABI and the drivers.
 static pr_status propagate(const Op &op, int mode, int q0, int m, int B, int vpi,
                            const pr_source *f, const double *in, long ld_in, double *out,
@@ -1013,6 +1030,46 @@ pr_status pr_build_coarse(pr_op h, int N_total, int first_interval, int n_local,
     return PR_OK;
 }
 
+pr_status pr_build_coarse_adaptive(pr_op h, int N_total, int first_interval, int n_local, int m, int k,
+                                   int p0, int p_max, double tol, int r, uint64_t seed,
+                                   const pr_rsvd_opts *opts, pr_comm comm, void *stream, pr_coarse *out,
+                                   int *p_used)
+{
+    PR_REQUIRE(h && out && p_used, PR_EINVAL, "NULL argument");
+    PR_REQUIRE(p0 >= 1 && p_max >= p0 && tol > 0.0 && r >= 1, PR_EINVAL, "need 1 <= p0 <= p_max, tol > 0, r >= 1");
+    *out = nullptr;
+    int p = p0;
+    for (;;) {
+        pr_coarse G = nullptr;
+        pr_status st = pr_build_coarse(h, N_total, first_interval, n_local, m, k, p, seed, opts, comm, stream, &G);
+        if (st != PR_OK) return st;
+        std::vector<double> est(G->nloc);
+        st = pr_coarse_estimate(G, h, r, seed, est.data(), stream);
+        if (st != PR_OK) { pr_coarse_destroy(G); return st; }
+        double mx = 0.0;
+        for (double e : est) mx = std::max(mx, e);
+        if (comm) {                      // the same decision on every rank
+            cudaStream_t s = (cudaStream_t)stream;
+            Scratch Sd(s);
+            double *dg = Sd.get<double>(1);
+            if (!dg) { pr_coarse_destroy(G); set_error("out of device memory"); return PR_EOOM; }
+            cudaError_t e = cudaMemcpyAsync(dg, &mx, sizeof(double), cudaMemcpyHostToDevice, s);
+            if (e == cudaSuccess) st = comm_of(comm)->all_reduce_max(dg, 1, s);
+            if (e == cudaSuccess && st == PR_OK) e = cudaMemcpyAsync(&mx, dg, sizeof(double), cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) { pr_coarse_destroy(G); return cuda_fail(e, "adaptive p reduction"); }
+            if (st != PR_OK) { pr_coarse_destroy(G); return st; }
+        }
+        if (mx <= tol || p >= p_max) {
+            *out = G;
+            *p_used = p;
+            return PR_OK;
+        }
+        pr_coarse_destroy(G);
+        p = std::min(2 * p, p_max);
+    }
+}
+
 pr_status pr_coarse_info(pr_coarse G, int *k, int *l, int *n_local, int *first_interval, int *m,
                          double *delta, double *eps, double *sigma_host, int *qr_passes)
 {
@@ -1047,21 +1104,13 @@ pr_status pr_coarse_factors(pr_coarse G, const double **U, const double **V, con
     return PR_OK;
 }
 
-pr_status pr_coarse_apply(pr_coarse G, int q_local, int nvec, const double *X, long ldx, double *Y,
-                          long ldy, void *stream)
+// Y = G_q' X for nvec vectors with general strides (the body of pr_coarse_apply)
+static pr_status coarse_apply(pr_coarse G, int q_local, int nvec, const double *X, Lay Lx, double *Y, Lay Ly,
+                              cudaStream_t s)
 {
-    PR_REQUIRE(G && X && Y, PR_EINVAL, "NULL argument");
-    PR_REQUIRE(q_local >= 0 && q_local < G->nloc && nvec >= 1 && nvec <= 128, PR_EINVAL,
-               "bad interval or nvec (1..128)");
     const long rows = G->rows;
     const int k = G->k;
-    long minld = (G->dim == 1) ? nvec : rows;
-    PR_REQUIRE(ldx >= minld && ldy >= minld, PR_EDIM, "leading dimension too small");
-    cudaStream_t s = (cudaStream_t)stream;
-    G->stream = s;
     Scratch S(s);
-    Lay Lx = (G->dim == 1) ? Lay{ldx, 1} : Lay{1, ldx};
-    Lay Ly = (G->dim == 1) ? Lay{ldy, 1} : Lay{1, ldy};
     int nchunk = xty_chunks(rows, 1);
     long cr = (rows + nchunk - 1) / nchunk;
     double *part, *ev;
@@ -1074,6 +1123,73 @@ pr_status pr_coarse_apply(pr_coarse G, int q_local, int nvec, const double *X, l
     PR_CUDA(launch_reduce_parts(part, 1, nchunk, k, nvec, G->sigma + (long)q_local * G->l, 0, ev, s));
     Expand ex{Y, Ly.rs, Ly.vs, nullptr, 0, 0, Uq, 0, ev, k, nvec, 1, rows, nchunk, cr, nullptr};
     PR_CUDA(launch_expand(ex, s));
+    return PR_OK;
+}
+
+pr_status pr_coarse_apply(pr_coarse G, int q_local, int nvec, const double *X, long ldx, double *Y,
+                          long ldy, void *stream)
+{
+    PR_REQUIRE(G && X && Y, PR_EINVAL, "NULL argument");
+    PR_REQUIRE(q_local >= 0 && q_local < G->nloc && nvec >= 1 && nvec <= 128, PR_EINVAL,
+               "bad interval or nvec (1..128)");
+    const long rows = G->rows;
+    long minld = (G->dim == 1) ? nvec : rows;
+    PR_REQUIRE(ldx >= minld && ldy >= minld, PR_EDIM, "leading dimension too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    G->stream = s;
+    Lay Lx = (G->dim == 1) ? Lay{ldx, 1} : Lay{1, ldx};
+    Lay Ly = (G->dim == 1) ? Lay{ldy, 1} : Lay{1, ldy};
+    return coarse_apply(G, q_local, nvec, X, Lx, Y, Ly, s);
+}
+
+pr_status pr_coarse_estimate(pr_coarse G, pr_op h, int r, uint64_t seed, double *est_host, void *stream)
+{
+    PR_REQUIRE(G && h && est_host, PR_EINVAL, "NULL argument");
+    const Op &op = h->op;
+    PR_REQUIRE(G->rows == op.rows && G->dim == op.dim, PR_EDIM, "coarse handle / operator mismatch");
+    PR_REQUIRE(r >= 1 && r <= 64, PR_EINVAL, "r must be 1..64");
+    cudaStream_t s = (cudaStream_t)stream;
+    G->stream = s;
+    Scratch S(s);
+    const int nq = G->nloc, q0 = G->first;
+    const long rows = op.rows;
+    const long B = (long)nq * r;
+    const long ld = (op.dim == 1) ? ((B + 1) & ~1L) : rows;
+    Lay L = lay(op, ld);
+    const size_t arr = (op.dim == 1) ? (size_t)rows * ld : (size_t)B * ld;
+    double *Om, *Y, *Z, *npart, *nrm;
+    PR_ALLOC(Om, double, arr, S);
+    PR_ALLOC(Y, double, arr, S);
+    PR_ALLOC(Z, double, arr, S);
+    const int nchunk = xty_chunks(rows, nq);
+    const long cr = (rows + nchunk - 1) / nchunk;
+    PR_ALLOC(npart, double, (size_t)B * nchunk, S);
+    PR_ALLOC(nrm, double, (size_t)B, S);
+    if (op.dim == 2) PR_CUDA(cudaMemsetAsync(Om, 0, arr * sizeof(double), s));
+    // fresh Gaussian probes (Philox counter word 3 = 3), F' and G' applied to them
+    PR_CUDA(launch_sketch(op.dim, op.n, rows, q0, nq, r, seed, Om, L.rs, L.vs, s, 0.0, 3ULL));
+    pr_status st = propagate(op, PR_LINEAR, q0, G->m, (int)B, r, nullptr, Om, ld, Y, ld, nullptr, 0, 0, 0, s);
+    if (st != PR_OK) return st;
+    for (int q = 0; q < nq; ++q) {
+        const long off = (long)q * r * L.vs;
+        if ((st = coarse_apply(G, q, r, Om + off, L, Z + off, L, s)) != PR_OK) return st;
+    }
+    note_launch();
+    k_vdiff<<<(unsigned)((rows * B + 255) / 256), 256, 0, s>>>(Y, Z, L.rs, L.vs, rows, (int)B, Y);
+    PR_CHECK_LAUNCH("k_vdiff");
+    PR_CUDA(launch_vecnorm_parts(Y, L.rs, L.vs, rows, (int)B, nchunk, cr, npart, s));
+    PR_CUDA(launch_norm_finish(npart, (int)B, nchunk, nrm, s));
+    std::vector<double> h_n(B);
+    PR_CUDA(cudaMemcpyAsync(h_n.data(), nrm, B * sizeof(double), cudaMemcpyDeviceToHost, s));
+    PR_CUDA(cudaStreamSynchronize(s));
+    // Halko, Martinsson & Tropp, Lemma 4.1: ||B|| <= 10 sqrt(2/pi) max_i ||B omega_i||
+    // with probability >= 1 - 10^{-r}
+    const double c = 10.0 * sqrt(2.0 / M_PI);
+    for (int q = 0; q < nq; ++q) {
+        double mx = 0.0;
+        for (int i = 0; i < r; ++i) mx = std::max(mx, h_n[(size_t)q * r + i]);
+        est_host[q] = c * mx;
+    }
     return PR_OK;
 }
 
@@ -1551,23 +1667,6 @@ pr_status pr_bounds(double delta, double eps, int N, int K, const double *bnorm,
 // (the sequential fine reference, the max-over-time error
 // of the paper's figures, the estimator efficiency eta^k, and the classical
 // Parareal baselines G = 0 and G = one coarse backward-Euler step.)
-
-// out = x - y (op-layout vector blocks)
-__global__ void k_vdiff(const double *x, const double *y, long rs, long vs, long rows, int nvec, double *out)
-{
-    const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= rows * nvec) return;
-    const long v = idx % nvec, i = idx / nvec;
-    const long o = i * rs + v * vs;
-    out[o] = x[o] - y[o];
-}
-
-// mx[c] = max(mx[c], nrm[c]) for c < cnt (c >= lo only)
-__global__ void k_runmax(double *mx, const double *nrm, int lo, int cnt)
-{
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c < cnt && c >= lo) mx[c] = fmax(mx[c], nrm[c]);
-}
 
 pr_status pr_sequential(pr_op h, int nsrc, const double *u0, long ld_u0, const pr_source *f, int N, int m,
                         double *U_out, long ld_out, void *stream)

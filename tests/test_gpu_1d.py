@@ -341,3 +341,30 @@ def test_part_stepper_bitwise_repeatable(name, B, env, monkeypatch):
         if env:
             monkeypatch.delenv(env)
         lib().pr_reload_env()
+
+
+def test_coarse_estimate_and_adaptive_p_match_oracle():
+    """pr_coarse_estimate against the oracle's estimator on every interval, and
+    pr_build_coarse_adaptive stopping at the p the estimates prescribe."""
+    from paper_2508_08873_b200 import Coarse
+    from oracle.rsvd import coarse_error_estimate
+    cfg = get("T1")
+    op = gpu_op(cfg)
+    op_o = make_op(cfg)
+    ests = {}
+    for p in (1, 2, 4):
+        Gg = Coarse.build(op, cfg.N, cfg.m, cfg.k, p, cfg.seed_omega)
+        est = Gg.estimate(op, 10, cfg.seed_omega)
+        ref = []
+        for q in range(cfg.N):
+            tr = rsvd_interval(op_o, q + 1, cfg.k, p, cfg.seed_omega)
+            ref.append(coarse_error_estimate(op_o, tr, q + 1, 10, cfg.seed_omega))
+            # probes have norm ~ sqrt(n); the estimate is a norm of F'w - G'w
+            assert abs(est[q] - ref[-1]) <= TAU_1D * tr.sigma[0] * 20 * np.sqrt(cfg.n), (p, q)
+        ests[p] = max(ref)
+    # a tolerance between the p = 2 and the p = 1 estimates: doubling stops at p = 2
+    if ests[2] < ests[1]:
+        tol = np.sqrt(ests[1] * ests[2])
+        Ga, pu = Coarse.build_adaptive(op, cfg.N, cfg.m, cfg.k, 1, 8, tol, cfg.seed_omega, r=10)
+        assert pu == 2
+        assert Ga.info()["l"] == cfg.k + 2

@@ -58,3 +58,26 @@ def test_independent_adjoint_on_heat_matches_closed_form():
     lam = 4.0 / h ** 2 * np.sin(np.arange(1, cfg.n + 1) * np.pi * h / 2) ** 2
     exact = np.sort((1.0 + cfg.dt * lam) ** (-cfg.m))[::-1]
     np.testing.assert_allclose(tr.sigma[:cfg.k], exact[:cfg.k], rtol=0, atol=1e-12 * exact[0])
+
+
+def test_coarse_error_estimate_brackets_the_true_error():
+    """Halko-Martinsson-Tropp Lemma 4.1 estimator (adaptive p):
+    the true ||F' - G'|| (dense F', tiny grid) lies below the estimate (r = 10,
+    failure probability 1e-10), and the estimate is below 10 sqrt(2/pi) times
+    the true norm times the largest probe norm (Cauchy-Schwarz)."""
+    import numpy as np
+    from oracle.fine import make_op
+    from oracle.rng import gaussian_sketch
+    from oracle.rsvd import coarse_error_estimate, dense_transfer, rsvd_interval
+    from workloads.configs import get
+    cfg = get("T1")
+    op = make_op(cfg)
+    for q in (1, 4):
+        F = dense_transfer(op, q)
+        for k, p in ((2, 1), (3, 2)):
+            t = rsvd_interval(op, q, k, p, cfg.seed_omega)
+            G = t.U @ np.diag(t.sigma[:k]) @ t.V.T
+            true = np.linalg.norm(F - G, 2)
+            est = coarse_error_estimate(op, t, q, 10, cfg.seed_omega)
+            om = gaussian_sketch(cfg.seed_omega, q - 1, cfg.n, 10, stream=3)
+            assert true <= est <= 10 * np.sqrt(2 / np.pi) * true * np.max(np.linalg.norm(om, axis=0)) * (1 + 1e-12)
