@@ -124,7 +124,18 @@ class Workload:
         self.q0, self.nq = _shard(cfg.N, rank, world)
         self.s0, self.ns = 0, cfg.nsrc
         u0 = G.initial_value(cfg)
-        if cfg.dim == 1:
+        if cfg.dim == 1 and cfg.problem.startswith("exp2"):
+            # the time-dependent pencil of Exp 2
+            from workloads import exp2
+            L, rs, M = exp2.step_matrices(cfg.problem, cfg.n, cfg.T, cfg.N * cfg.m)
+            self.host = dict(pencil=(L, rs, M))
+            space, time_, amp = G.source_1d(cfg)
+            self.host.update(space=space, time=time_, amp=amp[self.s0:self.s0 + self.ns])
+            self.host["u0"] = np.ascontiguousarray(np.stack([u0] * self.ns).T)
+            self.op = Operator.pencil(*L, cfg.dt, lrowsum=rs, mass=M)
+            self.src = SourceTerm.sep1d(space, time_, self.host["amp"])
+            self.U = torch.empty((cfg.n, (self.nq + 1) * self.ns), dtype=torch.float64, device=dev)
+        elif cfg.dim == 1:
             self.host = dict(op=G.operator_1d(cfg), sums=G.operator_1d_sums(cfg))
             space, time_, amp = G.source_1d(cfg)
             self.host.update(space=space, time=time_, amp=amp[self.s0:self.s0 + self.ns])
@@ -379,6 +390,22 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # memory plan: the coarse factors U, V of a
+    # rank's intervals plus the Parareal state arrays must fit in HBM; C5 (205 GB
+    # of factors) does not fit one B200 -- say so instead of failing inside libpr
+    q0_, nq_ = _shard(cfg.N, rank, world)
+    rows = cfg.n if cfg.dim == 1 else (cfg.n + 1) ** 2
+    need = (2.0 * nq_ * rows * cfg.k + 4.0 * (nq_ + 1) * rows * max(cfg.nsrc, 1)) * 8
+    free = torch.cuda.mem_get_info(dev)[0]
+    if need > 0.95 * free:
+        if rank == 0:
+            per = 2.0 * cfg.N * rows * cfg.k * 8
+            print(json.dumps({"metric": METRIC, "unit": "DOF-steps/s", "n_gpus": world, "config": config,
+                              "unavailable": "%s needs %.1f GB of coarse factors + state on each of %d GPU(s) "
+                                             "(%.1f GB free); run with --gpus >= %d"
+                                             % (cfg.name, need / 1e9, world, free / 1e9,
+                                                int(np.ceil(per / (0.8 * free))))}), flush=True)
+        return
     wl = Workload(cfg, rank, world, dev)
     peaks = _fp64_peaks(dev)
     sampler = ClockSampler(local_rank)
@@ -478,7 +505,17 @@ def _timed(wl, steps, warmup, barrier, world, dev, peaks):
     st_ms = ctr["stepper_ms"] / max(ctr["stepper_launches"], 1)
     st_dof = ctr["stepper_dof_steps"] / max(ctr["stepper_launches"], 1)
     st_fl = ctr["stepper_flops"] / max(ctr["stepper_launches"], 1)
-    if cfg.dim == 1 and st_fl > 0:
+    if cfg.dim == 1 and cfg.problem.startswith("exp2"):
+        # K1T (time-dependent pencil): two streaming passes per step over the
+        # state (down: read + write, up: read + write): 32 B per DOF-step of HBM
+        peak, peak_kind = _peaks()
+        achieved = 32.0 * st_dof / (st_ms / 1e3) / 1e9 if st_ms > 0 else None
+        roofline = {"kernel": "k_pencil_cta / k_pencil_step (K1T, time-dependent pencil; 32 B per DOF-step of per-step factors)", "bound": "hbm",
+                    "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": (achieved / peak) if achieved else None,
+                    "traffic": None, "algorithmic_bytes_per_launch": 32.0 * st_dof,
+                    "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
+    elif cfg.dim == 1 and st_fl > 0:
         # K1P: the state stays on chip for all m steps, so HBM carries only the
         # input and output (16 B per DOF per launch); the bound is the FP64
         # pipe: 5 algorithmic flops per DOF-step (+2R with an R-term source)
@@ -536,13 +573,23 @@ def _e2e(wl, steps, barrier, world):
     keys = ("space", "time", "amp", "u0") if c.dim == 1 else ("gx", "gy", "u0")
     pin = {k: torch.from_numpy(np.ascontiguousarray(wl.host[k])).pin_memory() for k in keys}
     out_host = torch.empty(tuple(wl.U.shape), dtype=torch.float64).pin_memory()
-    h2d = sum(t.numel() * 8 for t in pin.values()) + (5 * c.n * 8 if c.dim == 1 else 0)
+    pencil = "pencil" in wl.host
+    if pencil:
+        L_, rs_, M_ = wl.host["pencil"]
+        h2d_op = sum(a.size for a in L_) * 8 + rs_.size * 8 + (3 * c.n * 8 if M_ is not None else 0)
+    else:
+        h2d_op = 5 * c.n * 8 if c.dim == 1 else 0
+    h2d = sum(t.numel() * 8 for t in pin.values()) + h2d_op
     d2h = out_host.numel() * 8
     barrier()
     e0 = _event()
     for _ in range(steps):
         dv = {k: v.to(wl.dev, non_blocking=True) for k, v in pin.items()}
-        if c.dim == 1:
+        if pencil:
+            op = Operator.pencil(*L_, c.dt, lrowsum=rs_, mass=M_)                   # host arrays
+            src = SourceTerm(1, dv["time"].shape[0], dv["amp"].shape[0], dv["time"].shape[1],
+                             {"space": dv["space"], "time": dv["time"], "amp": dv["amp"]})
+        elif c.dim == 1:
             rs, cs = wl.host["sums"]
             op = Operator.tridiag(*wl.host["op"], c.dt, rowsum=rs, colsum=cs)      # host arrays
             src = SourceTerm(1, dv["time"].shape[0], dv["amp"].shape[0], dv["time"].shape[1],

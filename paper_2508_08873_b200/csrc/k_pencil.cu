@@ -215,6 +215,210 @@ cudaError_t launch_bidiag(int mode, int n, const double *cdiag, const double *cs
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// K1T-CTA: one thread block per vector for SMALL batches (the Parareal fine
+// solves have one vector per interval and source).  The T threads of the block
+// own RR consecutive rows each; the state stays in shared memory (row t*RR + i
+// at xs[i*T + t], conflict-free) for all m steps.  Each step's two sweeps are
+// first-order linear recurrences, y_i = a_i y_{i-1} + b_i, solved exactly by a
+// block scan of the affine maps (a, b) of the thread segments: a local pass
+// composes the segment map, a warp-shuffle + shared-memory scan gives every
+// segment its carried-in value, a second local pass runs the recurrence from
+// it (the same pivots and multipliers as the thread-per-vector kernel; all
+// terms non-negative for an M-matrix, so no cancellation).
+struct Aff {
+    double A, B;                       // y -> A y + B
+};
+
+// inclusive scan over the block in thread order (REV: descending thread order)
+// of maps composed as later o earlier; returns the EXCLUSIVE prefix applied to 0
+template <int T, bool REV>
+__device__ __forceinline__ double block_affine_carry(Aff f, Aff *sh)
+{
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    constexpr int NW = T / 32;
+    const int rl = REV ? 31 - lane : lane;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const double pA = REV ? __shfl_down_sync(0xffffffffu, f.A, d) : __shfl_up_sync(0xffffffffu, f.A, d);
+        const double pB = REV ? __shfl_down_sync(0xffffffffu, f.B, d) : __shfl_up_sync(0xffffffffu, f.B, d);
+        if (rl >= d) f = Aff{f.A * pA, fma(f.A, pB, f.B)};
+    }
+    // warp totals (the last lane in scan order holds it)
+    if (rl == 31) sh[w] = f;
+    __syncthreads();
+    if (t < 32) {
+        const int rw = REV ? NW - 1 - t : t;          // warp index in scan order
+        Aff g = (t < NW) ? sh[rw] : Aff{1.0, 0.0};
+#pragma unroll
+        for (int d = 1; d < NW; d <<= 1) {
+            const double pA = __shfl_up_sync(0xffffffffu, g.A, d);
+            const double pB = __shfl_up_sync(0xffffffffu, g.B, d);
+            if (t >= d && t < NW) g = Aff{g.A * pA, fma(g.A, pB, g.B)};
+        }
+        if (t < NW) sh[NW + t] = g;                    // inclusive prefix at scan position t
+    }
+    __syncthreads();
+    // exclusive prefix of this thread: own warp's inclusive up to the previous
+    // lane, composed after the preceding warps' total
+    const double eA = REV ? __shfl_down_sync(0xffffffffu, f.A, 1) : __shfl_up_sync(0xffffffffu, f.A, 1);
+    const double eB = REV ? __shfl_down_sync(0xffffffffu, f.B, 1) : __shfl_up_sync(0xffffffffu, f.B, 1);
+    const int rw = REV ? NW - 1 - w : w;
+    const bool firstw = (rw == 0);
+    const double carryw = firstw ? 0.0 : sh[NW + rw - 1].B;   // value entering this warp (scan position rw)
+    double c;
+    if (rl == 0) c = carryw;
+    else c = fma(eA, carryw, eB);
+    __syncthreads();                                    // sh reused by the next scan
+    return c;
+}
+
+template <int MODE, int RR>            // MODE: 0 linear, 1 affine, 2 adjoint
+__global__ void __launch_bounds__(256) k_pencil_cta(PencilArgs a)
+{
+    constexpr int T = 256;
+    extern __shared__ __align__(16) double xs[];       // [RR][T]
+    __shared__ Aff sh[2 * (T / 32)];
+    const long v = blockIdx.x;
+    const int t = threadIdx.x;
+    const int n = a.n;
+    const int q = a.q0 + (int)(v / a.vpi);
+    const bool hasM = a.mdiag != nullptr;
+    auto row_of = [&](int i) { return t * RR + i; };
+    auto X = [&](int row) -> double {                  // state at a row (0 outside)
+        if (row < 0 || row >= n) return 0.0;
+        return xs[(row % RR) * T + row / RR];
+    };
+    for (int i = 0; i < RR; ++i) {
+        const int row = row_of(i);
+        xs[i * T + t] = (a.in && row < n) ? a.in[(long)row * a.ld_in + v] : 0.0;
+    }
+    __syncthreads();
+    double al[8];
+    for (int s = 0; s < a.m; ++s) {
+        const int j = (MODE == 2) ? a.m - s : s + 1;
+        const long g = (long)q * a.mstride + a.step0 + j;
+        const Coef *F = a.fac + (g - 1) * n;
+        if (MODE == 1) {
+            const int src = (int)(v % a.nsrc);
+            for (int r = 0; r < 8; ++r) al[r] = 0.0;
+            for (int r = 0; r < a.R && r < 8; ++r)
+                al[r] = a.dt * a.amp[(long)src * a.R + r] * a.time[(long)r * a.nsteps + g - 1];
+        }
+        // right-hand sides r_i (M x + dt f, or M^T z after the first adjoint step)
+        double rv[RR], av[RR];
+#pragma unroll
+        for (int i = 0; i < RR; ++i) {
+            const int row = row_of(i);
+            double r = 0.0;
+            if (row < n) {
+                const double x0 = X(row);
+                if (MODE == 2) {
+                    r = (hasM && s > 0) ? fma(a.mdiag[row], x0, (row > 0 ? a.msup[row - 1] * X(row - 1) : 0.0) +
+                                                                    (row + 1 < n ? a.msub[row + 1] * X(row + 1) : 0.0))
+                                        : x0;
+                } else {
+                    r = hasM ? fma(a.mdiag[row], x0, (row > 0 ? a.msub[row] * X(row - 1) : 0.0) +
+                                                         (row + 1 < n ? a.msup[row] * X(row + 1) : 0.0))
+                             : x0;
+                    if (MODE == 1) {
+                        double f = 0.0;
+                        for (int k = 0; k < a.R && k < 8; ++k) f = fma(al[k], a.spaceT[(long)row * a.rs + k], f);
+                        r += f;
+                    }
+                }
+            }
+            rv[i] = r;
+        }
+        __syncthreads();                                // everyone read xs
+        // down sweep: y_i = a_i y_{i-1} + b_i
+        Aff f{1.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < RR; ++i) {
+            const int row = row_of(i);
+            double ai = 0.0, bi = 0.0;
+            if (row < n) {
+                if (MODE == 2) {
+                    ai = (row > 0) ? -F[row - 1].c : 0.0;          // v_i = r_i - cp_{i-1} v_{i-1}
+                    bi = rv[i];
+                } else {
+                    const Coef c = F[row];
+                    ai = -c.b;                                    // y_i = w_i r_i - ga_i y_{i-1}
+                    bi = c.a * rv[i];
+                }
+            }
+            av[i] = ai;
+            rv[i] = bi;
+            f = Aff{ai * f.A, fma(ai, f.B, bi)};
+        }
+        double y = block_affine_carry<T, false>(f, sh);
+#pragma unroll
+        for (int i = 0; i < RR; ++i) {
+            y = fma(av[i], y, rv[i]);
+            rv[i] = y;
+        }
+        // up sweep: x_i = c_i x_{i+1} + e_i (rows descending)
+        Aff gb{1.0, 0.0};
+#pragma unroll
+        for (int i = RR - 1; i >= 0; --i) {
+            const int row = row_of(i);
+            double ci = 0.0, ei = 0.0;
+            if (row < n) {
+                const Coef c = F[row];
+                if (MODE == 2) {
+                    ci = -c.d;                                    // z_i = w_i v_i - gt_i z_{i+1}
+                    ei = c.a * rv[i];
+                } else {
+                    ci = -c.c;                                    // x_i = y_i - cp_i x_{i+1}
+                    ei = rv[i];
+                }
+            }
+            av[i] = ci;
+            rv[i] = ei;
+            gb = Aff{ci * gb.A, fma(ci, gb.B, ei)};
+        }
+        double x = block_affine_carry<T, true>(gb, sh);
+#pragma unroll
+        for (int i = RR - 1; i >= 0; --i) {
+            x = fma(av[i], x, rv[i]);
+            xs[i * T + t] = x;
+        }
+        __syncthreads();
+    }
+    // output (adjoint: the last factor M^T first)
+    double outv[RR];
+#pragma unroll
+    for (int i = 0; i < RR; ++i) {
+        const int row = row_of(i);
+        double x = (row < n) ? X(row) : 0.0;
+        if (MODE == 2 && hasM && a.m > 0 && row < n)
+            x = fma(a.mdiag[row], x, (row > 0 ? a.msup[row - 1] * X(row - 1) : 0.0) +
+                                         (row + 1 < n ? a.msub[row + 1] * X(row + 1) : 0.0));
+        outv[i] = x;
+    }
+#pragma unroll
+    for (int i = 0; i < RR; ++i) {
+        const int row = row_of(i);
+        if (row < n) {
+            double x = outv[i];
+            if (a.off) x += a.off[(long)row * a.ld_off + v];
+            a.out[(long)row * a.ld_out + v] = x;
+        }
+    }
+}
+
+template <int MODE>
+static cudaError_t launch_cta_mode(const PencilArgs &a, cudaStream_t s)
+{
+    const int n = a.n;
+    const unsigned blocks = (unsigned)a.B;
+    if (n <= 256 * 2) { k_pencil_cta<MODE, 2><<<blocks, 256, 2 * 256 * 8, s>>>(a); return cudaGetLastError(); }
+    if (n <= 256 * 4) { k_pencil_cta<MODE, 4><<<blocks, 256, 4 * 256 * 8, s>>>(a); return cudaGetLastError(); }
+    if (n <= 256 * 8) { k_pencil_cta<MODE, 8><<<blocks, 256, 8 * 256 * 8, s>>>(a); return cudaGetLastError(); }
+    if (n <= 256 * 16) { k_pencil_cta<MODE, 16><<<blocks, 256, 16 * 256 * 8, s>>>(a); return cudaGetLastError(); }
+    return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_pencil_factor(int n, int nsteps, const double *lsub, const double *ldiag,
                                  const double *lsup, const double *lrs, Coef *fac, int *bad,
                                  cudaStream_t s)
@@ -243,9 +447,18 @@ cudaError_t launch_stepper_pencil(const Op &op, int mode, const StepArgs &sa, cu
     const bool prof = profiling();
     if (prof) stepper_timed_begin(s);
     note_launch();
-    if (mode == PR_ADJOINT) k_pencil_step<2><<<blocks, threads, 0, s>>>(a);
+    // a block per vector while the batch leaves the thread-per-vector kernel
+    // with fewer than ~4 resident warps per SM (and n fits the block's rows)
+    const bool cta = sa.n >= 256 && sa.n <= 256 * 16 && sa.B <= 4L * num_sms() * 32 && !flags().no_part;
+    cudaError_t e = cudaSuccess;
+    if (cta) {
+        if (mode == PR_ADJOINT) e = launch_cta_mode<2>(a, s);
+        else if (sa.R > 0) e = launch_cta_mode<1>(a, s);
+        else e = launch_cta_mode<0>(a, s);
+    } else if (mode == PR_ADJOINT) k_pencil_step<2><<<blocks, threads, 0, s>>>(a);
     else if (sa.R > 0) k_pencil_step<1><<<blocks, threads, 0, s>>>(a);
     else k_pencil_step<0><<<blocks, threads, 0, s>>>(a);
+    if (e != cudaSuccess) return e;
     if (prof) {
         const double dof = (double)sa.n * (double)sa.B * (double)sa.m;
         stepper_timed_end(s, dof, (5.0 + (op.pen_m ? 5.0 : 0.0) + 2.0 * sa.R) * dof);
