@@ -358,6 +358,7 @@ struct PartArgs {
     const double *time;
     const double *amp;
     int nsteps, nsrc, q0, vpi;
+    long groups;                       // vector groups (VPG vectors each) over the persistent clusters
     double dt;
     unsigned long long *prof;          // dev aid (PR_PART_PROF): per-phase clock sums, or null
     unsigned idle_ns;                  // interface-warp poll back-off
@@ -371,12 +372,33 @@ constexpr int PART_RSM = 8;            // shared-memory stride of the source row
 // (double2) | interface data | per chunk: {w, -ga, V2, W2} [L] | -cp [L] | {V, W} [L] |
 // source rows [L][8] (AFF) | cluster addresses [2][CL] (u32) | local solution [2][2K][32]
 // (vector slots: 32 = the largest group, VPG <= 32)
+// | staged input of the next group [K*L][VPG] (when it fits; not AFF: the
+// offsets launch has no input and its source rows take the space)
 template <int CL, int W, int H, int L, int VPT, bool AFF>
-constexpr size_t part_smem_t()
+__host__ __device__ constexpr size_t part_smem_base()
 {
     constexpr int K = W * H;
     return (6 + (size_t)4 * CL * 32 + (size_t)4 * K * 32 + 4 * 32 + PART_CTAD +
             (size_t)K * (L * (4 + (AFF ? PART_RSM : 0)) + 4) + CL + (size_t)4 * K * 32 + 4 * 32) * sizeof(double);
+}
+
+template <int CL, int W, int H, int L, int VPT, bool AFF>
+__host__ __device__ constexpr size_t part_stage_bytes()
+{
+    return (size_t)W * H * L * (32 / H) * VPT * sizeof(double);
+}
+
+template <int CL, int W, int H, int L, int VPT, bool AFF>
+__host__ __device__ constexpr bool part_stage()
+{
+    return !AFF && part_smem_base<CL, W, H, L, VPT, AFF>() + part_stage_bytes<CL, W, H, L, VPT, AFF>() <= 227 * 1024;
+}
+
+template <int CL, int W, int H, int L, int VPT, bool AFF>
+constexpr size_t part_smem_t()
+{
+    return part_smem_base<CL, W, H, L, VPT, AFF>() +
+           (part_stage<CL, W, H, L, VPT, AFF>() ? part_stage_bytes<CL, W, H, L, VPT, AFF>() : 0);
 }
 
 __device__ __forceinline__ unsigned smem_u32(const void *p)
@@ -636,7 +658,7 @@ __device__ __forceinline__ void half_dots(int hf, const double2 *__restrict__ g,
 // step of parity p written), cbar[p] (publish + gather arrive: interface
 // values of a step of parity p written); gbar[p] counts the gather bytes.
 template <int CL, int W, int H, int L, int VPT, bool AFF>
-__global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
+__global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W + 2))) / 8 * 8 > 255 ? 255 : (65536 / (32 * (W + 2))) / 8 * 8) k_part_step(PartArgs a)
 {
     constexpr int LPC = 32 / H;          // lanes per chunk
     constexpr int VPG = LPC * VPT;       // vectors per cluster group
@@ -646,11 +668,15 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
     constexpr int M = 2 * K;             // local interface unknowns
     constexpr bool SPLIT = K >= 16;      // split band solve (two halves)
     constexpr int RSM = AFF ? PART_RSM : 0;
+    constexpr bool STAGE = part_stage<CL, W, H, L, VPT, AFF>();   // next group's input prefetched into shared memory
     extern __shared__ __align__(16) double sm[];
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.block_rank();
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long gbase = (long)(blockIdx.x / CL) * VPG;                // first vector of the group
+    // persistent clusters: cluster cid runs the vector groups cid, cid + ncl, ...
+    // (its CTAs keep their coefficients in shared memory across groups)
+    const long cid = (long)(blockIdx.x / CL), ncl = (long)(gridDim.x / CL);
+    const long ngrp = (cid < a.groups) ? (a.groups - 1 - cid) / ncl + 1 : 0;
     unsigned long long *bar = reinterpret_cast<unsigned long long *>(sm);   // gbar[2] ebar[2] cbar[2]
     double2 *gth = reinterpret_cast<double2 *>(sm + 6);              // [2][CL][32]
     double2 *rawE = gth + 2 * CL * 32;                               // [2][K][32]
@@ -663,6 +689,7 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
     unsigned *rmap = reinterpret_cast<unsigned *>(regions + (size_t)K * RSTR);  // [2][CL]
     double *zs = reinterpret_cast<double *>(rmap + 2 * CL);                     // [2][M][32]
     double2 *zfx = reinterpret_cast<double2 *>(zs + 2 * M * 32);                // [2][32]
+    double *stg = reinterpret_cast<double *>(zfx + 2 * 32);                     // [K*L][VPG] (STAGE)
     // chunk region: {V2~, W2~} [L] (double2) | nl [L] | w [L] | scaled source rows [L][RSM]
     auto cd_of = [&](int u) { return reinterpret_cast<double2 *>(regions + (size_t)u * RSTR); };
     const unsigned bar0 = smem_u32(bar), gth0 = smem_u32(gth);
@@ -718,39 +745,34 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
         const double *sp = wv + L;
         const double *rowc_u = a.rowc + (size_t)c * L * PART_ROWC;     // this chunk's rows (global)
         const double dbot = rowc_u[(L - 1) * PART_ROWC + 6];            // d_{L-1} (d_0 = 1)
-        long vv[VPT];
-        bool valid[VPT];
-#pragma unroll
-        for (int t = 0; t < VPT; ++t) {
-            vv[t] = gbase + li + t * LPC;
-            valid[t] = vv[t] < a.B;
-        }
-        // the state in the chunk's scaled coordinates x~ = x / d.  Loads are
-        // issued unconditionally from clamped addresses (no per-row branch, so
-        // all rows are in flight together) and masked afterwards.
-        double S[VPT][L];
-        {
-            long vc[VPT];
-#pragma unroll
-            for (int t = 0; t < VPT; ++t) vc[t] = valid[t] ? vv[t] : 0;
-            if (a.in) {
-#pragma unroll
-                for (int i = 0; i < L; ++i) {
-                    const int row = (s0 + i < a.n) ? s0 + i : a.n - 1;
-                    const double dinv = (s0 + i < a.n) ? rowc_u[i * PART_ROWC + 7] : 0.0;
-#pragma unroll
-                    for (int t = 0; t < VPT; ++t) {
-                        const double v = __ldg(a.in + (long)row * a.ld_in + vc[t]);
-                        S[t][i] = valid[t] ? v * dinv : 0.0;
-                    }
+        // staged input of a group: this warp's H chunks, [H*L rows][VPG vectors]
+        double *stw = stg + (size_t)w * H * L * VPG;
+        // asynchronous copy of group grp's input rows into the staging buffer
+        // (pairs of vectors by 16-byte cp.async where aligned and both valid,
+        // else 8-byte copies; rows >= n and vectors >= B are zero-filled)
+        auto prefetch = [&](long grp) {
+            const long gb = grp * VPG;
+            const bool al16 = ((a.ld_in & 1) == 0) && ((reinterpret_cast<size_t>(a.in) & 15) == 0);
+#pragma unroll 4
+            for (int e = lane; e < H * L * VPG / 2; e += 32) {
+                const int r = e / (VPG / 2), vp = 2 * (e % (VPG / 2));
+                const int grow = (w * H) * L + r + C * K * L;            // row of the vector
+                const bool rok = grow < a.n;
+                const long v0 = gb + vp;
+                const double *src = a.in + (long)(rok ? grow : 0) * a.ld_in;
+                const unsigned dst = smem_u32(stw + (size_t)r * VPG + vp);
+                if (al16 && rok && v0 + 1 < a.B) {
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src + v0) : "memory");
+                } else {
+                    const int n0 = (rok && v0 < a.B) ? 8 : 0, n1 = (rok && v0 + 1 < a.B) ? 8 : 0;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;"
+                                 :: "r"(dst), "l"(src + (n0 ? v0 : 0)), "r"(n0) : "memory");
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;"
+                                 :: "r"(dst + 8), "l"(src + (n1 ? v0 + 1 : 0)), "r"(n1) : "memory");
                 }
-            } else {
-#pragma unroll
-                for (int i = 0; i < L; ++i)
-#pragma unroll
-                    for (int t = 0; t < VPT; ++t) S[t][i] = 0.0;
             }
-        }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
         // (b_{c-1}, t_{c+1}) of a step from the CTA's (B_{C-1}, T_{C+1}), this
         // chunk's super-spike entries and the local solution z.  Split solve:
         // the first half's z still lacks x_K BR + x_{K+1} BT, applied here.
@@ -772,124 +794,204 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
             t = (u == K - 1) ? bt.y
                              : fma(ctad[CTAD_A + 2 * u + 2], bt.x, fma(ctad[CTAD_B + 2 * u + 2], bt.y, zval(2 * u + 2)));
         };
-        cluster.sync();
-        int q[VPT], src[VPT];
-#pragma unroll
-        for (int t = 0; t < VPT; ++t) {
-            q[t] = valid[t] ? a.q0 + (int)(vv[t] / a.vpi) : a.q0;
-            src[t] = (AFF && valid[t]) ? (int)(vv[t] % a.nsrc) : 0;
-        }
-        double ca[VPT], cc[VPT];     // (b_{c-1}, t_{c+1}) of step j-1: coefficients of V2~, W2~
-#pragma unroll
-        for (int t = 0; t < VPT; ++t) ca[t] = cc[t] = 0.0;
-#ifdef PR_PART_PROBES
-        unsigned long long pacc[PART_NPROBE] = {};
-        PROBE_T(tl0);
-#endif
-        for (int j = 1; j <= a.m; ++j) {
-            PROBE_T(t0);
-            double alpha[VPT][AFF ? PART_RSM : 1];
-            if constexpr (AFF) {
-#pragma unroll
-                for (int t = 0; t < VPT; ++t)
-#pragma unroll
-                    for (int r = 0; r < PART_RSM; ++r) {
-                        double al = 0.0;
-                        if (r < a.R && valid[t])
-                            al = a.dt * a.amp[(long)src[t] * a.R + r] *
-                                 a.time[(long)r * a.nsteps + (long)q[t] * a.m + j - 1];
-                        alpha[t][r] = al;
-                    }
-            }
-            // S_j = T_c^{-1}(S_{j-1} + ca V2 + cc W2 + dt f_j) in scaled form:
-            // down z_i = x_i + nl_i z_{i-1}, up S_i = w_i z_i + S_{i+1}
-            double zp[VPT];
-#pragma unroll
-            for (int i = 0; i < L; ++i) {
-                const double2 q2 = cd[i];
-                const double nli = nl[i];
-#pragma unroll
-                for (int t = 0; t < VPT; ++t) {
-                    double x = fma(q2.x, ca[t], fma(q2.y, cc[t], S[t][i]));
-                    if constexpr (AFF) {
-#pragma unroll
-                        for (int r = 0; r < PART_RSM; ++r) x = fma(alpha[t][r], sp[i * RSM + r], x);
-                    }
-                    zp[t] = (i == 0) ? x : fma(nli, zp[t], x);
-                    S[t][i] = zp[t];
-                }
-            }
-            PROBE_T(t1);
-            PROBE_ADD(0, t1 - t0);
-            double gn[VPT];
-#pragma unroll
-            for (int i = L - 1; i >= 0; --i) {
-                const double wi = wv[i];
-#pragma unroll
-                for (int t = 0; t < VPT; ++t) {
-                    gn[t] = (i == L - 1) ? wi * S[t][i] : fma(wi, S[t][i], gn[t]);
-                    S[t][i] = gn[t];
-                }
-            }
-            const int p = j & 1;
-            PROBE_T(t2);
-            PROBE_ADD(1, t2 - t1);
-            if (j >= 2 && !a.noiface) {   // interface values of step j-1 (formed during this sweep)
-                const int pp = (j - 1) & 1;
-                mbar_wait(cbar + 8 * pp, ((j - 2) >> 1) & 1);
-#pragma unroll
-                for (int t = 0; t < VPT; ++t) neighbours(pp, li + t * LPC, ca[t], cc[t]);
-            }
-            PROBE_T(t3);
-            PROBE_ADD(2, t3 - t2);
-            {                          // physical chunk ends of g_j = S_j + ca V2 + cc W2
-                const double2 q0 = cd[0], q1 = cd[L - 1];
-#pragma unroll
-                for (int t = 0; t < VPT; ++t)
-                    rawE[(p * K + u) * 32 + li + t * LPC] =
-                        make_double2(fma(q0.x, ca[t], fma(q0.y, cc[t], S[t][0])),
-                                     dbot * fma(q1.x, ca[t], fma(q1.y, cc[t], S[t][L - 1])));
-            }
-            __syncwarp();
-            if (lane == 0 && !a.noiface) mbar_arrive(ebar + 8 * p);
-            PROBE_T(t4);
-            PROBE_ADD(3, t4 - t3);
-        }
-#ifdef PR_PART_PROBES
-        PROBE_T(tl1);
-        PROBE_ADD(11, tl1 - tl0);
-        if (lane == 0 && w == 0 && a.prof)
-            for (int k = 0; k < 4; ++k) atomicAdd(a.prof + k, pacc[k]);
-        if (lane == 0 && w == 0 && a.prof) atomicAdd(a.prof + 11, pacc[11]);
-        if (lane == 0 && w == 0 && a.prof) atomicAdd(a.prof + 10, (unsigned long long)a.m);
-#endif
-        // x_m = S_m + ca V2 + cc W2 + b_m V + t_m W, branch-free per row (the
-        // row data loads are uniform over the chunk's lanes), masked stores
-        const int pm = a.m & 1;
-        double ex[VPT], ey[VPT];                     // (b_m, t_m) of the neighbours
-#pragma unroll
-        for (int t = 0; t < VPT; ++t) ex[t] = ey[t] = 0.0;
-        if (!a.noiface) {
-            mbar_wait(cbar + 8 * pm, ((a.m - 1) >> 1) & 1);
-#pragma unroll
-            for (int t = 0; t < VPT; ++t) neighbours(pm, li + t * LPC, ex[t], ey[t]);
-        }
-#pragma unroll
-        for (int i = 0; i < L; ++i) {
-            const double2 q2 = cd[i];
-            const double2 *R = reinterpret_cast<const double2 *>(rowc_u + i * PART_ROWC);
-            const double2 VW = __ldg(R + 2), dd = __ldg(R + 3);
-            const bool rok = s0 + i < a.n;
+        if (STAGE && a.in && ngrp > 0) prefetch(cid);
+        bool synced = false;
+        for (long gi = 0; gi < ngrp; ++gi) {
+            const long grp = cid + gi * ncl;
+            const long gbase = grp * VPG;            // first vector of the group
+            const long J0 = gi * a.m;                // global step index of step 0 of this group
+            long vv[VPT];
+            bool valid[VPT];
 #pragma unroll
             for (int t = 0; t < VPT; ++t) {
-                double x = fma(q2.x, ca[t], fma(q2.y, cc[t], S[t][i]));
-                x = fma(VW.x, ex[t], fma(VW.y, ey[t], dd.x * x));
-                if (rok && valid[t]) {
-                    if (a.off) x += a.off[(long)(s0 + i) * a.ld_off + vv[t]];
-                    a.out[(long)(s0 + i) * a.ld_out + vv[t]] = x;
+                vv[t] = gbase + li + t * LPC;
+                valid[t] = vv[t] < a.B;
+            }
+            // the state in the chunk's scaled coordinates x~ = x / d
+            double S[VPT][L];
+            if (a.in && STAGE) {
+                // staged by the previous group (or above): wait, read, and start
+                // the next group's copy into the same buffer
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                __syncwarp();
+                const double *st = stw + (size_t)h * L * VPG;
+#pragma unroll
+                for (int i = 0; i < L; ++i) {
+                    const double dinv = (s0 + i < a.n) ? rowc_u[i * PART_ROWC + 7] : 0.0;
+#pragma unroll
+                    for (int t = 0; t < VPT; ++t) S[t][i] = st[(size_t)i * VPG + li + t * LPC] * dinv;
+                }
+                __syncwarp();
+                if (gi + 1 < ngrp) prefetch(grp + ncl);
+            } else if (a.in) {
+                // loads issued unconditionally from clamped addresses (no per-row
+                // branch, so all rows are in flight together), masked afterwards
+                long vc[VPT];
+#pragma unroll
+                for (int t = 0; t < VPT; ++t) vc[t] = valid[t] ? vv[t] : 0;
+#pragma unroll
+                for (int i = 0; i < L; ++i) {
+                    const int row = (s0 + i < a.n) ? s0 + i : a.n - 1;
+                    const double dinv = (s0 + i < a.n) ? rowc_u[i * PART_ROWC + 7] : 0.0;
+#pragma unroll
+                    for (int t = 0; t < VPT; ++t) {
+                        const double v = __ldg(a.in + (long)row * a.ld_in + vc[t]);
+                        S[t][i] = valid[t] ? v * dinv : 0.0;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < L; ++i)
+#pragma unroll
+                    for (int t = 0; t < VPT; ++t) S[t][i] = 0.0;
+            }
+            if (!synced) {
+                cluster.sync();
+                synced = true;
+            }
+            int q[VPT], src[VPT];
+#pragma unroll
+            for (int t = 0; t < VPT; ++t) {
+                q[t] = valid[t] ? a.q0 + (int)(vv[t] / a.vpi) : a.q0;
+                src[t] = (AFF && valid[t]) ? (int)(vv[t] % a.nsrc) : 0;
+            }
+            double ca[VPT], cc[VPT];     // (b_{c-1}, t_{c+1}) of step j-1: coefficients of V2~, W2~
+#pragma unroll
+            for (int t = 0; t < VPT; ++t) ca[t] = cc[t] = 0.0;
+#ifdef PR_PART_PROBES
+            unsigned long long pacc[PART_NPROBE] = {};
+            PROBE_T(tl0);
+#endif
+            for (int j = 1; j <= a.m; ++j) {
+                PROBE_T(t0);
+                const long J = J0 + j;                   // global step (mbarrier slot / phase)
+                double alpha[VPT][AFF ? PART_RSM : 1];
+                if constexpr (AFF) {
+#pragma unroll
+                    for (int t = 0; t < VPT; ++t)
+#pragma unroll
+                        for (int r = 0; r < PART_RSM; ++r) {
+                            double al = 0.0;
+                            if (r < a.R && valid[t])
+                                al = a.dt * a.amp[(long)src[t] * a.R + r] *
+                                     a.time[(long)r * a.nsteps + (long)q[t] * a.m + j - 1];
+                            alpha[t][r] = al;
+                        }
+                }
+                // S_j = T_c^{-1}(S_{j-1} + ca V2 + cc W2 + dt f_j) in scaled form:
+                // down z_i = x_i + nl_i z_{i-1}, up S_i = w_i z_i + S_{i+1}
+                double zp[VPT];
+#pragma unroll
+                for (int i = 0; i < L; ++i) {
+                    const double2 q2 = cd[i];
+                    const double nli = nl[i];
+#pragma unroll
+                    for (int t = 0; t < VPT; ++t) {
+                        double x = fma(q2.x, ca[t], fma(q2.y, cc[t], S[t][i]));
+                        if constexpr (AFF) {
+#pragma unroll
+                            for (int r = 0; r < PART_RSM; ++r) x = fma(alpha[t][r], sp[i * RSM + r], x);
+                        }
+                        zp[t] = (i == 0) ? x : fma(nli, zp[t], x);
+                        S[t][i] = zp[t];
+                    }
+                }
+                PROBE_T(t1);
+                PROBE_ADD(0, t1 - t0);
+                double gn[VPT];
+#pragma unroll
+                for (int i = L - 1; i >= 0; --i) {
+                    const double wi = wv[i];
+#pragma unroll
+                    for (int t = 0; t < VPT; ++t) {
+                        gn[t] = (i == L - 1) ? wi * S[t][i] : fma(wi, S[t][i], gn[t]);
+                        S[t][i] = gn[t];
+                    }
+                }
+                const int p = (int)(J & 1);
+                PROBE_T(t2);
+                PROBE_ADD(1, t2 - t1);
+                if (j >= 2 && !a.noiface) {   // interface values of step j-1 (formed during this sweep)
+                    const int pp = (int)((J - 1) & 1);
+                    mbar_wait(cbar + 8 * pp, (unsigned)(((J - 2) >> 1) & 1));
+#pragma unroll
+                    for (int t = 0; t < VPT; ++t) neighbours(pp, li + t * LPC, ca[t], cc[t]);
+                }
+                PROBE_T(t3);
+                PROBE_ADD(2, t3 - t2);
+                {                          // physical chunk ends of g_j = S_j + ca V2 + cc W2
+                    const double2 q0 = cd[0], q1 = cd[L - 1];
+#pragma unroll
+                    for (int t = 0; t < VPT; ++t)
+                        rawE[(p * K + u) * 32 + li + t * LPC] =
+                            make_double2(fma(q0.x, ca[t], fma(q0.y, cc[t], S[t][0])),
+                                         dbot * fma(q1.x, ca[t], fma(q1.y, cc[t], S[t][L - 1])));
+                }
+                __syncwarp();
+                if (lane == 0 && !a.noiface) mbar_arrive(ebar + 8 * p);
+                PROBE_T(t4);
+                PROBE_ADD(3, t4 - t3);
+            }
+#ifdef PR_PART_PROBES
+            PROBE_T(tl1);
+            PROBE_ADD(11, tl1 - tl0);
+            if (lane == 0 && w == 0 && a.prof)
+                for (int k = 0; k < 4; ++k) atomicAdd(a.prof + k, pacc[k]);
+            if (lane == 0 && w == 0 && a.prof) atomicAdd(a.prof + 11, pacc[11]);
+            if (lane == 0 && w == 0 && a.prof) atomicAdd(a.prof + 10, (unsigned long long)a.m);
+#endif
+            // x_m = S_m + ca V2 + cc W2 + b_m V + t_m W, branch-free per row (the
+            // row data loads are uniform over the chunk's lanes), masked stores
+            const long Jm = J0 + a.m;
+            const int pm = (int)(Jm & 1);
+            double ex[VPT], ey[VPT];                     // (b_m, t_m) of the neighbours
+#pragma unroll
+            for (int t = 0; t < VPT; ++t) ex[t] = ey[t] = 0.0;
+            if (!a.noiface) {
+                mbar_wait(cbar + 8 * pm, (unsigned)(((Jm - 1) >> 1) & 1));
+#pragma unroll
+                for (int t = 0; t < VPT; ++t) neighbours(pm, li + t * LPC, ex[t], ey[t]);
+            }
+            // the stored offsets are read in blocks of EB rows from clamped
+            // addresses BEFORE the block's stores (off may alias out, so loads
+            // interleaved with the stores would be serialised behind them: one
+            // HBM latency per row)
+            constexpr int EB = 16;
+            long vc[VPT];
+#pragma unroll
+            for (int t = 0; t < VPT; ++t) vc[t] = valid[t] ? vv[t] : 0;
+#pragma unroll
+            for (int i0 = 0; i0 < L; i0 += EB) {
+                double ofs[VPT][EB];
+#pragma unroll
+                for (int r = 0; r < EB; ++r)
+#pragma unroll
+                    for (int t = 0; t < VPT; ++t) ofs[t][r] = 0.0;
+                if (a.off) {
+#pragma unroll
+                    for (int r = 0; r < EB; ++r) {
+                        const int row = (s0 + i0 + r < a.n) ? s0 + i0 + r : a.n - 1;
+#pragma unroll
+                        for (int t = 0; t < VPT; ++t) ofs[t][r] = a.off[(long)row * a.ld_off + vc[t]];
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < EB; ++r) {
+                    const int i = i0 + r;
+                    const double2 q2 = cd[i];
+                    const double2 *R = reinterpret_cast<const double2 *>(rowc_u + i * PART_ROWC);
+                    const double2 VW = __ldg(R + 2), dd = __ldg(R + 3);
+                    const bool rok = s0 + i < a.n;
+#pragma unroll
+                    for (int t = 0; t < VPT; ++t) {
+                        double x = fma(q2.x, ca[t], fma(q2.y, cc[t], S[t][i]));
+                        x = fma(VW.x, ex[t], fma(VW.y, ey[t], dd.x * x));
+                        if (rok && valid[t]) a.out[(long)(s0 + i) * a.ld_out + vv[t]] = x + ofs[t][r];
+                    }
                 }
             }
         }
+        if (!synced) cluster.sync();
     } else {
         // ------------------------------------------------ interface warps
         // lane = (part hi, vector vl); with HI = 2 the two half-warps split the
@@ -901,13 +1003,13 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
         cluster.sync();
         constexpr int CLH = CL / HI;                                     // CTAs per lane part
         // step j's values from every super-chunk -> (B_{C-1}, T_{C+1}) of step j
-        auto gather = [&](int j) {
-            const int p = j & 1;
+        auto gather = [&](long j) {
+            const int p = (int)(j & 1);
             if (lane == 0)
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
                              :: "r"(gbar + 8 * p), "r"((unsigned)(CL * VPG * sizeof(double2))) : "memory");
             PROBE_T(g0);
-            mbar_wait_idle(gbar + 8 * p, ((j - 1) >> 1) & 1, a.idle_ns);
+            mbar_wait_idle(gbar + 8 * p, (unsigned)(((j - 1) >> 1) & 1), a.idle_ns);
             PROBE_T(g1);
             PROBE_ADD(8, g1 - g0);
             const double2 *Gt = gth + (size_t)p * CL * 32 + vl;
@@ -948,10 +1050,10 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
         };
         // chunk end values of step j -> (T_C, B_C) to every CTA, then the local
         // solve z = M_C^{-1} g_C (off the exchange's critical path)
-        auto publish = [&](int j) {
-            const int p = j & 1;
+        auto publish = [&](long j) {
+            const int p = (int)(j & 1);
             PROBE_T(p0);
-            mbar_wait_idle(ebar + 8 * p, ((j - 1) >> 1) & 1, a.idle_ns);
+            mbar_wait_idle(ebar + 8 * p, (unsigned)(((j - 1) >> 1) & 1), a.idle_ns);
             PROBE_T(p1);
             PROBE_ADD(4, p1 - p0);
             const double2 *rE = rawE + (size_t)p * K * 32 + vl;
@@ -1026,14 +1128,16 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) k_part_step(PartArgs a)
                 __syncwarp();
             }
         };
+        // global step index over this cluster's groups (mbarrier slots and phases)
+        const long nJ = ngrp * (long)a.m;
         if (a.noiface) {
         } else if (w == W) {
-            for (int j = 1; j <= a.m; ++j) {
+            for (long j = 1; j <= nJ; ++j) {
                 publish(j);
-                if (lane == 0) mbar_arrive(cbar + 8 * (j & 1));
+                if (lane == 0) mbar_arrive(cbar + 8 * (int)(j & 1));
             }
         } else {
-            for (int j = 1; j <= a.m; ++j) gather(j);
+            for (long j = 1; j <= nJ; ++j) gather(j);
         }
 #ifdef PR_PART_PROBES
         if (lane == 0 && a.prof)
@@ -1109,6 +1213,26 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // persistent clusters: as many as are co-resident (queried once per device),
+    // each looping over vector groups; clusters never wait on one another, so
+    // fewer resident clusters (another kernel sharing the GPU) only serialise
+    static std::atomic<int> max_cl[64];
+    int ncl = max_cl[dev & 63].load(std::memory_order_acquire);
+    if (ncl == 0) {
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, VPT, AFF>, &cfg) != cudaSuccess ||
+            nc < 1) {
+            (void)cudaGetLastError();
+            nc = -1;                   // unknown: one cluster per group
+        }
+        max_cl[dev & 63].store(nc, std::memory_order_release);
+        ncl = nc;
+    }
+    if (flags().part_nopersist) ncl = -1;
+    const long grid_cl = (ncl > 0 && ncl < groups) ? ncl : groups;
+    cfg.gridDim = dim3((unsigned)(grid_cl * CL));
+    PartArgs ag = a;
+    ag.groups = groups;
     if (flags().part_prof) {
         int nc = -1;
         cudaError_t eo = cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, VPT, AFF>, &cfg);
@@ -1119,7 +1243,7 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     note_launch();
 #ifdef PR_PART_PROBES
     if (flags().part_prof) {
-        PartArgs b = a;
+        PartArgs b = ag;
         cudaMalloc(&b.prof, PART_NPROBE * sizeof(unsigned long long));
         cudaMemsetAsync(b.prof, 0, PART_NPROBE * sizeof(unsigned long long), s);
         cudaError_t e = cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF>, b);
@@ -1136,7 +1260,7 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
         return e;
     }
 #endif
-    return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF>, a);
+    return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF>, ag);
 }
 
 template <int CL, int W, int H, int L, int VPT = 1>

@@ -52,8 +52,9 @@ struct Flags {
          no_expand_mma = false, part_prof = false, qr_trace = false, debug_sync = false;
     bool part_vpt2 = false, no_src_basis = false;
     int part_h = 0, stepper_pd = 0, stepper_vpt = 0;
-    int part_idle_ns = -1;
-    bool part_noiface = false; // PR_PART_NOIFACE: K1P sweeps without the interface (timing aid; wrong results)     // PR_PART_IDLE_NS: interface-warp poll back-off (dev aid; -1 = default)
+    int part_idle_ns = -1;       // PR_PART_IDLE_NS: interface-warp poll back-off (dev aid; -1 = default)
+    bool part_nopersist = false; // PR_PART_NOPERSIST: one K1P cluster per vector group (no staging reuse)
+    bool part_noiface = false;   // PR_PART_NOIFACE: K1P sweeps without the interface (timing aid; wrong results)
 };
 const Flags &flags();
 

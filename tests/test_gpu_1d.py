@@ -343,6 +343,48 @@ def test_part_stepper_bitwise_repeatable(name, B, env, monkeypatch):
         lib().pr_reload_env()
 
 
+@pytest.mark.parametrize("name,n,m,B,ld", [("C4", 16383, 9, 341, 343),   # ragged last group, odd ld (8-byte staging)
+                                           ("C4", 16383, 5, 1000, 1000),  # 16-byte staging
+                                           ("C2", 4095, 7, 777, 778),
+                                           ("T4", 301, 6, 1500, 1501)])
+def test_part_persistent_clusters(name, n, m, B, ld, pr_env):
+    """K1P runs as many clusters as are co-resident, each looping over vector
+    groups with the next group's input staged in shared memory by cp.async
+    (k_part.cu).  Batches of many groups per cluster, a ragged last group, odd
+    and even leading dimensions, a stored offset and in-place operation must
+    give the one-cluster-per-group launch bit for bit, and the oracle on
+    sampled vectors."""
+    import torch
+    from paper_2508_08873_b200 import PR_ADJOINT, PR_LINEAR
+    cfg = replace(get(name), n=n, m=m)
+    op_g = gpu_op(cfg)
+    op_o = make_op(cfg)
+    rng = np.random.default_rng(B + ld)
+    X = rng.standard_normal((B, n))
+    Off = rng.standard_normal((B, n))
+    res = {}
+    for persist in (True, False):
+        pr_env(PR_PART_NOPERSIST=None if persist else "1")
+        for mode in (PR_LINEAR, PR_ADJOINT):
+            Ug = to_gpu(cfg, X, ld)
+            out = empty_batch(cfg, B, ld)
+            op_g.fine_propagate(mode, 1, m, Ug, out, B=B)
+            Og = to_gpu(cfg, Off, ld)
+            op_g.fine_propagate(mode, 1, m, Ug, Ug, offset=Og, B=B)     # in place, + offset
+            res[(persist, mode)] = (out.clone(), Ug.clone())
+    for mode in (PR_LINEAR, PR_ADJOINT):
+        a, b = res[(True, mode)], res[(False, mode)]
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]), mode
+    sample = np.unique(np.r_[0, 1, 15, 16, B // 2, B - 17, B - 2, B - 1])
+    for mode, mname in ((PR_LINEAR, "linear"), (PR_ADJOINT, "adjoint")):
+        ref = fine(op_o, 2, X[sample], mname)
+        got = from_gpu(cfg, res[(True, mode)][0], B)[sample]
+        got2 = from_gpu(cfg, res[(True, mode)][1], B)[sample]
+        for i in range(len(sample)):
+            assert relnorm(got[i], ref[i]) <= TAU_1D, (mname, sample[i])
+            assert relnorm(got2[i], ref[i] + Off[sample[i]]) <= TAU_1D, (mname, sample[i])
+
+
 def test_coarse_estimate_and_adaptive_p_match_oracle():
     """pr_coarse_estimate against the oracle's estimator on every interval, and
     pr_build_coarse_adaptive stopping at the p the estimates prescribe."""

@@ -1,6 +1,7 @@
 """Dev aid: device time of one 1D fine-propagation launch (K1P unless
 PR_NO_PART=1) per config / batch / mode, CUDA events, after warm-up.
-    python tools/k1p_time.py C4 16384 [linear|adjoint|affine] [reps]"""
+    python tools/k1p_time.py C4 16384 [linear|adjoint|affine|offset] [reps]
+(offset: LINEAR with a stored offset added, as in a Parareal iteration)"""
 import os
 import sys
 
@@ -21,6 +22,7 @@ op = gpu_op(cfg)
 X = torch.randn(cfg.n, B, dtype=torch.float64, device="cuda")
 Y = torch.empty_like(X)
 src = gpu_source(cfg) if mode == "affine" else None
+OFF = torch.randn_like(X) if mode == "offset" else None
 S = cfg.nsrc if mode == "affine" else 1
 
 
@@ -28,7 +30,7 @@ def run():
     if mode == "affine":
         op.fine_propagate(PR_AFFINE, 0, cfg.m, None, Y, vecs_per_interval=S, source=src)
     else:
-        op.fine_propagate(PR_ADJOINT if mode == "adjoint" else PR_LINEAR, 0, cfg.m, X, Y)
+        op.fine_propagate(PR_ADJOINT if mode == "adjoint" else PR_LINEAR, 0, cfg.m, X, Y, offset=OFF)
 
 
 for _ in range(3):
