@@ -37,6 +37,7 @@
 #include <stdlib.h>
 
 #include <atomic>
+#include <type_traits>
 
 #include "pr_internal.cuh"
 
@@ -48,9 +49,13 @@ namespace pr {
 // registers); PR_PART_PROF=1 then prints per-step phase cycles per CTA
 #ifdef PR_PART_PROBES
 #define PROBE_T(v) const long long v = clock64()
+#define PROBE_DECL(v) long long v = 0
+#define PROBE_SET(v) (v = clock64())
 #define PROBE_ADD(slot, v) (pacc[slot] += (unsigned long long)(v))
 #else
 #define PROBE_T(v)
+#define PROBE_DECL(v)
+#define PROBE_SET(v)
 #define PROBE_ADD(slot, v)
 #endif
 constexpr int PART_NPROBE = 16;
@@ -451,6 +456,41 @@ __device__ __forceinline__ void mbar_arrive(unsigned bar)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
 }
 
+// ---- tensor memory (TMEM) as a per-lane coefficient store (TM variants).
+// The sweeps are bound by the shared-memory coefficient stream (one LSU cycle
+// per warp-wide LDS.64, broadcast or not): the two LU coefficients {nl, w} of
+// a lane's chunk are kept in the SM's tensor memory instead (512 columns x
+// 128 lanes x 32 bit; a warp reaches the 32 lanes of its quadrant, warps w and
+// w + 4 share one: 256 columns = 128 doubles each) and read with
+// tcgen05.ld.32x32b.x8 (4 rows per instruction, double buffered), which does
+// not go through the LSU.  The spike coefficients stay in shared memory.
+__device__ __forceinline__ void tm_ld8(unsigned addr, unsigned (&r)[8])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(addr));
+}
+
+// the loaded registers are operands so that no consumer is scheduled above the
+// wait (no memory clobber: shared-memory loads may move across TMEM reads)
+__device__ __forceinline__ void tm_wait8(unsigned (&r)[8])
+{
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]));
+}
+
+__device__ __forceinline__ void tm_st8(unsigned addr, const unsigned (&r)[8])
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                 :: "r"(addr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+
+__device__ __forceinline__ double tm_dbl(const unsigned (&r)[8], int e)
+{
+    return __hiloint2double((int)r[2 * e + 1], (int)r[2 * e]);
+}
+
 // The interface warp's banded solve, streamed through shared memory: rows are
 // processed in blocks of 8 whose operands are loaded (restrict: no aliasing
 // with the stores) before the block's dependent chain runs, so each row
@@ -657,9 +697,30 @@ __device__ __forceinline__ void half_dots(int hf, const double2 *__restrict__ g,
 // Hand-offs use mbarriers: ebar[p] (W compute warps arrive: raw ends of a
 // step of parity p written), cbar[p] (publish + gather arrive: interface
 // values of a step of parity p written); gbar[p] counts the gather bytes.
-template <int CL, int W, int H, int L, int VPT, bool AFF>
-__global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W + 2))) / 8 * 8 > 255 ? 255 : (65536 / (32 * (W + 2))) / 8 * 8) k_part_step(PartArgs a)
+// TM variants (W = 8: every C4 / C2-sized launch) run 12 warps = 3 warpgroups:
+// the two compute warpgroups raise their register budget to PART_TM_CREGS with
+// setmaxnreg (room for the TMEM / spike-coefficient prefetch buffers next to the
+// 128 state registers), the interface warpgroup (publish, gather, local solver,
+// one idle warp) drops to PART_TM_IREGS.  setmaxnreg.inc blocks until the
+// CTA's register pool (launch registers x threads) holds the increase, so the
+// 8 compute warps may only take what the 4 interface warps released:
+// 8 * (216 - 168) = 4 * (168 - 72).
+constexpr int PART_TM_CREGS = 216, PART_TM_IREGS = 72, PART_TM_LREGS = 168;
+static_assert(8 * (PART_TM_CREGS - PART_TM_LREGS) <= 4 * (PART_TM_LREGS - PART_TM_IREGS),
+              "setmaxnreg.inc would wait forever for registers nobody releases");
+template <bool TM> __host__ __device__ constexpr int part_ni() { return TM ? 4 : 2; }
+template <int W, bool TM> __host__ __device__ constexpr int part_maxreg()
 {
+    constexpr int r = (65536 / (32 * (W + part_ni<TM>()))) / 8 * 8;
+    return r > 255 ? 255 : r;
+}
+
+template <int CL, int W, int H, int L, int VPT, bool AFF, bool TM = false>
+__global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part_maxreg<W, TM>())) k_part_step(PartArgs a)
+{
+    static_assert(!TM || (L == 64 && W == 8), "TMEM coefficient store: 2 x 64 doubles per lane, two warps per quadrant");
+    static_assert(!TM || part_maxreg<W, TM>() == PART_TM_LREGS, "register pool accounting of the TM variants");
+    __shared__ unsigned tm_slot;
     constexpr int LPC = 32 / H;          // lanes per chunk
     constexpr int VPG = LPC * VPT;       // vectors per cluster group
     static_assert(VPG == 16 || VPG == 32, "the interface warp splits 32 lanes over VPG vectors");
@@ -667,6 +728,7 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W
     constexpr int K = W * H;             // chunks per CTA
     constexpr int M = 2 * K;             // local interface unknowns
     constexpr bool SPLIT = K >= 16;      // split band solve (two halves)
+    constexpr bool SOLVER = TM && SPLIT; // the local band solve on its own warp (W + 2), off the publish warp
     constexpr int RSM = AFF ? PART_RSM : 0;
     constexpr bool STAGE = part_stage<CL, W, H, L, VPT, AFF>();   // next group's input prefetched into shared memory
     extern __shared__ __align__(16) double sm[];
@@ -710,12 +772,26 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if constexpr (TM) {            // the publish warp allocates all 512 TMEM columns (one CTA per SM)
+        if (w == W) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                         :: "r"(smem_u32(&tm_slot)) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    }
     // ctad / rmap are written by all warps and read below (neighbours) by
     // warps that may run ahead: make the copies visible before any use
     __syncthreads();
+    unsigned tm_base = 0;
+    if constexpr (TM) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tm_base = tm_slot;
+    }
 
     if (w < W) {
         // ------------------------------------------------ compute warp: chunk c
+        if constexpr (TM) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" :: "n"(PART_TM_CREGS));
         const int h = lane / LPC, li = lane % LPC;
         const int u = w * H + h;                     // chunk within the CTA
         const int c = C * K + u;
@@ -743,6 +819,22 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W
         const double *nl = reinterpret_cast<const double *>(cd) + 2 * L;
         const double *wv = nl + L;
         const double *sp = wv + L;
+        // TM: this lane's {nl, w} in its TMEM lane: columns 0..127 nl (rows 0..63), 128..255 w
+        const unsigned tm_my = tm_base + ((unsigned)(32 * (w & 3)) << 16) + (unsigned)((w >> 2) * 256);
+        if constexpr (TM) {
+#pragma unroll 1
+            for (int b = 0; b < 32; ++b) {
+                unsigned r[8];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const double v = (b < 16) ? nl[b * 4 + e] : wv[(b - 16) * 4 + e];
+                    r[2 * e] = (unsigned)__double2loint(v);
+                    r[2 * e + 1] = (unsigned)__double2hiint(v);
+                }
+                tm_st8(tm_my + b * 8, r);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
         const double *rowc_u = a.rowc + (size_t)c * L * PART_ROWC;     // this chunk's rows (global)
         const double dbot = rowc_u[(L - 1) * PART_ROWC + 6];            // d_{L-1} (d_0 = 1)
         // staged input of a group: this warp's H chunks, [H*L rows][VPG vectors]
@@ -881,6 +973,62 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W
                 // S_j = T_c^{-1}(S_{j-1} + ca V2 + cc W2 + dt f_j) in scaled form:
                 // down z_i = x_i + nl_i z_{i-1}, up S_i = w_i z_i + S_{i+1}
                 double zp[VPT];
+                double gn[VPT];
+                PROBE_DECL(t1);
+                if constexpr (TM) {
+                    // {nl, w} from TMEM, 4 rows per load, the next block in flight
+                    // while the current one is used
+                    unsigned tb[2][8];
+                    double2 qn[2][4];                        // spike coefficients, one block ahead
+                    tm_ld8(tm_my, tb[0]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) qn[0][e] = cd[e];
+#pragma unroll
+                    for (int b = 0; b < L / 4; ++b) {
+                        tm_wait8(tb[b & 1]);
+                        // after the last nl block: the first w block of the up sweep
+                        tm_ld8(b + 1 < L / 4 ? tm_my + (b + 1) * 8 : tm_my + 128 + (L / 4 - 1) * 8, tb[(b + 1) & 1]);
+                        if (b + 1 < L / 4) {
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) qn[(b + 1) & 1][e] = cd[(b + 1) * 4 + e];
+                        }
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int i = b * 4 + e;
+                            const double2 q2 = qn[b & 1][e];
+                            const double nli = tm_dbl(tb[b & 1], e);
+#pragma unroll
+                            for (int t = 0; t < VPT; ++t) {
+                                double x = fma(q2.x, ca[t], fma(q2.y, cc[t], S[t][i]));
+                                if constexpr (AFF) {
+#pragma unroll
+                                    for (int r = 0; r < PART_RSM; ++r) x = fma(alpha[t][r], sp[i * RSM + r], x);
+                                }
+                                zp[t] = (i == 0) ? x : fma(nli, zp[t], x);
+                                S[t][i] = zp[t];
+                            }
+                        }
+                    }
+                    PROBE_SET(t1);
+                    PROBE_ADD(0, t1 - t0);
+#pragma unroll
+                    for (int b = L / 4 - 1; b >= 0; --b) {
+                        constexpr int S0 = (L / 4) & 1;          // buffer of the first w block
+                        const int sb = (S0 + (L / 4 - 1 - b)) & 1;
+                        tm_wait8(tb[sb]);
+                        if (b > 0) tm_ld8(tm_my + 128 + (b - 1) * 8, tb[sb ^ 1]);
+#pragma unroll
+                        for (int e = 3; e >= 0; --e) {
+                            const int i = b * 4 + e;
+                            const double wi = tm_dbl(tb[sb], e);
+#pragma unroll
+                            for (int t = 0; t < VPT; ++t) {
+                                gn[t] = (i == L - 1) ? wi * S[t][i] : fma(wi, S[t][i], gn[t]);
+                                S[t][i] = gn[t];
+                            }
+                        }
+                    }
+                } else {
 #pragma unroll
                 for (int i = 0; i < L; ++i) {
                     const double2 q2 = cd[i];
@@ -896,9 +1044,8 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W
                         S[t][i] = zp[t];
                     }
                 }
-                PROBE_T(t1);
+                PROBE_SET(t1);
                 PROBE_ADD(0, t1 - t0);
-                double gn[VPT];
 #pragma unroll
                 for (int i = L - 1; i >= 0; --i) {
                     const double wi = wv[i];
@@ -907,6 +1054,7 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W
                         gn[t] = (i == L - 1) ? wi * S[t][i] : fma(wi, S[t][i], gn[t]);
                         S[t][i] = gn[t];
                     }
+                }
                 }
                 const int p = (int)(J & 1);
                 PROBE_T(t2);
@@ -996,6 +1144,7 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W
         // ------------------------------------------------ interface warps
         // lane = (part hi, vector vl); with HI = 2 the two half-warps split the
         // cluster sends, the solve halves and the gather dot products
+        if constexpr (TM) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" :: "n"(PART_TM_IREGS));
         const int hi = lane / VPG, vl = lane % VPG;
 #ifdef PR_PART_PROBES
         unsigned long long pacc[PART_NPROBE] = {};
@@ -1050,15 +1199,21 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W
         };
         // chunk end values of step j -> (T_C, B_C) to every CTA, then the local
         // solve z = M_C^{-1} g_C (off the exchange's critical path)
-        auto publish = [&](long j) {
+        // SEND / SOLVE: with a solver warp (SOLVER) the publish warp only forms and
+        // sends the super-values and warp W + 2 runs the band solve concurrently
+        auto publish = [&](long j, auto send_c, auto solve_c) {
+            constexpr bool SEND = decltype(send_c)::value, SOLVE = decltype(solve_c)::value;
             const int p = (int)(j & 1);
             PROBE_T(p0);
             mbar_wait_idle(ebar + 8 * p, (unsigned)(((j - 1) >> 1) & 1), a.idle_ns);
             PROBE_T(p1);
-            PROBE_ADD(4, p1 - p0);
+            if (SEND) PROBE_ADD(4, p1 - p0);
             const double2 *rE = rawE + (size_t)p * K * 32 + vl;
             const unsigned off = (unsigned)(((p * CL + C) * 32 + vl) * sizeof(double2));
             if constexpr (SPLIT) {
+                PROBE_DECL(p2);
+                PROBE_SET(p2);
+                if constexpr (SEND) {
                 // (T, B) partial sums of half 0 and half 1, added in that order
                 double T0h, T1h, B0h, B1h;
                 if constexpr (HI == 2) {
@@ -1080,8 +1235,10 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W
                     const int r = hi * CLH + rr;
                     st_async_v2(rmap[r] + off, Tv, Bv, rmap[CL + r] + 8 * p);
                 }
-                PROBE_T(p2);
+                PROBE_SET(p2);
                 PROBE_ADD(5, p2 - p1);
+                }
+                if constexpr (SOLVE) {
                 // split solve: all lanes write the common result slot vl
                 double *zc = zs + (size_t)p * M * 32 + vl;
                 double y2c, y1c;                      // half 0's carried pair
@@ -1111,7 +1268,9 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W
                 __syncwarp();
                 PROBE_T(p4);
                 PROBE_ADD(7, p4 - p3);
+                }
             } else {
+                static_assert(SPLIT || !SOLVER, "the unsplit solve runs on the publish warp");
                 double *zl = zs + (size_t)p * M * 32 + vl + VPG * hi;
                 // forward elimination y = L^{-1} g (stored), and (T_C, B_C) from the
                 // two stored rows of M_C^{-1} applied to g (independent FMAs)
@@ -1133,11 +1292,20 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W
         if (a.noiface) {
         } else if (w == W) {
             for (long j = 1; j <= nJ; ++j) {
-                publish(j);
+                if constexpr (SOLVER) {
+                    publish(j, std::true_type{}, std::false_type{});
+                } else {
+                    publish(j, std::true_type{}, std::true_type{});
+                    if (lane == 0) mbar_arrive(cbar + 8 * (int)(j & 1));
+                }
+            }
+        } else if (w == W + 1) {
+            for (long j = 1; j <= nJ; ++j) gather(j);
+        } else if (SOLVER && w == W + 2) {
+            for (long j = 1; j <= nJ; ++j) {
+                publish(j, std::false_type{}, std::true_type{});
                 if (lane == 0) mbar_arrive(cbar + 8 * (int)(j & 1));
             }
-        } else {
-            for (long j = 1; j <= nJ; ++j) gather(j);
         }
 #ifdef PR_PART_PROBES
         if (lane == 0 && a.prof)
@@ -1145,7 +1313,11 @@ __global__ void __launch_bounds__(32 * (W + 2), 1) __maxnreg__((65536 / (32 * (W
                 if (pacc[k]) atomicAdd(a.prof + k, pacc[k]);
 #endif
     }
+    if constexpr (TM) asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     cluster.sync();                // no CTA leaves while cluster peers may still target it
+    if constexpr (TM) {
+        if (w == W) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" :: "r"(tm_base) : "memory");
+    }
 }
 
 // ---------------------------------------------------------------- driver
@@ -1181,7 +1353,7 @@ cudaError_t launch_part_setup(int n, int P, int L, int CL, int K, const double *
     return cudaGetLastError();
 }
 
-template <int CL, int W, int H, int L, int VPT, bool AFF>
+template <int CL, int W, int H, int L, int VPT, bool AFF, bool TM = false>
 static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
 {
     constexpr size_t smem = part_smem_t<CL, W, H, L, VPT, AFF>();
@@ -1193,17 +1365,17 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     cudaGetDevice(&dev);
     const unsigned long long bit = 1ULL << (dev & 63);
     if (!(attr_mask.load(std::memory_order_acquire) & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, VPT, AFF>,
+        cudaError_t e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, VPT, AFF, TM>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess && CL > 8)
-            e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, VPT, AFF>,
+            e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, VPT, AFF, TM>,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         attr_mask.fetch_or(bit, std::memory_order_release);
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)(groups * CL));
-    cfg.blockDim = dim3(32 * (W + 2));
+    cfg.blockDim = dim3(32 * (W + part_ni<TM>()));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -1220,7 +1392,7 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     int ncl = max_cl[dev & 63].load(std::memory_order_acquire);
     if (ncl == 0) {
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, VPT, AFF>, &cfg) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, VPT, AFF, TM>, &cfg) != cudaSuccess ||
             nc < 1) {
             (void)cudaGetLastError();
             nc = -1;                   // unknown: one cluster per group
@@ -1235,7 +1407,7 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     ag.groups = groups;
     if (flags().part_prof) {
         int nc = -1;
-        cudaError_t eo = cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, VPT, AFF>, &cfg);
+        cudaError_t eo = cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, VPT, AFF, TM>, &cfg);
         fprintf(stderr, "part: max active clusters %d (%s), smem %zu B, groups %ld\n", nc,
                 eo == cudaSuccess ? "ok" : cudaGetErrorString(eo), smem, groups);
         (void)cudaGetLastError();
@@ -1246,7 +1418,7 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
         PartArgs b = ag;
         cudaMalloc(&b.prof, PART_NPROBE * sizeof(unsigned long long));
         cudaMemsetAsync(b.prof, 0, PART_NPROBE * sizeof(unsigned long long), s);
-        cudaError_t e = cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF>, b);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF, TM>, b);
         unsigned long long h[PART_NPROBE];
         cudaMemcpyAsync(h, b.prof, sizeof(h), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
@@ -1260,7 +1432,7 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
         return e;
     }
 #endif
-    return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF>, ag);
+    return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF, TM>, ag);
 }
 
 template <int CL, int W, int H, int L, int VPT = 1>
@@ -1268,6 +1440,13 @@ static cudaError_t part_launch_aff(const PartArgs &a, long B, cudaStream_t s)
 {
     constexpr long VPG = (32 / H) * VPT;
     const long groups = (B + VPG - 1) / VPG;
+    // TM: {nl, w} in tensor memory (64-row chunks, up to 8 compute warps);
+    // PR_PART_NOTMEM=1 keeps every coefficient in shared memory
+    if constexpr (L == 64 && VPT == 1 && W == 8) {
+        if (!flags().part_notmem)
+            return a.R > 0 ? part_launch<CL, W, H, L, VPT, true, true>(a, groups, s)
+                           : part_launch<CL, W, H, L, VPT, false, true>(a, groups, s);
+    }
     return a.R > 0 ? part_launch<CL, W, H, L, VPT, true>(a, groups, s)
                    : part_launch<CL, W, H, L, VPT, false>(a, groups, s);
 }
