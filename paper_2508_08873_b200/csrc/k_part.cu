@@ -78,6 +78,13 @@ constexpr int CTAD_FP = CTAD_RM + 2 * PART_KMAX;
 constexpr int CTAD_FQ = CTAD_FP + PART_KMAX;
 constexpr int CTAD_BR = CTAD_FQ + PART_KMAX;
 constexpr int CTAD_BT = CTAD_BR + PART_KMAX;
+// second half's back substitution (zero carried state) applied to the forward
+// responses FP / FQ: with the forward and backward passes on separate warps
+// (TM variants) the carried-pair correction of rows K..2K-1 is applied to the
+// solution by the consumer, x_i += y_{K-2} PP_i + y_{K-1} PQ_i (linearity)
+constexpr int CTAD_PP = CTAD_BT + PART_KMAX;
+constexpr int CTAD_PQ = CTAD_PP + PART_KMAX;
+static_assert(CTAD_PQ + PART_KMAX == PART_CTAD, "per-CTA interface data layout");
 
 // ------------------------------------------------------------------ setup
 // One thread per chunk c (rows s0..s0+L-1): local LU of T_c in row-sum form
@@ -303,6 +310,19 @@ __global__ void k_part_iface(int CL, int K, const double *ends, double *ctad, in
                 }
             }
         }
+        if (K >= 2) {                                // PP / PQ: back substitution of FP / FQ over rows K..2K-1
+            for (int e = 0; e < 2; ++e) {
+                double t1 = 0.0, t2 = 0.0;
+                for (int r = M - 1; r >= K; --r) {
+                    double t = D[(e == 0 ? CTAD_FP : CTAD_FQ) + r - K] * F[r][2];
+                    if (r + 2 < M) t = fma(-(F[r][4] * F[r][2]), t2, t);
+                    if (r + 1 < M) t = fma(-(F[r][3] * F[r][2]), t1, t);
+                    D[(e == 0 ? CTAD_PP : CTAD_PQ) + r - K] = t;
+                    t2 = t1;
+                    t1 = t;
+                }
+            }
+        }
         for (int col = 0; col < M; ++col) {          // rows 0 and M-1 of M_C^{-1}
             for (int r = 0; r < M; ++r) x[r] = (r == col) ? 1.0 : 0.0;
             band_solve(M, F, x);
@@ -372,19 +392,20 @@ struct PartArgs {
 
 constexpr int PART_RSM = 8;            // shared-memory stride of the source rows
 
-// CTA shared memory (doubles): 6 mbarriers | gathered super-chunk values [2][CL][32]
+// CTA shared memory (doubles): 8 mbarriers | gathered super-chunk values [2][CL][32]
 // (double2) | chunk end values [2][K][32] (double2) | (B_{C-1}, T_{C+1}) [2][32]
 // (double2) | interface data | per chunk: {w, -ga, V2, W2} [L] | -cp [L] | {V, W} [L] |
 // source rows [L][8] (AFF) | cluster addresses [2][CL] (u32) | local solution [2][2K][32]
 // (vector slots: 32 = the largest group, VPG <= 32)
+// | carried pairs of the forward halves [2][32] (double2)
 // | staged input of the next group [K*L][VPG] (when it fits; not AFF: the
 // offsets launch has no input and its source rows take the space)
 template <int CL, int W, int H, int L, int VPT, bool AFF>
 __host__ __device__ constexpr size_t part_smem_base()
 {
     constexpr int K = W * H;
-    return (6 + (size_t)4 * CL * 32 + (size_t)4 * K * 32 + 4 * 32 + PART_CTAD +
-            (size_t)K * (L * (4 + (AFF ? PART_RSM : 0)) + 4) + CL + (size_t)4 * K * 32 + 4 * 32) * sizeof(double);
+    return (8 + (size_t)4 * CL * 32 + (size_t)4 * K * 32 + 4 * 32 + PART_CTAD +
+            (size_t)K * (L * (4 + (AFF ? PART_RSM : 0)) + 4) + CL + (size_t)4 * K * 32 + 4 * 32 + 4 * 32) * sizeof(double);
 }
 
 template <int CL, int W, int H, int L, int VPT, bool AFF>
@@ -626,7 +647,7 @@ __device__ __forceinline__ void half_forward(int hf, const double2 *__restrict__
 // back substitution over half hf from a zero carried state; returns the first
 // two values of the half.  fix: the half's forward values first get the
 // carried-pair correction y_i += y_{K-2} FP_i + y_{K-1} FQ_i (second half)
-template <int K>
+template <int K, bool NOFIX = false>
 __device__ __forceinline__ void half_backward(int hf, const double *__restrict__ F, double *__restrict__ z,
                                               double &x0o, double &x1o, bool fix, double ym2, double ym1)
 {
@@ -640,7 +661,8 @@ __device__ __forceinline__ void half_backward(int hf, const double *__restrict__
 #pragma unroll
         for (int r = 0; r < BR; ++r) {
             const int i = r0 + i0 + r;
-            zv[r] = fma(F[CTAD_FP + i0 + r], ym2, fma(F[CTAD_FQ + i0 + r], ym1, z[(size_t)i * 32]));
+            if constexpr (NOFIX) zv[r] = z[(size_t)i * 32];
+            else zv[r] = fma(F[CTAD_FP + i0 + r], ym2, fma(F[CTAD_FQ + i0 + r], ym1, z[(size_t)i * 32]));
             inv[r] = F[i * 5 + 2];
             u1[r] = F[i * 5 + 3];
             u2[r] = F[i * 5 + 4];
@@ -739,8 +761,8 @@ __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part
     // (its CTAs keep their coefficients in shared memory across groups)
     const long cid = (long)(blockIdx.x / CL), ncl = (long)(gridDim.x / CL);
     const long ngrp = (cid < a.groups) ? (a.groups - 1 - cid) / ncl + 1 : 0;
-    unsigned long long *bar = reinterpret_cast<unsigned long long *>(sm);   // gbar[2] ebar[2] cbar[2]
-    double2 *gth = reinterpret_cast<double2 *>(sm + 6);              // [2][CL][32]
+    unsigned long long *bar = reinterpret_cast<unsigned long long *>(sm);   // gbar[2] ebar[2] cbar[2] fbar[2]
+    double2 *gth = reinterpret_cast<double2 *>(sm + 8);              // [2][CL][32]
     double2 *rawE = gth + 2 * CL * 32;                               // [2][K][32]
     double2 *coef = rawE + 2 * K * 32;                               // [2][32]: (B_{C-1}, T_{C+1})
     double *ctad = reinterpret_cast<double *>(coef + 2 * 32);
@@ -751,11 +773,12 @@ __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part
     unsigned *rmap = reinterpret_cast<unsigned *>(regions + (size_t)K * RSTR);  // [2][CL]
     double *zs = reinterpret_cast<double *>(rmap + 2 * CL);                     // [2][M][32]
     double2 *zfx = reinterpret_cast<double2 *>(zs + 2 * M * 32);                // [2][32]
-    double *stg = reinterpret_cast<double *>(zfx + 2 * 32);                     // [K*L][VPG] (STAGE)
+    double2 *zcar = zfx + 2 * 32;                                               // [2][32]
+    double *stg = reinterpret_cast<double *>(zcar + 2 * 32);                    // [K*L][VPG] (STAGE)
     // chunk region: {V2~, W2~} [L] (double2) | nl [L] | w [L] | scaled source rows [L][RSM]
     auto cd_of = [&](int u) { return reinterpret_cast<double2 *>(regions + (size_t)u * RSTR); };
     const unsigned bar0 = smem_u32(bar), gth0 = smem_u32(gth);
-    const unsigned gbar = bar0, ebar = bar0 + 16, cbar = bar0 + 32;
+    const unsigned gbar = bar0, ebar = bar0 + 16, cbar = bar0 + 32, fbar = bar0 + 48;
 
     for (int i = threadIdx.x; i < PART_CTAD; i += blockDim.x) ctad[i] = a.ctad[(size_t)C * PART_CTAD + i];
     if (threadIdx.x < CL) {        // cluster addresses of every CTA's gather buffer and barriers
@@ -769,6 +792,8 @@ __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part
             // interface values of a step are complete when both the publish warp
             // (local solution z) and the gather warp ((B_{C-1}, T_{C+1})) arrived
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" :: "r"(cbar + 8 * q) : "memory");
+            // forward pass of a step done (solver warps of the TM variants)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(fbar + 8 * q) : "memory");
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -878,6 +903,9 @@ __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part
                     if (pos < K) {
                         const double2 fx = zfx[pp * 32 + vs];
                         v = fma(ctad[CTAD_BR + pos], fx.x, fma(ctad[CTAD_BT + pos], fx.y, v));
+                    } else if constexpr (SOLVER) {
+                        const double2 ym = zcar[pp * 32 + vs];
+                        v = fma(ctad[CTAD_PP + pos - K], ym.x, fma(ctad[CTAD_PQ + pos - K], ym.y, v));
                     }
                 }
                 return v;
@@ -1199,13 +1227,18 @@ __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part
         };
         // chunk end values of step j -> (T_C, B_C) to every CTA, then the local
         // solve z = M_C^{-1} g_C (off the exchange's critical path)
-        // SEND / SOLVE: with a solver warp (SOLVER) the publish warp only forms and
-        // sends the super-values and warp W + 2 runs the band solve concurrently
-        auto publish = [&](long j, auto send_c, auto solve_c) {
-            constexpr bool SEND = decltype(send_c)::value, SOLVE = decltype(solve_c)::value;
+        // Roles: SEND (super-values formed and sent), FWD / BWD (the two passes of
+        // the band solve).  Without solver warps the publish warp does all three;
+        // the TM variants (SOLVER) run them on warps W, W + 2 and W + 3, one per SM
+        // sub-partition, so no sub-partition's compute warps lose much more FP64
+        // issue than the others (the step ends with the slowest compute warp)
+        auto publish = [&](long j, auto send_c, auto fwd_c, auto bwd_c) {
+            constexpr bool SEND = decltype(send_c)::value, FWD = decltype(fwd_c)::value, BWD = decltype(bwd_c)::value;
             const int p = (int)(j & 1);
+            const unsigned ph = (unsigned)(((j - 1) >> 1) & 1);
             PROBE_T(p0);
-            mbar_wait_idle(ebar + 8 * p, (unsigned)(((j - 1) >> 1) & 1), a.idle_ns);
+            if constexpr (SEND || FWD) mbar_wait_idle(ebar + 8 * p, ph, a.idle_ns);
+            else mbar_wait_idle(fbar + 8 * p, ph, a.idle_ns);
             PROBE_T(p1);
             if (SEND) PROBE_ADD(4, p1 - p0);
             const double2 *rE = rawE + (size_t)p * K * 32 + vl;
@@ -1214,60 +1247,87 @@ __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part
                 PROBE_DECL(p2);
                 PROBE_SET(p2);
                 if constexpr (SEND) {
-                // (T, B) partial sums of half 0 and half 1, added in that order
-                double T0h, T1h, B0h, B1h;
-                if constexpr (HI == 2) {
-                    double Tm, Bm;
-                    half_dots<K>(hi, rE, ctad, Tm, Bm);
-                    const double To = __shfl_xor_sync(0xffffffffu, Tm, 16);
-                    const double Bo = __shfl_xor_sync(0xffffffffu, Bm, 16);
-                    T0h = hi ? To : Tm;
-                    T1h = hi ? Tm : To;
-                    B0h = hi ? Bo : Bm;
-                    B1h = hi ? Bm : Bo;
-                } else {
-                    half_dots<K>(0, rE, ctad, T0h, B0h);
-                    half_dots<K>(1, rE, ctad, T1h, B1h);
-                }
-                const double Tv = T0h + T1h, Bv = B0h + B1h;
+                    // (T, B) partial sums of half 0 and half 1, added in that order
+                    double T0h, T1h, B0h, B1h;
+                    if constexpr (HI == 2) {
+                        double Tm, Bm;
+                        half_dots<K>(hi, rE, ctad, Tm, Bm);
+                        const double To = __shfl_xor_sync(0xffffffffu, Tm, 16);
+                        const double Bo = __shfl_xor_sync(0xffffffffu, Bm, 16);
+                        T0h = hi ? To : Tm;
+                        T1h = hi ? Tm : To;
+                        B0h = hi ? Bo : Bm;
+                        B1h = hi ? Bm : Bo;
+                    } else {
+                        half_dots<K>(0, rE, ctad, T0h, B0h);
+                        half_dots<K>(1, rE, ctad, T1h, B1h);
+                    }
+                    const double Tv = T0h + T1h, Bv = B0h + B1h;
 #pragma unroll
-                for (int rr = 0; rr < CLH; ++rr) {
-                    const int r = hi * CLH + rr;
-                    st_async_v2(rmap[r] + off, Tv, Bv, rmap[CL + r] + 8 * p);
+                    for (int rr = 0; rr < CLH; ++rr) {
+                        const int r = hi * CLH + rr;
+                        st_async_v2(rmap[r] + off, Tv, Bv, rmap[CL + r] + 8 * p);
+                    }
+                    PROBE_SET(p2);
+                    PROBE_ADD(5, p2 - p1);
                 }
-                PROBE_SET(p2);
-                PROBE_ADD(5, p2 - p1);
-                }
-                if constexpr (SOLVE) {
                 // split solve: all lanes write the common result slot vl
                 double *zc = zs + (size_t)p * M * 32 + vl;
-                double y2c, y1c;                      // half 0's carried pair
-                if constexpr (HI == 2) {
-                    double y2m, y1m;
-                    half_forward<K>(hi, rE, ctad, zc, y2m, y1m);
-                    y2c = __shfl_xor_sync(0xffffffffu, y2m, 16);
-                    y1c = __shfl_xor_sync(0xffffffffu, y1m, 16);
-                } else {
-                    double y2x, y1x;
-                    half_forward<K>(0, rE, ctad, zc, y2c, y1c);
-                    half_forward<K>(1, rE, ctad, zc, y2x, y1x);
-                }
-                PROBE_T(p3);
-                PROBE_ADD(6, p3 - p2);
                 double2 *zfix = zfx + p * 32 + vl;
-                if constexpr (HI == 2) {
-                    double x0m, x1m;
-                    half_backward<K>(hi, ctad, zc, x0m, x1m, hi == 1, y2c, y1c);
-                    if (hi == 1) *zfix = make_double2(x0m, x1m);
-                } else {
-                    double xk, xk1, x0x, x1x;
-                    half_backward<K>(1, ctad, zc, xk, xk1, true, y2c, y1c);
-                    half_backward<K>(0, ctad, zc, x0x, x1x, false, 0.0, 0.0);
-                    *zfix = make_double2(xk, xk1);
-                }
-                __syncwarp();
-                PROBE_T(p4);
-                PROBE_ADD(7, p4 - p3);
+                if constexpr (SOLVER) {
+                    static_assert(!SOLVER || HI == 2, "solver warps: one half per half-warp");
+                    if constexpr (FWD) {
+                        double y2m, y1m;
+                        half_forward<K>(hi, rE, ctad, zc, y2m, y1m);
+                        if (hi == 0) zcar[p * 32 + vl] = make_double2(y2m, y1m);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(fbar + 8 * p);
+                        PROBE_T(p3);
+                        PROBE_ADD(6, p3 - p2);
+                    }
+                    if constexpr (BWD) {
+                        // both halves from a zero carried state; the second half's
+                        // carried-pair correction is the consumer's (PP / PQ), except
+                        // for the two values the first half's consumers need
+                        double x0m, x1m;
+                        half_backward<K, true>(hi, ctad, zc, x0m, x1m, false, 0.0, 0.0);
+                        if (hi == 1) {
+                            const double2 ym = zcar[p * 32 + vl];
+                            x0m = fma(ctad[CTAD_PP], ym.x, fma(ctad[CTAD_PQ], ym.y, x0m));
+                            x1m = fma(ctad[CTAD_PP + 1], ym.x, fma(ctad[CTAD_PQ + 1], ym.y, x1m));
+                            *zfix = make_double2(x0m, x1m);
+                        }
+                        __syncwarp();
+                        PROBE_T(p4);
+                        PROBE_ADD(7, p4 - p1);
+                    }
+                } else if constexpr (FWD && BWD) {
+                    double y2c, y1c;                      // half 0's carried pair
+                    if constexpr (HI == 2) {
+                        double y2m, y1m;
+                        half_forward<K>(hi, rE, ctad, zc, y2m, y1m);
+                        y2c = __shfl_xor_sync(0xffffffffu, y2m, 16);
+                        y1c = __shfl_xor_sync(0xffffffffu, y1m, 16);
+                    } else {
+                        double y2x, y1x;
+                        half_forward<K>(0, rE, ctad, zc, y2c, y1c);
+                        half_forward<K>(1, rE, ctad, zc, y2x, y1x);
+                    }
+                    PROBE_T(p3);
+                    PROBE_ADD(6, p3 - p2);
+                    if constexpr (HI == 2) {
+                        double x0m, x1m;
+                        half_backward<K>(hi, ctad, zc, x0m, x1m, hi == 1, y2c, y1c);
+                        if (hi == 1) *zfix = make_double2(x0m, x1m);
+                    } else {
+                        double xk, xk1, x0x, x1x;
+                        half_backward<K>(1, ctad, zc, xk, xk1, true, y2c, y1c);
+                        half_backward<K>(0, ctad, zc, x0x, x1x, false, 0.0, 0.0);
+                        *zfix = make_double2(xk, xk1);
+                    }
+                    __syncwarp();
+                    PROBE_T(p4);
+                    PROBE_ADD(7, p4 - p3);
                 }
             } else {
                 static_assert(SPLIT || !SOLVER, "the unsplit solve runs on the publish warp");
@@ -1293,17 +1353,19 @@ __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part
         } else if (w == W) {
             for (long j = 1; j <= nJ; ++j) {
                 if constexpr (SOLVER) {
-                    publish(j, std::true_type{}, std::false_type{});
+                    publish(j, std::true_type{}, std::false_type{}, std::false_type{});
                 } else {
-                    publish(j, std::true_type{}, std::true_type{});
+                    publish(j, std::true_type{}, std::true_type{}, std::true_type{});
                     if (lane == 0) mbar_arrive(cbar + 8 * (int)(j & 1));
                 }
             }
         } else if (w == W + 1) {
             for (long j = 1; j <= nJ; ++j) gather(j);
         } else if (SOLVER && w == W + 2) {
+            for (long j = 1; j <= nJ; ++j) publish(j, std::false_type{}, std::true_type{}, std::false_type{});
+        } else if (SOLVER && w == W + 3) {
             for (long j = 1; j <= nJ; ++j) {
-                publish(j, std::false_type{}, std::true_type{});
+                publish(j, std::false_type{}, std::false_type{}, std::true_type{});
                 if (lane == 0) mbar_arrive(cbar + 8 * (int)(j & 1));
             }
         }

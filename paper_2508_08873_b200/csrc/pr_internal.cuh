@@ -155,7 +155,7 @@ cudaError_t launch_bidiag(int mode, int n, const double *cdiag, const double *cs
 // setup (ends: P x 8 scratch), selection and launch
 constexpr int PART_KMAX = 32;                  // chunks per CTA
 constexpr int PART_CLMAX = 16;                 // CTAs per cluster
-constexpr int PART_CTAD = 5 * 2 * PART_KMAX + 12 * PART_KMAX + 4 * PART_CLMAX;
+constexpr int PART_CTAD = 5 * 2 * PART_KMAX + 14 * PART_KMAX + 4 * PART_CLMAX;
 constexpr int PART_ROWC = 8;                   // doubles per row of the K1P row data
 constexpr int PART_ENDS = 8;                   // doubles per chunk of the K1P end data
 // P = CL * K chunks of L rows (K chunks per CTA)
