@@ -323,11 +323,16 @@ __global__ void k_part_iface(int CL, int K, const double *ends, double *ctad, in
                 }
             }
         }
-        for (int col = 0; col < M; ++col) {          // rows 0 and M-1 of M_C^{-1}
+        // rows 0 and M-1 of M_C^{-1}; for M = 32 the whole inverse (row-major)
+        // for the tensor-core interface of the DM variant
+        double *MI = ctad + (size_t)CL * PART_CTAD + (size_t)C * PART_MINV;
+        for (int col = 0; col < M; ++col) {
             for (int r = 0; r < M; ++r) x[r] = (r == col) ? 1.0 : 0.0;
             band_solve(M, F, x);
             D[CTAD_R0 + col] = x[0];
             D[CTAD_RM + col] = x[M - 1];
+            if (M * M == PART_MINV)
+                for (int r = 0; r < M; ++r) MI[r * M + col] = x[r];
         }
         const double *E0 = ends + (size_t)(C * K) * PART_ENDS, *E1 = ends + (size_t)(C * K + K - 1) * PART_ENDS;
         for (int r = 0; r < M; ++r) x[r] = 0.0;
@@ -373,7 +378,7 @@ struct PartArgs {
     int n, m;
     long B;
     const double *rowc;                // (P*L) x 8
-    const double *ctad;                // CL x PART_CTAD
+    const double *ctad;                // CL x PART_CTAD, then CL x PART_MINV
     const double *in; long ld_in;      // null -> zero
     double *out; long ld_out;
     const double *off; long ld_off;
@@ -750,12 +755,22 @@ __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part
     constexpr int K = W * H;             // chunks per CTA
     constexpr int M = 2 * K;             // local interface unknowns
     constexpr bool SPLIT = K >= 16;      // split band solve (two halves)
-    constexpr bool SOLVER = TM && SPLIT; // the local band solve on its own warp (W + 2), off the publish warp
+    constexpr bool SOLVER = TM && SPLIT; // the local band solve on its own warps, off the publish warp
+    // DM: the local solve as a dense product z = M_C^{-1} g on the FP64 tensor cores
+    // (32 x 32 inverse, 16 vectors), one 8-row tile per interface warp; T_C, B_C are
+    // rows 0 and M-1 of the same product (-DPR_PART_NODM: the banded solver warps)
+#ifdef PR_PART_NODM
+    constexpr bool DM = false;
+#else
+    constexpr bool DM = SOLVER && M * M == PART_MINV && VPG == 16;
+#endif
     constexpr int RSM = AFF ? PART_RSM : 0;
     constexpr bool STAGE = part_stage<CL, W, H, L, VPT, AFF>();   // next group's input prefetched into shared memory
     extern __shared__ __align__(16) double sm[];
     cg::cluster_group cluster = cg::this_cluster();
     const int C = (int)cluster.block_rank();
+    // (measured: making the interface warps the hardware warps 0..3, the oldest of
+    // each SM sub-partition, slows the C4 launch from 26.6 to 28.5 ms)
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // persistent clusters: cluster cid runs the vector groups cid, cid + ncl, ...
     // (its CTAs keep their coefficients in shared memory across groups)
@@ -791,7 +806,8 @@ __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part
             asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(ebar + 8 * q), "r"(W) : "memory");
             // interface values of a step are complete when both the publish warp
             // (local solution z) and the gather warp ((B_{C-1}, T_{C+1})) arrived
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" :: "r"(cbar + 8 * q) : "memory");
+            // (DM: the four tile warps and the gather warp)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(cbar + 8 * q), "r"(DM ? 5 : 2) : "memory");
             // forward pass of a step done (solver warps of the TM variants)
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(fbar + 8 * q) : "memory");
         }
@@ -899,7 +915,7 @@ __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part
             const double *zz = zsb + (size_t)pp * M * 32 + vs;
             auto zval = [&](int pos) {
                 double v = zz[pos * 32];
-                if constexpr (SPLIT) {
+                if constexpr (SPLIT && !DM) {
                     if (pos < K) {
                         const double2 fx = zfx[pp * 32 + vs];
                         v = fma(ctad[CTAD_BR + pos], fx.x, fma(ctad[CTAD_BT + pos], fx.y, v));
@@ -1347,9 +1363,77 @@ __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part
                 __syncwarp();
             }
         };
+        // DM: interface warp q = w - W forms rows tile(q) of z = M_C^{-1} g with
+        // mma.m8n8k4.f64 (A: 8 rows of the inverse, kept in registers; B: the raw
+        // ends of 8 vectors, from shared memory), two column tiles (16 vectors),
+        // the k range in two halves (four independent accumulator chains), summed
+        // in fixed order.  Tile 0 holds rows {0, M-1, 1..6}: the publish warp owns
+        // T_C and B_C and sends them right after its product.
+        const int gq = lane >> 2, tq = lane & 3;
+        const int dm_q = w - W;
+        const int dm_row = (dm_q == 0) ? (gq == 0 ? 0 : (gq == 1 ? M - 1 : gq - 1)) : 7 + 8 * (dm_q - 1) + gq;
+        constexpr int DKS = DM ? M / 4 : 1, DKH = DM ? M / 8 : 1;   // k steps (of 4), per accumulator half
+        double afr[DKS] = {};
+        if constexpr (DM) {
+            const double *MI = a.ctad + (size_t)CL * PART_CTAD + (size_t)C * PART_MINV + (size_t)dm_row * M;
+#pragma unroll
+            for (int ks = 0; ks < DKS; ++ks) afr[ks] = __ldg(MI + 4 * ks + tq);
+        }
+        auto dm_tile = [&](auto j) {   // generic: instantiated for the DM variants only
+            const int p = (int)(j & 1);
+            const unsigned ph = (unsigned)(((j - 1) >> 1) & 1);
+            PROBE_T(p0);
+            mbar_wait_idle(ebar + 8 * p, ph, a.idle_ns);
+            PROBE_T(p1);
+            if (dm_q == 0) PROBE_ADD(4, p1 - p0);
+            const double *gE = reinterpret_cast<const double *>(rawE + (size_t)p * K * 32);
+            double bfr[DKS][2];
+#pragma unroll
+            for (int ks = 0; ks < DKS; ++ks)
+#pragma unroll
+                for (int ct = 0; ct < 2; ++ct)
+                    bfr[ks][ct] = gE[(size_t)((2 * ks + (tq >> 1)) * 32 + ct * 8 + gq) * 2 + (tq & 1)];
+            double acc[2][2][2];
+#pragma unroll
+            for (int ct = 0; ct < 2; ++ct)
+#pragma unroll
+                for (int kh = 0; kh < 2; ++kh) acc[ct][kh][0] = acc[ct][kh][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < DKS; ++ks)
+#pragma unroll
+                for (int ct = 0; ct < 2; ++ct)
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                 : "+d"(acc[ct][ks / DKH][0]), "+d"(acc[ct][ks / DKH][1])
+                                 : "d"(afr[ks]), "d"(bfr[ks][ct]));
+            double2 *zrow = reinterpret_cast<double2 *>(zs + ((size_t)p * M + dm_row) * 32);
+#pragma unroll
+            for (int ct = 0; ct < 2; ++ct)
+                zrow[ct * 4 + tq] = make_double2(acc[ct][0][0] + acc[ct][1][0], acc[ct][0][1] + acc[ct][1][1]);
+            __syncwarp();
+            if (dm_q == 0) {           // (T_C, B_C) = rows 0 and M-1 to every CTA of the cluster
+                const double Tv = zs[((size_t)p * M) * 32 + vl], Bv = zs[((size_t)p * M + M - 1) * 32 + vl];
+                const unsigned off = (unsigned)(((p * CL + C) * 32 + vl) * sizeof(double2));
+#pragma unroll
+                for (int rr = 0; rr < CLH; ++rr) {
+                    const int r = hi * CLH + rr;
+                    st_async_v2(rmap[r] + off, Tv, Bv, rmap[CL + r] + 8 * p);
+                }
+            }
+            if (lane == 0) mbar_arrive(cbar + 8 * p);
+            PROBE_T(p2);
+            if (dm_q == 0) PROBE_ADD(5, p2 - p1);
+            if (dm_q == 2) PROBE_ADD(6, p2 - p1);
+        };
         // global step index over this cluster's groups (mbarrier slots and phases)
         const long nJ = ngrp * (long)a.m;
         if (a.noiface) {
+        } else if (DM) {
+            if constexpr (DM) {
+                for (long j = 1; j <= nJ; ++j) {
+                    dm_tile(j);
+                    if (w == W + 1) gather(j);
+                }
+            }
         } else if (w == W) {
             for (long j = 1; j <= nJ; ++j) {
                 if constexpr (SOLVER) {

@@ -549,7 +549,7 @@ pr_status pr_op_create_tridiag(int n, const double *sub, const double *diag, con
     double *d_ends = nullptr;
     if (e == cudaSuccess && part_config(n, pP, pL, pCL, pK)) {
         op.part_P = pP; op.part_L = pL; op.part_CL = pCL; op.part_K = pK;
-        const size_t rb = (size_t)pP * pL * PART_ROWC * sizeof(double), cb = (size_t)pCL * PART_CTAD * sizeof(double);
+        const size_t rb = (size_t)pP * pL * PART_ROWC * sizeof(double), cb = (size_t)pCL * (PART_CTAD + PART_MINV) * sizeof(double);
         e = cudaMalloc(&op.part_rowc_fw, rb);
         if (e == cudaSuccess) e = cudaMalloc(&op.part_rowc_tr, rb);
         if (e == cudaSuccess) e = cudaMalloc(&op.part_ctad_fw, cb);

@@ -156,6 +156,9 @@ cudaError_t launch_bidiag(int mode, int n, const double *cdiag, const double *cs
 constexpr int PART_KMAX = 32;                  // chunks per CTA
 constexpr int PART_CLMAX = 16;                 // CTAs per cluster
 constexpr int PART_CTAD = 5 * 2 * PART_KMAX + 14 * PART_KMAX + 4 * PART_CLMAX;
+// dense inverse of a CTA's local interface matrix (M = 32 unknowns: K = 16 chunks),
+// row-major, stored behind the CL x PART_CTAD interface data (k_part.cu, DM variant)
+constexpr int PART_MINV = 32 * 32;
 constexpr int PART_ROWC = 8;                   // doubles per row of the K1P row data
 constexpr int PART_ENDS = 8;                   // doubles per chunk of the K1P end data
 // P = CL * K chunks of L rows (K chunks per CTA)
