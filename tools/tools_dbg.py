@@ -1,4 +1,7 @@
 import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+import os, sys
 import numpy as np
 import torch
 from paper_2508_08873_b200 import Operator, Coarse

@@ -1,4 +1,7 @@
 """One C3 build (for ncu on the K2 DMMA GEMM)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import torch
 from paper_2508_08873_b200 import Operator, Coarse
 from workloads.configs import get

@@ -1,4 +1,6 @@
 """One C4 Parareal run (for ncu on the affine stepper / sweep / expand)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 from paper_2508_08873_b200 import Operator, Coarse, SourceTerm, parareal
 from workloads import generators as G

@@ -1,4 +1,7 @@
 """One stepper launch at C4 build size (for ncu)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import sys
 import torch
 from paper_2508_08873_b200 import Operator, PR_LINEAR

@@ -1,4 +1,7 @@
 """Quick timing probe of the 1D stepper (development aid)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
 import sys, time
 import numpy as np
 import torch
