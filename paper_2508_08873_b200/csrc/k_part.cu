@@ -742,7 +742,7 @@ template <int W, bool TM> __host__ __device__ constexpr int part_maxreg()
     return r > 255 ? 255 : r;
 }
 
-template <int CL, int W, int H, int L, int VPT, bool AFF, bool TM = false>
+template <int CL, int W, int H, int L, int VPT, bool AFF, bool TM = false, bool DMV = true>
 __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part_maxreg<W, TM>())) k_part_step(PartArgs a)
 {
     static_assert(!TM || (L == 64 && W == 8), "TMEM coefficient store: 2 x 64 doubles per lane, two warps per quadrant");
@@ -758,12 +758,9 @@ __global__ void __launch_bounds__(32 * (W + part_ni<TM>()), 1) __maxnreg__((part
     constexpr bool SOLVER = TM && SPLIT; // the local band solve on its own warps, off the publish warp
     // DM: the local solve as a dense product z = M_C^{-1} g on the FP64 tensor cores
     // (32 x 32 inverse, 16 vectors), one 8-row tile per interface warp; T_C, B_C are
-    // rows 0 and M-1 of the same product (-DPR_PART_NODM: the banded solver warps)
-#ifdef PR_PART_NODM
-    constexpr bool DM = false;
-#else
-    constexpr bool DM = SOLVER && M * M == PART_MINV && VPG == 16;
-#endif
+    // rows 0 and M-1 of the same product (DMV = false, PR_PART_NODM=1: the banded
+    // solver warps instead)
+    constexpr bool DM = DMV && SOLVER && M * M == PART_MINV && VPG == 16;
     constexpr int RSM = AFF ? PART_RSM : 0;
     constexpr bool STAGE = part_stage<CL, W, H, L, VPT, AFF>();   // next group's input prefetched into shared memory
     extern __shared__ __align__(16) double sm[];
@@ -1499,7 +1496,7 @@ cudaError_t launch_part_setup(int n, int P, int L, int CL, int K, const double *
     return cudaGetLastError();
 }
 
-template <int CL, int W, int H, int L, int VPT, bool AFF, bool TM = false>
+template <int CL, int W, int H, int L, int VPT, bool AFF, bool TM = false, bool DMV = true>
 static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
 {
     constexpr size_t smem = part_smem_t<CL, W, H, L, VPT, AFF>();
@@ -1511,10 +1508,10 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     cudaGetDevice(&dev);
     const unsigned long long bit = 1ULL << (dev & 63);
     if (!(attr_mask.load(std::memory_order_acquire) & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, VPT, AFF, TM>,
+        cudaError_t e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, VPT, AFF, TM, DMV>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e == cudaSuccess && CL > 8)
-            e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, VPT, AFF, TM>,
+            e = cudaFuncSetAttribute(k_part_step<CL, W, H, L, VPT, AFF, TM, DMV>,
                                      cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         if (e != cudaSuccess) return e;
         attr_mask.fetch_or(bit, std::memory_order_release);
@@ -1538,7 +1535,7 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     int ncl = max_cl[dev & 63].load(std::memory_order_acquire);
     if (ncl == 0) {
         int nc = 0;
-        if (cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, VPT, AFF, TM>, &cfg) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, VPT, AFF, TM, DMV>, &cfg) != cudaSuccess ||
             nc < 1) {
             (void)cudaGetLastError();
             nc = -1;                   // unknown: one cluster per group
@@ -1553,7 +1550,7 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
     ag.groups = groups;
     if (flags().part_prof) {
         int nc = -1;
-        cudaError_t eo = cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, VPT, AFF, TM>, &cfg);
+        cudaError_t eo = cudaOccupancyMaxActiveClusters(&nc, (void *)k_part_step<CL, W, H, L, VPT, AFF, TM, DMV>, &cfg);
         fprintf(stderr, "part: max active clusters %d (%s), smem %zu B, groups %ld\n", nc,
                 eo == cudaSuccess ? "ok" : cudaGetErrorString(eo), smem, groups);
         (void)cudaGetLastError();
@@ -1564,7 +1561,7 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
         PartArgs b = ag;
         cudaMalloc(&b.prof, PART_NPROBE * sizeof(unsigned long long));
         cudaMemsetAsync(b.prof, 0, PART_NPROBE * sizeof(unsigned long long), s);
-        cudaError_t e = cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF, TM>, b);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF, TM, DMV>, b);
         unsigned long long h[PART_NPROBE];
         cudaMemcpyAsync(h, b.prof, sizeof(h), cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
@@ -1578,7 +1575,7 @@ static cudaError_t part_launch(const PartArgs &a, long groups, cudaStream_t s)
         return e;
     }
 #endif
-    return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF, TM>, ag);
+    return cudaLaunchKernelEx(&cfg, k_part_step<CL, W, H, L, VPT, AFF, TM, DMV>, ag);
 }
 
 template <int CL, int W, int H, int L, int VPT = 1>
@@ -1589,9 +1586,17 @@ static cudaError_t part_launch_aff(const PartArgs &a, long B, cudaStream_t s)
     // TM: {nl, w} in tensor memory (64-row chunks, up to 8 compute warps);
     // PR_PART_NOTMEM=1 keeps every coefficient in shared memory
     if constexpr (L == 64 && VPT == 1 && W == 8) {
-        if (!flags().part_notmem)
+        if (!flags().part_notmem) {
+            // PR_PART_NODM=1: the banded interface solve on the solver warps instead
+            // of the tensor-core product (K = 16 chunks per CTA only)
+            if constexpr (W * H == 16) {
+                if (flags().part_nodm)
+                    return a.R > 0 ? part_launch<CL, W, H, L, VPT, true, true, false>(a, groups, s)
+                                   : part_launch<CL, W, H, L, VPT, false, true, false>(a, groups, s);
+            }
             return a.R > 0 ? part_launch<CL, W, H, L, VPT, true, true>(a, groups, s)
                            : part_launch<CL, W, H, L, VPT, false, true>(a, groups, s);
+        }
     }
     return a.R > 0 ? part_launch<CL, W, H, L, VPT, true>(a, groups, s)
                    : part_launch<CL, W, H, L, VPT, false>(a, groups, s);

@@ -130,6 +130,7 @@ static void read_flags()
     if (getenv("PR_PART_IDLE_NS")) f.part_idle_ns = num("PR_PART_IDLE_NS");
     f.part_noiface = on("PR_PART_NOIFACE");
     f.part_notmem = on("PR_PART_NOTMEM");
+    f.part_nodm = on("PR_PART_NODM");
     f.part_nopersist = on("PR_PART_NOPERSIST");
     g_flags = f;
 }

@@ -54,6 +54,7 @@ struct Flags {
     int part_h = 0, stepper_pd = 0, stepper_vpt = 0;
     int part_idle_ns = -1;       // PR_PART_IDLE_NS: interface-warp poll back-off (dev aid; -1 = default)
     bool part_nopersist = false; // PR_PART_NOPERSIST: one K1P cluster per vector group (no staging reuse)
+    bool part_nodm = false;      // PR_PART_NODM: K1P TM variants solve the CTA-local interface system with the banded solver warps instead of the FP64 tensor-core product
     bool part_notmem = false;    // PR_PART_NOTMEM: K1P keeps {nl, w} in shared memory instead of tensor memory
     bool part_noiface = false;   // PR_PART_NOIFACE: K1P sweeps without the interface (timing aid; wrong results)
 };

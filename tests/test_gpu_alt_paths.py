@@ -9,6 +9,9 @@ kernel of the default path by its simpler fallback:
   PR_NO_TRSM_DMMA   row-wise substitution instead of the blocked DMMA TRSM
   PR_NO_RINV_CM     generic R^{-1} apply instead of the column-major DMMA one (2D)
   PR_NO_EXPAND_MMA  CUDA-core lift / reconstruction instead of the DMMA ones
+  PR_PART_NOTMEM    K1P with every coefficient in shared memory (no tensor memory)
+  PR_PART_NODM      K1P (tensor-memory variant, K = 16) with the banded interface
+                    solve on the solver warps instead of the FP64 tensor-core product
 
 A whole rSVD build + Parareal run (T4 in 1D, T2D in 2D) goes through the
 switched kernel and is compared with the oracle at
@@ -94,6 +97,37 @@ def test_two_vectors_per_lane_layout_at_c4_size(mode, pr_env):
     op_o, op_g = make_op(cfg), gpu_op(cfg)
     S = 4
     X = np.random.default_rng(3).standard_normal((2 * S, cfg.n))
+    out = empty_batch(cfg, 2 * S)
+    if mode == "affine":
+        from dataclasses import replace
+        cfg_s = replace(cfg, nsrc=S)
+        op_g.fine_propagate(PR_AFFINE, 5, cfg.m, to_gpu(cfg, X), out, vecs_per_interval=S,
+                            source=gpu_source(cfg_s))
+        src = G.source_1d(cfg_s)
+        ref = np.concatenate([fine(op_o, 6 + j, X[j * S:(j + 1) * S], "affine", src, np.arange(S))
+                              for j in range(2)])
+    else:
+        op_g.fine_propagate(PR_LINEAR if mode == "linear" else PR_ADJOINT, 5, cfg.m, to_gpu(cfg, X), out)
+        ref = fine(op_o, 6, X, mode)
+    got = from_gpu(cfg, out)
+    for v in range(2 * S):
+        assert relnorm(got[v], ref[v]) <= TAU_1D
+
+
+@pytest.mark.parametrize("switch", ["PR_PART_NOTMEM", "PR_PART_NODM"])
+@pytest.mark.parametrize("mode", ["linear", "adjoint", "affine"])
+def test_part_interface_variants_at_c4_size(mode, switch, pr_env):
+    """K1P's alternate coefficient store / interface solve at C4's full grid
+    (non-symmetric C4N: K = 16 chunks per CTA, the shape the tensor-memory and
+    tensor-core variants serve) against the oracle's Thomas steps."""
+    from gpu_util import relnorm
+    from oracle.fine import fine
+    from paper_2508_08873_b200 import PR_ADJOINT, PR_AFFINE, PR_LINEAR
+    pr_env(**{switch: "1"})
+    cfg = get("C4N")
+    op_o, op_g = make_op(cfg), gpu_op(cfg)
+    S = 4
+    X = np.random.default_rng(5).standard_normal((2 * S, cfg.n))
     out = empty_batch(cfg, 2 * S)
     if mode == "affine":
         from dataclasses import replace
