@@ -27,13 +27,24 @@ int xty_chunks(long rows, int nbatch)
 {
     // enough CTAs to fill the machine four times (the DMMA kernels run one or
     // two CTAs per SM; more, shorter CTAs shrink the last-wave tail), at least
-    // 64 rows per chunk
+    // 64 rows per chunk; among up to three times that many chunks the count whose
+    // grid (chunks x nbatch CTAs, two per SM) leaves the emptiest last wave
+    // fullest (C4: 8 chunks x 256 intervals = 6.92 waves instead of 3 x 256 = 2.59)
     long want = (4L * num_sms() + nbatch - 1) / nbatch;
     long maxc = (rows + 63) / 64;
-    long c = want < maxc ? want : maxc;
-    if (c < 1) c = 1;
-    if (c > 256) c = 256;
-    return (int)c;
+    if (maxc > 256) maxc = 256;
+    if (want < 1) want = 1;
+    if (want >= maxc) return (int)(maxc < 1 ? 1 : maxc);
+    long hi = 3 * want < maxc ? 3 * want : maxc;
+    const long slots = 2L * num_sms();
+    long best = want;
+    double best_eff = 0.0;
+    for (long c = want; c <= hi; ++c) {
+        const long total = c * nbatch;
+        const double eff = (double)total / (double)(((total + slots - 1) / slots) * slots);
+        if (eff > best_eff + 0.02) { best_eff = eff; best = c; }
+    }
+    return (int)best;
 }
 
 template <int BPT>
@@ -618,7 +629,8 @@ cudaError_t launch_reduce_parts(const double *part, int nbatch, int nchunk, int 
 // ---------------------------------------------------------- CholeskyQR control
 // One CTA per interval.  Shifted CholeskyQR (Fukaya et al. 2020):
 //   G = Q^T Q, s = 11 (rows*l + l(l+1)) u ||G||_F, R^T R = G + s I, Q <- Q R^{-1};
-// repeated while ||G - I||_F >= 1/2, then two unshifted passes (CholeskyQR2).
+// repeated while ||G - I||_F >= 1/2, then unshifted passes: one if it starts
+// from ||G - I||_F < 1/8, else two (CholeskyQR2).
 constexpr int CH_THREADS = 256;
 
 __global__ void __launch_bounds__(CH_THREADS) k_chol(CholArgs a)
@@ -756,7 +768,10 @@ __global__ void __launch_bounds__(CH_THREADS) k_chol(CholArgs a)
         }
     }
     if (threadIdx.x == 0) {
-        int ns = plain ? (st == 1 ? 2 : 1) : 0;
+        // An unshifted pass from ||G - I||_F = d leaves an orthogonality error of
+        // O(l u (1 + d) / (1 - d)): for d < 1/8 this pass is the last one (no
+        // second CholeskyQR2 pass, no verification Gram); else one more follows.
+        int ns = plain ? ((st == 1 || offI < 0.125) ? 2 : 1) : 0;
         a.state[b] = ns;
         a.act[b] = use_inv ? 2 : 1;
         if (ns != 2 && a.active) atomicAdd(a.active, 1);

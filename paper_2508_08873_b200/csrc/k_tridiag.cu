@@ -152,8 +152,12 @@ __global__ void k_sketch(int dim, int n, long rows, int q0, int nint, int l,
     long tid = (long)blockIdx.x * blockDim.x + threadIdx.x;
     long total = nb * (long)nint * l;
     if (tid >= total) return;
-    long blk = tid % nb;
-    long v = tid / nb;                // vector within the output
+    // consecutive threads run along the contiguous direction of the output:
+    // vectors in the 1D layout (vs == 1: a warp stores 32 consecutive doubles
+    // of a row), rows in the 2D layout (the values depend on (blk, col, q) only)
+    const long nvec = (long)nint * l;
+    long blk = (vs == 1) ? tid / nvec : tid % nb;
+    long v = (vs == 1) ? tid % nvec : tid / nb;   // vector within the output
     int q = q0 + (int)(v / l);
     int col = (int)(v % l);
     double z[4];

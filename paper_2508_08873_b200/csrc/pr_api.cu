@@ -1222,16 +1222,21 @@ __global__ void k_eye(double *E, int R)
 __global__ void k_combine_offsets(const double *basis, long ldb, int R, const double *amp, int S, int nq,
                                   long rows, double *out, long ld)
 {
-    const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long per = (long)nq * S;
-    if (idx >= per * rows) return;
-    const long i = idx / per, c = idx % per;
-    const int q = (int)(c / S), sI = (int)(c % S);
-    const double *bv = basis + i * ldb + (long)q * R;
-    const double *av = amp + (long)sI * R;
-    double acc = 0.0;
-    for (int r = 0; r < R; ++r) acc = fma(av[r], bv[r], acc);
-    out[i * ld + c] = acc;
+    // grid.y strides over the rows, grid.x * block over the nq * S columns of a
+    // row (coalesced stores; no 64-bit index division per element)
+    const int per = nq * S;
+    for (long i = blockIdx.y; i < rows; i += gridDim.y) {
+        const double *bi = basis + i * ldb;
+        double *oi = out + i * ld;
+        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < per; c += gridDim.x * blockDim.x) {
+            const int q = c / S, sI = c - q * S;
+            const double *bv = bi + (long)q * R;
+            const double *av = amp + (long)sI * R;
+            double acc = 0.0;
+            for (int r = 0; r < R; ++r) acc = fma(av[r], bv[r], acc);
+            oi[c] = acc;
+        }
+    }
 }
 
 // ---------------------------------------------------------------- Parareal
@@ -1345,10 +1350,10 @@ static pr_status parareal_core(pr_coarse G, pr_op h, int nsrc, const double *u0,
             fb.amp = eye;
             st = propagate(op, PR_AFFINE, q0, m, nq * R, R, &fb, nullptr, ldb, basis, ldb, nullptr, 0, 0, 0, s);
             if (st != PR_OK) return st;
-            const long tot = rows * nq * S;
+            const long per = (long)nq * S;
+            dim3 cgrid((unsigned)std::min<long>((per + 255) / 256, 1024), (unsigned)std::min<long>(rows, 65535));
             note_launch();
-            k_combine_offsets<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(basis, ldb, R, f->amp, S, nq, rows,
-                                                                            bb + blk, ld);
+            k_combine_offsets<<<cgrid, 256, 0, s>>>(basis, ldb, R, f->amp, S, nq, rows, bb + blk, ld);
             PR_CHECK_LAUNCH("k_combine_offsets");
         } else {
             st = propagate(op, PR_AFFINE, q0, m, nq * S, S, f, nullptr, ld, bb + blk, ld, nullptr, 0, 0, 0, s);
