@@ -1222,19 +1222,33 @@ __global__ void k_eye(double *E, int R)
 __global__ void k_combine_offsets(const double *basis, long ldb, int R, const double *amp, int S, int nq,
                                   long rows, double *out, long ld)
 {
-    // grid.y strides over the rows, grid.x * block over the nq * S columns of a
-    // row (coalesced stores; no 64-bit index division per element)
+    // a thread owns column c = (q, s) (grid.x * block over the nq * S columns:
+    // coalesced stores) and walks the rows i = blockIdx.y, + gridDim.y, ...;
+    // its R amplitudes stay in registers (R <= 8), the basis values of a row
+    // are the same address for the S threads of an interval
     const int per = nq * S;
-    for (long i = blockIdx.y; i < rows; i += gridDim.y) {
-        const double *bi = basis + i * ldb;
-        double *oi = out + i * ld;
-        for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < per; c += gridDim.x * blockDim.x) {
-            const int q = c / S, sI = c - q * S;
-            const double *bv = bi + (long)q * R;
-            const double *av = amp + (long)sI * R;
-            double acc = 0.0;
-            for (int r = 0; r < R; ++r) acc = fma(av[r], bv[r], acc);
-            oi[c] = acc;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < per; c += gridDim.x * blockDim.x) {
+        const int q = c / S, sI = c - q * S;
+        const double *av = amp + (long)sI * R;
+        if (R <= 8) {
+            double ar[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) ar[r] = (r < R) ? av[r] : 0.0;
+            for (long i = blockIdx.y; i < rows; i += gridDim.y) {
+                const double *bv = basis + i * ldb + (long)q * R;
+                double acc = 0.0;
+#pragma unroll
+                for (int r = 0; r < 8; ++r)
+                    if (r < R) acc = fma(ar[r], bv[r], acc);
+                out[i * ld + c] = acc;
+            }
+        } else {
+            for (long i = blockIdx.y; i < rows; i += gridDim.y) {
+                const double *bv = basis + i * ldb + (long)q * R;
+                double acc = 0.0;
+                for (int r = 0; r < R; ++r) acc = fma(av[r], bv[r], acc);
+                out[i * ld + c] = acc;
+            }
         }
     }
 }
@@ -1351,7 +1365,7 @@ static pr_status parareal_core(pr_coarse G, pr_op h, int nsrc, const double *u0,
             st = propagate(op, PR_AFFINE, q0, m, nq * R, R, &fb, nullptr, ldb, basis, ldb, nullptr, 0, 0, 0, s);
             if (st != PR_OK) return st;
             const long per = (long)nq * S;
-            dim3 cgrid((unsigned)std::min<long>((per + 255) / 256, 1024), (unsigned)std::min<long>(rows, 65535));
+            dim3 cgrid((unsigned)std::min<long>((per + 255) / 256, 1024), (unsigned)std::min<long>(rows, 128));
             note_launch();
             k_combine_offsets<<<cgrid, 256, 0, s>>>(basis, ldb, R, f->amp, S, nq, rows, bb + blk, ld);
             PR_CHECK_LAUNCH("k_combine_offsets");
