@@ -613,6 +613,9 @@ def _e2e(wl, steps, barrier, world):
         ready = torch.cuda.Event()
         ready.record(main_stream)
         op.close()                 # frees device memory (a device-wide wait): before the copy is queued
+        if os.environ.get("BENCH_E2E_SERIAL"):     # dev aid: the copy on the compute stream
+            out_host.copy_(U, non_blocking=True)
+            continue
         with torch.cuda.stream(copy_stream):
             copy_stream.wait_event(ready)
             out_host.copy_(U, non_blocking=True)

@@ -259,15 +259,19 @@ __device__ void band_solve(int M, const double (*F)[5], double *x)
 // of the full rows).  Global rows of C:
 //   T_C - alpha_C[0] B_{C-1} - beta_C[0] T_{C+1} = zloc_C[0]
 //   B_C - alpha_C[2K-1] B_{C-1} - beta_C[2K-1] T_{C+1} = zloc_C[2K-1],  zloc_C = M_C^{-1} g_C.
-__global__ void k_part_iface(int CL, int K, const double *ends, double *ctad, int *bad)
+// One block of 32 threads: thread C < CL prepares super-chunk C (local factors,
+// responses, inverse rows, its two rows of the cluster-level system in shared
+// memory); thread 0 then factors and inverts the cluster-level system.
+__global__ void __launch_bounds__(32) k_part_iface(int CL, int K, const double *ends, double *ctad, int *bad)
 {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (blockIdx.x != 0) return;
     constexpr int MX = 2 * (PART_KMAX > PART_CLMAX ? PART_KMAX : PART_CLMAX);
     double A[MX][5], rs[MX], F[MX][5], x[MX];
-    double gA[2 * PART_CLMAX][5], grs[2 * PART_CLMAX];
+    __shared__ double gA[2 * PART_CLMAX][5], grs[2 * PART_CLMAX];
     const int M = 2 * K;
     bool ok = true;
-    for (int C = 0; C < CL; ++C) {
+    const int C = threadIdx.x;
+    if (C < CL) {
         double *D = ctad + (size_t)C * PART_CTAD;
         for (int i = 0; i < PART_CTAD; ++i) D[i] = 0.0;
         for (int r = 0; r < M; ++r) {
@@ -359,6 +363,10 @@ __global__ void k_part_iface(int CL, int K, const double *ends, double *ctad, in
             grs[r] = e ? x[M - 1] : x[0];
         }
     }
+    if (!ok) atomicExch(bad, 1);
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    ok = true;
     const int MG = 2 * CL;
     ok = band_factor(MG, gA, grs, F) && ok;
     for (int col = 0; col < MG; ++col) {
